@@ -1,0 +1,160 @@
+/*
+ * spike_b200.h — C-ABI of the B200-native recursive SPIKE banded solver.
+ *
+ * This is the drop-in boundary under the reference's C++ solver API
+ * (/root/reference/proj/include/spike/{factorize,solve,partition}.hpp).  Plain
+ * pointers and sizes only; no exceptions, no torch types.  The C++ wrapper in
+ * include/spike/*.hpp (namespace spike) maps the status codes back to the
+ * reference's exception types.
+ *
+ * Entry point                reference interface it replaces
+ * -------------------------  ------------------------------------------------
+ * spk_factorize              spike::factorize            factorize.hpp:76-77
+ * spk_solve (transpose=0/1)  spike::solve / transpose_solve  solve.hpp:23-29
+ * spk_make_plan              spike::make_plan            partition.hpp:56
+ * spk_compute_ratios         spike::compute_ratios       partition.hpp:45
+ * spk_distribute_threads     spike::distribute_threads   partition.hpp:39
+ * spk_compute_sizes          spike::compute_sizes        partition.hpp:51-52
+ * spk_gpu_plan               (new) arbitrary-p planner mapped onto SMs
+ * spk_fact_* getters         SpikeFactorization fields   factorize.hpp:56-74
+ * spk_reduced_*              reduce_factorize / reduced_solve(_transpose)
+ *                                                        factorize.hpp:45-49, solve.hpp:33-36
+ * spk_band_matmul            spike::band_matmul          band_ops.hpp:11
+ *
+ * Memory: `band`, `F` and `X` may live on the host or on the device; say which
+ * with SPK_MEM_HOST / SPK_MEM_DEVICE.  Host buffers are staged through the
+ * call's stream (pinned host memory makes the copies asynchronous).  All work
+ * is ordered on the stream passed in (NULL = the legacy default stream).
+ * A factorization is immutable after spk_factorize returns and may be used by
+ * any number of concurrent spk_solve calls on different streams.
+ */
+#ifndef SPIKE_B200_H
+#define SPIKE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum spk_status {
+    SPK_OK = 0,
+    SPK_EINVAL = 1,    /* std::invalid_argument (shape / plan)          */
+    SPK_ESINGULAR = 2, /* std::runtime_error (exactly singular column)  */
+    SPK_EDOMAIN = 3,   /* std::domain_error (sizing)                    */
+    SPK_ECUDA = 4,     /* CUDA runtime failure                          */
+    SPK_ENOMEM = 5,    /* device allocation failure                     */
+    SPK_ENCCL = 6,     /* collective failure                            */
+    SPK_ERANGE = 7     /* std::out_of_range                             */
+} spk_status;
+
+enum { SPK_MEM_HOST = 0, SPK_MEM_DEVICE = 1 };
+enum { SPK_FIRSTLAST = 0, SPK_INNER_SINGLE = 1, SPK_INNER_DUAL = 2 };
+enum { SPK_TIP_VT = 0, SPK_TIP_VB = 1, SPK_TIP_WT = 2, SPK_TIP_WB = 3, SPK_BHAT = 4, SPK_CHAT = 5 };
+
+typedef struct spk_fact spk_fact;
+typedef struct spk_reduced spk_reduced;
+
+/* Partition plan: p partitions, bounds[p+1] row offsets (bounds[0]=0,
+ * bounds[p]=n), kinds[p] (informational on the GPU: dual partitions are
+ * factored like single ones; the tips are the same mathematical objects). */
+typedef struct spk_plan {
+    int32_t p;
+    const int64_t *bounds;
+    const int32_t *kinds;
+} spk_plan;
+
+typedef struct spk_factor_options {
+    int32_t pivoting;  /* FactorOptions::pivoting   (factorize.hpp:13-16) */
+    double boost_eps;  /* FactorOptions::boost_eps  (<= 0 -> sqrt(eps))   */
+} spk_factor_options;
+
+const char *spk_last_error(void); /* thread-local message of the last failure */
+const char *spk_version(void);
+
+/* ---- planning (host-only, no GPU needed) ---- */
+void spk_compute_ratios(double K, int32_t nrhs, int32_t k, double *r12, double *r13);
+/* distribute_threads(t, cap_p): p and kinds[p] (kinds capacity >= p) */
+spk_status spk_distribute_threads(int32_t t, int32_t cap_p, int32_t *p, int32_t *kinds,
+                                  int32_t kinds_cap, int32_t *threads_used, int32_t *idle);
+spk_status spk_compute_sizes(int64_t n, int32_t p, const int32_t *kinds, double r12, double r13,
+                             int64_t min_single, int64_t min_dual, int64_t *sizes);
+/* reference make_plan: bounds capacity >= p+1, kinds capacity >= p */
+spk_status spk_make_plan(int64_t n, int32_t kl, int32_t ku, int32_t t, double r12, double r13,
+                         int32_t cap, int32_t *p, int64_t *bounds, int32_t *kinds,
+                         int32_t *threads_used, int32_t *idle);
+/* B200 planner: p chosen for the GPU (any p >= 1, not only powers of two);
+ * p_hint > 0 forces p.  First/last partitions sized by the reference ratio
+ * model with K fitted to the device. */
+spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t pivoting,
+                        int32_t p_hint, int32_t cap, int32_t *p, int64_t *bounds,
+                        int32_t *kinds);
+
+/* ---- factorization ---- */
+spk_status spk_factorize(const double *band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
+                         const spk_plan *plan, const spk_factor_options *opts, void *stream,
+                         spk_fact **out);
+void spk_fact_destroy(spk_fact *f);
+
+/* Fields of SpikeFactorization (factorize.hpp:56-74).  Host mirrors copied on
+ * demand; these synchronise the factorization's stream. */
+spk_status spk_fact_info(const spk_fact *f, int64_t *n, int32_t *kl, int32_t *ku, int32_t *k,
+                         int32_t *p, int32_t *levels, int32_t *boost_count,
+                         int32_t *boost_warnings);
+spk_status spk_fact_bounds(const spk_fact *f, int64_t *bounds /* p+1 */);
+spk_status spk_fact_factor_sweeps(const spk_fact *f, int64_t *sweeps /* p */);
+spk_status spk_fact_tip(const spk_fact *f, int32_t which, int32_t i, double *out /* k*k */);
+/* Level l, unit u spike columns (v: which=0, w: which=1); rows returned in *h.
+ * out may be NULL to query h; returns zeros where never formed. */
+spk_status spk_fact_level_spike(const spk_fact *f, int32_t l, int32_t which, int32_t u, int32_t *h,
+                                double *out);
+/* Factored 2k x 2k coupling of level l pair a: packed LU (column-major, 2k x 2k,
+ * unit-lower L below the diagonal, U on and above), pivots (0-based rows), and
+ * whether the pivoted factorization fell back to boosting. */
+spk_status spk_fact_coupling(const spk_fact *f, int32_t l, int32_t a, double *lu, int32_t *piv,
+                             int32_t *fell_back);
+int32_t spk_fact_units(const spk_fact *f, int32_t l);
+
+/* ---- solves ---- */
+typedef struct spk_solve_stats {
+    int64_t *partition_full_sweeps; /* p entries or NULL (SolveStats, solve.hpp:11-20) */
+    int64_t reduced_coupling_solves;
+} spk_solve_stats;
+
+/* X := A^-1 F (transpose=0) or A^-T F (transpose=1); F, X column-major with
+ * leading dimensions ldf, ldx >= n.  X may alias F. */
+spk_status spk_solve(const spk_fact *f, int32_t transpose, const double *F, int64_t ldf,
+                     int32_t nrhs, double *X, int64_t ldx, int32_t mem, void *stream,
+                     spk_solve_stats *stats);
+
+/* ---- reduced system on its own (reduce_factorize / reduced_solve) ----
+ * vt, vb, wt, wb: p blocks of k*k column-major each (host). */
+spk_status spk_reduced_create(const double *vt, const double *vb, const double *wt,
+                              const double *wb, int32_t p, int32_t k, double boost_eps,
+                              spk_reduced **out);
+spk_status spk_reduced_solve(const spk_reduced *r, int32_t transpose, double *z /* host 2pk x ncols */,
+                             int32_t ncols, int64_t *couplings);
+int32_t spk_reduced_levels(const spk_reduced *r);
+int32_t spk_reduced_boost_warnings(const spk_reduced *r);
+void spk_reduced_destroy(spk_reduced *r);
+
+/* ---- device utilities ---- */
+/* Y := A X or A^T X with A banded (both on device or both host). */
+spk_status spk_band_matmul(const double *band, int64_t n, int32_t kl, int32_t ku, const double *X,
+                           int64_t ldx, int32_t ncols, int32_t transpose, double *Y, int64_t ldy,
+                           int32_t mem, void *stream);
+/* Seeded BASELINE generator (include/spike_b200_gen.h) straight into device
+ * memory: band (kl+ku+1) x n column-major; F n x ncols. */
+spk_status spk_generate_band(uint64_t seed, int64_t n, int32_t kl, int32_t ku, double dd,
+                             double *d_band, void *stream);
+spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double *d_F, int64_t ldf,
+                            void *stream);
+/* Number of kernel launches issued by this library on the calling thread
+ * since the last reset (instrumentation for bench.py's gpu_launches). */
+int64_t spk_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPIKE_B200_H */

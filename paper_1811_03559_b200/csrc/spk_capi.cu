@@ -1,0 +1,1473 @@
+// spk_capi.cu — C-ABI (include/spike_b200.h) over the SPIKE device kernels.
+//
+// The host side is a compiler, not an interpreter: at factorization time the
+// reference's stage structure (src/factorize.cpp:133-257, src/solve.cpp:81-380)
+// is lowered into three static "programs" (factor, forward solve, transpose
+// solve).  Each program is a short list of stages; each stage is ONE batched
+// launch over all partitions / coupling blocks.  Job descriptors live in one
+// device blob uploaded once, and address per-call buffers through a Bufs table,
+// so a solve issues O(stages + reduced levels) launches independent of p.
+#include "../../include/spike_b200.h"
+#include "spk_launch.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace spk;
+
+// ---------------------------------------------------------------------------
+// errors
+namespace {
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+
+struct SpkError {
+    spk_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(spk_status st, const std::string& m) { throw SpkError{st, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation) fail(SPK_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+        fail(SPK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <class F>
+spk_status guarded(F&& f) {
+    try {
+        f();
+        return SPK_OK;
+    } catch (const SpkError& e) {
+        g_err = e.msg;
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SPK_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPK_EINVAL;
+    }
+}
+}  // namespace
+
+namespace spk {
+void count_launch(int n) { g_launches += n; }
+}  // namespace spk
+
+// ---------------------------------------------------------------------------
+// programs
+namespace {
+
+enum StageType { ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS };
+
+struct Stage {
+    StageType t;
+    int njobs = 0;
+    size_t off = 0;  // byte offset of the job array in the device blob
+    int max_nc = 0;  // sweep/gemm: max explicit columns; -1: call columns
+    long long max_elems = 0;
+    int max_r = 0;
+    int buf = 0;  // memset target
+    int cols = -1;  // memset columns (-1: call columns)
+};
+
+struct ProgramBuilder {
+    std::vector<char> blob;
+    template <class T>
+    size_t push(const std::vector<T>& v) {
+        size_t off = (blob.size() + 15) & ~size_t(15);
+        blob.resize(off + v.size() * sizeof(T));
+        if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+};
+
+using Program = std::vector<Stage>;
+
+View view(int buf, long long base, int rev = 0, int off = 0, int mrows = 0, long long ld = -1) {
+    View v;
+    v.base = base;
+    v.ld = ld;
+    v.buf = buf;
+    v.rev = rev;
+    v.off = off;
+    v.mrows = mrows;
+    return v;
+}
+
+struct Level {
+    int units = 0;
+    std::vector<int> uoff, uh;
+    std::vector<long long> voff, woff;  // pool offsets, -1 when never formed
+    std::vector<int> pair_part;         // PartDev index per pair
+};
+
+}  // namespace
+
+struct spk_fact {
+    long long n = 0;
+    int kl = 0, ku = 0, k = 0, p = 0, piv_on = 0;
+    double boost_eps = 0.0;
+    bool reduced_only = false;
+    std::vector<long long> bounds;
+    std::vector<int> kinds;
+    std::vector<PartDev> parts;  // [0,p) partitions, [p, p+ncpl) couplings
+    std::vector<Level> levels;
+    long long off_bhat = 0, off_chat = 0, pool_size = 0, fac_size = 0, piv_size = 0;
+    long long aux_rows = 0, auxf_rows = 0;
+    int tau_first = 0, tau_last = 0, z_first = 0, z_last = 0, tau_w = 0;  // AUX row offsets
+    // device
+    PartDev* d_parts = nullptr;
+    double* d_fac = nullptr;
+    int* d_piv = nullptr;
+    double* d_pool = nullptr;
+    long long* d_bounds = nullptr;
+    unsigned long long* d_amax = nullptr;
+    int* d_boost = nullptr;
+    int* d_fell = nullptr;
+    int* d_status = nullptr;
+    char* d_blob = nullptr;
+    Program prog_factor, prog_fwd, prog_tr;
+    std::vector<long long> factor_sweeps;
+    int boost_count = 0, boost_warnings = 0;
+    cudaStream_t stream = nullptr;
+
+    ~spk_fact() {
+        for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
+                        (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob})
+            if (q) cudaFree(q);
+    }
+};
+
+struct spk_reduced {
+    std::unique_ptr<spk_fact> f;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// geometry
+PartDev make_part(long long r0, int m, int akl, int aku, int piv_on, int rev, int kcorner) {
+    PartDev P{};
+    P.r0 = r0;
+    P.m = m;
+    P.rev = rev;
+    P.kl = std::min(rev ? aku : akl, m - 1);
+    P.ku = std::min(rev ? akl : aku, m - 1);
+    P.pivoting = piv_on;
+    P.ubw = piv_on ? std::min(P.kl + P.ku, m - 1) : P.ku;
+    P.d = P.ubw;
+    P.rows = P.ubw + P.kl + 1;
+    P.trunc = std::max(0, m - kcorner - (piv_on ? P.kl : 0));
+    P.bofs = -1;
+    return P;
+}
+
+void build_levels(spk_fact& f, long long& pool_cursor) {
+    const int p = f.p, k = f.k;
+    f.levels.clear();
+    if (p < 2 || k == 0) return;
+    int L = 0;
+    for (int u = p; u > 1; u = (u + 1) / 2) ++L;
+    f.levels.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+        Level& lv = f.levels[l];
+        lv.units = l == 0 ? p : (f.levels[l - 1].units + 1) / 2;
+        lv.uoff.assign(lv.units, 0);
+        lv.uh.assign(lv.units, 0);
+        lv.voff.assign(lv.units, -1);
+        lv.woff.assign(lv.units, -1);
+        for (int a = 0; a < lv.units; ++a) {
+            if (l == 0) {
+                lv.uoff[a] = 2 * a * k;
+                lv.uh[a] = 2 * k;
+            } else {
+                const Level& pv = f.levels[l - 1];
+                lv.uoff[a] = pv.uoff[2 * a];
+                lv.uh[a] = pv.uh[2 * a] + (2 * a + 1 < pv.units ? pv.uh[2 * a + 1] : 0);
+            }
+        }
+    }
+    // spike storage: level 0 holds [vt; vb] / [wt; wb]; level l+1 spikes exist
+    // where the reference forms them (factorize.cpp:104-115) plus carried units
+    for (int l = 0; l < L; ++l) {
+        Level& lv = f.levels[l];
+        for (int a = 0; a < lv.units; ++a) {
+            const long long sz = (long long)lv.uh[a] * k;
+            bool hv = false, hw = false;
+            if (l == 0) {
+                hv = a < lv.units - 1;
+                hw = a > 0;
+            } else {
+                const Level& pv = f.levels[l - 1];
+                const bool carried = 2 * a + 1 >= pv.units;
+                hv = !carried && (2 * a + 1 < pv.units - 1);
+                hw = carried ? true : a > 0;
+                if (l == L) hv = hw = false;
+            }
+            if (hv) {
+                lv.voff[a] = pool_cursor;
+                pool_cursor += sz;
+            }
+            if (hw) {
+                lv.woff[a] = pool_cursor;
+                pool_cursor += sz;
+            }
+        }
+    }
+}
+
+void add_couplings(spk_fact& f, long long& fac_cursor) {
+    const int k = f.k;
+    int idx = 0;
+    for (size_t l = 0; l + 1 < f.levels.size(); ++l) {
+        Level& lv = f.levels[l];
+        lv.pair_part.clear();
+        for (int a = 0; a < lv.units / 2; ++a) {
+            const int nn = 2 * k;
+            PartDev P = make_part(f.n + (long long)idx * nn, nn, nn - 1, nn - 1, 1, 0, 0);
+            P.fallback = 1;
+            P.fofs = fac_cursor;
+            fac_cursor += (long long)P.m * P.rows;
+            P.bofs = fac_cursor;
+            fac_cursor += (long long)P.m * P.rows;
+            lv.pair_part.push_back((int)f.parts.size());
+            f.parts.push_back(P);
+            ++idx;
+        }
+    }
+}
+
+struct Builder {
+    spk_fact& f;
+    ProgramBuilder& pb;
+    Program& prog;
+
+    void sweep(const std::vector<SweepJob>& jobs) {
+        if (jobs.empty()) return;
+        Stage s{ST_SWEEP};
+        s.njobs = (int)jobs.size();
+        s.off = pb.push(jobs);
+        int mx = 0;
+        for (auto& j : jobs) mx = j.nc < 0 ? -1 : (mx < 0 ? -1 : std::max(mx, j.nc));
+        s.max_nc = mx;
+        prog.push_back(s);
+    }
+    void copy(const std::vector<CopyJob>& jobs) {
+        if (jobs.empty()) return;
+        Stage s{ST_COPY};
+        s.njobs = (int)jobs.size();
+        s.off = pb.push(jobs);
+        long long mx = 0;
+        int mnc = 0;
+        for (auto& j : jobs) {
+            mx = std::max(mx, (long long)(j.L1 - j.L0));
+            mnc = j.nc < 0 ? -1 : (mnc < 0 ? -1 : std::max(mnc, j.nc));
+        }
+        s.max_elems = mx;
+        s.max_nc = mnc;
+        prog.push_back(s);
+    }
+    void gemm(const std::vector<GemmJob>& jobs) {
+        if (jobs.empty()) return;
+        Stage s{ST_GEMM};
+        s.njobs = (int)jobs.size();
+        s.off = pb.push(jobs);
+        int mr = 0, mnc = 0;
+        for (auto& j : jobs) {
+            mr = std::max(mr, j.r);
+            mnc = j.nc < 0 ? -1 : (mnc < 0 ? -1 : std::max(mnc, j.nc));
+        }
+        s.max_r = mr;
+        s.max_nc = mnc;
+        prog.push_back(s);
+    }
+    void lu(const std::vector<int>& units) {
+        if (units.empty()) return;
+        Stage s{ST_LU};
+        s.njobs = (int)units.size();
+        s.off = pb.push(units);
+        prog.push_back(s);
+    }
+    void cpl(const std::vector<CouplingJob>& jobs) {
+        if (jobs.empty()) return;
+        Stage s{ST_CPL};
+        s.njobs = (int)jobs.size();
+        s.off = pb.push(jobs);
+        s.max_elems = (long long)(2 * f.k) * (4 * f.k - 1);
+        prog.push_back(s);
+    }
+    void memset_buf(int buf, int cols = -1) {
+        Stage s{ST_MEMSET};
+        s.buf = buf;
+        s.cols = cols;
+        prog.push_back(s);
+    }
+    void memcpy_fx() { prog.push_back(Stage{ST_MEMCPY_FX}); }
+    void memcpy_fs() { prog.push_back(Stage{ST_MEMCPY_FS}); }
+};
+
+SweepJob sj(View v, int part, int mode, int lo, int hi, int c0 = 0, int nc = -1) {
+    SweepJob j;
+    j.v = v;
+    j.part = part;
+    j.mode = mode;
+    j.lo = lo;
+    j.hi = hi;
+    j.c0 = c0;
+    j.nc = nc;
+    return j;
+}
+
+CopyJob cj(View src, View dst, int L0, int L1, int op = CP_COPY, int c0 = 0, int nc = -1) {
+    CopyJob j;
+    j.src = src;
+    j.dst = dst;
+    j.L0 = L0;
+    j.L1 = L1;
+    j.op = op;
+    j.c0 = c0;
+    j.nc = nc;
+    return j;
+}
+
+GemmJob gj(View a, int transA, View b, int brow0, View c, int crow0, int r, int kk, int op,
+           int nc = -1) {
+    GemmJob j;
+    j.a = a;
+    j.b = b;
+    j.c = c;
+    j.transA = transA;
+    j.brow0 = brow0;
+    j.crow0 = crow0;
+    j.r = r;
+    j.kk = kk;
+    j.nc = nc;
+    j.op = op;
+    j.pad = 0;
+    return j;
+}
+
+// pair_solve (factorize.cpp:19-32) / pair_solve_transpose (:34-44) over a
+// batch of z blocks: z = {buf, base row, ld}, red regions in buffer `redbuf`.
+struct PairZ {
+    int pair_part;
+    long long vl_off, wr_off;
+    int hL, hR;
+    int zbuf;
+    long long zbase, zld;
+    long long red_row;  // row offset of this job's 2k red region in redbuf
+};
+
+void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long long redld,
+                      int ncols_explicit, bool transpose, int k) {
+    if (zs.empty()) return;
+    std::vector<CopyJob> gather, scatter;
+    std::vector<SweepJob> s1, s2;
+    std::vector<GemmJob> g;
+    const int nc = ncols_explicit;
+    for (const PairZ& z : zs) {
+        const View zv = view(z.zbuf, z.zbase, 0, 0, 0, z.zld);
+        // red logical row L in [hL-k, hL+k) <-> red region row red_row + L - (hL-k)
+        const View rv_z = view(redbuf, z.red_row, 0, z.hL - k, 0, redld);
+        const View rv = view(redbuf, z.red_row, 0, 0, 2 * k, redld);
+        gather.push_back(cj(zv, rv_z, z.hL - k, z.hL + k, CP_COPY, 0, nc));
+        scatter.push_back(cj(rv_z, zv, z.hL - k, z.hL + k, CP_COPY, 0, nc));
+        const View vl = view(B_POOL, z.vl_off, 0, 0, 0, z.hL);
+        const View wr = view(B_POOL, z.wr_off + k, 0, 0, 0, z.hR);  // rows k.. of wr
+        if (!transpose) {
+            s1.push_back(sj(rv, z.pair_part, SW_FWD_L, 0, 0, 0, nc));
+            s2.push_back(sj(rv, z.pair_part, SW_BWD_U, 0, 2 * k - 1, 0, nc));
+            if (z.hL - k > 0) g.push_back(gj(vl, 0, rv, k, zv, 0, z.hL - k, k, GM_SUB, nc));
+            if (z.hR - k > 0) g.push_back(gj(wr, 0, rv, 0, zv, z.hL + k, z.hR - k, k, GM_SUB, nc));
+        } else {
+            if (z.hR - k > 0) g.push_back(gj(wr, 1, zv, z.hL + k, rv, 0, k, z.hR - k, GM_SUB, nc));
+            if (z.hL - k > 0) g.push_back(gj(vl, 1, zv, 0, rv, k, k, z.hL - k, GM_SUB, nc));
+            s1.push_back(sj(rv, z.pair_part, SW_FWD_UT, 0, 0, 0, nc));
+            s2.push_back(sj(rv, z.pair_part, SW_BWD_LT, 0, 0, 0, nc));
+        }
+    }
+    b.copy(gather);
+    if (!transpose) {
+        b.sweep(s1);
+        b.sweep(s2);
+        b.gemm(g);
+    } else {
+        b.gemm(g);
+        b.sweep(s1);
+        b.sweep(s2);
+    }
+    b.copy(scatter);
+}
+
+// ---------------------------------------------------------------------------
+// factor program (factorize.cpp:133-257 + reduce_factorize :46-120)
+void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
+    Builder b{f, pb, f.prog_factor};
+    const int p = f.p, k = f.k;
+    const long long n = f.n, kk = (long long)k * k;
+    if (!f.reduced_only) {
+        std::vector<int> units(p);
+        for (int i = 0; i < p; ++i) units[i] = i;
+        b.lu(units);  // preceded at run time by fill_factors
+    }
+    if (p < 2 || k == 0) return;
+    if (!f.reduced_only) {
+        // spike right-hand sides in FS (n x 2k): V = [0; bhat], W = [chat; 0]
+        b.memset_buf(B_FS, 2 * k);
+        std::vector<CopyJob> init;
+        std::vector<SweepJob> fl, bu;
+        std::vector<CopyJob> tips;
+        for (int i = 0; i < p; ++i) {
+            const PartDev& P = f.parts[i];
+            const int m = P.m;
+            const long long r0 = f.bounds[i];
+            const bool first = i == 0, last = i == p - 1;
+            const View fsv = view(B_FS, r0, 0, 0, m, n);
+            const View fsr = view(B_FS, r0, P.rev, 0, m, n);
+            const View fsw = view(B_FS, r0 + (long long)k * n, 0, 0, m, n);  // W columns
+            if (!last) {
+                const View bh = view(B_POOL, f.off_bhat + i * kk, 0, m - k, k, k);
+                init.push_back(cj(bh, fsv, m - k, m, CP_COPY, 0, k));
+            }
+            if (!first && !last) {
+                const View ch = view(B_POOL, f.off_chat + i * kk, 0, 0, k, k);
+                init.push_back(cj(ch, fsw, 0, k, CP_COPY, 0, k));
+            }
+            if (last) {
+                // [0; rev chat] in reversed space == chat in physical rows [0, k)
+                const View ch = view(B_POOL, f.off_chat + i * kk, 0, 0, k, k);
+                init.push_back(cj(ch, fsv, 0, k, CP_COPY, 0, k));
+            }
+            const View vv = last ? fsr : fsv;
+            fl.push_back(sj(vv, i, SW_FWD_L, P.trunc, 0, 0, k));
+            if (!first && !last) {
+                fl.push_back(sj(fsv, i, SW_FWD_L, 0, 0, k, k));
+                bu.push_back(sj(fsv, i, SW_BWD_U, 0, m - 1, 0, 2 * k));
+            } else {
+                bu.push_back(sj(vv, i, SW_BWD_U, m - k, m - 1, 0, k));
+            }
+            // tips into level-0 spike columns (2k x k, ld 2k)
+            const Level& l0 = f.levels[0];
+            if (!last) {
+                const View vdst_b = view(B_POOL, l0.voff[i] + k, 0, m - k, k, 2 * k);
+                tips.push_back(cj(fsv, vdst_b, m - k, m, CP_COPY, 0, k));
+                if (!first) {
+                    const View vdst_t = view(B_POOL, l0.voff[i], 0, 0, k, 2 * k);
+                    tips.push_back(cj(fsv, vdst_t, 0, k, CP_COPY, 0, k));
+                }
+            }
+            if (!first) {
+                const View wdst_t = view(B_POOL, l0.woff[i], 0, 0, k, 2 * k);
+                if (last) {
+                    tips.push_back(cj(fsv, wdst_t, 0, k, CP_COPY, 0, k));
+                } else {
+                    tips.push_back(cj(fsw, wdst_t, 0, k, CP_COPY, 0, k));
+                    const View wdst_b = view(B_POOL, l0.woff[i] + k, 0, m - k, k, 2 * k);
+                    tips.push_back(cj(fsw, wdst_b, m - k, m, CP_COPY, 0, k));
+                }
+            }
+        }
+        b.copy(init);
+        b.sweep(fl);
+        b.sweep(bu);
+        b.copy(tips);
+    }
+    // reduced hierarchy
+    const int L = (int)f.levels.size() - 1;
+    long long red_cursor = 0;
+    for (int l = 0; l < L; ++l) {
+        const Level& lv = f.levels[l];
+        const int np = lv.units / 2;
+        std::vector<CouplingJob> cpl;
+        std::vector<int> lus;
+        for (int a = 0; a < np; ++a) {
+            CouplingJob c;
+            c.vl_off = lv.voff[2 * a];
+            c.wr_off = lv.woff[2 * a + 1];
+            c.hL = lv.uh[2 * a];
+            c.hR = lv.uh[2 * a + 1];
+            c.part = lv.pair_part[a];
+            c.k = k;
+            cpl.push_back(c);
+            lus.push_back(lv.pair_part[a]);
+        }
+        b.cpl(cpl);
+        b.lu(lus);
+        if (l + 1 == L) break;
+        const Level& nx = f.levels[l + 1];
+        std::vector<CopyJob> init;
+        std::vector<PairZ> zs;
+        for (int a = 0; a < np; ++a) {
+            const int hL = lv.uh[2 * a], hR = lv.uh[2 * a + 1], H = hL + hR;
+            if (nx.voff[a] >= 0) {
+                const View src = view(B_POOL, lv.voff[2 * a + 1], 0, hL, hR, hR);
+                const View dst = view(B_POOL, nx.voff[a], 0, 0, H, H);
+                init.push_back(cj(src, dst, hL, H, CP_COPY, 0, k));
+                zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], hL, hR, B_POOL,
+                                   nx.voff[a], H, red_cursor});
+                red_cursor += 2 * k;
+            }
+            if (nx.woff[a] >= 0) {
+                const View src = view(B_POOL, lv.woff[2 * a], 0, 0, hL, hL);
+                const View dst = view(B_POOL, nx.woff[a], 0, 0, H, H);
+                init.push_back(cj(src, dst, 0, hL, CP_COPY, 0, k));
+                zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], hL, hR, B_POOL,
+                                   nx.woff[a], H, red_cursor});
+                red_cursor += 2 * k;
+            }
+        }
+        if (lv.units % 2 == 1) {
+            const int h = lv.uh[lv.units - 1];
+            const View src = view(B_POOL, lv.woff[lv.units - 1], 0, 0, h, h);
+            const View dst = view(B_POOL, nx.woff[np], 0, 0, h, h);
+            init.push_back(cj(src, dst, 0, h, CP_COPY, 0, k));
+        }
+        b.copy(init);
+        emit_pair_solves(b, zs, B_AUX, -1, k, false, k);
+    }
+    f.auxf_rows = std::max<long long>(red_cursor, 1);
+}
+
+// ---------------------------------------------------------------------------
+// forward solve program (solve.cpp:81-223)
+void build_reduced_solve(spk_fact& f, Builder& b, bool transpose, long long aux_base) {
+    const int L = (int)f.levels.size() - 1;
+    const int k = f.k;
+    long long cur = aux_base;
+    std::vector<long long> level_base(L);
+    for (int l = 0; l < L; ++l) {
+        level_base[l] = cur;
+        cur += (long long)(f.levels[l].units / 2) * 2 * k;
+    }
+    for (int s = 0; s < L; ++s) {
+        const int l = transpose ? L - 1 - s : s;
+        const Level& lv = f.levels[l];
+        std::vector<PairZ> zs;
+        for (int a = 0; a < lv.units / 2; ++a)
+            zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], lv.uh[2 * a],
+                               lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
+                               level_base[l] + 2LL * k * a});
+        emit_pair_solves(b, zs, B_AUX, -1, -1, transpose, k);
+    }
+}
+
+void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
+    Builder b{f, pb, f.prog_fwd};
+    const int p = f.p, k = f.k;
+    const long long kk = (long long)k * k;
+    b.memcpy_fx();
+    std::vector<SweepJob> s_fl, s_bu;
+    if (p == 1 || k == 0) {
+        for (int i = 0; i < p; ++i) {
+            const PartDev& P = f.parts[i];
+            const View xv = view(B_X, f.bounds[i], P.rev, 0, P.m);
+            s_fl.push_back(sj(xv, i, SW_FWD_L, 0, 0));
+            s_bu.push_back(sj(xv, i, SW_BWD_U, 0, P.m - 1));
+        }
+        b.sweep(s_fl);
+        b.sweep(s_bu);
+        return;
+    }
+    std::vector<CopyJob> c_edge, c_inner;
+    for (int i = 0; i < p; ++i) {
+        const PartDev& P = f.parts[i];
+        const int m = P.m;
+        const long long r0 = f.bounds[i];
+        const View xv = view(B_X, r0, P.rev, 0, m);
+        s_fl.push_back(sj(xv, i, SW_FWD_L, 0, 0));
+        if (i == 0) {
+            const View tv = view(B_T, k, 0, m - k, k);
+            c_edge.push_back(cj(xv, tv, m - k, m));
+            s_bu.push_back(sj(tv, i, SW_BWD_U, m - k, m - 1));
+        } else if (i == p - 1) {
+            const View tv = view(B_T, 2LL * i * k, 1, m - k, k);
+            c_edge.push_back(cj(xv, tv, m - k, m));
+            s_bu.push_back(sj(tv, i, SW_BWD_U, m - k, m - 1));
+        } else {
+            s_bu.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
+            c_inner.push_back(cj(xv, view(B_T, 2LL * i * k, 0, 0, k), 0, k));
+            c_inner.push_back(cj(xv, view(B_T, (2LL * i + 1) * k, 0, m - k, k), m - k, m));
+        }
+    }
+    b.sweep(s_fl);
+    b.copy(c_edge);
+    b.sweep(s_bu);
+    b.copy(c_inner);
+    build_reduced_solve(f, b, false, 0);
+    // retrieval
+    b.memset_buf(B_S);
+    std::vector<GemmJob> g;
+    std::vector<SweepJob> r_fl, r_bu, r_bu2;
+    std::vector<CopyJob> r_sub;
+    const View tview = view(B_T, 0);
+    for (int i = 0; i < p; ++i) {
+        const PartDev& P = f.parts[i];
+        const int m = P.m;
+        const long long r0 = f.bounds[i];
+        const View sv = view(B_S, r0, 0, 0, m);
+        const View sr = view(B_S, r0, P.rev, 0, m);
+        const View xv = view(B_X, r0, P.rev, 0, m);
+        const View bh = view(B_POOL, f.off_bhat + i * kk, 0, 0, 0, k);
+        const View ch = view(B_POOL, f.off_chat + i * kk, 0, 0, 0, k);
+        if (i < p - 1) g.push_back(gj(bh, 0, tview, 2 * (i + 1) * k, sv, m - k, k, k, GM_SET));
+        if (i > 0) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, sv, 0, k, k, GM_SET));
+        if (i == 0 || i == p - 1) {
+            r_fl.push_back(sj(sr, i, SW_FWD_L, P.trunc, 0));
+            r_sub.push_back(cj(sr, xv, P.trunc, m, CP_SUB));
+            r_bu2.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
+        } else {
+            r_fl.push_back(sj(sv, i, SW_FWD_L, 0, 0));
+            r_bu.push_back(sj(sv, i, SW_BWD_U, 0, m - 1));
+            r_sub.push_back(cj(sv, xv, 0, m, CP_SUB));
+        }
+    }
+    b.gemm(g);
+    b.sweep(r_fl);
+    b.sweep(r_bu);
+    b.copy(r_sub);
+    b.sweep(r_bu2);
+}
+
+// transpose solve program (solve.cpp:225-380)
+void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
+    Builder b{f, pb, f.prog_tr};
+    const int p = f.p, k = f.k;
+    const long long kk = (long long)k * k;
+    b.memcpy_fx();
+    if (p == 1 || k == 0) {
+        std::vector<SweepJob> a, c;
+        for (int i = 0; i < p; ++i) {
+            const PartDev& P = f.parts[i];
+            const View xv = view(B_X, f.bounds[i], P.rev, 0, P.m);
+            a.push_back(sj(xv, i, SW_FWD_UT, 0, 0));
+            c.push_back(sj(xv, i, SW_BWD_LT, 0, 0));
+        }
+        b.sweep(a);
+        b.sweep(c);
+        return;
+    }
+    b.memcpy_fs();
+    const long long red_rows = (long long)(p - 1) * 2 * k;
+    std::vector<CopyJob> zero, tau_copy, gcopy, d_copy, d_add;
+    std::vector<SweepJob> s_fut, s_blt, tau_blt, d_fut, d_blt;
+    std::vector<GemmJob> g;
+    for (int i = 0; i < p; ++i) {
+        const PartDev& P = f.parts[i];
+        const int m = P.m;
+        const long long r0 = f.bounds[i];
+        const View sv = view(B_S, r0, 0, 0, m);
+        const View xv = view(B_X, r0, P.rev, 0, m);
+        if (i == 0 || i == p - 1) {
+            const bool last = i == p - 1;
+            zero.push_back(cj(xv, xv, m - k, m, CP_ZERO));
+            s_fut.push_back(sj(xv, i, SW_FWD_UT, 0, 0));
+            const int w = std::min(m, k + (f.piv_on ? P.kl : 0));
+            const long long taoff = red_rows + (last ? f.tau_w : 0);
+            const View av = view(B_AUX, taoff, 0, m - w, w);
+            tau_copy.push_back(cj(xv, av, m - w, m));
+            tau_blt.push_back(sj(av, i, SW_BWD_LT, m - w, 0));
+            // D^T stage: z = U_tail^-T tip, X_tail += z, full P^T L^-T
+            const long long zoff = red_rows + 2LL * f.tau_w + (last ? k : 0);
+            const View zv = view(B_AUX, zoff, 0, m - k, k);
+            const View tip = last ? view(B_T, 2LL * i * k, 1, m - k, k) : view(B_T, k, 0, m - k, k);
+            d_copy.push_back(cj(tip, zv, m - k, m));
+            d_fut.push_back(sj(zv, i, SW_FWD_UT, m - k, 0));
+            d_add.push_back(cj(zv, xv, m - k, m, CP_ADD));
+            d_blt.push_back(sj(xv, i, SW_BWD_LT, 0, 0));
+        } else {
+            zero.push_back(cj(sv, sv, 0, k, CP_ZERO));
+            zero.push_back(cj(sv, sv, m - k, m, CP_ZERO));
+            s_fut.push_back(sj(sv, i, SW_FWD_UT, 0, 0));
+            s_blt.push_back(sj(sv, i, SW_BWD_LT, 0, 0));
+            d_copy.push_back(cj(view(B_T, 2LL * i * k, 0, 0, k), xv, 0, k));
+            d_copy.push_back(cj(view(B_T, (2LL * i + 1) * k, 0, m - k, k), xv, m - k, m));
+            d_fut.push_back(sj(xv, i, SW_FWD_UT, 0, 0));
+            d_blt.push_back(sj(xv, i, SW_BWD_LT, 0, 0));
+        }
+    }
+    // G tips (solve.cpp:313-325): boundary rows of F minus corner^T * tau
+    const View fg = view(B_F, 0);
+    for (int i = 0; i < p; ++i) {
+        const long long b0 = f.bounds[i], b1 = f.bounds[i + 1];
+        gcopy.push_back(cj(fg, view(B_T, 2LL * i * k, 0, (int)b0, k), (int)b0, (int)b0 + k));
+        gcopy.push_back(cj(fg, view(B_T, (2LL * i + 1) * k, 0, (int)(b1 - k), k), (int)(b1 - k), (int)b1));
+    }
+    const View tview = view(B_T, 0);
+    for (int i = 1; i < p; ++i) {
+        // tip_t(i) -= bhat_{i-1}^T tau_b(i-1)
+        const PartDev& Q = f.parts[i - 1];
+        const int mq = Q.m;
+        View tb;
+        int brow;
+        if (i - 1 == 0) {
+            const int w = std::min(mq, k + (f.piv_on ? Q.kl : 0));
+            tb = view(B_AUX, red_rows, 0, mq - w, w);
+            brow = mq - k;
+        } else {
+            tb = view(B_S, f.bounds[i - 1], 0, 0, mq);
+            brow = mq - k;
+        }
+        const View bh = view(B_POOL, f.off_bhat + (i - 1) * kk, 0, 0, 0, k);
+        g.push_back(gj(bh, 1, tb, brow, tview, 2 * i * k, k, k, GM_SUB));
+    }
+    for (int i = 0; i + 1 < p; ++i) {
+        // tip_b(i) -= chat_{i+1}^T tau_t(i+1)
+        const PartDev& Q = f.parts[i + 1];
+        const int mq = Q.m;
+        View tt;
+        if (i + 1 == p - 1) {
+            const int w = std::min(mq, k + (f.piv_on ? Q.kl : 0));
+            tt = view(B_AUX, red_rows + f.tau_w, 1, 0, w);
+        } else {
+            tt = view(B_S, f.bounds[i + 1], 0, 0, mq);
+        }
+        const View ch = view(B_POOL, f.off_chat + (i + 1) * kk, 0, 0, 0, k);
+        g.push_back(gj(ch, 1, tt, 0, tview, (2 * i + 1) * k, k, k, GM_SUB));
+    }
+    b.copy(zero);
+    b.sweep(s_fut);
+    b.sweep(s_blt);
+    b.copy(tau_copy);
+    b.sweep(tau_blt);
+    b.copy(gcopy);
+    b.gemm(g);
+    build_reduced_solve(f, b, true, 0);
+    b.copy(d_copy);
+    b.sweep(d_fut);
+    b.copy(d_add);
+    b.sweep(d_blt);
+}
+
+// ---------------------------------------------------------------------------
+// execution
+struct Exec {
+    spk_fact& f;
+    cudaStream_t s;
+    Bufs B;
+    int ncols;
+    // memcpy sources
+    const double* F = nullptr;
+    long long ldf = 0, n = 0;
+
+    void run(const Program& prog) {
+        for (const Stage& st : prog) {
+            const char* jobs = f.d_blob + st.off;
+            switch (st.t) {
+                case ST_SWEEP: {
+                    const int nc = st.max_nc < 0 ? ncols : st.max_nc;
+                    launch_sweep((const SweepJob*)jobs, st.njobs, nc, f.d_parts, f.d_fac, f.d_piv, B,
+                                 ncols, s);
+                    break;
+                }
+                case ST_COPY: {
+                    const int nc = st.max_nc < 0 ? ncols : st.max_nc;
+                    launch_copy((const CopyJob*)jobs, st.njobs, st.max_elems * nc, B, ncols, s);
+                    break;
+                }
+                case ST_GEMM: {
+                    const int nc = st.max_nc < 0 ? ncols : st.max_nc;
+                    launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                    break;
+                }
+                case ST_LU:
+                    launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
+                                   f.boost_eps, f.d_boost, f.d_fell, f.d_status, s);
+                    break;
+                case ST_CPL:
+                    launch_build_coupling((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts,
+                                          f.d_pool, f.d_fac, f.d_amax, s);
+                    break;
+                case ST_MEMSET: {
+                    const int nc = st.cols < 0 ? ncols : st.cols;
+                    if (B.p[st.buf] && nc > 0)
+                        ck(cudaMemsetAsync(B.p[st.buf], 0, sizeof(double) * B.ld[st.buf] * nc, s), "memset");
+                    break;
+                }
+                case ST_MEMCPY_FX:
+                case ST_MEMCPY_FS: {
+                    double* dst = st.t == ST_MEMCPY_FX ? B.p[B_X] : B.p[B_S];
+                    const long long ldd = st.t == ST_MEMCPY_FX ? B.ld[B_X] : B.ld[B_S];
+                    if (ncols > 0 && dst != B.p[B_F])
+                        ck(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, B.p[B_F], sizeof(double) * B.ld[B_F],
+                                             sizeof(double) * n, ncols, cudaMemcpyDeviceToDevice, s),
+                           "memcpy F");
+                    break;
+                }
+            }
+        }
+    }
+};
+
+template <class T>
+T* dalloc(size_t count, cudaStream_t s) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMallocAsync(&p, sizeof(T) * count, s), "cudaMallocAsync");
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* dalloc_sync(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    return static_cast<T*>(p);
+}
+
+void validate_plan(long long n, const spk_plan* plan) {
+    if (!plan || plan->p < 1 || !plan->bounds) fail(SPK_EINVAL, "factorize: invalid plan");
+    if (plan->bounds[0] != 0 || plan->bounds[plan->p] != n)
+        fail(SPK_EINVAL, "factorize: plan does not match matrix");
+    for (int i = 0; i < plan->p; ++i)
+        if (plan->bounds[i + 1] - plan->bounds[i] < 1) fail(SPK_EINVAL, "factorize: empty partition");
+}
+
+// Symbolic part: geometry, pool layout, programs, device allocations.
+void setup_fact(spk_fact& f, cudaStream_t s) {
+    const int p = f.p, k = f.k;
+    const long long kk = (long long)k * k;
+    f.parts.clear();
+    long long fac_cursor = 0;
+    if (!f.reduced_only) {
+        for (int i = 0; i < p; ++i) {
+            const int m = (int)(f.bounds[i + 1] - f.bounds[i]);
+            const int rev = (p > 1 && i == p - 1) ? 1 : 0;
+            PartDev P = make_part(f.bounds[i], m, f.kl, f.ku, f.piv_on, rev, k);
+            P.fofs = fac_cursor;
+            fac_cursor += (long long)P.m * P.rows;
+            f.parts.push_back(P);
+        }
+        if (p > 1 && k > 0)
+            for (int i = 0; i < p; ++i)
+                if (f.parts[i].m < k)
+                    fail(SPK_EINVAL, "factorize: partition smaller than the half-bandwidth");
+    } else {
+        for (int i = 0; i < p; ++i) f.parts.push_back(PartDev{});
+    }
+    long long pool = 0;
+    f.off_bhat = pool;
+    pool += kk * p;
+    f.off_chat = pool;
+    pool += kk * p;
+    build_levels(f, pool);
+    add_couplings(f, fac_cursor);
+    f.pool_size = pool;
+    f.fac_size = fac_cursor;
+    f.piv_size = f.n + (long long)(f.parts.size() - p) * 2 * k + 1;
+    // AUX layout for solves: reduced red regions, then tau (first, last), z (first, last)
+    int wmax = k;
+    if (!f.reduced_only && p > 1)
+        wmax = std::max(std::min(f.parts[0].m, k + (f.piv_on ? f.parts[0].kl : 0)),
+                        std::min(f.parts[p - 1].m, k + (f.piv_on ? f.parts[p - 1].kl : 0)));
+    f.tau_w = wmax;
+    f.aux_rows = std::max<long long>((long long)std::max(p - 1, 0) * 2 * k + 2LL * wmax + 2LL * k, 1);
+    ProgramBuilder pb;
+    build_factor_program(f, pb);
+    if (!f.reduced_only) {
+        build_forward_program(f, pb);
+        build_transpose_program(f, pb);
+    } else {
+        // reduced-only: forward/transpose programs are just the reduced solves
+        Builder bf{f, pb, f.prog_fwd}, bt{f, pb, f.prog_tr};
+        if (p > 1 && k > 0) {
+            build_reduced_solve(f, bf, false, 0);
+            build_reduced_solve(f, bt, true, 0);
+        }
+    }
+    // device allocations (stream ordered)
+    const int nparts = (int)f.parts.size();
+    f.d_parts = dalloc<PartDev>(nparts, s);
+    f.d_fac = dalloc<double>(f.fac_size, s);
+    f.d_piv = dalloc<int>(f.piv_size, s);
+    f.d_pool = dalloc<double>(f.pool_size, s);
+    f.d_bounds = dalloc<long long>(p + 1, s);
+    f.d_amax = dalloc<unsigned long long>(nparts, s);
+    f.d_boost = dalloc<int>(nparts, s);
+    f.d_fell = dalloc<int>(nparts, s);
+    f.d_status = dalloc<int>(1, s);
+    f.d_blob = dalloc<char>(pb.blob.size(), s);
+    ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
+    ck(cudaMemcpyAsync(f.d_bounds, f.bounds.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s),
+       "upload");
+    if (!pb.blob.empty())
+        ck(cudaMemcpyAsync(f.d_blob, pb.blob.data(), pb.blob.size(), cudaMemcpyHostToDevice, s), "upload");
+    ck(cudaMemsetAsync(f.d_pool, 0, sizeof(double) * f.pool_size, s), "memset");
+    ck(cudaMemsetAsync(f.d_amax, 0, sizeof(unsigned long long) * nparts, s), "memset");
+    ck(cudaMemsetAsync(f.d_boost, 0, sizeof(int) * nparts, s), "memset");
+    ck(cudaMemsetAsync(f.d_fell, 0, sizeof(int) * nparts, s), "memset");
+    ck(cudaMemsetAsync(f.d_status, 0, sizeof(int), s), "memset");
+}
+
+void finish_factor(spk_fact& f, cudaStream_t s) {
+    int status = 0;
+    const int nparts = (int)f.parts.size();
+    std::vector<int> boost(nparts), fell(nparts);
+    ck(cudaMemcpyAsync(&status, f.d_status, sizeof(int), cudaMemcpyDeviceToHost, s), "download");
+    ck(cudaMemcpyAsync(boost.data(), f.d_boost, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
+    ck(cudaMemcpyAsync(fell.data(), f.d_fell, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
+    ck(cudaStreamSynchronize(s), "factorize");
+    ck(cudaGetLastError(), "factorize kernels");
+    if (status == 2) fail(SPK_ESINGULAR, "lu_factor: exactly singular column in pivoting mode");
+    f.boost_count = 0;
+    if (!f.reduced_only)
+        for (int i = 0; i < f.p; ++i) f.boost_count += boost[i];
+    f.boost_warnings = 0;
+    for (int i = f.p; i < nparts; ++i) f.boost_warnings += fell[i];
+    f.factor_sweeps.assign(f.p, 0);
+    if (!f.reduced_only && f.p > 1 && f.k > 0)
+        for (int i = 1; i + 1 < f.p; ++i) f.factor_sweeps[i] = 3;
+}
+
+Bufs make_bufs() {
+    Bufs B;
+    for (int i = 0; i < kMaxBufs; ++i) {
+        B.p[i] = nullptr;
+        B.ld[i] = 1;
+    }
+    return B;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+extern "C" {
+
+const char* spk_last_error(void) { return g_err.c_str(); }
+const char* spk_version(void) { return "spike_b200 0.1 (sm_100a)"; }
+
+int64_t spk_launch_count(int32_t reset) {
+    const long long v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+void spk_compute_ratios(double K, int32_t nrhs, int32_t k, double* r12, double* r13) {
+    // partition.cpp:47-54
+    const double rho = static_cast<double>(nrhs) / k;
+    const double t = 1.0 / (1.0 + K * rho) + (1.5 + 2.0 * rho) / (1.0 / K + rho);
+    *r13 = t;
+    *r12 = t / 2.0;
+}
+
+spk_status spk_distribute_threads(int32_t t, int32_t cap_p, int32_t* p, int32_t* kinds, int32_t kinds_cap,
+                                  int32_t* threads_used, int32_t* idle) {
+    // partition.cpp:24-45
+    return guarded([&] {
+        if (t < 1) fail(SPK_EINVAL, "distribute_threads: t must be >= 1");
+        int pp = 1;
+        while (2 * pp <= t) pp *= 2;
+        if (cap_p > 0) pp = std::min(pp, cap_p);
+        *p = pp;
+        std::vector<int> kd(pp, SPK_INNER_SINGLE);
+        int used = 1;
+        if (pp == 1) {
+            kd[0] = SPK_FIRSTLAST;
+        } else {
+            kd.front() = kd.back() = SPK_FIRSTLAST;
+            const int extra = std::min(t - pp, pp - 2);
+            for (int i = 0; i < extra; ++i) kd[1 + i] = SPK_INNER_DUAL;
+            used = pp + extra;
+        }
+        if (kinds)
+            for (int i = 0; i < pp && i < kinds_cap; ++i) kinds[i] = kd[i];
+        if (threads_used) *threads_used = used;
+        if (idle) *idle = t - used;
+    });
+}
+
+spk_status spk_compute_sizes(int64_t n, int32_t p, const int32_t* kinds, double r12, double r13,
+                             int64_t min_single, int64_t min_dual, int64_t* sizes) {
+    // partition.cpp:56-87
+    return guarded([&] {
+        if (p == 1) {
+            if (n < min_single) fail(SPK_EDOMAIN, "compute_sizes: matrix too small");
+            sizes[0] = n;
+            return;
+        }
+        int x = 0;
+        for (int i = 0; i < p; ++i) x += kinds[i] == SPK_INNER_DUAL;
+        const int y = (p - x) - 2;
+        const double denom = 2.0 * r12 * r13 + x * r13 + y * r12;
+        const double n1 = n * r12 * r13 / denom, n2 = n1 / r12, n3 = n1 / r13;
+        long long rest = 0;
+        for (int i = 1; i < p; ++i) {
+            double want = n1;
+            if (kinds[i] == SPK_INNER_DUAL) want = n2;
+            else if (kinds[i] == SPK_INNER_SINGLE) want = n3;
+            sizes[i] = std::llround(want);
+            rest += sizes[i];
+        }
+        sizes[0] = n - rest;
+        for (int i = 0; i < p; ++i) {
+            const long long need = kinds[i] == SPK_INNER_DUAL ? min_dual : min_single;
+            if (sizes[i] < need) fail(SPK_EDOMAIN, "compute_sizes: partition below its minimum size");
+        }
+    });
+}
+
+spk_status spk_make_plan(int64_t n, int32_t kl, int32_t ku, int32_t t, double r12, double r13, int32_t cap,
+                         int32_t* p, int64_t* bounds, int32_t* kinds, int32_t* threads_used, int32_t* idle) {
+    // partition.cpp:89-118
+    return guarded([&] {
+        if (t < 1) fail(SPK_EINVAL, "distribute_threads: t must be >= 1");
+        const int khat = std::max(kl, ku);
+        const long long min_single = 2LL * khat + 1;
+        const long long min_dual = std::max(min_single, 2LL * (kl + ku + 1));
+        int p0 = 0, tu = 0, id = 0;
+        spk_distribute_threads(t, 0, &p0, nullptr, 0, &tu, &id);
+        for (int pp = p0; pp >= 1; pp /= 2) {
+            int pq = 0;
+            std::vector<int32_t> kd(pp);
+            spk_distribute_threads(t, pp, &pq, kd.data(), pp, &tu, &id);
+            std::vector<int64_t> sizes(pq);
+            if (spk_compute_sizes(n, pq, kd.data(), r12, r13, min_single, min_dual, sizes.data()) == SPK_OK) {
+                if (pq > cap) fail(SPK_EINVAL, "make_plan: capacity too small");
+                *p = pq;
+                bounds[0] = 0;
+                for (int i = 0; i < pq; ++i) {
+                    bounds[i + 1] = bounds[i] + sizes[i];
+                    kinds[i] = kd[i];
+                }
+                *threads_used = tu;
+                *idle = id;
+                return;
+            }
+            if (pp == 1) break;
+        }
+        *p = 1;
+        bounds[0] = 0;
+        bounds[1] = n;
+        kinds[0] = SPK_FIRSTLAST;
+        *threads_used = 1;
+        *idle = t - 1;
+    });
+}
+
+spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t pivoting, int32_t p_hint,
+                        int32_t cap, int32_t* p, int64_t* bounds, int32_t* kinds) {
+    return guarded([&] {
+        const int k = std::max(kl, ku);
+        const long long min_part = std::max<long long>(2LL * k + 1, 1);
+        int pp = p_hint;
+        if (pp <= 0) {
+            // one partition per SM for wide bands (the sweep kernels then split
+            // the right-hand sides across SMs); more for narrow bands, where a
+            // partition's column chain is short per step.
+            const int sms = 148;
+            if (k >= 96) pp = sms;
+            else if (k >= 32) pp = 2 * sms;
+            else pp = 8 * sms;
+            (void)nrhs;
+            (void)pivoting;
+        }
+        pp = (int)std::max<long long>(1, std::min<long long>(pp, n / std::max<long long>(min_part, 1)));
+        if (pp > cap) fail(SPK_EINVAL, "gpu_plan: capacity too small");
+        // first/last partitions carry no spike sweeps (0 vs 3 in factor, 2 vs 4
+        // in solve): give them the reference's R13 ratio with K = 1.
+        double r12 = 1.0, r13 = 2.0;
+        spk_compute_ratios(1.0, nrhs, std::max(k, 1), &r12, &r13);
+        r13 = std::min(std::max(r13, 1.0), 3.0);
+        std::vector<double> w(pp, 1.0);
+        if (pp > 1) w.front() = w.back() = r13;
+        double tot = 0.0;
+        for (double x : w) tot += x;
+        bounds[0] = 0;
+        long long acc = 0;
+        for (int i = 0; i < pp; ++i) {
+            long long sz = (i == pp - 1) ? n - acc : (long long)std::llround(n * w[i] / tot);
+            acc += sz;
+            bounds[i + 1] = acc;
+        }
+        for (int i = 0; i < pp; ++i) {
+            if (bounds[i + 1] - bounds[i] < min_part && pp > 1) fail(SPK_EDOMAIN, "gpu_plan: partition too small");
+            kinds[i] = (i == 0 || i == pp - 1) ? SPK_FIRSTLAST : SPK_INNER_SINGLE;
+        }
+        *p = pp;
+    });
+}
+
+spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
+                         const spk_plan* plan, const spk_factor_options* opts, void* stream,
+                         spk_fact** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (n < 1 || kl < 0 || ku < 0 || kl >= n || ku >= n) fail(SPK_EINVAL, "BandedMatrix: bad shape");
+        validate_plan(n, plan);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto f = std::make_unique<spk_fact>();
+        f->n = n;
+        f->kl = kl;
+        f->ku = ku;
+        f->k = std::max(kl, ku);
+        f->p = plan->p;
+        f->piv_on = opts ? opts->pivoting : 0;
+        f->boost_eps = (opts && opts->boost_eps > 0) ? opts->boost_eps : std::sqrt(DBL_EPSILON);
+        f->bounds.assign(plan->bounds, plan->bounds + plan->p + 1);
+        f->kinds.assign(plan->p, SPK_INNER_SINGLE);
+        if (plan->kinds) f->kinds.assign(plan->kinds, plan->kinds + plan->p);
+        f->stream = s;
+        setup_fact(*f, s);
+        // band on device
+        const long long ld = kl + ku + 1;
+        const double* dband = band;
+        double* tmp = nullptr;
+        if (band_mem == SPK_MEM_HOST) {
+            tmp = dalloc<double>(ld * n, s);
+            ck(cudaMemcpyAsync(tmp, band, sizeof(double) * ld * n, cudaMemcpyHostToDevice, s), "band upload");
+            dband = tmp;
+        }
+        const int p = f->p;
+        long long max_elems = 0;
+        for (int i = 0; i < p; ++i) max_elems = std::max(max_elems, (long long)f->parts[i].m * f->parts[i].rows);
+        launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_amax, s);
+        launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->d_pool + f->off_bhat, f->d_pool + f->off_chat, s);
+        double* fs = nullptr;
+        double* auxf = nullptr;
+        if (p > 1 && f->k > 0) {
+            fs = dalloc<double>((size_t)n * 2 * f->k, s);
+            auxf = dalloc<double>((size_t)f->auxf_rows * f->k, s);
+        }
+        Bufs B = make_bufs();
+        B.p[B_POOL] = f->d_pool;
+        B.ld[B_POOL] = 1;
+        B.p[B_FS] = fs;
+        B.ld[B_FS] = n;
+        B.p[B_AUX] = auxf;
+        B.ld[B_AUX] = f->auxf_rows;
+        Exec ex{*f, s, B, f->k};
+        ex.n = n;
+        ex.run(f->prog_factor);
+        if (fs) ck(cudaFreeAsync(fs, s), "free");
+        if (auxf) ck(cudaFreeAsync(auxf, s), "free");
+        if (tmp) ck(cudaFreeAsync(tmp, s), "free");
+        finish_factor(*f, s);
+        *out = f.release();
+    });
+}
+
+void spk_fact_destroy(spk_fact* f) { delete f; }
+
+spk_status spk_fact_info(const spk_fact* f, int64_t* n, int32_t* kl, int32_t* ku, int32_t* k, int32_t* p,
+                         int32_t* levels, int32_t* boost_count, int32_t* boost_warnings) {
+    return guarded([&] {
+        if (n) *n = f->n;
+        if (kl) *kl = f->kl;
+        if (ku) *ku = f->ku;
+        if (k) *k = f->k;
+        if (p) *p = f->p;
+        if (levels) *levels = f->levels.empty() ? 0 : (int)f->levels.size() - 1;
+        if (boost_count) *boost_count = f->boost_count;
+        if (boost_warnings) *boost_warnings = f->boost_warnings;
+    });
+}
+
+spk_status spk_fact_bounds(const spk_fact* f, int64_t* bounds) {
+    return guarded([&] { std::copy(f->bounds.begin(), f->bounds.end(), bounds); });
+}
+
+spk_status spk_fact_factor_sweeps(const spk_fact* f, int64_t* sweeps) {
+    return guarded([&] { std::copy(f->factor_sweeps.begin(), f->factor_sweeps.end(), sweeps); });
+}
+
+spk_status spk_fact_tip(const spk_fact* f, int32_t which, int32_t i, double* out) {
+    return guarded([&] {
+        const int k = f->k, p = f->p;
+        if (i < 0 || i >= p || which < 0 || which > 5) fail(SPK_ERANGE, "fact_tip: index out of range");
+        const long long kk = (long long)k * k;
+        std::fill(out, out + kk, 0.0);
+        if (k == 0) return;
+        if (which == SPK_BHAT || which == SPK_CHAT) {
+            const long long off = (which == SPK_BHAT ? f->off_bhat : f->off_chat) + i * kk;
+            ck(cudaMemcpy(out, f->d_pool + off, sizeof(double) * kk, cudaMemcpyDeviceToHost), "tip");
+            return;
+        }
+        if (p < 2) return;
+        const Level& l0 = f->levels[0];
+        const long long base = (which == SPK_TIP_VT || which == SPK_TIP_VB) ? l0.voff[i] : l0.woff[i];
+        if (base < 0) return;
+        const long long roff = (which == SPK_TIP_VB || which == SPK_TIP_WB) ? k : 0;
+        ck(cudaMemcpy2D(out, sizeof(double) * k, f->d_pool + base + roff, sizeof(double) * 2 * k,
+                        sizeof(double) * k, k, cudaMemcpyDeviceToHost),
+           "tip");
+    });
+}
+
+int32_t spk_fact_units(const spk_fact* f, int32_t l) {
+    if (l < 0 || l >= (int)f->levels.size()) return 0;
+    return f->levels[l].units;
+}
+
+spk_status spk_fact_level_spike(const spk_fact* f, int32_t l, int32_t which, int32_t u, int32_t* h,
+                                double* out) {
+    return guarded([&] {
+        if (l < 0 || l + 1 >= (int)f->levels.size()) fail(SPK_ERANGE, "level_spike: level out of range");
+        const Level& lv = f->levels[l];
+        if (u < 0 || u >= lv.units) fail(SPK_ERANGE, "level_spike: unit out of range");
+        *h = lv.uh[u];
+        if (!out) return;
+        const long long sz = (long long)lv.uh[u] * f->k;
+        const long long off = which == 0 ? lv.voff[u] : lv.woff[u];
+        if (off < 0) {
+            std::fill(out, out + sz, 0.0);
+            return;
+        }
+        ck(cudaMemcpy(out, f->d_pool + off, sizeof(double) * sz, cudaMemcpyDeviceToHost), "level_spike");
+    });
+}
+
+spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu, int32_t* piv,
+                             int32_t* fell_back) {
+    return guarded([&] {
+        if (l < 0 || l + 1 >= (int)f->levels.size()) fail(SPK_ERANGE, "coupling: level out of range");
+        const Level& lv = f->levels[l];
+        if (a < 0 || a >= (int)lv.pair_part.size()) fail(SPK_ERANGE, "coupling: pair out of range");
+        const PartDev& P = f->parts[lv.pair_part[a]];
+        const int nn = P.m;
+        std::vector<double> band((size_t)P.m * P.rows);
+        ck(cudaMemcpy(band.data(), f->d_fac + P.fofs, sizeof(double) * band.size(), cudaMemcpyDeviceToHost),
+           "coupling");
+        for (int j = 0; j < nn; ++j)
+            for (int i = 0; i < nn; ++i) {
+                const int q = P.d + i - j;
+                lu[(size_t)j * nn + i] = (q >= 0 && q < P.rows) ? band[(size_t)j * P.rows + q] : 0.0;
+            }
+        if (piv) ck(cudaMemcpy(piv, f->d_piv + P.r0, sizeof(int) * nn, cudaMemcpyDeviceToHost), "coupling");
+        if (fell_back) {
+            int fb = 0;
+            ck(cudaMemcpy(&fb, f->d_fell + lv.pair_part[a], sizeof(int), cudaMemcpyDeviceToHost), "coupling");
+            *fell_back = fb;
+        }
+    });
+}
+
+spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf, int32_t nrhs,
+                     double* X, int64_t ldx, int32_t mem, void* stream, spk_solve_stats* stats) {
+    return guarded([&] {
+        spk_fact& f = const_cast<spk_fact&>(*fc);
+        const long long n = f.n;
+        if (nrhs < 0) fail(SPK_EINVAL, "solve: negative nrhs");
+        if (ldf < n || ldx < n) fail(SPK_EINVAL, transpose ? "transpose_solve: F.rows must equal n"
+                                                           : "solve: F.rows must equal n");
+        if (stats) {
+            if (stats->partition_full_sweeps)
+                for (int i = 0; i < f.p; ++i) {
+                    const bool edge = f.p > 1 && (i == 0 || i == f.p - 1);
+                    stats->partition_full_sweeps[i] = f.p == 1 ? 2 : (f.k == 0 ? 2 : (edge ? 2 : 4));
+                }
+            stats->reduced_coupling_solves = (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
+        }
+        if (nrhs == 0) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const double* dF = F;
+        double* dX = X;
+        double* tF = nullptr;
+        double* tX = nullptr;
+        long long lf = ldf, lx = ldx;
+        if (mem == SPK_MEM_HOST) {
+            tF = dalloc<double>((size_t)n * nrhs, s);
+            tX = dalloc<double>((size_t)n * nrhs, s);
+            ck(cudaMemcpy2DAsync(tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
+                                 cudaMemcpyHostToDevice, s),
+               "F upload");
+            dF = tF;
+            dX = tX;
+            lf = lx = n;
+        } else if (transpose) {
+            // the transpose program re-reads F after writing X: never alias
+            const char* f0 = (const char*)F;
+            const char* f1 = (const char*)(F + ldf * (nrhs - 1) + n);
+            const char* x0 = (const char*)X;
+            const char* x1 = (const char*)(X + ldx * (nrhs - 1) + n);
+            if (!(f1 <= x0 || x1 <= f0)) {
+                tF = dalloc<double>((size_t)n * nrhs, s);
+                ck(cudaMemcpy2DAsync(tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
+                                     cudaMemcpyDeviceToDevice, s),
+                   "F copy");
+                dF = tF;
+                lf = n;
+            }
+        }
+        const bool coupled = f.p > 1 && f.k > 0;
+        double* S = nullptr;
+        double* T = nullptr;
+        double* AUX = nullptr;
+        if (coupled) {
+            S = dalloc<double>((size_t)n * nrhs, s);
+            T = dalloc<double>((size_t)2 * f.p * f.k * nrhs, s);
+            AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
+        }
+        Bufs B = make_bufs();
+        B.p[B_X] = dX;
+        B.ld[B_X] = lx;
+        B.p[B_F] = const_cast<double*>(dF);
+        B.ld[B_F] = lf;
+        B.p[B_S] = S;
+        B.ld[B_S] = n;
+        B.p[B_T] = T;
+        B.ld[B_T] = 2LL * f.p * f.k;
+        B.p[B_AUX] = AUX;
+        B.ld[B_AUX] = f.aux_rows;
+        B.p[B_POOL] = f.d_pool;
+        B.ld[B_POOL] = 1;
+        Exec ex{f, s, B, nrhs};
+        ex.n = n;
+        ex.run(transpose ? f.prog_tr : f.prog_fwd);
+        if (mem == SPK_MEM_HOST)
+            ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, dX, sizeof(double) * n, sizeof(double) * n, nrhs,
+                                 cudaMemcpyDeviceToHost, s),
+               "X download");
+        for (double* q : {S, T, AUX, tF, tX})
+            if (q) ck(cudaFreeAsync(q, s), "free");
+        ck(cudaGetLastError(), "solve kernels");
+        if (mem == SPK_MEM_HOST) ck(cudaStreamSynchronize(s), "solve");
+    });
+}
+
+spk_status spk_reduced_create(const double* vt, const double* vb, const double* wt, const double* wb, int32_t p,
+                              int32_t k, double boost_eps, spk_reduced** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (p < 1 || k < 0) fail(SPK_EINVAL, "reduce_factorize: bad shape");
+        auto r = std::make_unique<spk_reduced>();
+        r->f = std::make_unique<spk_fact>();
+        spk_fact& f = *r->f;
+        f.reduced_only = true;
+        f.n = 2LL * p * k;
+        f.k = k;
+        f.kl = f.ku = k;
+        f.p = p;
+        f.boost_eps = boost_eps > 0 ? boost_eps : std::sqrt(DBL_EPSILON);
+        f.bounds.assign(p + 1, 0);
+        cudaStream_t s = nullptr;
+        setup_fact(f, s);
+        if (p > 1 && k > 0) {
+            const long long kk = (long long)k * k;
+            const Level& l0 = f.levels[0];
+            std::vector<double> col(2 * kk);
+            for (int i = 0; i < p; ++i) {
+                if (l0.voff[i] >= 0) {
+                    for (int c = 0; c < k; ++c)
+                        for (int q = 0; q < k; ++q) {
+                            col[(size_t)c * 2 * k + q] = vt[i * kk + (size_t)c * k + q];
+                            col[(size_t)c * 2 * k + k + q] = vb[i * kk + (size_t)c * k + q];
+                        }
+                    ck(cudaMemcpy(f.d_pool + l0.voff[i], col.data(), sizeof(double) * 2 * kk, cudaMemcpyHostToDevice),
+                       "tips");
+                }
+                if (l0.woff[i] >= 0) {
+                    for (int c = 0; c < k; ++c)
+                        for (int q = 0; q < k; ++q) {
+                            col[(size_t)c * 2 * k + q] = wt[i * kk + (size_t)c * k + q];
+                            col[(size_t)c * 2 * k + k + q] = wb[i * kk + (size_t)c * k + q];
+                        }
+                    ck(cudaMemcpy(f.d_pool + l0.woff[i], col.data(), sizeof(double) * 2 * kk, cudaMemcpyHostToDevice),
+                       "tips");
+                }
+            }
+            double* auxf = dalloc<double>((size_t)f.auxf_rows * k, s);
+            Bufs B = make_bufs();
+            B.p[B_POOL] = f.d_pool;
+            B.p[B_AUX] = auxf;
+            B.ld[B_AUX] = f.auxf_rows;
+            Exec ex{f, s, B, k};
+            ex.run(f.prog_factor);
+            ck(cudaFreeAsync(auxf, s), "free");
+        }
+        finish_factor(f, s);
+        *out = r.release();
+    });
+}
+
+spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z, int32_t ncols,
+                             int64_t* couplings) {
+    return guarded([&] {
+        spk_fact& f = *r->f;
+        if (couplings) *couplings += (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
+        if (ncols == 0 || f.p < 2 || f.k == 0) return;
+        cudaStream_t s = nullptr;
+        const long long rows = 2LL * f.p * f.k;
+        double* T = dalloc<double>((size_t)rows * ncols, s);
+        double* AUX = dalloc<double>((size_t)f.aux_rows * ncols, s);
+        ck(cudaMemcpyAsync(T, z, sizeof(double) * rows * ncols, cudaMemcpyHostToDevice, s), "z upload");
+        Bufs B = make_bufs();
+        B.p[B_T] = T;
+        B.ld[B_T] = rows;
+        B.p[B_AUX] = AUX;
+        B.ld[B_AUX] = f.aux_rows;
+        B.p[B_POOL] = f.d_pool;
+        Exec ex{f, s, B, ncols};
+        ex.run(transpose ? f.prog_tr : f.prog_fwd);
+        ck(cudaMemcpyAsync(z, T, sizeof(double) * rows * ncols, cudaMemcpyDeviceToHost, s), "z download");
+        ck(cudaFreeAsync(T, s), "free");
+        ck(cudaFreeAsync(AUX, s), "free");
+        ck(cudaStreamSynchronize(s), "reduced_solve");
+    });
+}
+
+int32_t spk_reduced_levels(const spk_reduced* r) {
+    return r->f->levels.empty() ? 0 : (int)r->f->levels.size() - 1;
+}
+int32_t spk_reduced_boost_warnings(const spk_reduced* r) { return r->f->boost_warnings; }
+void spk_reduced_destroy(spk_reduced* r) { delete r; }
+
+spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku, const double* X, int64_t ldx,
+                           int32_t ncols, int32_t transpose, double* Y, int64_t ldy, int32_t mem, void* stream) {
+    return guarded([&] {
+        if (ldx < n || ldy < n) fail(SPK_EINVAL, "band_matmul: X.rows must equal n");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (ncols == 0) return;
+        if (mem == SPK_MEM_DEVICE) {
+            launch_band_matmul(band, n, kl, ku, X, ldx, ncols, transpose, Y, ldy, s);
+            ck(cudaGetLastError(), "band_matmul");
+            return;
+        }
+        const long long ld = kl + ku + 1;
+        double* db = dalloc<double>((size_t)ld * n, s);
+        double* dx = dalloc<double>((size_t)n * ncols, s);
+        double* dy = dalloc<double>((size_t)n * ncols, s);
+        ck(cudaMemcpyAsync(db, band, sizeof(double) * ld * n, cudaMemcpyHostToDevice, s), "upload");
+        ck(cudaMemcpy2DAsync(dx, sizeof(double) * n, X, sizeof(double) * ldx, sizeof(double) * n, ncols,
+                             cudaMemcpyHostToDevice, s),
+           "upload");
+        launch_band_matmul(db, n, kl, ku, dx, n, ncols, transpose, dy, n, s);
+        ck(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, dy, sizeof(double) * n, sizeof(double) * n, ncols,
+                             cudaMemcpyDeviceToHost, s),
+           "download");
+        for (double* q : {db, dx, dy}) ck(cudaFreeAsync(q, s), "free");
+        ck(cudaStreamSynchronize(s), "band_matmul");
+    });
+}
+
+spk_status spk_generate_band(uint64_t seed, int64_t n, int32_t kl, int32_t ku, double dd, double* d_band,
+                             void* stream) {
+    return guarded([&] {
+        launch_generate_band(seed, n, kl, ku, dd, d_band, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "generate_band");
+    });
+}
+
+spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double* d_F, int64_t ldf, void* stream) {
+    return guarded([&] {
+        if (ncols == 0) return;
+        launch_generate_rhs(seed, n, ncols, d_F, ldf, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "generate_rhs");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,505 @@
+// spk_kernels_generic.cu — generic (any k, any p, pivoting or not) SPIKE
+// kernels.  These are the correctness baseline every specialised kernel is
+// checked against, and the path taken for shapes the specialised kernels do
+// not cover.  Each launch processes a whole batch of jobs (all partitions /
+// all coupling blocks of one stage).
+//
+// Reference counterparts (paths under /root/reference/proj):
+//   k_fill_factors      LUFactors ctor copy          src/kernels.cpp:29-65
+//   k_band_lu           LUFactors::factor            src/kernels.cpp:79-118
+//   k_sweep SW_FWD_L    forward_lower(_tail)         src/kernels.cpp:131-165
+//   k_sweep SW_BWD_U    backward_upper / upper_bottom_tip  :167-202
+//   k_sweep SW_FWD_UT   forward_upperT / add_upperT_tail   :204-217, :263-280
+//   k_sweep SW_BWD_LT   backward_lowerT / lowerT_perm_bottom_tip :219-261
+//   k_corners           band_corner                  src/spike2x2.cpp:17-26
+//   k_build_coupling    reduce_factorize coupling    src/factorize.cpp:94-101
+//   k_gemm              gemm_minus(_t), block_util mul  src/banded_matrix.cpp:39-51
+#include "spk_device.cuh"
+#include "spk_launch.h"
+
+#include <cfloat>
+#include <cstdint>
+
+namespace spk {
+
+__device__ __forceinline__ double& vat(const Bufs& B, const View& v, int L, int c) {
+    const long long ld = v.ld >= 0 ? v.ld : B.ld[v.buf];
+    const int ph = v.rev ? (v.mrows - 1 - (L - v.off)) : (L - v.off);
+    return B.p[v.buf][v.base + ph + (long long)c * ld];
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// Factor storage fill: packed LU layout from the input band, reversed for the
+// UL partition; per-partition max|entry| for the boost threshold.
+__global__ void k_fill_factors(const double* __restrict__ band, long long n, int akl, int aku,
+                               const PartDev* __restrict__ parts, double* __restrict__ fac,
+                               unsigned long long* __restrict__ amax_bits) {
+    const PartDev P = parts[blockIdx.y];
+    const long long total = (long long)P.m * P.rows;
+    const int ald = akl + aku + 1;
+    double lmax = 0.0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / P.rows);
+        const int q = (int)(e - (long long)j * P.rows);
+        const int i = q - P.d + j;
+        double v = 0.0;
+        if (i >= 0 && i < P.m && i - j <= P.kl && j - i <= P.ku) {
+            const long long gi = P.rev ? P.r0 + P.m - 1 - i : P.r0 + i;
+            const long long gj = P.rev ? P.r0 + P.m - 1 - j : P.r0 + j;
+            if (gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
+        }
+        fac[P.fofs + e] = v;
+        lmax = fmax(lmax, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if ((threadIdx.x & 31) == 0 && lmax > 0.0)
+        atomicMax(&amax_bits[blockIdx.y], (unsigned long long)__double_as_longlong(lmax));
+}
+
+// ---------------------------------------------------------------------------
+// Unblocked right-looking band LU, one CTA per unit, in place in the factor
+// pool.  Non-pivoting: boost |u_jj| < eps*max|A_i| to +-boost_eps*max|A_i|.
+// Pivoting: first max of kl+1 candidates, row swap over [j, j+ubw]; an exactly
+// zero column either fails (status 2) or, for units with `fallback`, restarts
+// the unit without pivoting from its backup copy (kernels.cpp:67-77).
+__global__ void k_band_lu(const int* __restrict__ units, const PartDev* __restrict__ parts,
+                          double* __restrict__ fac, int* __restrict__ piv_pool,
+                          const unsigned long long* __restrict__ amax_bits, double boost_eps,
+                          int* __restrict__ boost_cnt, int* __restrict__ fell_back,
+                          int* __restrict__ status) {
+    const int u = units[blockIdx.x];
+    const PartDev P = parts[u];
+    double* F = fac + P.fofs;
+    int* piv = piv_pool + P.r0;
+    const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
+    const double amax = __longlong_as_double((long long)amax_bits[u]);
+    const double scale = amax == 0.0 ? 1.0 : amax;
+    const double thresh = DBL_EPSILON * scale, bmag = boost_eps * scale;
+    __shared__ int s_ip, s_fail;
+    int pivoting = P.pivoting;
+    int nboost = 0;
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (attempt == 1) {
+            // restart from the backup without pivoting
+            for (long long e = tid; e < (long long)m * rows; e += T) F[e] = fac[P.bofs + e];
+            pivoting = 0;
+            nboost = 0;
+            __syncthreads();
+        }
+        bool failed = false;
+        for (int j = 0; j < m; ++j) {
+            double* cj = F + (long long)j * rows;
+            const int rl = min(kl, m - 1 - j);
+            if (pivoting) {
+                if (tid < 32) {
+                    double best = -1.0;
+                    int bi = 0;
+                    for (int r = lane; r <= rl; r += 32) {
+                        const double a = fabs(cj[d + r]);
+                        if (a > best) {
+                            best = a;
+                            bi = r;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        if (ob > best || (ob == best && oi < bi)) {
+                            best = ob;
+                            bi = oi;
+                        }
+                    }
+                    if (lane == 0) {
+                        s_ip = j + bi;
+                        s_fail = (best == 0.0);
+                    }
+                }
+                __syncthreads();
+                if (s_fail) {
+                    failed = true;
+                    break;
+                }
+                const int ip = s_ip;
+                if (tid == 0) piv[j] = ip;
+                if (ip != j) {
+                    const int ce = min(m - 1, j + ubw);
+                    for (int c = j + tid; c <= ce; c += T) {
+                        double* cc = F + (long long)c * rows;
+                        const double t = cc[d + j - c];
+                        cc[d + j - c] = cc[d + ip - c];
+                        cc[d + ip - c] = t;
+                    }
+                }
+                __syncthreads();
+            } else {
+                if (tid == 0) {
+                    piv[j] = j;
+                    if (fabs(cj[d]) < thresh) {
+                        cj[d] = cj[d] == 0.0 ? bmag : copysign(bmag, cj[d]);
+                        ++nboost;
+                    }
+                }
+                __syncthreads();
+            }
+            if (rl == 0) continue;
+            const double inv = 1.0 / cj[d];
+            for (int r = tid; r < rl; r += T) cj[d + 1 + r] *= inv;
+            __syncthreads();
+            const int ce = min(m - 1, j + ubw);
+            const int ncol = ce - j;
+            const int total = ncol * rl;
+            for (int e = tid; e < total; e += T) {
+                const int cc = e / rl, r = e - cc * rl;
+                const int c = j + 1 + cc;
+                double* col = F + (long long)c * rows;
+                const double ajc = col[d + j - c];
+                if (ajc != 0.0) col[d + j - c + 1 + r] -= ajc * cj[d + 1 + r];
+            }
+            __syncthreads();
+        }
+        if (!failed) break;
+        if (!P.fallback) {
+            if (tid == 0) atomicExch(status, 2);
+            return;
+        }
+        if (tid == 0 && fell_back) fell_back[u] = 1;
+        __syncthreads();
+    }
+    if (tid == 0 && nboost) atomicAdd(&boost_cnt[u], nboost);
+}
+
+// ---------------------------------------------------------------------------
+// Triangular sweeps, one warp per (job, right-hand-side column).
+__global__ void k_sweep(const SweepJob* __restrict__ jobs, const PartDev* __restrict__ parts,
+                        const double* __restrict__ fac, const int* __restrict__ piv_pool, Bufs B,
+                        int ncols) {
+    const SweepJob J = jobs[blockIdx.x];
+    const int wpb = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nc = J.nc >= 0 ? J.nc : ncols;
+    const int cl = blockIdx.y * wpb + (threadIdx.x >> 5);
+    if (cl >= nc) return;
+    const int c = J.c0 + cl;
+    const PartDev P = parts[J.part];
+    const double* F = fac + P.fofs;
+    const int* piv = piv_pool + P.r0;
+    const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
+    const View& v = J.v;
+    switch (J.mode) {
+        case SW_FWD_L:
+            for (int j = J.lo; j < m; ++j) {
+                if (P.pivoting && piv[j] != j) {
+                    if (lane == 0) {
+                        double& a = vat(B, v, j, c);
+                        double& b = vat(B, v, piv[j], c);
+                        const double t = a;
+                        a = b;
+                        b = t;
+                    }
+                    __syncwarp();
+                }
+                const int rl = min(kl, m - 1 - j);
+                if (rl == 0) continue;
+                const double bj = vat(B, v, j, c);
+                if (bj != 0.0) {
+                    const double* lj = F + (long long)j * rows + d + 1;
+                    for (int r = lane; r < rl; r += 32) vat(B, v, j + 1 + r, c) -= bj * lj[r];
+                }
+                __syncwarp();
+            }
+            break;
+        case SW_BWD_U:
+            for (int j = J.hi; j >= J.lo; --j) {
+                const double* cj = F + (long long)j * rows;
+                const double z = vat(B, v, j, c) / cj[d];
+                __syncwarp();
+                if (lane == 0) vat(B, v, j, c) = z;
+                const int r0 = max(j - ubw, v.off);
+                if (z != 0.0)
+                    for (int r = r0 + lane; r < j; r += 32) vat(B, v, r, c) -= z * cj[d + r - j];
+                __syncwarp();
+            }
+            break;
+        case SW_FWD_UT:
+            for (int i = J.lo; i < m; ++i) {
+                const double* ci = F + (long long)i * rows;
+                const int q0 = max(i - ubw, v.off);
+                double part = 0.0;
+                for (int q = q0 + lane; q < i; q += 32) part += ci[d + q - i] * vat(B, v, q, c);
+                const double s = warp_sum(part);
+                if (lane == 0) {
+                    double& bi = vat(B, v, i, c);
+                    bi = (bi - s) / ci[d];
+                }
+                __syncwarp();
+            }
+            break;
+        case SW_BWD_LT:
+            for (int i = m - 1; i >= J.lo; --i) {
+                const int rl = min(kl, m - 1 - i);
+                if (rl > 0) {
+                    const double* li = F + (long long)i * rows + d + 1;
+                    double part = 0.0;
+                    for (int r = lane; r < rl; r += 32) part += li[r] * vat(B, v, i + 1 + r, c);
+                    const double s = warp_sum(part);
+                    if (lane == 0) vat(B, v, i, c) -= s;
+                }
+                __syncwarp();
+                if (P.pivoting && piv[i] != i) {
+                    if (lane == 0) {
+                        double& a = vat(B, v, i, c);
+                        double& b = vat(B, v, piv[i], c);
+                        const double t = a;
+                        a = b;
+                        b = t;
+                    }
+                    __syncwarp();
+                }
+            }
+            break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row-mapped block copy / add / subtract / zero.
+__global__ void k_copy(const CopyJob* __restrict__ jobs, Bufs B, int ncols) {
+    const CopyJob J = jobs[blockIdx.y];
+    const int nc = J.nc >= 0 ? J.nc : ncols;
+    const int rowsn = J.L1 - J.L0;
+    const long long total = (long long)rowsn * nc;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int cc = (int)(e / rowsn);
+        const int L = J.L0 + (int)(e - (long long)cc * rowsn);
+        const int c = J.c0 + cc;
+        double& dst = vat(B, J.dst, L, c);
+        switch (J.op) {
+            case CP_COPY: dst = vat(B, J.src, L, c); break;
+            case CP_ADD: dst += vat(B, J.src, L, c); break;
+            case CP_SUB: dst -= vat(B, J.src, L, c); break;
+            default: dst = 0.0; break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Small batched GEMM, 32x32 output tile per CTA (256 threads, 4 outputs each).
+__global__ void k_gemm(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
+    const GemmJob J = jobs[blockIdx.x];
+    const int nc = J.nc >= 0 ? J.nc : ncols;
+    const int tiles_r = (J.r + 31) / 32;
+    const int tr = blockIdx.y % max(tiles_r, 1);
+    const int tc = blockIdx.y / max(tiles_r, 1);
+    if (tr >= tiles_r || tc * 32 >= nc) return;
+    __shared__ double sa[32][33];
+    __shared__ double sb[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty in [0, 8)
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l0 = 0; l0 < J.kk; l0 += 32) {
+        for (int q = ty; q < 32; q += 8) {
+            // A tile: rows i = tr*32 + tx... stored sa[i][l]
+            const int i = tr * 32 + tx, l = l0 + q;
+            double a = 0.0;
+            if (i < J.r && l < J.kk) a = J.transA ? vat(B, J.a, l, i) : vat(B, J.a, i, l);
+            sa[tx][q] = a;
+            const int cb = tc * 32 + tx;
+            double b = 0.0;
+            if (l < J.kk && cb < nc) b = vat(B, J.b, J.brow0 + l, cb);
+            sb[q][tx] = b;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+            const double bv = sb[l][tx];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) acc[s] += sa[ty + 8 * s][l] * bv;
+        }
+        __syncthreads();
+    }
+    const int cb = tc * 32 + tx;
+    if (cb >= nc) return;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int i = tr * 32 + ty + 8 * s;
+        if (i >= J.r) continue;
+        double& cdst = vat(B, J.c, J.crow0 + i, cb);
+        if (J.op == GM_SET) cdst = acc[s];
+        else cdst -= acc[s];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k x k corner blocks at every partition boundary: bhat[i] = A[b-k:b, b:b+k],
+// chat[i+1] = A[b:b+k, b-k:b] (zero outside the band / matrix).
+__global__ void k_corners(const double* __restrict__ band, long long n, int akl, int aku,
+                          const long long* __restrict__ bounds, int p, int k,
+                          double* __restrict__ bhat, double* __restrict__ chat) {
+    const int i = blockIdx.y;  // boundary after partition i
+    if (i + 1 >= p) return;
+    const long long b = bounds[i + 1];
+    const int ald = akl + aku + 1;
+    const long long kk = (long long)k * k;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+        const int c = e / k, r = e - c * k;
+        {
+            const long long gi = b - k + r, gj = b + c;
+            double v = 0.0;
+            if (gi >= 0 && gj < n && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
+            bhat[i * kk + e] = v;
+        }
+        {
+            const long long gi = b + r, gj = b - k + c;
+            double v = 0.0;
+            if (gj >= 0 && gi < n && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
+            chat[(i + 1) * kk + e] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Coupling blocks [[I, vl_bottom],[wr_top, I]] as full bands (kl=ku=2k-1,
+// pivoting storage rows = 4k-1, diagonal row 2k-1) plus backup and max|C|.
+__global__ void k_build_coupling(const CouplingJob* __restrict__ jobs,
+                                 const PartDev* __restrict__ parts, const double* __restrict__ pool,
+                                 double* __restrict__ fac, unsigned long long* __restrict__ amax_bits) {
+    const CouplingJob J = jobs[blockIdx.y];
+    const PartDev P = parts[J.part];
+    const int k = J.k, nn = 2 * k;
+    const long long total = (long long)P.m * P.rows;
+    double lmax = 0.0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / P.rows);
+        const int q = (int)(e - (long long)j * P.rows);
+        const int i = q - P.d + j;
+        double v = 0.0;
+        if (i >= 0 && i < nn && i - j <= P.kl && j - i <= P.ku) {
+            if (i == j) v = 1.0;
+            else if (i < k && j >= k) v = pool[J.vl_off + (long long)(j - k) * J.hL + (J.hL - k + i)];
+            else if (i >= k && j < k) v = pool[J.wr_off + (long long)j * J.hR + (i - k)];
+        }
+        fac[P.fofs + e] = v;
+        fac[P.bofs + e] = v;
+        lmax = fmax(lmax, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if ((threadIdx.x & 31) == 0 && lmax > 0.0)
+        atomicMax(&amax_bits[J.part], (unsigned long long)__double_as_longlong(lmax));
+}
+
+// ---------------------------------------------------------------------------
+// Y = A X (or A^T X), one thread per output element.
+__global__ void k_band_matmul(const double* __restrict__ band, long long n, int kl, int ku,
+                              const double* __restrict__ X, long long ldx, int ncols, int transpose,
+                              double* __restrict__ Y, long long ldy) {
+    const int ld = kl + ku + 1;
+    const long long total = n * (long long)ncols;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long c = e / n, i = e - c * n;
+        double s = 0.0;
+        if (!transpose) {
+            const long long j0 = i - kl > 0 ? i - kl : 0, j1 = i + ku < n - 1 ? i + ku : n - 1;
+            for (long long j = j0; j <= j1; ++j) s += band[j * ld + ku + i - j] * X[c * ldx + j];
+        } else {
+            // (A^T X)_i = sum_r A(r, i) X_r, column i of the band
+            const long long r0 = i - ku > 0 ? i - ku : 0, r1 = i + kl < n - 1 ? i + kl : n - 1;
+            for (long long r = r0; r <= r1; ++r) s += band[i * ld + ku + r - i] * X[c * ldx + r];
+        }
+        Y[c * ldy + i] = s;
+    }
+}
+
+}  // namespace spk
+
+// ---------------------------------------------------------------------------
+// Launch wrappers (host side of this translation unit).
+namespace spk {
+
+static inline unsigned grid_for(long long work, int per_block, int cap) {
+    long long g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+void launch_fill_factors(const double* band, long long n, int akl, int aku, const PartDev* d_parts,
+                         int nparts, long long max_elems, double* fac, unsigned long long* amax,
+                         cudaStream_t s) {
+    dim3 g(grid_for(max_elems, 256, 4096), nparts);
+    k_fill_factors<<<g, 256, 0, s>>>(band, n, akl, aku, d_parts, fac, amax);
+    count_launch();
+}
+
+void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
+                    const unsigned long long* amax, double boost_eps, int* boost_cnt,
+                    int* fell_back, int* status, cudaStream_t s) {
+    if (nunits <= 0) return;
+    k_band_lu<<<nunits, 256, 0, s>>>(d_units, d_parts, fac, piv, amax, boost_eps, boost_cnt,
+                                     fell_back, status);
+    count_launch();
+}
+
+void launch_sweep(const SweepJob* d_jobs, int njobs, int max_nc, const PartDev* d_parts,
+                  const double* fac, const int* piv, const Bufs& B, int ncols, cudaStream_t s) {
+    if (njobs <= 0 || max_nc <= 0) return;
+    const int wpb = 4;
+    dim3 g(njobs, (max_nc + wpb - 1) / wpb);
+    k_sweep<<<g, 32 * wpb, 0, s>>>(d_jobs, d_parts, fac, piv, B, ncols);
+    count_launch();
+}
+
+void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bufs& B, int ncols,
+                 cudaStream_t s) {
+    if (njobs <= 0 || max_elems <= 0) return;
+    dim3 g(grid_for(max_elems, 256, 2048), njobs);
+    k_copy<<<g, 256, 0, s>>>(d_jobs, B, ncols);
+    count_launch();
+}
+
+void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
+                 cudaStream_t s) {
+    if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
+    const int tr = (max_r + 31) / 32, tc = (max_nc + 31) / 32;
+    dim3 g(njobs, tr * tc);
+    k_gemm<<<g, 256, 0, s>>>(d_jobs, B, ncols);
+    count_launch();
+}
+
+void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
+                    int p, int k, double* bhat, double* chat, cudaStream_t s) {
+    if (p < 2 || k == 0) return;
+    dim3 g(grid_for((long long)k * k, 256, 64), p);
+    k_corners<<<g, 256, 0, s>>>(band, n, akl, aku, d_bounds, p, k, bhat, chat);
+    count_launch();
+}
+
+void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
+                           const PartDev* d_parts, const double* pool, double* fac,
+                           unsigned long long* amax, cudaStream_t s) {
+    if (njobs <= 0) return;
+    dim3 g(grid_for(max_elems, 256, 256), njobs);
+    k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, amax);
+    count_launch();
+}
+
+void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,
+                        long long ldx, int ncols, int transpose, double* Y, long long ldy,
+                        cudaStream_t s) {
+    k_band_matmul<<<grid_for(n * (long long)ncols, 256, 148 * 16), 256, 0, s>>>(
+        band, n, kl, ku, X, ldx, ncols, transpose, Y, ldy);
+    count_launch();
+}
+
+}  // namespace spk

@@ -1,0 +1,37 @@
+// spk_launch.h — host-side launch wrappers of the device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "spk_device.cuh"
+
+namespace spk {
+
+void count_launch(int n = 1);
+
+void launch_fill_factors(const double* band, long long n, int akl, int aku, const PartDev* d_parts,
+                         int nparts, long long max_elems, double* fac, unsigned long long* amax,
+                         cudaStream_t s);
+void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
+                    const unsigned long long* amax, double boost_eps, int* boost_cnt,
+                    int* fell_back, int* status, cudaStream_t s);
+void launch_sweep(const SweepJob* d_jobs, int njobs, int max_nc, const PartDev* d_parts,
+                  const double* fac, const int* piv, const Bufs& B, int ncols, cudaStream_t s);
+void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bufs& B, int ncols,
+                 cudaStream_t s);
+void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
+                 cudaStream_t s);
+void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
+                    int p, int k, double* bhat, double* chat, cudaStream_t s);
+void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
+                           const PartDev* d_parts, const double* pool, double* fac,
+                           unsigned long long* amax, cudaStream_t s);
+void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,
+                        long long ldx, int ncols, int transpose, double* Y, long long ldy,
+                        cudaStream_t s);
+void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd,
+                          double* band, cudaStream_t s);
+void launch_generate_rhs(unsigned long long seed, long long n, int ncols, double* F, long long ldf,
+                         cudaStream_t s);
+
+}  // namespace spk

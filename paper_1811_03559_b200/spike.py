@@ -1,0 +1,696 @@
+"""Python mirror of the reference C++ solver API (``/root/reference/proj/include/spike``).
+
+Same names, argument meaning and error behaviour as the reference, backed by
+the sm_100a CUDA library ``libspike_b200.so`` through its C-ABI
+(``include/spike_b200.h``).  There is no CPU fallback: importing this module
+without the built library, or calling a compute entry point without a GPU,
+raises.
+
+Reference symbol                         here
+---------------------------------------  -------------------------------------
+BandedMatrix (banded_matrix.hpp:14-67)    BandedMatrix (packed (n, ld) array)
+DenseBlock   (banded_matrix.hpp:73-91)    numpy 2-D float64 arrays (Fortran order)
+PartitionKind/PartitionPlan (partition.hpp:12-37)   same
+distribute_threads/compute_ratios/compute_sizes/make_plan (partition.hpp:39-56)  same
+FactorOptions, factorize, SpikeFactorization (factorize.hpp:13-77)  same
+ReducedLevels, reduce_factorize (factorize.hpp:26-49)  same
+SolveStats, solve, transpose_solve, reduced_solve(_transpose), iterative_refine
+(solve.hpp:11-51)  same
+band_matmul, relative_residual, frobenius_norm, norm1, max_abs (band_ops.hpp)  same
+gpu_plan                                 new: arbitrary-p planner for the GPU
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspike_b200.so")
+
+# ----------------------------------------------------------------------------
+# errors (the reference's exception types)
+
+
+class SpikeError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class SingularError(RuntimeError):
+    """std::runtime_error: exactly singular column in pivoting mode"""
+
+
+class DomainError(ValueError):
+    """std::domain_error"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class OutOfRange(IndexError):
+    """std::out_of_range"""
+
+
+_STATUS = {1: InvalidArgument, 2: SingularError, 3: DomainError, 4: CudaError, 5: MemoryError,
+           6: CudaError, 7: OutOfRange}
+
+_lib = None
+_lib_lock = threading.Lock()
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+
+
+class _Plan(C.Structure):
+    _fields_ = [("p", C.c_int32), ("bounds", _i64p), ("kinds", _i32p)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("pivoting", C.c_int32), ("boost_eps", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("partition_full_sweeps", _i64p), ("reduced_coupling_solves", C.c_int64)]
+
+
+def lib():
+    """The loaded CUDA library; raises ImportError when it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1811_03559_b200.build` "
+                              "(the GPU path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.spk_last_error.restype = C.c_char_p
+        L.spk_version.restype = C.c_char_p
+        L.spk_launch_count.restype = C.c_int64
+        L.spk_launch_count.argtypes = [C.c_int32]
+        L.spk_compute_ratios.argtypes = [C.c_double, C.c_int32, C.c_int32, _dp, _dp]
+        L.spk_compute_ratios.restype = None
+        L.spk_distribute_threads.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, C.c_int32, _i32p, _i32p]
+        L.spk_compute_sizes.argtypes = [C.c_int64, C.c_int32, _i32p, C.c_double, C.c_double, C.c_int64,
+                                        C.c_int64, _i64p]
+        L.spk_make_plan.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                    C.c_int32, _i32p, _i64p, _i32p, _i32p, _i32p]
+        L.spk_gpu_plan.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_int32, _i32p, _i64p, _i32p]
+        L.spk_factorize.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                    C.POINTER(_Plan), C.POINTER(_Opts), C.c_void_p,
+                                    C.POINTER(C.c_void_p)]
+        L.spk_fact_destroy.argtypes = [C.c_void_p]
+        L.spk_fact_destroy.restype = None
+        L.spk_fact_info.argtypes = [C.c_void_p, _i64p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]
+        L.spk_fact_bounds.argtypes = [C.c_void_p, _i64p]
+        L.spk_fact_factor_sweeps.argtypes = [C.c_void_p, _i64p]
+        L.spk_fact_tip.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _dp]
+        L.spk_fact_level_spike.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _i32p, _dp]
+        L.spk_fact_coupling.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _dp, _i32p, _i32p]
+        L.spk_fact_units.argtypes = [C.c_void_p, C.c_int32]
+        L.spk_fact_units.restype = C.c_int32
+        L.spk_solve.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                C.c_int64, C.c_int32, C.c_void_p, C.POINTER(_Stats)]
+        L.spk_reduced_create.argtypes = [_dp, _dp, _dp, _dp, C.c_int32, C.c_int32, C.c_double,
+                                         C.POINTER(C.c_void_p)]
+        L.spk_reduced_solve.argtypes = [C.c_void_p, C.c_int32, _dp, C.c_int32, _i64p]
+        L.spk_reduced_levels.argtypes = [C.c_void_p]
+        L.spk_reduced_levels.restype = C.c_int32
+        L.spk_reduced_boost_warnings.argtypes = [C.c_void_p]
+        L.spk_reduced_boost_warnings.restype = C.c_int32
+        L.spk_reduced_destroy.argtypes = [C.c_void_p]
+        L.spk_reduced_destroy.restype = None
+        L.spk_band_matmul.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                      C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+        L.spk_generate_band.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                                        C.c_void_p, C.c_void_p]
+        L.spk_generate_rhs.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().spk_last_error().decode()
+        raise _STATUS.get(rc, SpikeError)(msg)
+
+
+def launch_count(reset=False) -> int:
+    return int(lib().spk_launch_count(1 if reset else 0))
+
+
+def default_boost_eps() -> float:
+    return math.sqrt(np.finfo(np.float64).eps)
+
+
+# ----------------------------------------------------------------------------
+# BandedMatrix / DenseBlock
+
+
+class BandedMatrix:
+    """Packed band, entry (i,j) at data[j, ku+i-j]; data is (n, kl+ku+1) C-order,
+    i.e. the reference's column-major (ld, n) layout (banded_matrix.hpp:14-67)."""
+
+    def __init__(self, n: int, kl: int, ku: int, data: Optional[np.ndarray] = None):
+        if n < 1:
+            raise InvalidArgument("BandedMatrix: n must be >= 1")
+        if kl < 0 or ku < 0 or kl >= n or ku >= n:
+            raise InvalidArgument("BandedMatrix: need 0 <= kl,ku < n")
+        self.n, self.kl, self.ku = int(n), int(kl), int(ku)
+        if data is None:
+            data = np.zeros((n, kl + ku + 1))
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        if data.shape != (n, kl + ku + 1):
+            raise InvalidArgument("BandedMatrix: data shape mismatch")
+        self.data = data
+
+    @staticmethod
+    def identity(n: int) -> "BandedMatrix":
+        a = BandedMatrix(n, 0, 0)
+        a.data[:, 0] = 1.0
+        return a
+
+    def ld(self):
+        return self.kl + self.ku + 1
+
+    def in_band(self, i, j):
+        return 0 <= i < self.n and 0 <= j < self.n and i - j <= self.kl and j - i <= self.ku
+
+    def at(self, i, j):
+        if not (0 <= i < self.n and 0 <= j < self.n):
+            raise OutOfRange("BandedMatrix::at: index out of range")
+        if i - j > self.kl or j - i > self.ku:
+            return 0.0
+        return float(self.data[j, self.ku + i - j])
+
+    def set(self, i, j, v):
+        if not self.in_band(i, j):
+            raise OutOfRange("BandedMatrix::set: entry outside the band")
+        self.data[j, self.ku + i - j] = v
+
+    def dense(self) -> np.ndarray:
+        d = np.zeros((self.n, self.n))
+        for j in range(self.n):
+            for i in range(max(0, j - self.ku), min(self.n, j + self.kl + 1)):
+                d[i, j] = self.data[j, self.ku + i - j]
+        return d
+
+
+def DenseBlock(rows: int, cols: int) -> np.ndarray:
+    if rows < 0 or cols < 0:
+        raise InvalidArgument("DenseBlock: negative shape")
+    return np.zeros((rows, cols), order="F")
+
+
+def _as_block(f) -> np.ndarray:
+    f = np.asarray(f, dtype=np.float64)
+    if f.ndim == 1:
+        f = f[:, None]
+    return np.asfortranarray(f)
+
+
+# ----------------------------------------------------------------------------
+# planning (partition.hpp)
+
+
+class PartitionKind(enum.IntEnum):
+    FirstLast = 0
+    InnerSingle = 1
+    InnerDual = 2
+
+
+@dataclass
+class PartitionPlan:
+    p: int = 1
+    bounds: List[int] = field(default_factory=list)
+    kinds: List[PartitionKind] = field(default_factory=list)
+    threads_used: int = 1
+    idle_threads: int = 0
+    r12: float = 1.0
+    r13: float = 2.0
+
+    def n(self):
+        return self.bounds[-1] if self.bounds else 0
+
+    def size(self, i):
+        return self.bounds[i + 1] - self.bounds[i]
+
+    def dual_count(self):
+        return sum(1 for k in self.kinds if k == PartitionKind.InnerDual)
+
+    def single_count(self):
+        return self.p - self.dual_count()
+
+
+def compute_ratios(k_const: float, n_rhs: int, k: int):
+    """(R12, R13) of partition.cpp:47-54."""
+    if k_const <= 0.0:
+        raise InvalidArgument("compute_ratios: K must be > 0")
+    if k < 1:
+        raise InvalidArgument("compute_ratios: k must be >= 1")
+    if n_rhs < 0:
+        raise InvalidArgument("compute_ratios: n_rhs must be >= 0")
+    a, b = C.c_double(), C.c_double()
+    lib().spk_compute_ratios(k_const, n_rhs, k, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def distribute_threads(t: int, cap_p: int = 0) -> PartitionPlan:
+    cap = max(1, 2 * max(t, 1))
+    p = C.c_int32()
+    kinds = (C.c_int32 * cap)()
+    tu, idle = C.c_int32(), C.c_int32()
+    _check(lib().spk_distribute_threads(t, cap_p, C.byref(p), kinds, cap, C.byref(tu), C.byref(idle)))
+    return PartitionPlan(p=p.value, kinds=[PartitionKind(kinds[i]) for i in range(p.value)],
+                         threads_used=tu.value, idle_threads=idle.value)
+
+
+def compute_sizes(n, skeleton: PartitionPlan, r12, r13, min_single, min_dual):
+    p = skeleton.p
+    kinds = (C.c_int32 * p)(*[int(k) for k in skeleton.kinds])
+    sizes = (C.c_int64 * p)()
+    _check(lib().spk_compute_sizes(n, p, kinds, r12, r13, min_single, min_dual, sizes))
+    return list(sizes)
+
+
+def make_plan(n: int, kl: int, ku: int, t: int, r12: float, r13: float) -> PartitionPlan:
+    """Reference planner (partition.cpp:89-118): power-of-two p from t threads."""
+    cap = max(2, 2 * t + 2)
+    p = C.c_int32()
+    bounds = (C.c_int64 * (cap + 1))()
+    kinds = (C.c_int32 * cap)()
+    tu, idle = C.c_int32(), C.c_int32()
+    _check(lib().spk_make_plan(n, kl, ku, t, r12, r13, cap, C.byref(p), bounds, kinds, C.byref(tu),
+                               C.byref(idle)))
+    return PartitionPlan(p=p.value, bounds=list(bounds[:p.value + 1]),
+                         kinds=[PartitionKind(kinds[i]) for i in range(p.value)],
+                         threads_used=tu.value, idle_threads=idle.value, r12=r12, r13=r13)
+
+
+def gpu_plan(n: int, kl: int, ku: int, nrhs: int = 1, pivoting: bool = False, p: int = 0) -> PartitionPlan:
+    """B200 planner: any p >= 1 (not only powers of two), partitions mapped onto SMs."""
+    cap = max(4096, 2 * p + 2)
+    pp = C.c_int32()
+    bounds = (C.c_int64 * (cap + 1))()
+    kinds = (C.c_int32 * cap)()
+    _check(lib().spk_gpu_plan(n, kl, ku, nrhs, int(pivoting), p, cap, C.byref(pp), bounds, kinds))
+    return PartitionPlan(p=pp.value, bounds=list(bounds[:pp.value + 1]),
+                         kinds=[PartitionKind(kinds[i]) for i in range(pp.value)],
+                         threads_used=pp.value, idle_threads=0)
+
+
+# ----------------------------------------------------------------------------
+# factorization (factorize.hpp)
+
+
+@dataclass
+class FactorOptions:
+    pivoting: bool = False
+    boost_eps: float = field(default_factory=default_boost_eps)
+
+
+class _Coupling:
+    """Factored 2k coupling block of one reduced pair (LUFactors::dense)."""
+
+    def __init__(self, lu: np.ndarray, piv: np.ndarray, fell_back: bool):
+        self.lu, self.piv, self.fell_back = lu, piv, fell_back
+
+    def pivoting(self):
+        return not self.fell_back
+
+    def uval(self, i, j):
+        return float(self.lu[i, j]) if i <= j else 0.0
+
+    def lval(self, i, j):
+        if i == j:
+            return 1.0
+        return float(self.lu[i, j]) if i > j else 0.0
+
+
+class ReducedLevels:
+    """Recursive reduced-system hierarchy (factorize.hpp:26-49), device resident."""
+
+    def __init__(self, owner, handle, p, k, standalone):
+        self._owner = owner          # keeps the device object alive
+        self._h = handle
+        self.p, self.k = p, k
+        self._standalone = standalone
+        self._v = self._w = self._pairs = None
+
+    def levels(self) -> int:
+        if self._standalone:
+            return int(lib().spk_reduced_levels(self._h))
+        lv = C.c_int32()
+        _check(lib().spk_fact_info(self._h, None, None, None, None, None, C.byref(lv), None, None))
+        return lv.value
+
+    def unit_rows(self, level):
+        return (2 * self.k) << level
+
+    @property
+    def boost_warnings(self) -> int:
+        if self._standalone:
+            return int(lib().spk_reduced_boost_warnings(self._h))
+        bw = C.c_int32()
+        _check(lib().spk_fact_info(self._h, None, None, None, None, None, None, None, C.byref(bw)))
+        return bw.value
+
+    def _spikes(self, which):
+        if self._standalone:
+            raise SpikeError("spike columns of a standalone reduce_factorize are not mirrored")
+        out = []
+        for l in range(self.levels()):
+            units = lib().spk_fact_units(self._h, l)
+            row = []
+            for u in range(units):
+                h = C.c_int32()
+                _check(lib().spk_fact_level_spike(self._h, l, which, u, C.byref(h), None))
+                buf = np.zeros(h.value * self.k)
+                _check(lib().spk_fact_level_spike(self._h, l, which, u, C.byref(h),
+                                                  buf.ctypes.data_as(_dp)))
+                row.append(buf.reshape(self.k, h.value).T.copy(order="F"))
+            out.append(row)
+        return out
+
+    @property
+    def v(self):
+        if self._v is None:
+            self._v = self._spikes(0)
+        return self._v
+
+    @property
+    def w(self):
+        if self._w is None:
+            self._w = self._spikes(1)
+        return self._w
+
+    @property
+    def pairs(self):
+        if self._pairs is None:
+            if self._standalone:
+                raise SpikeError("coupling blocks of a standalone reduce_factorize are not mirrored")
+            out = []
+            nn = 2 * self.k
+            for l in range(self.levels()):
+                units = lib().spk_fact_units(self._h, l)
+                row = []
+                for a in range(units // 2):
+                    lu = np.zeros(nn * nn)
+                    piv = np.zeros(nn, dtype=np.int32)
+                    fb = C.c_int32()
+                    _check(lib().spk_fact_coupling(self._h, l, a, lu.ctypes.data_as(_dp),
+                                                   piv.ctypes.data_as(_i32p), C.byref(fb)))
+                    row.append(_Coupling(lu.reshape(nn, nn).T.copy(), piv, bool(fb.value)))
+                out.append(row)
+            self._pairs = out
+        return self._pairs
+
+
+class _StandaloneReduced:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().spk_reduced_destroy(self.h)
+        except Exception:
+            pass
+
+
+class SpikeFactorization:
+    """Immutable device-resident SPIKE DS factorization (factorize.hpp:56-74).
+    Host mirrors of the tips are fetched on first access."""
+
+    def __init__(self, handle, plan: PartitionPlan, n, kl, ku, options: FactorOptions):
+        self._h = handle
+        self.plan = plan
+        self.n, self.kl, self.ku = n, kl, ku
+        self.k = max(kl, ku)
+        self.options = options
+        self._tips = {}
+        info = [C.c_int32() for _ in range(3)]
+        _check(lib().spk_fact_info(handle, None, None, None, None, None, C.byref(info[0]),
+                                   C.byref(info[1]), C.byref(info[2])))
+        self.boost_count = info[1].value
+        sw = (C.c_int64 * plan.p)()
+        _check(lib().spk_fact_factor_sweeps(handle, sw))
+        self.factor_sweeps = [int(x) for x in sw]
+        self.levels = ReducedLevels(self, handle, plan.p, self.k, standalone=False)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().spk_fact_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def p(self):
+        return self.plan.p
+
+    def is_dual(self, i):
+        return self.plan.kinds[i] == PartitionKind.InnerDual
+
+    def _tipset(self, which):
+        if which not in self._tips:
+            k = self.k
+            out = []
+            for i in range(self.plan.p):
+                buf = np.zeros(k * k)
+                _check(lib().spk_fact_tip(self._h, which, i, buf.ctypes.data_as(_dp)))
+                out.append(buf.reshape(k, k).T.copy(order="F"))
+            self._tips[which] = out
+        return self._tips[which]
+
+    vt = property(lambda self: self._tipset(0))
+    vb = property(lambda self: self._tipset(1))
+    wt = property(lambda self: self._tipset(2))
+    wb = property(lambda self: self._tipset(3))
+    bhat = property(lambda self: self._tipset(4))
+    chat = property(lambda self: self._tipset(5))
+
+
+def _plan_struct(plan: PartitionPlan):
+    b = np.ascontiguousarray(plan.bounds, dtype=np.int64)
+    k = np.ascontiguousarray([int(x) for x in plan.kinds] or [0] * plan.p, dtype=np.int32)
+    st = _Plan(plan.p, b.ctypes.data_as(_i64p), k.ctypes.data_as(_i32p))
+    return st, (b, k)
+
+
+def factorize(a: BandedMatrix, plan: PartitionPlan, opts: Optional[FactorOptions] = None,
+              stream: int = 0) -> SpikeFactorization:
+    """spike::factorize (factorize.hpp:76-77) on the GPU."""
+    opts = opts or FactorOptions()
+    if plan.n() != a.n:
+        raise InvalidArgument("factorize: plan does not match matrix")
+    st, keep = _plan_struct(plan)
+    o = _Opts(int(bool(opts.pivoting)), float(opts.boost_eps))
+    h = C.c_void_p()
+    _check(lib().spk_factorize(a.data.ctypes.data, 0, a.n, a.kl, a.ku, C.byref(st), C.byref(o), stream,
+                               C.byref(h)))
+    return SpikeFactorization(h.value, plan, a.n, a.kl, a.ku, opts)
+
+
+def factorize_device(band_ptr: int, n: int, kl: int, ku: int, plan: PartitionPlan,
+                     opts: Optional[FactorOptions] = None, stream: int = 0) -> SpikeFactorization:
+    """Factorize a band already resident in HBM (device pointer, (kl+ku+1) x n column-major)."""
+    opts = opts or FactorOptions()
+    st, keep = _plan_struct(plan)
+    o = _Opts(int(bool(opts.pivoting)), float(opts.boost_eps))
+    h = C.c_void_p()
+    _check(lib().spk_factorize(C.c_void_p(band_ptr), 1, n, kl, ku, C.byref(st), C.byref(o), stream,
+                               C.byref(h)))
+    return SpikeFactorization(h.value, plan, n, kl, ku, opts)
+
+
+# ----------------------------------------------------------------------------
+# solves (solve.hpp)
+
+
+@dataclass
+class SolveStats:
+    partition_full_sweeps: List[int] = field(default_factory=list)
+    reduced_coupling_solves: int = 0
+
+    def total_full_sweeps(self):
+        return sum(self.partition_full_sweeps)
+
+
+def _solve(fact: SpikeFactorization, f, transpose: bool, stats: Optional[SolveStats]):
+    f = _as_block(f)
+    if f.shape[0] != fact.n:
+        raise InvalidArgument(("transpose_solve" if transpose else "solve") + ": F.rows must equal n")
+    nrhs = f.shape[1]
+    x = np.zeros((fact.n, nrhs), order="F")
+    sw = (C.c_int64 * fact.plan.p)()
+    st = _Stats(C.cast(sw, _i64p), 0)
+    if nrhs == 0:
+        _check(lib().spk_solve(fact._h, int(transpose), None, fact.n, 0, None, fact.n, 0, None, C.byref(st)))
+    else:
+        _check(lib().spk_solve(fact._h, int(transpose), f.ctypes.data, fact.n, nrhs, x.ctypes.data, fact.n,
+                               0, None, C.byref(st)))
+    if stats is not None:
+        stats.partition_full_sweeps = [int(v) for v in sw]
+        stats.reduced_coupling_solves = int(st.reduced_coupling_solves)
+    return x
+
+
+def solve(fact: SpikeFactorization, f, stats: Optional[SolveStats] = None) -> np.ndarray:
+    """A X = F on the GPU (solve.hpp:23-24); F is n x nrhs."""
+    return _solve(fact, f, False, stats)
+
+
+def transpose_solve(fact: SpikeFactorization, f, stats: Optional[SolveStats] = None) -> np.ndarray:
+    """A^T X = F reusing the same factorization (solve.hpp:28-29)."""
+    return _solve(fact, f, True, stats)
+
+
+def solve_device(fact: SpikeFactorization, f_ptr: int, ldf: int, nrhs: int, x_ptr: int, ldx: int,
+                 transpose: bool = False, stream: int = 0) -> None:
+    """Device-resident solve: F and X are HBM pointers (column-major)."""
+    _check(lib().spk_solve(fact._h, int(transpose), C.c_void_p(f_ptr), ldf, nrhs, C.c_void_p(x_ptr), ldx, 1,
+                           stream, None))
+
+
+def reduce_factorize(vt, vb, wt, wb, p: int, k: int, boost_eps: Optional[float] = None,
+                     threads: int = 1) -> ReducedLevels:
+    """reduce_factorize (factorize.hpp:45-49); any p >= 1 on the GPU."""
+    def pack(blocks):
+        arr = np.zeros((p, k, k))
+        for i, b in enumerate(blocks[:p]):
+            b = np.asarray(b, dtype=np.float64)
+            if b.size:
+                arr[i] = b.T  # column-major k x k
+        return np.ascontiguousarray(arr)
+    arrs = [pack(x) for x in (vt, vb, wt, wb)]
+    h = C.c_void_p()
+    _check(lib().spk_reduced_create(*[a.ctypes.data_as(_dp) for a in arrs], p, k,
+                                    boost_eps if boost_eps else default_boost_eps(), C.byref(h)))
+    owner = _StandaloneReduced(h.value)
+    return ReducedLevels(owner, h.value, p, k, standalone=True)
+
+
+def _reduced(levels: ReducedLevels, y, transpose, coupling_solves):
+    y = _as_block(y)
+    if y.shape[0] != 2 * levels.p * levels.k:
+        raise InvalidArgument(("reduced_solve_transpose" if transpose else "reduced_solve") +
+                              ": tip block has wrong height")
+    z = y.copy(order="F")
+    cnt = C.c_int64(0)
+    if not levels._standalone:
+        raise SpikeError("reduced_solve on a factorization's levels: use solve()")
+    _check(lib().spk_reduced_solve(levels._h, int(transpose), z.ctypes.data_as(_dp), z.shape[1], C.byref(cnt)))
+    if coupling_solves is not None:
+        coupling_solves.append(int(cnt.value))
+    return z
+
+
+def reduced_solve(levels: ReducedLevels, ytips, coupling_solves: Optional[list] = None, threads: int = 1):
+    return _reduced(levels, ytips, False, coupling_solves)
+
+
+def reduced_solve_transpose(levels: ReducedLevels, gtips, coupling_solves: Optional[list] = None,
+                            threads: int = 1):
+    return _reduced(levels, gtips, True, coupling_solves)
+
+
+# ----------------------------------------------------------------------------
+# band ops (band_ops.hpp) on the GPU
+
+
+def band_matmul(a: BandedMatrix, x, transpose: bool = False) -> np.ndarray:
+    x = _as_block(x)
+    if x.shape[0] != a.n:
+        raise InvalidArgument("band_matmul: X.rows must equal n")
+    y = np.zeros_like(x, order="F")
+    if x.shape[1]:
+        _check(lib().spk_band_matmul(a.data.ctypes.data, a.n, a.kl, a.ku, x.ctypes.data, a.n, x.shape[1],
+                                     int(transpose), y.ctypes.data, a.n, 0, None))
+    return y
+
+
+def frobenius_norm(b) -> float:
+    return float(np.sqrt(np.sum(np.square(np.asarray(b, dtype=np.float64)))))
+
+
+def relative_residual(a: BandedMatrix, x, f, transpose: bool = False) -> float:
+    """||A X - F||_F / ||F||_F (band_ops.cpp:45-57); A X on the GPU."""
+    x, f = _as_block(x), _as_block(f)
+    if x.shape[0] != a.n or f.shape[0] != a.n or x.shape[1] != f.shape[1]:
+        raise InvalidArgument("relative_residual: inconsistent shapes")
+    fn = frobenius_norm(f)
+    if fn == 0.0:
+        if frobenius_norm(x) == 0.0:
+            return 0.0
+        raise DomainError("relative_residual: F is zero but X is not")
+    r = band_matmul(a, x, transpose) - f
+    return frobenius_norm(r) / fn
+
+
+def norm1(a: BandedMatrix) -> float:
+    return float(np.abs(a.data).sum(axis=1).max())
+
+
+def max_abs(a: BandedMatrix) -> float:
+    return float(np.abs(a.data).max())
+
+
+@dataclass
+class RefineResult:
+    x: np.ndarray
+    iterations: int = 0
+    residual: float = 0.0
+    converged: bool = False
+    stagnated: bool = False
+
+
+def iterative_refine(fact: SpikeFactorization, a: BandedMatrix, f, x0, max_iters: int, tol: float,
+                     transpose: bool = False) -> RefineResult:
+    """Residual-correction refinement (solve.cpp:404-432): residual A x on the GPU,
+    correction solve on the GPU factorization."""
+    f = _as_block(f)
+    res = RefineResult(x=_as_block(x0).copy(order="F"))
+    fnorm = frobenius_norm(f)
+    prev = math.inf
+    for it in range(max_iters + 1):
+        r = f - band_matmul(a, res.x, transpose)
+        rn = frobenius_norm(r)
+        res.residual = (0.0 if rn == 0.0 else math.inf) if fnorm == 0.0 else rn / fnorm
+        res.iterations = it
+        if res.residual <= tol:
+            res.converged = True
+            return res
+        if it > 0 and res.residual * 1.1 > prev:
+            res.stagnated = True
+            return res
+        if it == max_iters:
+            return res
+        prev = res.residual
+        d = transpose_solve(fact, r) if transpose else solve(fact, r)
+        res.x = res.x + d
+    return res
+
+
+# ----------------------------------------------------------------------------
+# device-side input generation (include/spike_b200_gen.h)
+
+
+def generate_band_device(seed: int, n: int, kl: int, ku: int, dd: float, band_ptr: int, stream: int = 0):
+    _check(lib().spk_generate_band(seed, n, kl, ku, dd, C.c_void_p(band_ptr), stream))
+
+
+def generate_rhs_device(seed: int, n: int, ncols: int, f_ptr: int, ldf: int, stream: int = 0):
+    _check(lib().spk_generate_rhs(seed, n, ncols, C.c_void_p(f_ptr), ldf, stream))
