@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 recursive SPIKE factor + solve (+ transpose solve) on B200.
+
+Default workload = BASELINE.json's metric config (configs[2], "C3"):
+n=1,000,000, kl=ku=160, nrhs=160, dd=1.5, non-pivoting, one factorization
+serving A X = F and A^T X = F.  One step = spk_factorize + spk_solve +
+spk_solve(transpose) over the whole system; the metric is fp64 GFLOP/s of the
+SPIKE-algorithmic work (factor 8nk^2, each solve 8nk*nrhs),
+higher is better, with time per step beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl ours|reference]
+
+Inputs are seeded synthetic data (include/spike_b200_gen.h), generated in HBM
+for the device-resident `value`, and in pinned host memory for `e2e`, which
+goes through the public C-ABI with host buffers (copies inside the timed
+region).  The CPU checkers/baselines under oracle/ are only used for the
+`cpu_baseline` object (rank 0, N=1) and the `--impl reference` arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(n=100_000, k=16, nrhs=1, dd=2.0, piv=False, transpose=False, bound="hbm",
+               desc="C1 n=1e5 kl=ku=16 nrhs=1 dd=2.0 non-pivoting"),
+    "c2": dict(n=1_000_000, k=64, nrhs=1, dd=1.1, piv=False, transpose=False, bound="fp64",
+               desc="C2 n=1e6 kl=ku=64 nrhs=1 dd=1.1 non-pivoting"),
+    "c3": dict(n=1_000_000, k=160, nrhs=160, dd=1.5, piv=False, transpose=True, bound="fp64",
+               desc="C3 n=1e6 kl=ku=160 nrhs=160 dd=1.5 non-pivoting, solve + transpose solve"),
+    "c4": dict(n=1_000_000, k=64, nrhs=4, dd=-1.0, piv=True, transpose=False, bound="fp64",
+               desc="C4 n=1e6 kl=ku=64 nrhs=4 no dominance, partial pivoting"),
+    "c5": dict(n=16_000_000, k=128, nrhs=32, dd=1.2, piv=False, transpose=False, bound="fp64",
+               desc="C5 n=16e6 kl=ku=128 nrhs=32 dd=1.2 non-pivoting"),
+}
+SEED_A = 20181108
+HBM_PEAK_FALLBACK = 6650.0
+FP64_PEAK_MEASURED = 37.1  # TFLOP/s, tools/fp64_peak.cu on this pool's B200 (DMMA 37.1, DFMA 36.9)
+
+
+def alg_flops(cfg):
+    n, k, r = cfg["n"], cfg["k"], cfg["nrhs"]
+    fac = (14.0 if cfg["piv"] else 8.0) * n * k * k
+    sol = (12.0 if cfg["piv"] else 8.0) * n * k * r
+    useful_fac = (4.0 if cfg["piv"] else 2.0) * n * k * k
+    useful_sol = (6.0 if cfg["piv"] else 4.0) * n * k * r
+    nsol = 2 if cfg["transpose"] else 1
+    return fac + nsol * sol, useful_fac + nsol * useful_sol
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# reference CPU arm (the compiled unmodified reference library, oracle/_ref)
+
+
+def _ref_libs():
+    from oracle.oracle import Oracle, Reference, build as obuild
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        obuild(with_ref=False)
+    ref = Reference.load()
+    return Oracle(), ref
+
+
+def reference_step_sample(cfg, target_s=8.0, t=None, calib=None):
+    """Pick a row count so one reference factor+solve(s) step takes ~target_s."""
+    o, ref = _ref_libs()
+    t = t or os.cpu_count()
+    k, nrhs = cfg["k"], cfg["nrhs"]
+    n0 = calib or max(40 * (2 * k + 1) * 4, 20000)
+    n0 = min(n0, cfg["n"])
+    band = o.generate_band(SEED_A, n0, k, k, cfg["dd"])
+    F = o.generate_rhs(SEED_A + 1, n0, nrhs)
+    r = ref.time_path(band, n0, k, k, F, t, 1.0, cfg["piv"], cfg["transpose"])
+    per_row = (r["factor"] + r["solve"] + r["tsolve"]) / n0
+    n_s = int(min(cfg["n"], max(n0, target_s / max(per_row, 1e-12))))
+    return n_s, t
+
+
+def run_reference_steps(cfg, n_s, t, steps):
+    o, ref = _ref_libs()
+    k, nrhs = cfg["k"], cfg["nrhs"]
+    band = o.generate_band(SEED_A, n_s, k, k, cfg["dd"])
+    F = o.generate_rhs(SEED_A + 1, n_s, nrhs)
+    times = []
+    p = None
+    for _ in range(steps):
+        r = ref.time_path(band, n_s, k, k, F, t, 1.0, cfg["piv"], cfg["transpose"])
+        times.append(r["factor"] + r["solve"] + r["tsolve"])
+        p = r["p"]
+    return times, p
+
+
+def impl_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle.oracle import Reference
+    if Reference.load() is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libspike_ref.so not built (reference sources absent at build time)"}))
+        return 0
+    budget = 150.0
+    target = max(1.0, min(10.0, budget / max(1, args.steps + args.warmup)))
+    n_s, t = reference_step_sample(cfg, target_s=target)
+    times, p = run_reference_steps(cfg, n_s, t, args.warmup + args.steps)
+    timed = times[args.warmup:]
+    sample_cfg = dict(cfg, n=n_s)
+    fl, useful = alg_flops(sample_cfg)
+    ms = 1e3 * sum(timed) / len(timed)
+    value = fl / (ms * 1e-3) / 1e9
+    sample = f"n={n_s} of {cfg['n']} rows, same k/nrhs/dd; make_plan(t={t}) -> p={p}; factorize+solve" + \
+             ("+transpose_solve" if cfg["transpose"] else "")
+    line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h)",
+            "config": {"workload": cfg["desc"], "sample_rows": n_s, "threads": t},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": t, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# our arm
+
+
+def impl_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    import paper_1811_03559_b200 as spk
+    from paper_1811_03559_b200 import build as pbuild
+    if not os.path.exists(spk.LIB_PATH):
+        pbuild.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    n, k, nrhs = cfg["n"], cfg["k"], cfg["nrhs"]
+    ld = 2 * k + 1
+    band = torch.empty((n, ld), dtype=torch.float64, device=dev)
+    F = torch.empty((nrhs, n), dtype=torch.float64, device=dev)   # column-major n x nrhs
+    X = torch.empty_like(F)
+    XT = torch.empty_like(F)
+    spk.generate_band_device(SEED_A, n, k, k, cfg["dd"], band.data_ptr(), sptr)
+    spk.generate_rhs_device(SEED_A + 1, n, nrhs, F.data_ptr(), n, sptr)
+    plan = spk.gpu_plan(n, k, k, nrhs, cfg["piv"], args.p)
+    opts = spk.FactorOptions(pivoting=cfg["piv"])
+    L2_BYTES = 126 * 2 ** 20
+    flush = None
+    if band.numel() * 8 < 2 * L2_BYTES:
+        flush = torch.empty(64 * 2 ** 20, dtype=torch.float64, device=dev)  # 512 MB
+
+    def step():
+        fact = spk.factorize_device(band.data_ptr(), n, k, k, plan, opts, sptr)
+        spk.solve_device(fact, F.data_ptr(), n, nrhs, X.data_ptr(), n, False, sptr)
+        if cfg["transpose"]:
+            spk.solve_device(fact, F.data_ptr(), n, nrhs, XT.data_ptr(), n, True, sptr)
+        return fact
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on the benchmarked system: normwise backward error on device
+    fact = step()
+    R = torch.empty_like(F)
+    lib = spk.lib()
+    lib.spk_band_matmul(band.data_ptr(), n, k, k, X.data_ptr(), n, nrhs, 0, R.data_ptr(), n, 1, sptr)
+    anorm = band.abs().sum(dim=1).max().item()  # ||A||_1 (column sums) as the scale
+    berr = ((R - F).abs().amax(dim=1) / (anorm * X.abs().amax(dim=1))).max().item()
+    del fact, R
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    spk.lib().spk_launch_count(1)
+    spk.lib().spk_profile_reset()
+    spk.lib().spk_profile_enable(1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    spk.lib().spk_profile_enable(0)
+    launches = int(spk.lib().spk_launch_count(1))
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    fl, useful = alg_flops(cfg)
+    value = world * fl / (ms * 1e-3) / 1e9
+
+    # per-kernel-class device time inside the timed region
+    import ctypes as C
+    prof = {}
+    ncls = spk.lib().spk_profile_classes()
+    spk.lib().spk_profile_read.restype = C.c_char_p
+    spk.lib().spk_profile_read.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    for c in range(ncls):
+        a, b, d, e = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+        name = spk.lib().spk_profile_read(c, C.byref(a), C.byref(b), C.byref(d), C.byref(e)).decode()
+        if e.value:
+            prof[name] = dict(ms=a.value / args.steps, flops=b.value / args.steps, bytes=d.value / args.steps,
+                              launches=e.value // args.steps)
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", dict(ms=1, flops=0, bytes=0, launches=1))
+    peaks = measured_peaks()
+    bound = cfg["bound"]
+    tms = top[1]["ms"]
+    if bound == "hbm":
+        ach = top[1]["bytes"] / (tms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
+        unit = "GB/s"
+    else:
+        ach = top[1]["flops"] / (tms * 1e-3) / 1e12
+        peak = FP64_PEAK_MEASURED
+        unit = "TFLOP/s"
+    roofline = {"bound": bound, "kernel": top[0], "achieved": round(ach, 3), "peak": peak, "unit": unit,
+                "frac": round(ach / peak, 4), "traffic": None,
+                "kernel_share_of_step": round(tms / ms, 4),
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm"
+                                else "tools/fp64_peak.cu measured DMMA/DFMA peak on this pool (B200)"),
+                "classes": {kk: {"ms": round(v["ms"], 4), "launches": v["launches"]} for kk, v in prof.items()}}
+
+    # e2e through the public C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hband = band.cpu().pin_memory()
+        hF = F.cpu().pin_memory()
+        hX = torch.empty_like(hF).pin_memory()
+        hXT = torch.empty_like(hF).pin_memory()
+
+        def e2e_step():
+            fct = spk.lib()
+            h = spk.spike.C.c_void_p()
+            st, keep = spk.spike._plan_struct(plan)
+            o = spk.spike._Opts(int(cfg["piv"]), opts.boost_eps)
+            spk.spike._check(fct.spk_factorize(hband.data_ptr(), 0, n, k, k, spk.spike.C.byref(st),
+                                               spk.spike.C.byref(o), sptr, spk.spike.C.byref(h)))
+            spk.spike._check(fct.spk_solve(h, 0, hF.data_ptr(), n, nrhs, hX.data_ptr(), n, 0, sptr, None))
+            if cfg["transpose"]:
+                spk.spike._check(fct.spk_solve(h, 1, hF.data_ptr(), n, nrhs, hXT.data_ptr(), n, 0, sptr, None))
+            fct.spk_fact_destroy(h)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e_steps = max(1, min(args.steps, 5))
+        for _ in range(e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        ems = (time.perf_counter() - t0) * 1e3 / e_steps
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        nsol = 2 if cfg["transpose"] else 1
+        e2e = {"value": round(world * fl / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+               "ms_per_step": round(ems, 3),
+               "h2d_bytes_per_step": int(hband.numel() * 8 + nsol * hF.numel() * 8),
+               "d2h_bytes_per_step": int(nsol * hX.numel() * 8)}
+
+    # CPU baseline: the compiled reference on the box's host cores (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle.oracle import Reference
+            if Reference.load() is not None:
+                n_s, t = reference_step_sample(cfg, target_s=12.0)
+                times, p = run_reference_steps(cfg, n_s, t, 1)
+                fls, _ = alg_flops(dict(cfg, n=n_s))
+                cpu = {"value": round(fls / times[0] / 1e9, 3), "unit": "GFLOP/s", "cores": t,
+                       "kind": "reference",
+                       "sample": f"n={n_s} of {n} rows (same k/nrhs/dd), reference make_plan(t={t}) -> p={p}, "
+                                 f"one factorize+solve" + ("+transpose_solve" if cfg["transpose"] else "") +
+                                 f" step in {times[0]:.2f} s"}
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h; generated in HBM)",
+                "config": {"workload": cfg["desc"], "n": n, "kl": k, "ku": k, "nrhs": nrhs,
+                           "partitions": plan.p, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                           "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
+                "useful_gflops": round(world * useful / (ms * 1e-3) / 1e9, 3),
+                "backward_error": berr,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "impl": "ours"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p", type=int, default=0, help="force the partition count")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    args.metric = "fp64 factor+solve GFLOP/s (SPIKE-algorithmic flops), " + CONFIGS[args.config]["desc"]
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return impl_reference(args, cfg)
+    return impl_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

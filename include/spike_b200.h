@@ -153,6 +153,14 @@ spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double *d_F
  * since the last reset (instrumentation for bench.py's gpu_launches). */
 int64_t spk_launch_count(int32_t reset);
 
+/* Optional per-kernel-class CUDA-event timing (calling thread): launches are
+ * bracketed by events on their stream; spk_profile_read drains and returns
+ * accumulated device time, algorithmic flops and bytes per class. */
+void spk_profile_enable(int32_t on);
+int32_t spk_profile_classes(void);
+const char *spk_profile_read(int32_t cls, double *ms, double *flops, double *bytes, int64_t *launches);
+void spk_profile_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

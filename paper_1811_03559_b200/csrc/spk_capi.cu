@@ -69,6 +69,75 @@ void count_launch(int n) { g_launches += n; }
 }  // namespace spk
 
 // ---------------------------------------------------------------------------
+// optional per-kernel-class CUDA-event profiling (bench.py roofline):
+// events are recorded on the launching stream around each stage launch.
+namespace {
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double flops, bytes;
+};
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfRec> g_prof;
+thread_local std::vector<cudaEvent_t> g_evpool;
+constexpr int kNumClasses = 10;
+const char* kClassName[kNumClasses] = {"sweep",     "copy",      "gemm", "band_lu", "coupling",
+                                       "memset",    "memcpy_fx", "memcpy_fs", "fill_factors", "corners"};
+enum { PC_FILL = 8, PC_CORNERS = 9 };
+struct ProfAcc {
+    double ms = 0, flops = 0, bytes = 0;
+    long long launches = 0;
+};
+thread_local ProfAcc g_acc[kNumClasses];
+
+cudaEvent_t prof_event() {
+    if (!g_evpool.empty()) {
+        cudaEvent_t e = g_evpool.back();
+        g_evpool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    bool on;
+    ProfRec r;
+    cudaStream_t s;
+    ProfScope(int cls, cudaStream_t st, double flops, double bytes) : on(g_prof_on), s(st) {
+        if (!on) return;
+        r.a = prof_event();
+        r.b = prof_event();
+        r.cls = cls;
+        r.flops = flops;
+        r.bytes = bytes;
+        cudaEventRecord(r.a, s);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.b, s);
+        g_prof.push_back(r);
+    }
+};
+
+void prof_drain() {
+    for (ProfRec& r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        g_acc[r.cls].ms += ms;
+        g_acc[r.cls].flops += r.flops;
+        g_acc[r.cls].bytes += r.bytes;
+        g_acc[r.cls].launches += 1;
+        g_evpool.push_back(r.a);
+        g_evpool.push_back(r.b);
+    }
+    g_prof.clear();
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // programs
 namespace {
 
@@ -83,6 +152,8 @@ struct Stage {
     int max_r = 0;
     int buf = 0;  // memset target
     int cols = -1;  // memset columns (-1: call columns)
+    // algorithmic work per call column (explicit-column stages: per launch)
+    double flops_per_col = 0.0, bytes_per_col = 0.0;
 };
 
 struct ProgramBuilder {
@@ -147,9 +218,11 @@ struct spk_fact {
     cudaStream_t stream = nullptr;
 
     ~spk_fact() {
+        // stream-ordered release on the factorization's stream (which must
+        // outlive it); no device-wide synchronisation
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob})
-            if (q) cudaFree(q);
+            if (q) cudaFreeAsync(q, stream);
     }
 };
 
@@ -263,7 +336,15 @@ struct Builder {
         s.njobs = (int)jobs.size();
         s.off = pb.push(jobs);
         int mx = 0;
-        for (auto& j : jobs) mx = j.nc < 0 ? -1 : (mx < 0 ? -1 : std::max(mx, j.nc));
+        for (auto& j : jobs) {
+            mx = j.nc < 0 ? -1 : (mx < 0 ? -1 : std::max(mx, j.nc));
+            const PartDev& P = f.parts[j.part];
+            const double rows = (j.mode == SW_BWD_U) ? (j.hi - j.lo + 1) : (P.m - j.lo);
+            const double bw = (j.mode == SW_FWD_L || j.mode == SW_BWD_LT) ? P.kl : P.ubw;
+            const double nc = j.nc < 0 ? 1.0 : j.nc;
+            s.flops_per_col += 2.0 * rows * bw * nc;
+            s.bytes_per_col += 8.0 * rows * (bw + 1) + 16.0 * rows * nc;
+        }
         s.max_nc = mx;
         prog.push_back(s);
     }
@@ -280,6 +361,7 @@ struct Builder {
         }
         s.max_elems = mx;
         s.max_nc = mnc;
+        for (auto& j : jobs) s.bytes_per_col += 16.0 * (j.L1 - j.L0) * (j.nc < 0 ? 1.0 : j.nc);
         prog.push_back(s);
     }
     void gemm(const std::vector<GemmJob>& jobs) {
@@ -294,6 +376,11 @@ struct Builder {
         }
         s.max_r = mr;
         s.max_nc = mnc;
+        for (auto& j : jobs) {
+            const double nc = j.nc < 0 ? 1.0 : j.nc;
+            s.flops_per_col += 2.0 * j.r * j.kk * nc;
+            s.bytes_per_col += 8.0 * (j.r * j.kk + (j.kk + 2.0 * j.r) * nc);
+        }
         prog.push_back(s);
     }
     void lu(const std::vector<int>& units) {
@@ -301,6 +388,11 @@ struct Builder {
         Stage s{ST_LU};
         s.njobs = (int)units.size();
         s.off = pb.push(units);
+        for (int u : units) {
+            const PartDev& P = f.parts[u];
+            s.flops_per_col += 2.0 * P.m * P.kl * P.ubw;
+            s.bytes_per_col += 16.0 * P.m * P.rows;
+        }
         prog.push_back(s);
     }
     void cpl(const std::vector<CouplingJob>& jobs) {
@@ -767,6 +859,8 @@ struct Exec {
     void run(const Program& prog) {
         for (const Stage& st : prog) {
             const char* jobs = f.d_blob + st.off;
+            const double mult = st.max_nc < 0 ? ncols : 1.0;
+            ProfScope ps((int)st.t, s, st.flops_per_col * mult, st.bytes_per_col * mult);
             switch (st.t) {
                 case ST_SWEEP: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
@@ -951,6 +1045,27 @@ extern "C" {
 const char* spk_last_error(void) { return g_err.c_str(); }
 const char* spk_version(void) { return "spike_b200 0.1 (sm_100a)"; }
 
+void spk_profile_enable(int32_t on) { g_prof_on = on != 0; }
+
+int32_t spk_profile_classes(void) { return kNumClasses; }
+
+/* Drains pending events (synchronising on them) and returns the accumulated
+ * per-class totals since the last reset. */
+const char* spk_profile_read(int32_t cls, double* ms, double* flops, double* bytes, int64_t* launches) {
+    prof_drain();
+    if (cls < 0 || cls >= kNumClasses) return nullptr;
+    if (ms) *ms = g_acc[cls].ms;
+    if (flops) *flops = g_acc[cls].flops;
+    if (bytes) *bytes = g_acc[cls].bytes;
+    if (launches) *launches = g_acc[cls].launches;
+    return kClassName[cls];
+}
+
+void spk_profile_reset(void) {
+    prof_drain();
+    for (auto& a : g_acc) a = ProfAcc{};
+}
+
 int64_t spk_launch_count(int32_t reset) {
     const long long v = g_launches;
     if (reset) g_launches = 0;
@@ -1087,12 +1202,21 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
         if (pp > 1) w.front() = w.back() = r13;
         double tot = 0.0;
         for (double x : w) tot += x;
-        bounds[0] = 0;
-        long long acc = 0;
-        for (int i = 0; i < pp; ++i) {
-            long long sz = (i == pp - 1) ? n - acc : (long long)std::llround(n * w[i] / tot);
-            acc += sz;
-            bounds[i + 1] = acc;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (attempt == 1) {  // weighted sizes undercut the minimum: equal sizes
+                std::fill(w.begin(), w.end(), 1.0);
+                tot = pp;
+            }
+            bounds[0] = 0;
+            long long acc = 0;
+            bool ok = true;
+            for (int i = 0; i < pp; ++i) {
+                long long sz = (i == pp - 1) ? n - acc : (long long)std::llround(n * w[i] / tot);
+                acc += sz;
+                bounds[i + 1] = acc;
+                ok = ok && (sz >= min_part || pp == 1);
+            }
+            if (ok) break;
         }
         for (int i = 0; i < pp; ++i) {
             if (bounds[i + 1] - bounds[i] < min_part && pp > 1) fail(SPK_EDOMAIN, "gpu_plan: partition too small");
@@ -1135,8 +1259,17 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         const int p = f->p;
         long long max_elems = 0;
         for (int i = 0; i < p; ++i) max_elems = std::max(max_elems, (long long)f->parts[i].m * f->parts[i].rows);
-        launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_amax, s);
-        launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->d_pool + f->off_bhat, f->d_pool + f->off_chat, s);
+        {
+            double bytes = 0;
+            for (int i = 0; i < p; ++i) bytes += 8.0 * f->parts[i].m * (f->parts[i].rows + ld);
+            ProfScope ps(PC_FILL, s, 0.0, bytes);
+            launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_amax, s);
+        }
+        {
+            ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);
+            launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->d_pool + f->off_bhat,
+                           f->d_pool + f->off_chat, s);
+        }
         double* fs = nullptr;
         double* auxf = nullptr;
         if (p > 1 && f->k > 0) {
