@@ -9,6 +9,7 @@
 // so a solve issues O(stages + reduced levels) launches independent of p.
 #include "../../include/spike_b200.h"
 #include "spk_launch.h"
+#include "spk_sweep_fast.cuh"
 
 #include <cuda_runtime.h>
 
@@ -141,7 +142,7 @@ void prof_drain() {
 // programs
 namespace {
 
-enum StageType { ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS };
+enum StageType { ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS, ST_TRANSPOSE };
 
 struct Stage {
     StageType t;
@@ -154,6 +155,10 @@ struct Stage {
     int cols = -1;  // memset columns (-1: call columns)
     // algorithmic work per call column (explicit-column stages: per launch)
     double flops_per_col = 0.0, bytes_per_col = 0.0;
+    // sweeps: register-window fast path (spk_sweep_fast.cuh) when every job is
+    // a SPIKE partition it supports
+    bool fast = false;
+    int mode = 0, kwmax = 0, tr = 0, piv = 0;
 };
 
 struct ProgramBuilder {
@@ -212,6 +217,9 @@ struct spk_fact {
     int* d_fell = nullptr;
     int* d_status = nullptr;
     char* d_blob = nullptr;
+    double* d_tfac = nullptr;
+    double* d_dinv = nullptr;
+    long long tfac_size = 0;
     Program prog_factor, prog_fwd, prog_tr;
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
@@ -221,7 +229,8 @@ struct spk_fact {
         // stream-ordered release on the factorization's stream (which must
         // outlive it); no device-wide synchronisation
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
-                        (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob})
+                        (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
+                        (void*)d_tfac, (void*)d_dinv})
             if (q) cudaFreeAsync(q, stream);
     }
 };
@@ -247,6 +256,8 @@ PartDev make_part(long long r0, int m, int akl, int aku, int piv_on, int rev, in
     P.rows = P.ubw + P.kl + 1;
     P.trunc = std::max(0, m - kcorner - (piv_on ? P.kl : 0));
     P.bofs = -1;
+    P.tofs = -1;
+    P.rowsT = 0;
     return P;
 }
 
@@ -346,8 +357,29 @@ struct Builder {
             s.bytes_per_col += 8.0 * rows * (bw + 1) + 16.0 * rows * nc;
         }
         s.max_nc = mx;
+        // fast-path eligibility
+        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
+        bool fast = !generic_only && !f.reduced_only;
+        int kwneed = 1, kwmax = 1;
+        for (auto& j : jobs) {
+            const PartDev& P = f.parts[j.part];
+            if (j.part >= f.p) fast = false;
+            if (j.mode == SW_BWD_LT && P.pivoting) fast = false;
+            if (j.mode != jobs[0].mode) fast = false;
+            const int kw = (j.mode == SW_FWD_L || j.mode == SW_BWD_LT) ? P.kl : P.ubw;
+            kwmax = std::max(kwmax, kw);
+            kwneed = std::max(kwneed, (j.mode == SW_FWD_L && P.pivoting) ? P.kl + 1 : kw);
+        }
+        const int tr = (kwneed + 31) / 32;
+        if (tr > 8) fast = false;
+        s.fast = fast;
+        s.mode = jobs[0].mode;
+        s.kwmax = kwmax;
+        s.tr = tr;
+        s.piv = f.piv_on && jobs[0].mode == SW_FWD_L;
         prog.push_back(s);
     }
+    void transpose_factors() { prog.push_back(Stage{ST_TRANSPOSE}); }
     void copy(const std::vector<CopyJob>& jobs) {
         if (jobs.empty()) return;
         Stage s{ST_COPY};
@@ -516,6 +548,7 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
         std::vector<int> units(p);
         for (int i = 0; i < p; ++i) units[i] = i;
         b.lu(units);  // preceded at run time by fill_factors
+        b.transpose_factors();
     }
     if (p < 2 || k == 0) return;
     if (!f.reduced_only) {
@@ -856,6 +889,31 @@ struct Exec {
     const double* F = nullptr;
     long long ldf = 0, n = 0;
 
+    bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
+        if (nc <= 0) return true;
+        int NC, nw;
+        if (nc >= 64) {
+            NC = 4;
+            nw = std::min(20, (nc + 3) / 4);
+        } else if (nc >= 8) {
+            NC = 2;
+            nw = std::min(16, (nc + 1) / 2);
+        } else {
+            NC = 1;
+            nw = nc;
+        }
+        const dim3 grid(st.njobs, (nc + nw * NC - 1) / (nw * NC));
+        const size_t smem = fast_sweep_smem(st.kwmax, nw, NC);
+        if (smem > 227 * 1024) return false;
+        FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
+        switch (st.mode) {
+            case SW_FWD_L: return launch_sweep_fast_fl(st.tr, NC, st.piv, nw, grid, smem, A, s);
+            case SW_BWD_U: return launch_sweep_fast_bu(st.tr, NC, false, nw, grid, smem, A, s);
+            case SW_FWD_UT: return launch_sweep_fast_fut(st.tr, NC, false, nw, grid, smem, A, s);
+            default: return launch_sweep_fast_blt(st.tr, NC, false, nw, grid, smem, A, s);
+        }
+    }
+
     void run(const Program& prog) {
         for (const Stage& st : prog) {
             const char* jobs = f.d_blob + st.off;
@@ -864,8 +922,15 @@ struct Exec {
             switch (st.t) {
                 case ST_SWEEP: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
+                    if (st.fast && run_fast_sweep(st, (const SweepJob*)jobs, nc)) break;
                     launch_sweep((const SweepJob*)jobs, st.njobs, nc, f.d_parts, f.d_fac, f.d_piv, B,
                                  ncols, s);
+                    break;
+                }
+                case ST_TRANSPOSE: {
+                    long long mx = 0;
+                    for (int i = 0; i < f.p; ++i) mx = std::max(mx, (long long)f.parts[i].m * f.parts[i].rowsT);
+                    launch_transpose_factors(f.d_parts, f.p, mx, f.d_fac, f.d_tfac, f.d_dinv, s);
                     break;
                 }
                 case ST_COPY: {
@@ -884,7 +949,7 @@ struct Exec {
                     break;
                 case ST_CPL:
                     launch_build_coupling((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts,
-                                          f.d_pool, f.d_fac, f.d_amax, s);
+                                          f.d_pool, f.d_fac, f.d_piv, f.d_amax, s);
                     break;
                 case ST_MEMSET: {
                     const int nc = st.cols < 0 ? ncols : st.cols;
@@ -944,6 +1009,9 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
             PartDev P = make_part(f.bounds[i], m, f.kl, f.ku, f.piv_on, rev, k);
             P.fofs = fac_cursor;
             fac_cursor += (long long)P.m * P.rows;
+            P.rowsT = P.kl + P.ubw + 1;
+            P.tofs = f.tfac_size;
+            f.tfac_size += (long long)P.m * P.rowsT;
             f.parts.push_back(P);
         }
         if (p > 1 && k > 0)
@@ -995,6 +1063,8 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     f.d_fell = dalloc<int>(nparts, s);
     f.d_status = dalloc<int>(1, s);
     f.d_blob = dalloc<char>(pb.blob.size(), s);
+    f.d_tfac = dalloc<double>(f.tfac_size, s);
+    f.d_dinv = dalloc<double>(f.n, s);
     ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
     ck(cudaMemcpyAsync(f.d_bounds, f.bounds.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s),
        "upload");
@@ -1263,7 +1333,7 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
             double bytes = 0;
             for (int i = 0; i < p; ++i) bytes += 8.0 * f->parts[i].m * (f->parts[i].rows + ld);
             ProfScope ps(PC_FILL, s, 0.0, bytes);
-            launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_amax, s);
+            launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_piv, f->d_amax, s);
         }
         {
             ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);

@@ -25,13 +25,14 @@ struct PartDev {
     long long r0;    // first system row (partitions) / unused (couplings)
     long long fofs;  // offset of the packed factor in the factor pool (doubles)
     long long bofs;  // offset of the backup copy (couplings; -1 if none)
+    long long tofs;  // offset of the row-major factor copy (partitions; -1 if none)
     int m;           // order
     int kl, ku, ubw, d, rows;
     int rev;         // factors of Q A_i Q (UL via reversed LU, kernels.cpp:51-62)
     int trunc;       // trunc_start (block_util.hpp:13-16)
     int pivoting;
     int fallback;    // pivoted-with-boosted-fallback (coupling blocks)
-    int pad;
+    int rowsT;       // row-major copy: row i holds (i, i-kl .. i+ubw) at [kl + c - i]
 };
 
 // Row-mapped view of a column-major buffer.  Logical row L maps to physical

@@ -39,8 +39,11 @@ __device__ __forceinline__ double warp_sum(double x) {
 // UL partition; per-partition max|entry| for the boost threshold.
 __global__ void k_fill_factors(const double* __restrict__ band, long long n, int akl, int aku,
                                const PartDev* __restrict__ parts, double* __restrict__ fac,
-                               unsigned long long* __restrict__ amax_bits) {
+                               int* __restrict__ piv_pool, unsigned long long* __restrict__ amax_bits) {
     const PartDev P = parts[blockIdx.y];
+    // identity pivots, so a unit whose LU aborts leaves no wild row indices
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.m; j += gridDim.x * blockDim.x)
+        piv_pool[P.r0 + j] = j;
     const long long total = (long long)P.m * P.rows;
     const int ald = akl + aku + 1;
     double lmax = 0.0;
@@ -371,10 +374,13 @@ __global__ void k_corners(const double* __restrict__ band, long long n, int akl,
 // pivoting storage rows = 4k-1, diagonal row 2k-1) plus backup and max|C|.
 __global__ void k_build_coupling(const CouplingJob* __restrict__ jobs,
                                  const PartDev* __restrict__ parts, const double* __restrict__ pool,
-                                 double* __restrict__ fac, unsigned long long* __restrict__ amax_bits) {
+                                 double* __restrict__ fac, int* __restrict__ piv_pool,
+                                 unsigned long long* __restrict__ amax_bits) {
     const CouplingJob J = jobs[blockIdx.y];
     const PartDev P = parts[J.part];
     const int k = J.k, nn = 2 * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nn; j += gridDim.x * blockDim.x)
+        piv_pool[P.r0 + j] = j;
     const long long total = (long long)P.m * P.rows;
     double lmax = 0.0;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -396,6 +402,27 @@ __global__ void k_build_coupling(const CouplingJob* __restrict__ jobs,
     for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     if ((threadIdx.x & 31) == 0 && lmax > 0.0)
         atomicMax(&amax_bits[J.part], (unsigned long long)__double_as_longlong(lmax));
+}
+
+// ---------------------------------------------------------------------------
+// Row-major copy of the packed factors (row i: L(i, i-kl..i-1), U(i, i..i+ubw)
+// at [kl + c - i]) and reciprocal diagonal, feeding the transpose sweeps and
+// the U sweeps.
+__global__ void k_transpose_factors(const PartDev* __restrict__ parts, const double* __restrict__ fac,
+                                    double* __restrict__ tfac, double* __restrict__ dinv) {
+    const PartDev P = parts[blockIdx.y];
+    const long long total = (long long)P.m * P.rowsT;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / P.rowsT);
+        const int q = (int)(e - (long long)i * P.rowsT);
+        const int c = i + q - P.kl;
+        double v = 0.0;
+        if (c >= 0 && c < P.m && c - i <= P.ubw && i - c <= P.kl) v = fac[P.fofs + (long long)c * P.rows + P.d + i - c];
+        tfac[P.tofs + e] = v;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x)
+        dinv[P.r0 + i] = 1.0 / fac[P.fofs + (long long)i * P.rows + P.d];
 }
 
 // ---------------------------------------------------------------------------
@@ -435,10 +462,10 @@ static inline unsigned grid_for(long long work, int per_block, int cap) {
 }
 
 void launch_fill_factors(const double* band, long long n, int akl, int aku, const PartDev* d_parts,
-                         int nparts, long long max_elems, double* fac, unsigned long long* amax,
+                         int nparts, long long max_elems, double* fac, int* piv, unsigned long long* amax,
                          cudaStream_t s) {
     dim3 g(grid_for(max_elems, 256, 4096), nparts);
-    k_fill_factors<<<g, 256, 0, s>>>(band, n, akl, aku, d_parts, fac, amax);
+    k_fill_factors<<<g, 256, 0, s>>>(band, n, akl, aku, d_parts, fac, piv, amax);
     count_launch();
 }
 
@@ -486,11 +513,18 @@ void launch_corners(const double* band, long long n, int akl, int aku, const lon
 }
 
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
-                           const PartDev* d_parts, const double* pool, double* fac,
+                           const PartDev* d_parts, const double* pool, double* fac, int* piv,
                            unsigned long long* amax, cudaStream_t s) {
     if (njobs <= 0) return;
     dim3 g(grid_for(max_elems, 256, 256), njobs);
-    k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, amax);
+    k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, piv, amax);
+    count_launch();
+}
+
+void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
+                              double* tfac, double* dinv, cudaStream_t s) {
+    dim3 g(grid_for(max_elems, 256, 4096), nparts);
+    k_transpose_factors<<<g, 256, 0, s>>>(d_parts, fac, tfac, dinv);
     count_launch();
 }
 

@@ -10,7 +10,7 @@ namespace spk {
 void count_launch(int n = 1);
 
 void launch_fill_factors(const double* band, long long n, int akl, int aku, const PartDev* d_parts,
-                         int nparts, long long max_elems, double* fac, unsigned long long* amax,
+                         int nparts, long long max_elems, double* fac, int* piv, unsigned long long* amax,
                          cudaStream_t s);
 void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
                     const unsigned long long* amax, double boost_eps, int* boost_cnt,
@@ -24,11 +24,23 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const 
 void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
                     int p, int k, double* bhat, double* chat, cudaStream_t s);
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
-                           const PartDev* d_parts, const double* pool, double* fac,
+                           const PartDev* d_parts, const double* pool, double* fac, int* piv,
                            unsigned long long* amax, cudaStream_t s);
 void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,
                         long long ldx, int ncols, int transpose, double* Y, long long ldy,
                         cudaStream_t s);
+struct FastSweepArgs;
+bool launch_sweep_fast_fl(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A,
+                          cudaStream_t s);
+bool launch_sweep_fast_bu(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A,
+                          cudaStream_t s);
+bool launch_sweep_fast_fut(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A,
+                           cudaStream_t s);
+bool launch_sweep_fast_blt(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A,
+                           cudaStream_t s);
+void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
+                              double* tfac, double* dinv, cudaStream_t s);
+
 void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd,
                           double* band, cudaStream_t s);
 void launch_generate_rhs(unsigned long long seed, long long n, int ncols, double* F, long long ldf,

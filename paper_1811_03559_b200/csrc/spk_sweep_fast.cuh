@@ -1,0 +1,250 @@
+// spk_sweep_fast.cuh — register-window triangular sweeps for SPIKE partitions.
+//
+// One CTA per (partition, group of right-hand-side columns); each warp owns NC
+// columns.  The active band window of every column (KW = 32*TR rows: the
+// current pivot row and the rows it still updates) lives in registers, one
+// circular slot per (lane, register).  Per step u of the sweep:
+//   x_c   = pivot row value (warp shuffle from the owning lane), scaled by the
+//           precomputed reciprocal diagonal for U sweeps;
+//   slot  <- next input row (recycled: the pivot row leaves, row u+KW enters);
+//   W    -= v_u (x) x   (rank-1 axpy over the window, DFMA)
+// where v_u is the step's factor vector (a column of L or U, or a row of L or
+// U for the transpose sweeps, read from the row-major factor copy).  Factor
+// vectors, reciprocal diagonals, pivots and the incoming rows are staged one
+// 32-step round at a time through a 3-stage cp.async ring in shared memory, so
+// HBM latency is hidden behind >= 2 rounds of arithmetic.  The pivot slot's
+// register index is a compile-time constant inside each round (rounds are
+// unrolled TR at a time), so the window never spills to local memory.
+//
+// Covers (reference /root/reference/proj/src/kernels.cpp):
+//   SW_FWD_L   forward_lower (+ LAPACK-style row interchanges)   :131-165
+//   SW_BWD_U   backward_upper / upper_bottom_tip                 :167-202
+//   SW_FWD_UT  forward_upperT / add_upperT_tail (row-major U)    :204-217, :263-280
+//   SW_BWD_LT  backward_lowerT, non-pivoting (row-major L)       :219-234
+#pragma once
+
+#include "spk_device.cuh"
+
+namespace spk {
+
+constexpr int kSweepStages = 3;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct FastSweepArgs {
+    const SweepJob* jobs;
+    const PartDev* parts;
+    const double* fac;   // column-major packed LU factors
+    const double* tfac;  // row-major copies (transpose sweeps)
+    const double* dinv;  // 1/u_jj per partition row
+    const int* piv;      // partition-local pivots per row
+    Bufs B;
+    int ncols;
+};
+
+// shared-memory bytes for a CTA of `nwarps` warps
+inline size_t fast_sweep_smem(int kw, int nwarps, int nc) {
+    const size_t per_stage = 32 * (size_t)kw * 8 + 32 * 8 + 32 * 4 + 32 * (size_t)nwarps * nc * 8;
+    return kSweepStages * per_stage + 64;
+}
+
+template <int TR, int NC, int MODE, bool PIV>
+__global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
+    constexpr int KW = 32 * TR;
+    constexpr bool kAsc = (MODE == SW_FWD_L || MODE == SW_FWD_UT);
+    constexpr bool kDiag = (MODE == SW_BWD_U || MODE == SW_FWD_UT);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const SweepJob J = A.jobs[blockIdx.x];
+    const PartDev P = A.parts[J.part];
+    const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
+    const int nwarps = blockDim.x >> 5;
+    const int ncta = nwarps * NC;
+    const int colbase = blockIdx.y * ncta;
+    if (colbase >= nc_total) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    const int lo = J.lo;
+    const int hi = (MODE == SW_BWD_U) ? J.hi : P.m - 1;
+    const int nsteps = hi - lo + 1;
+    if (nsteps <= 0) return;
+
+    int kw;
+    const double* vbase;
+    long long vstride;
+    int vdir;
+    if (MODE == SW_FWD_L) {
+        kw = P.kl;
+        vbase = A.fac + P.fofs + P.d + 1;
+        vstride = P.rows;
+        vdir = 1;
+    } else if (MODE == SW_BWD_U) {
+        kw = P.ubw;
+        vbase = A.fac + P.fofs + P.d - 1;
+        vstride = P.rows;
+        vdir = -1;
+    } else if (MODE == SW_FWD_UT) {
+        kw = P.ubw;
+        vbase = A.tfac + P.tofs + P.kl + 1;
+        vstride = P.rowsT;
+        vdir = 1;
+    } else {
+        kw = P.kl;
+        vbase = A.tfac + P.tofs + P.kl - 1;
+        vstride = P.rowsT;
+        vdir = -1;
+    }
+
+    // shared memory carve-up
+    double* s_vec = reinterpret_cast<double*>(smem_raw);                   // [st][32][kw]
+    double* s_dg = s_vec + (size_t)kSweepStages * 32 * kw;                 // [st][32]
+    double* s_in = s_dg + kSweepStages * 32;                               // [st][32][ncta]
+    int* s_pv = reinterpret_cast<int*>(s_in + (size_t)kSweepStages * 32 * ncta);  // [st][32]
+
+    // RHS view
+    const View& v = J.v;
+    const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
+    double* const bbase = A.B.p[v.buf] + v.base;
+    auto phys = [&](int r) -> long long { return v.rev ? (long long)(v.mrows - 1 - (r - v.off)) : (long long)(r - v.off); };
+    auto rowof = [&](int u) -> int { return kAsc ? lo + u : hi - u; };
+
+    const int c0 = J.c0 + colbase;              // first column of this CTA
+    const int ncta_valid = min(ncta, nc_total - colbase);
+    bool cval[NC];
+    long long coff[NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+        const int lc = warp * NC + cc;
+        cval[cc] = lc < ncta_valid;
+        coff[cc] = (long long)(c0 + lc) * ld;
+    }
+
+    auto load_round = [&](int R) {
+        const int st = R % kSweepStages;
+        const int u0 = 32 * R;
+        if (u0 < nsteps) {
+            double* dv = s_vec + (size_t)st * 32 * kw;
+            const int tot = 32 * kw;
+            for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+                const int t = idx / kw, dl = idx - t * kw;
+                const int u = u0 + t;
+                if (u < nsteps) cp_async8(dv + idx, vbase + (long long)rowof(u) * vstride + vdir * dl);
+            }
+            if (threadIdx.x < 32) {
+                const int u = u0 + threadIdx.x;
+                if (u < nsteps) {
+                    const int j = rowof(u);
+                    if (kDiag) cp_async8(s_dg + st * 32 + threadIdx.x, A.dinv + P.r0 + j);
+                    if (PIV) cp_async4(s_pv + st * 32 + threadIdx.x, A.piv + P.r0 + j);
+                }
+            }
+            double* di = s_in + (size_t)st * 32 * ncta;
+            const int tin = 32 * ncta;
+            for (int idx = threadIdx.x; idx < tin; idx += blockDim.x) {
+                const int t = idx & 31, col = idx >> 5;
+                const int uu = u0 + t + KW;
+                double* dst = di + t * ncta + col;
+                if (uu < nsteps && col < ncta_valid)
+                    cp_async8(dst, bbase + phys(rowof(uu)) + (long long)(c0 + col) * ld);
+                else
+                    *dst = 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+
+    // initial window: slot 32a+lane holds sweep row u = 32a+lane
+    double W[TR][NC];
+#pragma unroll
+    for (int a = 0; a < TR; ++a) {
+        const int u = 32 * a + lane;
+        const bool ok = u < nsteps;
+        const long long pr = ok ? phys(rowof(u)) : 0;
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) W[a][cc] = (ok && cval[cc]) ? bbase[pr + coff[cc]] : 0.0;
+    }
+
+#pragma unroll
+    for (int s = 0; s < kSweepStages - 1; ++s) load_round(s);
+
+    const int nrounds = (nsteps + 31) / 32;
+    for (int R0 = 0; R0 < nrounds; R0 += TR) {
+#pragma unroll
+        for (int a = 0; a < TR; ++a) {
+            const int R = R0 + a;
+            if (R < nrounds) {
+                cp_async_wait<kSweepStages - 2>();
+                __syncthreads();
+                load_round(R + kSweepStages - 1);
+                const int st = R % kSweepStages;
+                const double* vec = s_vec + (size_t)st * 32 * kw;
+                const double* dg = s_dg + st * 32;
+                const double* in = s_in + (size_t)st * 32 * ncta + warp * NC;
+                const int steps = min(32, nsteps - 32 * R);
+                for (int t = 0; t < steps; ++t) {
+                    const int pu = 32 * a + t;  // pivot slot
+                    if (PIV) {
+                        const int ip = s_pv[st * 32 + t];
+                        const int du = ip - rowof(32 * R + t);  // 0..kl
+                        int sl = pu + du;
+                        if (sl >= KW) sl -= KW;
+                        const int lip = sl & 31, rip = sl >> 5;
+#pragma unroll
+                        for (int cc = 0; cc < NC; ++cc) {
+                            double wsel = W[0][cc];
+#pragma unroll
+                            for (int q = 1; q < TR; ++q)
+                                if (rip == q) wsel = W[q][cc];
+                            const double vp = __shfl_sync(0xffffffffu, W[a][cc], t);
+                            const double vi = __shfl_sync(0xffffffffu, wsel, lip);
+                            if (lane == lip) {
+#pragma unroll
+                                for (int q = 0; q < TR; ++q)
+                                    if (rip == q) W[q][cc] = vp;
+                            }
+                            if (lane == t) W[a][cc] = vi;
+                        }
+                    }
+                    double x[NC];
+#pragma unroll
+                    for (int cc = 0; cc < NC; ++cc) {
+                        x[cc] = __shfl_sync(0xffffffffu, W[a][cc], t);
+                        if (kDiag) x[cc] *= dg[t];
+                    }
+                    if (lane == t) {
+                        const long long pr = phys(rowof(32 * R + t));
+#pragma unroll
+                        for (int cc = 0; cc < NC; ++cc) {
+                            if (cval[cc]) bbase[pr + coff[cc]] = x[cc];
+                            W[a][cc] = in[t * ncta + cc];
+                        }
+                    }
+                    const double* vr = vec + t * kw;
+#pragma unroll
+                    for (int a2 = 0; a2 < TR; ++a2) {
+                        int dd = 32 * a2 + lane - pu - 1;
+                        if (dd < 0) dd += KW;
+                        const double lv = dd < kw ? vr[dd] : 0.0;
+#pragma unroll
+                        for (int cc = 0; cc < NC; ++cc) W[a2][cc] = fma(-lv, x[cc], W[a2][cc]);
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+}  // namespace spk

@@ -1,0 +1,71 @@
+// spk_sweep_fast_fl.cu — instantiations of k_sweep_fast for SW_FWD_L.
+// (split per mode so nvcc builds the templates in parallel)
+#include "spk_sweep_fast.cuh"
+#include "spk_launch.h"
+
+#include <cuda_runtime.h>
+
+namespace spk {
+
+bool launch_sweep_fast_fl(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s) {
+    void (*fn)(FastSweepArgs) = nullptr;
+    if (tr == 1 && nc == 1 && piv == false) fn = k_sweep_fast<1, 1, SW_FWD_L, false>;
+    if (tr == 1 && nc == 2 && piv == false) fn = k_sweep_fast<1, 2, SW_FWD_L, false>;
+    if (tr == 1 && nc == 4 && piv == false) fn = k_sweep_fast<1, 4, SW_FWD_L, false>;
+    if (tr == 2 && nc == 1 && piv == false) fn = k_sweep_fast<2, 1, SW_FWD_L, false>;
+    if (tr == 2 && nc == 2 && piv == false) fn = k_sweep_fast<2, 2, SW_FWD_L, false>;
+    if (tr == 2 && nc == 4 && piv == false) fn = k_sweep_fast<2, 4, SW_FWD_L, false>;
+    if (tr == 3 && nc == 1 && piv == false) fn = k_sweep_fast<3, 1, SW_FWD_L, false>;
+    if (tr == 3 && nc == 2 && piv == false) fn = k_sweep_fast<3, 2, SW_FWD_L, false>;
+    if (tr == 3 && nc == 4 && piv == false) fn = k_sweep_fast<3, 4, SW_FWD_L, false>;
+    if (tr == 4 && nc == 1 && piv == false) fn = k_sweep_fast<4, 1, SW_FWD_L, false>;
+    if (tr == 4 && nc == 2 && piv == false) fn = k_sweep_fast<4, 2, SW_FWD_L, false>;
+    if (tr == 4 && nc == 4 && piv == false) fn = k_sweep_fast<4, 4, SW_FWD_L, false>;
+    if (tr == 5 && nc == 1 && piv == false) fn = k_sweep_fast<5, 1, SW_FWD_L, false>;
+    if (tr == 5 && nc == 2 && piv == false) fn = k_sweep_fast<5, 2, SW_FWD_L, false>;
+    if (tr == 5 && nc == 4 && piv == false) fn = k_sweep_fast<5, 4, SW_FWD_L, false>;
+    if (tr == 6 && nc == 1 && piv == false) fn = k_sweep_fast<6, 1, SW_FWD_L, false>;
+    if (tr == 6 && nc == 2 && piv == false) fn = k_sweep_fast<6, 2, SW_FWD_L, false>;
+    if (tr == 6 && nc == 4 && piv == false) fn = k_sweep_fast<6, 4, SW_FWD_L, false>;
+    if (tr == 7 && nc == 1 && piv == false) fn = k_sweep_fast<7, 1, SW_FWD_L, false>;
+    if (tr == 7 && nc == 2 && piv == false) fn = k_sweep_fast<7, 2, SW_FWD_L, false>;
+    if (tr == 7 && nc == 4 && piv == false) fn = k_sweep_fast<7, 4, SW_FWD_L, false>;
+    if (tr == 8 && nc == 1 && piv == false) fn = k_sweep_fast<8, 1, SW_FWD_L, false>;
+    if (tr == 8 && nc == 2 && piv == false) fn = k_sweep_fast<8, 2, SW_FWD_L, false>;
+    if (tr == 8 && nc == 4 && piv == false) fn = k_sweep_fast<8, 4, SW_FWD_L, false>;
+    if (tr == 1 && nc == 1 && piv == true) fn = k_sweep_fast<1, 1, SW_FWD_L, true>;
+    if (tr == 1 && nc == 2 && piv == true) fn = k_sweep_fast<1, 2, SW_FWD_L, true>;
+    if (tr == 1 && nc == 4 && piv == true) fn = k_sweep_fast<1, 4, SW_FWD_L, true>;
+    if (tr == 2 && nc == 1 && piv == true) fn = k_sweep_fast<2, 1, SW_FWD_L, true>;
+    if (tr == 2 && nc == 2 && piv == true) fn = k_sweep_fast<2, 2, SW_FWD_L, true>;
+    if (tr == 2 && nc == 4 && piv == true) fn = k_sweep_fast<2, 4, SW_FWD_L, true>;
+    if (tr == 3 && nc == 1 && piv == true) fn = k_sweep_fast<3, 1, SW_FWD_L, true>;
+    if (tr == 3 && nc == 2 && piv == true) fn = k_sweep_fast<3, 2, SW_FWD_L, true>;
+    if (tr == 3 && nc == 4 && piv == true) fn = k_sweep_fast<3, 4, SW_FWD_L, true>;
+    if (tr == 4 && nc == 1 && piv == true) fn = k_sweep_fast<4, 1, SW_FWD_L, true>;
+    if (tr == 4 && nc == 2 && piv == true) fn = k_sweep_fast<4, 2, SW_FWD_L, true>;
+    if (tr == 4 && nc == 4 && piv == true) fn = k_sweep_fast<4, 4, SW_FWD_L, true>;
+    if (tr == 5 && nc == 1 && piv == true) fn = k_sweep_fast<5, 1, SW_FWD_L, true>;
+    if (tr == 5 && nc == 2 && piv == true) fn = k_sweep_fast<5, 2, SW_FWD_L, true>;
+    if (tr == 5 && nc == 4 && piv == true) fn = k_sweep_fast<5, 4, SW_FWD_L, true>;
+    if (tr == 6 && nc == 1 && piv == true) fn = k_sweep_fast<6, 1, SW_FWD_L, true>;
+    if (tr == 6 && nc == 2 && piv == true) fn = k_sweep_fast<6, 2, SW_FWD_L, true>;
+    if (tr == 6 && nc == 4 && piv == true) fn = k_sweep_fast<6, 4, SW_FWD_L, true>;
+    if (tr == 7 && nc == 1 && piv == true) fn = k_sweep_fast<7, 1, SW_FWD_L, true>;
+    if (tr == 7 && nc == 2 && piv == true) fn = k_sweep_fast<7, 2, SW_FWD_L, true>;
+    if (tr == 7 && nc == 4 && piv == true) fn = k_sweep_fast<7, 4, SW_FWD_L, true>;
+    if (tr == 8 && nc == 1 && piv == true) fn = k_sweep_fast<8, 1, SW_FWD_L, true>;
+    if (tr == 8 && nc == 2 && piv == true) fn = k_sweep_fast<8, 2, SW_FWD_L, true>;
+    if (tr == 8 && nc == 4 && piv == true) fn = k_sweep_fast<8, 4, SW_FWD_L, true>;
+    if (!fn) return false;
+    static bool attr_done[2][9][5] = {};
+    if (!attr_done[piv][tr][nc]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_done[piv][tr][nc] = true;
+    }
+    fn<<<grid, 32 * nwarps, smem, s>>>(A);
+    count_launch();
+    return true;
+}
+
+}  // namespace spk
