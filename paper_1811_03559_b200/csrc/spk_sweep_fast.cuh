@@ -54,9 +54,9 @@ struct FastSweepArgs {
     int ncols;
 };
 
-// shared-memory bytes for a CTA of `nwarps` warps
-inline size_t fast_sweep_smem(int kw, int nwarps, int nc) {
-    const size_t per_stage = 32 * (size_t)kw * 8 + 32 * 8 + 32 * 4 + 32 * (size_t)nwarps * nc * 8;
+// shared-memory bytes for a CTA of `nwarps` warps (KW = 32*TR slots per step)
+inline size_t fast_sweep_smem(int KW, int nwarps, int nc) {
+    const size_t per_stage = 32 * (size_t)KW * 8 + 32 * 8 + 32 * 4 + 32 * (size_t)nwarps * nc * 8;
     return kSweepStages * per_stage + 64;
 }
 
@@ -107,40 +107,48 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
         vdir = -1;
     }
 
-    // shared memory carve-up
-    double* s_vec = reinterpret_cast<double*>(smem_raw);                   // [st][32][kw]
-    double* s_dg = s_vec + (size_t)kSweepStages * 32 * kw;                 // [st][32]
-    double* s_in = s_dg + kSweepStages * 32;                               // [st][32][ncta]
+    // shared memory: factor vectors in window-slot order (zero where the
+    // vector does not reach), reciprocal diagonal, pivots, incoming rows
+    double* s_vec = reinterpret_cast<double*>(smem_raw);                    // [st][32][KW]
+    double* s_dg = s_vec + (size_t)kSweepStages * 32 * KW;                  // [st][32]
+    double* s_in = s_dg + kSweepStages * 32;                                // [st][32][ncta]
     int* s_pv = reinterpret_cast<int*>(s_in + (size_t)kSweepStages * 32 * ncta);  // [st][32]
 
-    // RHS view
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
     double* const bbase = A.B.p[v.buf] + v.base;
-    auto phys = [&](int r) -> long long { return v.rev ? (long long)(v.mrows - 1 - (r - v.off)) : (long long)(r - v.off); };
+    auto phys = [&](int r) -> long long {
+        return v.rev ? (long long)(v.mrows - 1 - (r - v.off)) : (long long)(r - v.off);
+    };
     auto rowof = [&](int u) -> int { return kAsc ? lo + u : hi - u; };
 
-    const int c0 = J.c0 + colbase;              // first column of this CTA
+    const int c0 = J.c0 + colbase;
     const int ncta_valid = min(ncta, nc_total - colbase);
     bool cval[NC];
-    long long coff[NC];
+    double* cptr[NC];
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) {
         const int lc = warp * NC + cc;
         cval[cc] = lc < ncta_valid;
-        coff[cc] = (long long)(c0 + lc) * ld;
+        cptr[cc] = bbase + (long long)(c0 + (cval[cc] ? lc : 0)) * ld;
     }
 
     auto load_round = [&](int R) {
         const int st = R % kSweepStages;
         const int u0 = 32 * R;
         if (u0 < nsteps) {
-            double* dv = s_vec + (size_t)st * 32 * kw;
-            const int tot = 32 * kw;
-            for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-                const int t = idx / kw, dl = idx - t * kw;
+            const int pa = 32 * (R % TR);  // pivot slot of step 0 of the round
+            double* dv = s_vec + (size_t)st * 32 * KW;
+            for (int idx = threadIdx.x; idx < 32 * KW; idx += blockDim.x) {
+                const int t = idx / KW, sl = idx - t * KW;
+                int dl = sl - pa - t - 1;
+                if (dl < 0) dl += KW;
+                if (dl < 0) dl += KW;
                 const int u = u0 + t;
-                if (u < nsteps) cp_async8(dv + idx, vbase + (long long)rowof(u) * vstride + vdir * dl);
+                if (dl < kw && u < nsteps)
+                    cp_async8(dv + idx, vbase + (long long)rowof(u) * vstride + vdir * dl);
+                else
+                    dv[idx] = 0.0;
             }
             if (threadIdx.x < 32) {
                 const int u = u0 + threadIdx.x;
@@ -151,8 +159,7 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
                 }
             }
             double* di = s_in + (size_t)st * 32 * ncta;
-            const int tin = 32 * ncta;
-            for (int idx = threadIdx.x; idx < tin; idx += blockDim.x) {
+            for (int idx = threadIdx.x; idx < 32 * ncta; idx += blockDim.x) {
                 const int t = idx & 31, col = idx >> 5;
                 const int uu = u0 + t + KW;
                 double* dst = di + t * ncta + col;
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
         const bool ok = u < nsteps;
         const long long pr = ok ? phys(rowof(u)) : 0;
 #pragma unroll
-        for (int cc = 0; cc < NC; ++cc) W[a][cc] = (ok && cval[cc]) ? bbase[pr + coff[cc]] : 0.0;
+        for (int cc = 0; cc < NC; ++cc) W[a][cc] = (ok && cval[cc]) ? cptr[cc][pr] : 0.0;
     }
 
 #pragma unroll
@@ -189,16 +196,21 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
                 __syncthreads();
                 load_round(R + kSweepStages - 1);
                 const int st = R % kSweepStages;
-                const double* vec = s_vec + (size_t)st * 32 * kw;
+                const double* vec = s_vec + (size_t)st * 32 * KW + lane;
                 const double* dg = s_dg + st * 32;
-                const double* in = s_in + (size_t)st * 32 * ncta + warp * NC;
+                double inreg[NC], out[NC];
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) {
+                    inreg[cc] = s_in[(size_t)st * 32 * ncta + lane * ncta + warp * NC + cc];
+                    out[cc] = 0.0;
+                }
                 const int steps = min(32, nsteps - 32 * R);
+#pragma unroll 2
                 for (int t = 0; t < steps; ++t) {
-                    const int pu = 32 * a + t;  // pivot slot
                     if (PIV) {
                         const int ip = s_pv[st * 32 + t];
                         const int du = ip - rowof(32 * R + t);  // 0..kl
-                        int sl = pu + du;
+                        int sl = 32 * a + t + du;
                         if (sl >= KW) sl -= KW;
                         const int lip = sl & 31, rip = sl >> 5;
 #pragma unroll
@@ -218,28 +230,29 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
                         }
                     }
                     double x[NC];
+                    const double dgt = kDiag ? dg[t] : 1.0;
+                    const bool mine = lane == t;
 #pragma unroll
                     for (int cc = 0; cc < NC; ++cc) {
                         x[cc] = __shfl_sync(0xffffffffu, W[a][cc], t);
-                        if (kDiag) x[cc] *= dg[t];
+                        if (kDiag) x[cc] *= dgt;
+                        out[cc] = mine ? x[cc] : out[cc];
+                        W[a][cc] = mine ? inreg[cc] : W[a][cc];
                     }
-                    if (lane == t) {
-                        const long long pr = phys(rowof(32 * R + t));
-#pragma unroll
-                        for (int cc = 0; cc < NC; ++cc) {
-                            if (cval[cc]) bbase[pr + coff[cc]] = x[cc];
-                            W[a][cc] = in[t * ncta + cc];
-                        }
-                    }
-                    const double* vr = vec + t * kw;
+                    const double* vr = vec + t * KW;
 #pragma unroll
                     for (int a2 = 0; a2 < TR; ++a2) {
-                        int dd = 32 * a2 + lane - pu - 1;
-                        if (dd < 0) dd += KW;
-                        const double lv = dd < kw ? vr[dd] : 0.0;
+                        const double lv = vr[32 * a2];
 #pragma unroll
                         for (int cc = 0; cc < NC; ++cc) W[a2][cc] = fma(-lv, x[cc], W[a2][cc]);
                     }
+                }
+                // coalesced write-back of the round's finished rows
+                if (lane < steps) {
+                    const long long pr = phys(rowof(32 * R + lane));
+#pragma unroll
+                    for (int cc = 0; cc < NC; ++cc)
+                        if (cval[cc]) cptr[cc][pr] = out[cc];
                 }
             }
         }
