@@ -903,7 +903,7 @@ struct Exec {
             nw = nc;
         }
         const dim3 grid(st.njobs, (nc + nw * NC - 1) / (nw * NC));
-        const size_t smem = fast_sweep_smem(32 * st.tr, nw, NC);
+        const size_t smem = fast_sweep_smem(st.tr, nw, NC);
         if (smem > 227 * 1024) return false;
         FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
         switch (st.mode) {

@@ -27,7 +27,6 @@
 
 namespace spk {
 
-constexpr int kSweepStages = 3;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -54,15 +53,31 @@ struct FastSweepArgs {
     int ncols;
 };
 
-// shared-memory bytes for a CTA of `nwarps` warps (KW = 32*TR slots per step)
-inline size_t fast_sweep_smem(int KW, int nwarps, int nc) {
+// Window of TW = TR+1 register rows per column (KW = 32*TW slots): during round
+// R (32 steps) the pivots are register row R mod TW; the other TR rows cover
+// every row the round's pivots update.  A finished pivot row stays untouched
+// (its vector slots are zero) until the round ends; then it is written back
+// (times 1/u_jj for U sweeps) and refilled with the rows 32*TW further on.  No
+// per-step selects or divergent branches.
+template <int TR>
+struct SweepGeom {
+    static constexpr int TW = TR + 1;
+    static constexpr int KW = 32 * TW;
+    static constexpr int NST = (TR <= 5) ? 3 : 2;
+};
+
+inline size_t fast_sweep_smem(int tr, int nwarps, int nc) {
+    const int KW = 32 * (tr + 1);
+    const int nst = tr <= 5 ? 3 : 2;
     const size_t per_stage = 32 * (size_t)KW * 8 + 32 * 8 + 32 * 4 + 32 * (size_t)nwarps * nc * 8;
-    return kSweepStages * per_stage + 64;
+    return nst * per_stage + 64;
 }
 
 template <int TR, int NC, int MODE, bool PIV>
 __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
-    constexpr int KW = 32 * TR;
+    constexpr int TW = SweepGeom<TR>::TW;
+    constexpr int KW = SweepGeom<TR>::KW;
+    constexpr int NST = SweepGeom<TR>::NST;
     constexpr bool kAsc = (MODE == SW_FWD_L || MODE == SW_FWD_UT);
     constexpr bool kDiag = (MODE == SW_BWD_U || MODE == SW_FWD_UT);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -107,12 +122,10 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
         vdir = -1;
     }
 
-    // shared memory: factor vectors in window-slot order (zero where the
-    // vector does not reach), reciprocal diagonal, pivots, incoming rows
     double* s_vec = reinterpret_cast<double*>(smem_raw);                    // [st][32][KW]
-    double* s_dg = s_vec + (size_t)kSweepStages * 32 * KW;                  // [st][32]
-    double* s_in = s_dg + kSweepStages * 32;                                // [st][32][ncta]
-    int* s_pv = reinterpret_cast<int*>(s_in + (size_t)kSweepStages * 32 * ncta);  // [st][32]
+    double* s_dg = s_vec + (size_t)NST * 32 * KW;                           // [st][32]
+    double* s_in = s_dg + NST * 32;                                         // [st][32][ncta]
+    int* s_pv = reinterpret_cast<int*>(s_in + (size_t)NST * 32 * ncta);     // [st][32]
 
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -133,16 +146,17 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
         cptr[cc] = bbase + (long long)(c0 + (cval[cc] ? lc : 0)) * ld;
     }
 
+    // stage round R: vectors of steps 32R.. in slot order, 1/u_jj, pivots, and
+    // the rows that refill the window at the end of round R (rows 32(R+TW)+l)
     auto load_round = [&](int R) {
-        const int st = R % kSweepStages;
+        const int st = R % NST;
         const int u0 = 32 * R;
         if (u0 < nsteps) {
-            const int pa = 32 * (R % TR);  // pivot slot of step 0 of the round
+            const int pa = 32 * (R % TW);
             double* dv = s_vec + (size_t)st * 32 * KW;
             for (int idx = threadIdx.x; idx < 32 * KW; idx += blockDim.x) {
                 const int t = idx / KW, sl = idx - t * KW;
                 int dl = sl - pa - t - 1;
-                if (dl < 0) dl += KW;
                 if (dl < 0) dl += KW;
                 const int u = u0 + t;
                 if (dl < kw && u < nsteps)
@@ -172,10 +186,9 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
         cp_async_commit();
     };
 
-    // initial window: slot 32a+lane holds sweep row u = 32a+lane
-    double W[TR][NC];
+    double W[TW][NC];
 #pragma unroll
-    for (int a = 0; a < TR; ++a) {
+    for (int a = 0; a < TW; ++a) {
         const int u = 32 * a + lane;
         const bool ok = u < nsteps;
         const long long pr = ok ? phys(rowof(u)) : 0;
@@ -184,26 +197,20 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
     }
 
 #pragma unroll
-    for (int s = 0; s < kSweepStages - 1; ++s) load_round(s);
+    for (int s = 0; s < NST - 1; ++s) load_round(s);
 
     const int nrounds = (nsteps + 31) / 32;
-    for (int R0 = 0; R0 < nrounds; R0 += TR) {
+    for (int R0 = 0; R0 < nrounds; R0 += TW) {
 #pragma unroll
-        for (int a = 0; a < TR; ++a) {
+        for (int a = 0; a < TW; ++a) {
             const int R = R0 + a;
             if (R < nrounds) {
-                cp_async_wait<kSweepStages - 2>();
+                cp_async_wait<NST - 2>();
                 __syncthreads();
-                load_round(R + kSweepStages - 1);
-                const int st = R % kSweepStages;
+                load_round(R + NST - 1);
+                const int st = R % NST;
                 const double* vec = s_vec + (size_t)st * 32 * KW + lane;
                 const double* dg = s_dg + st * 32;
-                double inreg[NC], out[NC];
-#pragma unroll
-                for (int cc = 0; cc < NC; ++cc) {
-                    inreg[cc] = s_in[(size_t)st * 32 * ncta + lane * ncta + warp * NC + cc];
-                    out[cc] = 0.0;
-                }
                 const int steps = min(32, nsteps - 32 * R);
 #pragma unroll 2
                 for (int t = 0; t < steps; ++t) {
@@ -217,13 +224,13 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
                         for (int cc = 0; cc < NC; ++cc) {
                             double wsel = W[0][cc];
 #pragma unroll
-                            for (int q = 1; q < TR; ++q)
+                            for (int q = 1; q < TW; ++q)
                                 if (rip == q) wsel = W[q][cc];
                             const double vp = __shfl_sync(0xffffffffu, W[a][cc], t);
                             const double vi = __shfl_sync(0xffffffffu, wsel, lip);
                             if (lane == lip) {
 #pragma unroll
-                                for (int q = 0; q < TR; ++q)
+                                for (int q = 0; q < TW; ++q)
                                     if (rip == q) W[q][cc] = vp;
                             }
                             if (lane == t) W[a][cc] = vi;
@@ -231,29 +238,38 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
                     }
                     double x[NC];
                     const double dgt = kDiag ? dg[t] : 1.0;
-                    const bool mine = lane == t;
 #pragma unroll
                     for (int cc = 0; cc < NC; ++cc) {
                         x[cc] = __shfl_sync(0xffffffffu, W[a][cc], t);
                         if (kDiag) x[cc] *= dgt;
-                        out[cc] = mine ? x[cc] : out[cc];
-                        W[a][cc] = mine ? inreg[cc] : W[a][cc];
                     }
                     const double* vr = vec + t * KW;
+                    // the pivot register row first: it feeds the next step's shuffle
+                    {
+                        const double lv = vr[32 * a];
 #pragma unroll
-                    for (int a2 = 0; a2 < TR; ++a2) {
+                        for (int cc = 0; cc < NC; ++cc) W[a][cc] = fma(-lv, x[cc], W[a][cc]);
+                    }
+#pragma unroll
+                    for (int a2 = 0; a2 < TW; ++a2) {
+                        if (a2 == a) continue;
                         const double lv = vr[32 * a2];
 #pragma unroll
                         for (int cc = 0; cc < NC; ++cc) W[a2][cc] = fma(-lv, x[cc], W[a2][cc]);
                     }
                 }
-                // coalesced write-back of the round's finished rows
+                // register row a now holds this round's finished pivot rows:
+                // write them back, then refill with the rows 32*TW further on
                 if (lane < steps) {
                     const long long pr = phys(rowof(32 * R + lane));
+                    const double sc = kDiag ? dg[lane] : 1.0;
 #pragma unroll
                     for (int cc = 0; cc < NC; ++cc)
-                        if (cval[cc]) cptr[cc][pr] = out[cc];
+                        if (cval[cc]) cptr[cc][pr] = kDiag ? W[a][cc] * sc : W[a][cc];
                 }
+                const double* in = s_in + (size_t)st * 32 * ncta + lane * ncta + warp * NC;
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) W[a][cc] = in[cc];
             }
         }
     }
