@@ -11,6 +11,21 @@
 #include "spk_launch.h"
 #include "spk_sweep_fast.cuh"
 
+namespace spk {
+struct FastLuArgs {
+    const int* units;
+    const PartDev* parts;
+    const double* band;
+    int akl, aku;
+    double* fac;
+    double* tfac;
+    double* dinv;
+    int* piv;
+    double boost_eps;
+    int* boost_cnt;
+};
+}  // namespace spk
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -159,6 +174,7 @@ struct Stage {
     // a SPIKE partition it supports
     bool fast = false;
     int mode = 0, kwmax = 0, tr = 0, piv = 0;
+    bool partitions = false;  // ST_LU over SPIKE partitions (fill from the input band)
 };
 
 struct ProgramBuilder {
@@ -415,9 +431,10 @@ struct Builder {
         }
         prog.push_back(s);
     }
-    void lu(const std::vector<int>& units) {
+    void lu(const std::vector<int>& units, bool partitions = false) {
         if (units.empty()) return;
         Stage s{ST_LU};
+        s.partitions = partitions;
         s.njobs = (int)units.size();
         s.off = pb.push(units);
         for (int u : units) {
@@ -547,7 +564,7 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
     if (!f.reduced_only) {
         std::vector<int> units(p);
         for (int i = 0; i < p; ++i) units[i] = i;
-        b.lu(units);  // preceded at run time by fill_factors
+        b.lu(units, true);  // register-window LU from the band, or fill + generic LU
         b.transpose_factors();
     }
     if (p < 2 || k == 0) return;
@@ -888,6 +905,8 @@ struct Exec {
     // memcpy sources
     const double* F = nullptr;
     long long ldf = 0, n = 0;
+    const double* band = nullptr;  // factorization input (device)
+    bool lu_fast_done = false;
 
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
         if (nc <= 0) return true;
@@ -928,6 +947,7 @@ struct Exec {
                     break;
                 }
                 case ST_TRANSPOSE: {
+                    if (lu_fast_done) break;
                     long long mx = 0;
                     for (int i = 0; i < f.p; ++i) mx = std::max(mx, (long long)f.parts[i].m * f.parts[i].rowsT);
                     launch_transpose_factors(f.d_parts, f.p, mx, f.d_fac, f.d_tfac, f.d_dinv, s);
@@ -943,10 +963,28 @@ struct Exec {
                     launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
                     break;
                 }
-                case ST_LU:
+                case ST_LU: {
+                    if (st.partitions) {
+                        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
+                        const int kmax = std::max(f.kl, f.ku);
+                        if (!f.piv_on && !generic_only && kmax <= 160) {
+                            FastLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac, f.d_tfac,
+                                         f.d_dinv, f.d_piv, f.boost_eps, f.d_boost};
+                            if (launch_band_lu_fast((const int*)jobs, st.njobs, kmax, A, s)) {
+                                lu_fast_done = true;
+                                break;
+                            }
+                        }
+                        long long max_elems = 0;
+                        for (int i = 0; i < f.p; ++i)
+                            max_elems = std::max(max_elems, (long long)f.parts[i].m * f.parts[i].rows);
+                        launch_fill_factors(band, n, f.kl, f.ku, f.d_parts, f.p, max_elems, f.d_fac, f.d_piv,
+                                            f.d_amax, s);
+                    }
                     launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
                                    f.boost_eps, f.d_boost, f.d_fell, f.d_status, s);
                     break;
+                }
                 case ST_CPL:
                     launch_build_coupling((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts,
                                           f.d_pool, f.d_fac, f.d_piv, f.d_amax, s);
@@ -1265,11 +1303,12 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
         if (pp > cap) fail(SPK_EINVAL, "gpu_plan: capacity too small");
         // first/last partitions carry no spike sweeps (0 vs 3 in factor, 2 vs 4
         // in solve): give them the reference's R13 ratio with K = 1.
-        double r12 = 1.0, r13 = 2.0;
-        spk_compute_ratios(1.0, nrhs, std::max(k, 1), &r12, &r13);
-        r13 = std::min(std::max(r13, 1.0), 3.0);
+        // Equal sizes: on the GPU every stage is one launch over all
+        // partitions, so a stage costs its largest partition; first/last
+        // partitions do full sweeps in the D stage and the LU like everyone
+        // else, so the CPU ratio model (partition.cpp:47-54) would make them
+        // the critical path.
         std::vector<double> w(pp, 1.0);
-        if (pp > 1) w.front() = w.back() = r13;
         double tot = 0.0;
         for (double x : w) tot += x;
         for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1329,12 +1368,7 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         const int p = f->p;
         long long max_elems = 0;
         for (int i = 0; i < p; ++i) max_elems = std::max(max_elems, (long long)f->parts[i].m * f->parts[i].rows);
-        {
-            double bytes = 0;
-            for (int i = 0; i < p; ++i) bytes += 8.0 * f->parts[i].m * (f->parts[i].rows + ld);
-            ProfScope ps(PC_FILL, s, 0.0, bytes);
-            launch_fill_factors(dband, n, kl, ku, f->d_parts, p, max_elems, f->d_fac, f->d_piv, f->d_amax, s);
-        }
+        (void)max_elems;
         {
             ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);
             launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->d_pool + f->off_bhat,
@@ -1355,6 +1389,7 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         B.ld[B_AUX] = f->auxf_rows;
         Exec ex{*f, s, B, f->k};
         ex.n = n;
+        ex.band = dband;
         ex.run(f->prog_factor);
         if (fs) ck(cudaFreeAsync(fs, s), "free");
         if (auxf) ck(cudaFreeAsync(auxf, s), "free");
