@@ -1010,9 +1010,26 @@ struct Exec {
     }
 };
 
+// Keep freed stream-ordered allocations in the device's default pool: with
+// the default release threshold (0) every synchronisation hands gigabytes of
+// factor/scratch memory back to the driver and the next factorization pays
+// to map it again.
+void keep_pool_memory() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+        unsigned long long thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    });
+}
+
 template <class T>
 T* dalloc(size_t count, cudaStream_t s) {
     void* p = nullptr;
+    keep_pool_memory();
     if (count == 0) count = 1;
     ck(cudaMallocAsync(&p, sizeof(T) * count, s), "cudaMallocAsync");
     return static_cast<T*>(p);
@@ -1444,6 +1461,14 @@ spk_status spk_fact_tip(const spk_fact* f, int32_t which, int32_t i, double* out
                         sizeof(double) * k, k, cudaMemcpyDeviceToHost),
            "tip");
     });
+}
+
+int64_t spk_fact_dump(const spk_fact* f, int32_t which, double* out) {
+    // debug/test hook: 0 packed LU pool, 1 row-major copies, 2 1/u_jj
+    const long long sz = which == 0 ? f->fac_size : which == 1 ? f->tfac_size : f->n;
+    const double* src = which == 0 ? f->d_fac : which == 1 ? f->d_tfac : f->d_dinv;
+    if (out) cudaMemcpy(out, src, sizeof(double) * sz, cudaMemcpyDeviceToHost);
+    return sz;
 }
 
 int32_t spk_fact_units(const spk_fact* f, int32_t l) {

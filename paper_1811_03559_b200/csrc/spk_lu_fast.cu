@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
                         const int j = 32 * R + t;
                         TF[(long long)j * rowsT + kl + off] = (j + off < m) ? s_ur[t * (K + 1) + off] : 0.0;
                     }
-                    for (int idx = threadIdx.x; idx < nst * (ku + 1); idx += blockDim.x) {
+                    for (int idx = threadIdx.x; idx < 32 * (ku + 1); idx += blockDim.x) {
                         const int t = idx & 31, off = idx >> 5;
                         if (t >= nst) continue;
                         const int j = 32 * R + t;
