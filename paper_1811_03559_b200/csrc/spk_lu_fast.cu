@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
     double* s_ncu = s_nc + 2 * 32 * K;                   // [2][32]    A(j, j+K)
     double* s_ex = s_ncu + 2 * 32;                       // [2][32]    A(j+1+K, j+1)
     double* s_l = s_ex + 2 * 32;                         // [2][K]     published multipliers
-    double* s_ur = s_l + 2 * K;                          // [32][K+1]  U rows of the round
+    double* s_ur = s_l + 2 * K;                          // [32][K]    U rows of the round (slot order)
     __shared__ double s_red[2 * 32];
 
     const int u = A.units[blockIdx.x];
@@ -195,6 +195,11 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
                     const int st = R & 1;
                     const double* nr = s_nr + st * 32 * K;
                     const double* nc = s_nc + st * 32 * K;
+                    // max|A_i| over everything this round brings into the window
+                    for (int idx = threadIdx.x; idx < 2 * 32 * K; idx += blockDim.x)
+                        amax = fmax(amax, fabs((idx < 32 * K ? nr : nc - 32 * K)[idx]));
+                    if (threadIdx.x < 64)
+                        amax = fmax(amax, fabs((threadIdx.x < 32 ? s_ncu : s_ex)[st * 32 + (threadIdx.x & 31)]));
 #pragma unroll
                     for (int q = 0; q < 32 / NW; ++q) {
                         const int bq = (32 * a) / NW + q;  // register column of pivot column j
@@ -202,45 +207,32 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
                             const int t = q * NW + w2;
                             const int j = 32 * R + t;
                             if (j >= m) break;
-                            // 1. multipliers of this step (slot order)
                             double lv[TR];
 #pragma unroll
                             for (int a2 = 0; a2 < TR; ++a2) lv[a2] = s_l[(j & 1) * K + 32 * a2 + lane];
-                            const bool own = warp == w2;             // owner of pivot column j
-                            const bool last = w2 == NW - 1;          // column j+1 lives in register bq+1
+                            const bool own = warp == w2;
+                            const bool last = w2 == NW - 1;
                             const bool pub = warp == (w2 + 1) % NW && j + 1 < m;
-                            const double ucol = s_ncu[st * 32 + t];
-                            if (own && lane == 0) amax = fmax(amax, fabs(ucol));
-                            const int jmodk = j % K;
-                            // 2./3. per column, starting at the pivot column's register so
-                            // that column j+1 (register bq or bq+1) is updated first
+                            const bool mine = lane == t;
+                            const double* nrow = nr + t * K + warp;
+                            double* urow = s_ur + t * K + warp;  // U row j, column-slot order
 #pragma unroll
                             for (int bi = 0; bi < CPW; ++bi) {
                                 const int b = (bq + bi) % CPW;
                                 double ub = __shfl_sync(0xffffffffu, W[a][b], t);
-                                if (lane == t) {
-                                    int off = warp + NW * b - jmodk;
-                                    if (off < 0) off += K;
-                                    s_ur[t * (K + 1) + off] = ub;
-                                    const double nv = nr[t * K + warp + NW * b];
-                                    amax = fmax(amax, fabs(nv));
-                                    W[a][b] = nv;
-                                }
+                                urow[NW * b] = ub;
+                                const double nv = nrow[NW * b];
+                                W[a][b] = mine ? nv : W[a][b];
                                 if (bi == 0 && own) {
                                     // the pivot column's slot becomes column j+K
 #pragma unroll
-                                    for (int a2 = 0; a2 < TR; ++a2) {
-                                        const double nv = nc[t * K + 32 * a2 + lane];
-                                        amax = fmax(amax, fabs(nv));
-                                        W[a2][b] = nv;
-                                    }
-                                    ub = ucol;
-                                    if (lane == t) s_ur[t * (K + 1) + K] = ucol;
+                                    for (int a2 = 0; a2 < TR; ++a2) W[a2][b] = nc[t * K + 32 * a2 + lane];
+                                    ub = s_ncu[st * 32 + t];
                                 }
 #pragma unroll
                                 for (int a2 = 0; a2 < TR; ++a2) W[a2][b] = fma(-lv[a2], ub, W[a2][b]);
                                 if (pub && ((bi == 0 && !last) || (bi == 1 && last) || (CPW == 1 && last))) {
-                                    // 4. owner of column j+1: pivot, scale, publish l_{j+1}
+                                    // owner of column j+1: pivot, scale, publish l_{j+1}
                                     const int tn = (t + 1) & 31;
                                     const bool wrap = t == 31;
                                     const double wsel = wrap ? W[(a + 1) % TR][b] : W[a][b];
@@ -256,9 +248,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
                                     }
                                     const double inv = 1.0 / pv;
                                     const double ex = s_ex[st * 32 + t];
-                                    amax = fmax(amax, fabs(ex));
                                     const int jn = j + 1;
-                                    const int sn = jn % K;  // pivot slot of step j+1
+                                    const int sn = (32 * a + t + 1) % K;  // pivot slot of step j+1
 #pragma unroll
                                     for (int a2 = 0; a2 < TR; ++a2) {
                                         const int sl = 32 * a2 + lane;
@@ -278,18 +269,22 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
                             __syncthreads();
                         }
                     }
-                    // write back the round's U rows (both layouts)
+                    // write back the round's U rows (both layouts): slot s of row j
+                    // holds column j + ((s - j) mod K); column j+K comes from s_ncu
                     const int nst = min(32, m - 32 * R);
-                    for (int idx = threadIdx.x; idx < nst * (ku + 1); idx += blockDim.x) {
-                        const int t = idx / (ku + 1), off = idx - t * (ku + 1);
+                    for (int idx = threadIdx.x; idx < nst * (K + 1); idx += blockDim.x) {
+                        const int t = idx / (K + 1), sl = idx - t * (K + 1);
                         const int j = 32 * R + t;
-                        TF[(long long)j * rowsT + kl + off] = (j + off < m) ? s_ur[t * (K + 1) + off] : 0.0;
-                    }
-                    for (int idx = threadIdx.x; idx < 32 * (ku + 1); idx += blockDim.x) {
-                        const int t = idx & 31, off = idx >> 5;
-                        if (t >= nst) continue;
-                        const int j = 32 * R + t;
-                        if (j + off < m) F[(long long)(j + off) * rows + d - off] = s_ur[t * (K + 1) + off];
+                        int off = K;
+                        double val = s_ncu[st * 32 + t];
+                        if (sl < K) {
+                            off = sl - (32 * a + t) % K;
+                            if (off < 0) off += K;
+                            val = s_ur[t * K + sl];
+                        }
+                        if (off > ku) continue;
+                        TF[(long long)j * rowsT + kl + off] = (j + off < m) ? val : 0.0;
+                        if (j + off < m) F[(long long)(j + off) * rows + d - off] = val;
                     }
                 }
             }
