@@ -960,7 +960,9 @@ struct Exec {
                 }
                 case ST_GEMM: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
-                    launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                    static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
+                    if (generic_only) launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                    else launch_gemm_dmma((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
                     break;
                 }
                 case ST_LU: {

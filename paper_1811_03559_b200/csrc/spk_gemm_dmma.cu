@@ -1,0 +1,159 @@
+// spk_gemm_dmma.cu — batched FP64 GEMM on the tensor cores (DMMA).
+//
+// C[crow0+i, c] (=|-=) sum_l opA(A)[i, l] * B[brow0+l, c] for a batch of jobs
+// (GemmJob, row-mapped views), i.e. the reference's gemm_minus / gemm_minus_t
+// / block_util mul (src/banded_matrix.cpp:39-51, src/block_util.hpp:29-35)
+// for the reduced-system spike updates, the coupling Schur complements and the
+// retrieval corner products.
+//
+// sm_100a has no tcgen05 FP64 kind; FP64 tensor math is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA).  CTA tile 64x64, K-chunk 16,
+// 4 warps each owning a 32x32 sub-tile = 4x4 DMMA accumulators; A and B
+// chunks are staged through shared memory (cp.async, double-buffered).
+#include "spk_device.cuh"
+#include "spk_launch.h"
+#include "spk_sweep_fast.cuh"
+
+namespace spk {
+
+namespace {
+constexpr int TM = 64, TN = 64, TK = 16;
+// padded strides (doubles): 20 = 40 words keeps each 16-lane phase of the
+// 8-byte fragment loads on distinct banks
+constexpr int SA = TK + 4;  // A tile stored [m][k]
+constexpr int SB = TK + 4;  // B tile stored [n][k]
+
+// resolved view: element (L, c) at p + (rev ? mrows-1-(L-off) : L-off) + c*ld
+struct RV {
+    double* p;
+    long long ld;
+    int rev, off, mrows;
+    __device__ __forceinline__ double* at(int L, int c) const {
+        return p + (rev ? (mrows - 1 - (L - off)) : (L - off)) + (long long)c * ld;
+    }
+};
+__device__ __forceinline__ RV resolve(const Bufs& B, const View& v) {
+    RV r;
+    r.p = B.p[v.buf] + v.base;
+    r.ld = v.ld >= 0 ? v.ld : B.ld[v.buf];
+    r.rev = v.rev;
+    r.off = v.off;
+    r.mrows = v.mrows;
+    return r;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
+    const GemmJob& Jg = jobs[blockIdx.x];
+    const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
+    const int jr = Jg.r, jkk = Jg.kk, transA = Jg.transA, op = Jg.op, brow0 = Jg.brow0, crow0 = Jg.crow0;
+    const int tiles_r = (jr + TM - 1) / TM;
+    const int tr = blockIdx.y % tiles_r;
+    const int tc = blockIdx.y / tiles_r;
+    if (tc * TN >= nc || jr <= 0) return;
+    const RV va = resolve(B, Jg.a), vb = resolve(B, Jg.b), vc = resolve(B, Jg.c);
+    __shared__ __align__(16) double sA[2][TM * SA];
+    __shared__ __align__(16) double sB[2][TN * SB];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int g = lane >> 2, q = lane & 3;
+    const int row0 = tr * TM, col0 = tc * TN;
+
+    auto stage = [=](int buf, int k0) {
+        // A tile: TM x TK, element (i, l) of opA(A)
+        for (int idx = tid; idx < TM * TK; idx += 128) {
+            int i, l;
+            if (transA) {  // A is kk x r: consecutive threads walk down a column of A
+                l = idx % TK;
+                i = idx / TK;
+            } else {
+                i = idx % TM;
+                l = idx / TM;
+            }
+            double* dst = &sA[buf][i * SA + l];
+            const int gi = row0 + i, gl = k0 + l;
+            if (gi < jr && gl < jkk) {
+                const double* src = transA ? va.at(gl, gi) : va.at(gi, gl);
+                cp_async8(dst, src);
+            } else {
+                *dst = 0.0;
+            }
+        }
+        // B tile: TK x TN, stored [n][k]
+        for (int idx = tid; idx < TK * TN; idx += 128) {
+            const int l = idx % TK, c = idx / TK;
+            double* dst = &sB[buf][c * SB + l];
+            const int gl = k0 + l, gc = col0 + c;
+            if (gl < jkk && gc < nc) cp_async8(dst, vb.at(brow0 + gl, gc));
+            else *dst = 0.0;
+        }
+        cp_async_commit();
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    const int nk = (jkk + TK - 1) / TK;
+    stage(0, 0);
+    for (int kc = 0; kc < nk; ++kc) {
+        const int buf = kc & 1;
+        if (kc + 1 < nk) {
+            stage(buf ^ 1, (kc + 1) * TK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* a_s = sA[buf];
+        const double* b_s = sB[buf];
+#pragma unroll
+        for (int ks = 0; ks < TK; ks += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = a_s[(wm + 8 * a + g) * SA + ks + q];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = b_s[(wn + 8 * b + g) * SB + ks + q];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        __syncthreads();
+    }
+    // epilogue: C[row, col] with row = wm+8a+g, col = wn+8b+2q+{0,1}
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int i = row0 + wm + 8 * a + g;
+        if (i >= jr) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = col0 + wn + 8 * b + 2 * q + e;
+                if (c >= nc) continue;
+                double* dst = vc.at(crow0 + i, c);
+                if (op == GM_SET) *dst = acc[a][b][e];
+                else *dst -= acc[a][b][e];
+            }
+    }
+}
+
+void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
+                      cudaStream_t s) {
+    if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
+    const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
+    dim3 g(njobs, tr * tc);
+    k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols);
+    count_launch();
+}
+
+}  // namespace spk

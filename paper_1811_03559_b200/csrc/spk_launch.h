@@ -21,6 +21,8 @@ void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bu
                  cudaStream_t s);
 void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
                  cudaStream_t s);
+void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
+                      cudaStream_t s);
 void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
                     int p, int k, double* bhat, double* chat, cudaStream_t s);
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
