@@ -157,7 +157,10 @@ void prof_drain() {
 // programs
 namespace {
 
-enum StageType { ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS, ST_TRANSPOSE };
+enum StageType {
+    ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS, ST_TRANSPOSE,
+    ST_WCHECK, ST_SCHUR_INIT, ST_DENSE_LU
+};
 
 struct Stage {
     StageType t;
@@ -205,7 +208,9 @@ struct Level {
     int units = 0;
     std::vector<int> uoff, uh;
     std::vector<long long> voff, woff;  // pool offsets, -1 when never formed
-    std::vector<int> pair_part;         // PartDev index per pair
+    std::vector<int> pair_part;         // PartDev index per pair: generic 2k coupling unit
+    std::vector<int> spart;             // PartDev index per pair: k x k Schur-complement unit
+    std::vector<int> gidx;              // flag index per pair (1 = Schur path, 0 = generic)
 };
 
 }  // namespace
@@ -232,7 +237,11 @@ struct spk_fact {
     int* d_boost = nullptr;
     int* d_fell = nullptr;
     int* d_status = nullptr;
-    char* d_blob = nullptr;
+    char* d_blob = nullptr;   // factor program jobs
+    char* d_sblob = nullptr;  // solve program jobs (built once the coupling paths are known)
+    int* d_flags = nullptr;   // per-pair coupling path
+    std::vector<int> flags;   // host copy after factorization
+    int npairs = 0;
     double* d_tfac = nullptr;
     double* d_dinv = nullptr;
     long long tfac_size = 0;
@@ -246,7 +255,7 @@ struct spk_fact {
         // outlive it); no device-wide synchronisation
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
-                        (void*)d_tfac, (void*)d_dinv})
+                        (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags})
             if (q) cudaFreeAsync(q, stream);
     }
 };
@@ -274,6 +283,7 @@ PartDev make_part(long long r0, int m, int akl, int aku, int piv_on, int rev, in
     P.bofs = -1;
     P.tofs = -1;
     P.rowsT = 0;
+    P.guard = -1;
     return P;
 }
 
@@ -337,16 +347,27 @@ void add_couplings(spk_fact& f, long long& fac_cursor) {
     for (size_t l = 0; l + 1 < f.levels.size(); ++l) {
         Level& lv = f.levels[l];
         lv.pair_part.clear();
+        lv.spart.clear();
+        lv.gidx.clear();
         for (int a = 0; a < lv.units / 2; ++a) {
             const int nn = 2 * k;
+            // generic path: the full 2k coupling, pivoted with boosted fallback
             PartDev P = make_part(f.n + (long long)idx * nn, nn, nn - 1, nn - 1, 1, 0, 0);
             P.fallback = 1;
             P.fofs = fac_cursor;
             fac_cursor += (long long)P.m * P.rows;
             P.bofs = fac_cursor;
             fac_cursor += (long long)P.m * P.rows;
+            P.guard = 2 * f.npairs + 0;
             lv.pair_part.push_back((int)f.parts.size());
             f.parts.push_back(P);
+            // Schur path: S = I - W V as a pivoted dense k x k unit (full band)
+            PartDev S = make_part(f.n + (long long)idx * nn + k, k, k - 1, k - 1, 1, 0, 0);
+            S.fofs = fac_cursor;
+            fac_cursor += (long long)S.m * S.rows;
+            lv.spart.push_back((int)f.parts.size());
+            f.parts.push_back(S);
+            lv.gidx.push_back(f.npairs++);
             ++idx;
         }
     }
@@ -452,6 +473,14 @@ struct Builder {
         s.max_elems = (long long)(2 * f.k) * (4 * f.k - 1);
         prog.push_back(s);
     }
+    void cjobs(StageType t, const std::vector<CouplingJob>& jobs) {
+        if (jobs.empty()) return;
+        Stage s{t};
+        s.njobs = (int)jobs.size();
+        s.off = pb.push(jobs);
+        s.max_elems = (long long)f.k * (2 * f.k - 1);
+        prog.push_back(s);
+    }
     void memset_buf(int buf, int cols = -1) {
         Stage s{ST_MEMSET};
         s.buf = buf;
@@ -471,6 +500,7 @@ SweepJob sj(View v, int part, int mode, int lo, int hi, int c0 = 0, int nc = -1)
     j.hi = hi;
     j.c0 = c0;
     j.nc = nc;
+    j.guard = -1;
     return j;
 }
 
@@ -483,6 +513,7 @@ CopyJob cj(View src, View dst, int L0, int L1, int op = CP_COPY, int c0 = 0, int
     j.op = op;
     j.c0 = c0;
     j.nc = nc;
+    j.guard = -1;
     return j;
 }
 
@@ -499,49 +530,92 @@ GemmJob gj(View a, int transA, View b, int brow0, View c, int crow0, int r, int 
     j.kk = kk;
     j.nc = nc;
     j.op = op;
-    j.pad = 0;
+    j.guard = -1;
     return j;
 }
 
 // pair_solve (factorize.cpp:19-32) / pair_solve_transpose (:34-44) over a
-// batch of z blocks: z = {buf, base row, ld}, red regions in buffer `redbuf`.
+// batch of z blocks (z = {buf, base row, ld}).  Two realisations per pair:
+//  * generic: gather red = z[hL-k, hL+k) into its own region, solve with the
+//    pivoted 2k coupling unit, two GEMM updates, scatter back;
+//  * Schur (spk_coupling.cu): in place on z with the k x k unit S = I - W V:
+//      forward   z2 -= W z1; z2 = S^-1 z2; z[0:hL] -= vl z2; z[hL+k:] -= wr[k:] z1
+//      transpose z1 -= wr[k:]^T z[hL+k:]; z2 -= vl[0:hL-k]^T z[0:hL-k];
+//                z2 -= V^T z1; z2 = S^-T z2; z1 -= W^T z2
+// `path` bit 0 emits the generic jobs, bit 1 the Schur jobs; when both are
+// emitted (factor time, before the path is known) the jobs carry guards.
 struct PairZ {
+    int spart;  // Schur unit
+    int gidx;   // flag index of the pair
     int pair_part;
     long long vl_off, wr_off;
     int hL, hR;
     int zbuf;
     long long zbase, zld;
     long long red_row;  // row offset of this job's 2k red region in redbuf
+    int path;           // bit0 generic, bit1 Schur
 };
+
+template <class Jb>
+Jb guarded_job(Jb j, const PairZ& z, int want) {
+    j.guard = (z.path == 3) ? 2 * z.gidx + want : -1;
+    return j;
+}
 
 void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long long redld,
                       int ncols_explicit, bool transpose, int k) {
     if (zs.empty()) return;
     std::vector<CopyJob> gather, scatter;
-    std::vector<SweepJob> s1, s2;
-    std::vector<GemmJob> g;
+    std::vector<SweepJob> s1, s2, t1, t2;
+    std::vector<GemmJob> g, ga, gb, gd, ge;
     const int nc = ncols_explicit;
     for (const PairZ& z : zs) {
         const View zv = view(z.zbuf, z.zbase, 0, 0, 0, z.zld);
-        // red logical row L in [hL-k, hL+k) <-> red region row red_row + L - (hL-k)
-        const View rv_z = view(redbuf, z.red_row, 0, z.hL - k, 0, redld);
-        const View rv = view(redbuf, z.red_row, 0, 0, 2 * k, redld);
-        gather.push_back(cj(zv, rv_z, z.hL - k, z.hL + k, CP_COPY, 0, nc));
-        scatter.push_back(cj(rv_z, zv, z.hL - k, z.hL + k, CP_COPY, 0, nc));
-        const View vl = view(B_POOL, z.vl_off, 0, 0, 0, z.hL);
-        const View wr = view(B_POOL, z.wr_off + k, 0, 0, 0, z.hR);  // rows k.. of wr
-        if (!transpose) {
-            s1.push_back(sj(rv, z.pair_part, SW_FWD_L, 0, 0, 0, nc));
-            s2.push_back(sj(rv, z.pair_part, SW_BWD_U, 0, 2 * k - 1, 0, nc));
-            if (z.hL - k > 0) g.push_back(gj(vl, 0, rv, k, zv, 0, z.hL - k, k, GM_SUB, nc));
-            if (z.hR - k > 0) g.push_back(gj(wr, 0, rv, 0, zv, z.hL + k, z.hR - k, k, GM_SUB, nc));
-        } else {
-            if (z.hR - k > 0) g.push_back(gj(wr, 1, zv, z.hL + k, rv, 0, k, z.hR - k, GM_SUB, nc));
-            if (z.hL - k > 0) g.push_back(gj(vl, 1, zv, 0, rv, k, k, z.hL - k, GM_SUB, nc));
-            s1.push_back(sj(rv, z.pair_part, SW_FWD_UT, 0, 0, 0, nc));
-            s2.push_back(sj(rv, z.pair_part, SW_BWD_LT, 0, 0, 0, nc));
+        const int hL = z.hL, hR = z.hR;
+        if (z.path & 1) {
+            // red logical row L in [hL-k, hL+k) <-> red region row red_row + L - (hL-k)
+            const View rv_z = view(redbuf, z.red_row, 0, hL - k, 0, redld);
+            const View rv = view(redbuf, z.red_row, 0, 0, 2 * k, redld);
+            gather.push_back(guarded_job(cj(zv, rv_z, hL - k, hL + k, CP_COPY, 0, nc), z, 0));
+            scatter.push_back(guarded_job(cj(rv_z, zv, hL - k, hL + k, CP_COPY, 0, nc), z, 0));
+            const View vl = view(B_POOL, z.vl_off, 0, 0, 0, hL);
+            const View wr = view(B_POOL, z.wr_off + k, 0, 0, 0, hR);  // rows k.. of wr
+            if (!transpose) {
+                s1.push_back(guarded_job(sj(rv, z.pair_part, SW_FWD_L, 0, 0, 0, nc), z, 0));
+                s2.push_back(guarded_job(sj(rv, z.pair_part, SW_BWD_U, 0, 2 * k - 1, 0, nc), z, 0));
+                if (hL - k > 0) g.push_back(guarded_job(gj(vl, 0, rv, k, zv, 0, hL - k, k, GM_SUB, nc), z, 0));
+                if (hR - k > 0) g.push_back(guarded_job(gj(wr, 0, rv, 0, zv, hL + k, hR - k, k, GM_SUB, nc), z, 0));
+            } else {
+                if (hR - k > 0) g.push_back(guarded_job(gj(wr, 1, zv, hL + k, rv, 0, k, hR - k, GM_SUB, nc), z, 0));
+                if (hL - k > 0) g.push_back(guarded_job(gj(vl, 1, zv, 0, rv, k, k, hL - k, GM_SUB, nc), z, 0));
+                s1.push_back(guarded_job(sj(rv, z.pair_part, SW_FWD_UT, 0, 0, 0, nc), z, 0));
+                s2.push_back(guarded_job(sj(rv, z.pair_part, SW_BWD_LT, 0, 0, 0, nc), z, 0));
+            }
+        }
+        if (z.path & 2) {
+            const View z2 = view(z.zbuf, z.zbase + hL, 0, 0, k, z.zld);  // rows [hL, hL+k)
+            const View W = view(B_POOL, z.wr_off, 0, 0, 0, hR);            // wr[0:k]
+            const View Wk = view(B_POOL, z.wr_off + k, 0, 0, 0, hR);       // wr[k:hR]
+            const View V = view(B_POOL, z.vl_off + hL - k, 0, 0, 0, hL);   // vl[hL-k:hL]
+            const View Vt = view(B_POOL, z.vl_off, 0, 0, 0, hL);           // vl[0:hL-k]
+            if (!transpose) {
+                ga.push_back(guarded_job(gj(W, 0, zv, hL - k, zv, hL, k, k, GM_SUB, nc), z, 1));
+                t1.push_back(guarded_job(sj(z2, z.spart, SW_FWD_L, 0, 0, 0, nc), z, 1));
+                t2.push_back(guarded_job(sj(z2, z.spart, SW_BWD_U, 0, k - 1, 0, nc), z, 1));
+                gd.push_back(guarded_job(gj(V, 0, zv, hL, zv, hL - k, k, k, GM_SUB, nc), z, 1));
+                if (hL - k > 0) ge.push_back(guarded_job(gj(Vt, 0, zv, hL, zv, 0, hL - k, k, GM_SUB, nc), z, 1));
+                if (hR - k > 0) ge.push_back(guarded_job(gj(Wk, 0, zv, hL - k, zv, hL + k, hR - k, k, GM_SUB, nc), z, 1));
+            } else {
+                if (hR - k > 0) ga.push_back(guarded_job(gj(Wk, 1, zv, hL + k, zv, hL - k, k, hR - k, GM_SUB, nc), z, 1));
+                if (hL - k > 0) ga.push_back(guarded_job(gj(Vt, 1, zv, 0, zv, hL, k, hL - k, GM_SUB, nc), z, 1));
+                gb.push_back(guarded_job(gj(V, 1, zv, hL - k, zv, hL, k, k, GM_SUB, nc), z, 1));
+                t1.push_back(guarded_job(sj(z2, z.spart, SW_FWD_UT, 0, 0, 0, nc), z, 1));
+                t2.push_back(guarded_job(sj(z2, z.spart, SW_BWD_LT, 0, 0, 0, nc), z, 1));
+                ge.push_back(guarded_job(gj(W, 1, zv, hL, zv, hL - k, k, k, GM_SUB, nc), z, 1));
+            }
         }
     }
+    // generic path
     b.copy(gather);
     if (!transpose) {
         b.sweep(s1);
@@ -553,6 +627,20 @@ void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long
         b.sweep(s2);
     }
     b.copy(scatter);
+    // Schur path
+    if (!transpose) {
+        b.gemm(ga);
+        b.sweep(t1);
+        b.sweep(t2);
+        b.gemm(gd);
+        b.gemm(ge);
+    } else {
+        b.gemm(ga);
+        b.gemm(gb);
+        b.sweep(t1);
+        b.sweep(t2);
+        b.gemm(ge);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -629,13 +717,17 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
         b.sweep(bu);
         b.copy(tips);
     }
-    // reduced hierarchy
+    // reduced hierarchy: per level, both coupling paths guarded by the
+    // device-side per-pair flag (Schur when max|W| <= 1 and S is nonsingular)
     const int L = (int)f.levels.size() - 1;
+    const bool schur_ok = k <= 160;
+    const int both = schur_ok ? 3 : 1;
     long long red_cursor = 0;
     for (int l = 0; l < L; ++l) {
         const Level& lv = f.levels[l];
         const int np = lv.units / 2;
-        std::vector<CouplingJob> cpl;
+        std::vector<CouplingJob> cplS, cplG;
+        std::vector<GemmJob> sgemm;
         std::vector<int> lus;
         for (int a = 0; a < np; ++a) {
             CouplingJob c;
@@ -643,12 +735,31 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             c.wr_off = lv.woff[2 * a + 1];
             c.hL = lv.uh[2 * a];
             c.hR = lv.uh[2 * a + 1];
-            c.part = lv.pair_part[a];
             c.k = k;
-            cpl.push_back(c);
+            c.guard = lv.gidx[a];
+            c.pad = 0;
+            c.part = lv.pair_part[a];
+            cplG.push_back(c);
             lus.push_back(lv.pair_part[a]);
+            if (schur_ok) {
+                c.part = lv.spart[a];
+                cplS.push_back(c);
+                const PartDev& S = f.parts[lv.spart[a]];
+                const View Sv = view(B_FAC, S.fofs + (k - 1), 0, 0, 0, S.rows - 1);  // dense k x k
+                const View W = view(B_POOL, c.wr_off, 0, 0, 0, c.hR);
+                const View V = view(B_POOL, c.vl_off, 0, 0, 0, c.hL);
+                GemmJob gjb = gj(W, 0, V, c.hL - k, Sv, 0, k, k, GM_SUB, k);
+                gjb.guard = 2 * lv.gidx[a] + 1;
+                sgemm.push_back(gjb);
+            }
         }
-        b.cpl(cpl);
+        if (schur_ok) {
+            b.cjobs(ST_WCHECK, cplS);
+            b.cjobs(ST_SCHUR_INIT, cplS);
+            b.gemm(sgemm);
+            b.cjobs(ST_DENSE_LU, cplS);
+        }
+        b.cpl(cplG);
         b.lu(lus);
         if (l + 1 == L) break;
         const Level& nx = f.levels[l + 1];
@@ -660,16 +771,16 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
                 const View src = view(B_POOL, lv.voff[2 * a + 1], 0, hL, hR, hR);
                 const View dst = view(B_POOL, nx.voff[a], 0, 0, H, H);
                 init.push_back(cj(src, dst, hL, H, CP_COPY, 0, k));
-                zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], hL, hR, B_POOL,
-                                   nx.voff[a], H, red_cursor});
+                zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
+                                   hL, hR, B_POOL, nx.voff[a], H, red_cursor, both});
                 red_cursor += 2 * k;
             }
             if (nx.woff[a] >= 0) {
                 const View src = view(B_POOL, lv.woff[2 * a], 0, 0, hL, hL);
                 const View dst = view(B_POOL, nx.woff[a], 0, 0, H, H);
                 init.push_back(cj(src, dst, 0, hL, CP_COPY, 0, k));
-                zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], hL, hR, B_POOL,
-                                   nx.woff[a], H, red_cursor});
+                zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
+                                   hL, hR, B_POOL, nx.woff[a], H, red_cursor, both});
                 red_cursor += 2 * k;
             }
         }
@@ -701,9 +812,9 @@ void build_reduced_solve(spk_fact& f, Builder& b, bool transpose, long long aux_
         const Level& lv = f.levels[l];
         std::vector<PairZ> zs;
         for (int a = 0; a < lv.units / 2; ++a)
-            zs.push_back(PairZ{lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1], lv.uh[2 * a],
-                               lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
-                               level_base[l] + 2LL * k * a});
+            zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
+                               lv.uh[2 * a], lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
+                               level_base[l] + 2LL * k * a, f.flags[lv.gidx[a]] ? 2 : 1});
         emit_pair_solves(b, zs, B_AUX, -1, -1, transpose, k);
     }
 }
@@ -933,9 +1044,9 @@ struct Exec {
         }
     }
 
-    void run(const Program& prog) {
+    void run(const Program& prog, const char* blob) {
         for (const Stage& st : prog) {
-            const char* jobs = f.d_blob + st.off;
+            const char* jobs = blob + st.off;
             const double mult = st.max_nc < 0 ? ncols : 1.0;
             ProfScope ps((int)st.t, s, st.flops_per_col * mult, st.bytes_per_col * mult);
             switch (st.t) {
@@ -984,12 +1095,23 @@ struct Exec {
                                             f.d_amax, s);
                     }
                     launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
-                                   f.boost_eps, f.d_boost, f.d_fell, f.d_status, s);
+                                   f.boost_eps, f.d_boost, f.d_fell, f.d_status, f.d_flags, s);
                     break;
                 }
                 case ST_CPL:
                     launch_build_coupling((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts,
-                                          f.d_pool, f.d_fac, f.d_piv, f.d_amax, s);
+                                          f.d_pool, f.d_fac, f.d_piv, f.d_amax, f.d_flags, s);
+                    break;
+                case ST_WCHECK:
+                    launch_wcheck((const CouplingJob*)jobs, st.njobs, f.d_pool, f.d_flags, s);
+                    break;
+                case ST_SCHUR_INIT:
+                    launch_schur_init((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts, f.d_fac,
+                                      f.d_piv, f.d_flags, s);
+                    break;
+                case ST_DENSE_LU:
+                    launch_dense_lu((const CouplingJob*)jobs, st.njobs, f.k, f.d_parts, f.d_fac, f.d_piv,
+                                    f.d_flags, s);
                     break;
                 case ST_MEMSET: {
                     const int nc = st.cols < 0 ? ncols : st.cols;
@@ -1097,17 +1219,6 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     f.aux_rows = std::max<long long>((long long)std::max(p - 1, 0) * 2 * k + 2LL * wmax + 2LL * k, 1);
     ProgramBuilder pb;
     build_factor_program(f, pb);
-    if (!f.reduced_only) {
-        build_forward_program(f, pb);
-        build_transpose_program(f, pb);
-    } else {
-        // reduced-only: forward/transpose programs are just the reduced solves
-        Builder bf{f, pb, f.prog_fwd}, bt{f, pb, f.prog_tr};
-        if (p > 1 && k > 0) {
-            build_reduced_solve(f, bf, false, 0);
-            build_reduced_solve(f, bt, true, 0);
-        }
-    }
     // device allocations (stream ordered)
     const int nparts = (int)f.parts.size();
     f.d_parts = dalloc<PartDev>(nparts, s);
@@ -1122,6 +1233,8 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     f.d_blob = dalloc<char>(pb.blob.size(), s);
     f.d_tfac = dalloc<double>(f.tfac_size, s);
     f.d_dinv = dalloc<double>(f.n, s);
+    f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
+    ck(cudaMemsetAsync(f.d_flags, 0, sizeof(int) * std::max(f.npairs, 1), s), "memset");
     ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
     ck(cudaMemcpyAsync(f.d_bounds, f.bounds.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s),
        "upload");
@@ -1152,13 +1265,38 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     f.factor_sweeps.assign(f.p, 0);
     if (!f.reduced_only && f.p > 1 && f.k > 0)
         for (int i = 1; i + 1 < f.p; ++i) f.factor_sweeps[i] = 3;
+    // coupling paths are known now: compile the solve programs without guards
+    f.flags.assign(std::max(f.npairs, 1), 0);
+    if (f.npairs > 0)
+        ck(cudaMemcpy(f.flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost), "flags");
+    ProgramBuilder pb;
+    f.prog_fwd.clear();
+    f.prog_tr.clear();
+    if (!f.reduced_only) {
+        build_forward_program(f, pb);
+        build_transpose_program(f, pb);
+    } else {
+        Builder bf{f, pb, f.prog_fwd}, bt{f, pb, f.prog_tr};
+        if (f.p > 1 && f.k > 0) {
+            build_reduced_solve(f, bf, false, 0);
+            build_reduced_solve(f, bt, true, 0);
+        }
+    }
+    f.d_sblob = dalloc<char>(pb.blob.size(), s);
+    if (!pb.blob.empty())
+        ck(cudaMemcpyAsync(f.d_sblob, pb.blob.data(), pb.blob.size(), cudaMemcpyHostToDevice, s), "upload");
 }
 
-Bufs make_bufs() {
+Bufs make_bufs(const spk_fact* f = nullptr) {
     Bufs B;
     for (int i = 0; i < kMaxBufs; ++i) {
         B.p[i] = nullptr;
         B.ld[i] = 1;
+    }
+    B.flags = f ? f->d_flags : nullptr;
+    if (f) {
+        B.p[B_FAC] = f->d_fac;
+        B.p[B_POOL] = f->d_pool;
     }
     return B;
 }
@@ -1399,7 +1537,7 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
             fs = dalloc<double>((size_t)n * 2 * f->k, s);
             auxf = dalloc<double>((size_t)f->auxf_rows * f->k, s);
         }
-        Bufs B = make_bufs();
+        Bufs B = make_bufs(f.get());
         B.p[B_POOL] = f->d_pool;
         B.ld[B_POOL] = 1;
         B.p[B_FS] = fs;
@@ -1409,7 +1547,7 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         Exec ex{*f, s, B, f->k};
         ex.n = n;
         ex.band = dband;
-        ex.run(f->prog_factor);
+        ex.run(f->prog_factor, f->d_blob);
         if (fs) ck(cudaFreeAsync(fs, s), "free");
         if (auxf) ck(cudaFreeAsync(auxf, s), "free");
         if (tmp) ck(cudaFreeAsync(tmp, s), "free");
@@ -1502,22 +1640,59 @@ spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu
         if (l < 0 || l + 1 >= (int)f->levels.size()) fail(SPK_ERANGE, "coupling: level out of range");
         const Level& lv = f->levels[l];
         if (a < 0 || a >= (int)lv.pair_part.size()) fail(SPK_ERANGE, "coupling: pair out of range");
-        const PartDev& P = f->parts[lv.pair_part[a]];
-        const int nn = P.m;
-        std::vector<double> band((size_t)P.m * P.rows);
-        ck(cudaMemcpy(band.data(), f->d_fac + P.fofs, sizeof(double) * band.size(), cudaMemcpyDeviceToHost),
+        const int k = f->k, nn = 2 * k;
+        const bool schur = f->flags.size() > (size_t)lv.gidx[a] && f->flags[lv.gidx[a]] == 1;
+        auto unpack = [&](const PartDev& P, std::vector<double>& dense, std::vector<int>& pv) {
+            std::vector<double> band((size_t)P.m * P.rows);
+            ck(cudaMemcpy(band.data(), f->d_fac + P.fofs, sizeof(double) * band.size(), cudaMemcpyDeviceToHost),
+               "coupling");
+            dense.assign((size_t)P.m * P.m, 0.0);
+            for (int j = 0; j < P.m; ++j)
+                for (int i = 0; i < P.m; ++i) {
+                    const int q = P.d + i - j;
+                    dense[(size_t)j * P.m + i] = (q >= 0 && q < P.rows) ? band[(size_t)j * P.rows + q] : 0.0;
+                }
+            pv.resize(P.m);
+            ck(cudaMemcpy(pv.data(), f->d_piv + P.r0, sizeof(int) * P.m, cudaMemcpyDeviceToHost), "coupling");
+        };
+        std::vector<double> dense;
+        std::vector<int> pv;
+        if (!schur) {
+            unpack(f->parts[lv.pair_part[a]], dense, pv);
+            std::copy(dense.begin(), dense.end(), lu);
+            if (piv) std::copy(pv.begin(), pv.end(), piv);
+            if (fell_back) {
+                int fb = 0;
+                ck(cudaMemcpy(&fb, f->d_fell + lv.pair_part[a], sizeof(int), cudaMemcpyDeviceToHost), "coupling");
+                *fell_back = fb;
+            }
+            return;
+        }
+        // Schur path: [[I, 0], [W, L_S]] [[I, V], [0, U_S]] with rows k.. permuted by P_S
+        unpack(f->parts[lv.spart[a]], dense, pv);
+        const int hL = lv.uh[2 * a], hR = lv.uh[2 * a + 1];
+        std::vector<double> vl((size_t)hL * k), wr((size_t)hR * k);
+        ck(cudaMemcpy(vl.data(), f->d_pool + lv.voff[2 * a], sizeof(double) * vl.size(), cudaMemcpyDeviceToHost),
            "coupling");
+        ck(cudaMemcpy(wr.data(), f->d_pool + lv.woff[2 * a + 1], sizeof(double) * wr.size(), cudaMemcpyDeviceToHost),
+           "coupling");
+        std::fill(lu, lu + (size_t)nn * nn, 0.0);
         for (int j = 0; j < nn; ++j)
             for (int i = 0; i < nn; ++i) {
-                const int q = P.d + i - j;
-                lu[(size_t)j * nn + i] = (q >= 0 && q < P.rows) ? band[(size_t)j * P.rows + q] : 0.0;
+                double v = 0.0;
+                if (j < k) {
+                    if (i == j) v = 1.0;
+                    else if (i >= k) v = wr[(size_t)j * hR + (i - k)];
+                } else if (i < k) {
+                    v = vl[(size_t)(j - k) * hL + (hL - k + i)];
+                } else {
+                    v = dense[(size_t)(j - k) * k + (i - k)];
+                }
+                lu[(size_t)j * nn + i] = v;
             }
-        if (piv) ck(cudaMemcpy(piv, f->d_piv + P.r0, sizeof(int) * nn, cudaMemcpyDeviceToHost), "coupling");
-        if (fell_back) {
-            int fb = 0;
-            ck(cudaMemcpy(&fb, f->d_fell + lv.pair_part[a], sizeof(int), cudaMemcpyDeviceToHost), "coupling");
-            *fell_back = fb;
-        }
+        if (piv)
+            for (int i = 0; i < nn; ++i) piv[i] = i < k ? i : k + pv[i - k];
+        if (fell_back) *fell_back = 0;
     });
 }
 
@@ -1577,7 +1752,7 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
             T = dalloc<double>((size_t)2 * f.p * f.k * nrhs, s);
             AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
         }
-        Bufs B = make_bufs();
+        Bufs B = make_bufs(&f);
         B.p[B_X] = dX;
         B.ld[B_X] = lx;
         B.p[B_F] = const_cast<double*>(dF);
@@ -1592,7 +1767,7 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
         B.ld[B_POOL] = 1;
         Exec ex{f, s, B, nrhs};
         ex.n = n;
-        ex.run(transpose ? f.prog_tr : f.prog_fwd);
+        ex.run(transpose ? f.prog_tr : f.prog_fwd, f.d_sblob);
         if (mem == SPK_MEM_HOST)
             ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, dX, sizeof(double) * n, sizeof(double) * n, nrhs,
                                  cudaMemcpyDeviceToHost, s),
@@ -1646,12 +1821,12 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
                 }
             }
             double* auxf = dalloc<double>((size_t)f.auxf_rows * k, s);
-            Bufs B = make_bufs();
+            Bufs B = make_bufs(&f);
             B.p[B_POOL] = f.d_pool;
             B.p[B_AUX] = auxf;
             B.ld[B_AUX] = f.auxf_rows;
             Exec ex{f, s, B, k};
-            ex.run(f.prog_factor);
+            ex.run(f.prog_factor, f.d_blob);
             ck(cudaFreeAsync(auxf, s), "free");
         }
         finish_factor(f, s);
@@ -1670,14 +1845,14 @@ spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z,
         double* T = dalloc<double>((size_t)rows * ncols, s);
         double* AUX = dalloc<double>((size_t)f.aux_rows * ncols, s);
         ck(cudaMemcpyAsync(T, z, sizeof(double) * rows * ncols, cudaMemcpyHostToDevice, s), "z upload");
-        Bufs B = make_bufs();
+        Bufs B = make_bufs(&f);
         B.p[B_T] = T;
         B.ld[B_T] = rows;
         B.p[B_AUX] = AUX;
         B.ld[B_AUX] = f.aux_rows;
         B.p[B_POOL] = f.d_pool;
         Exec ex{f, s, B, ncols};
-        ex.run(transpose ? f.prog_tr : f.prog_fwd);
+        ex.run(transpose ? f.prog_tr : f.prog_fwd, f.d_sblob);
         ck(cudaMemcpyAsync(z, T, sizeof(double) * rows * ncols, cudaMemcpyDeviceToHost, s), "z download");
         ck(cudaFreeAsync(T, s), "free");
         ck(cudaFreeAsync(AUX, s), "free");

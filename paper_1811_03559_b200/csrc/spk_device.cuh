@@ -10,13 +10,19 @@
 namespace spk {
 
 constexpr int kMaxBufs = 8;
-enum BufId { B_X = 0, B_F = 1, B_S = 2, B_T = 3, B_AUX = 4, B_POOL = 5, B_FS = 6 };
+enum BufId { B_X = 0, B_F = 1, B_S = 2, B_T = 3, B_AUX = 4, B_POOL = 5, B_FS = 6, B_FAC = 7 };
 
 // Per call buffer table, passed by value.
 struct Bufs {
     double* p[kMaxBufs];
     long long ld[kMaxBufs];
+    const int* flags;  // per-pair coupling path flags (job guards)
 };
+
+// Job guard: -1 = unconditional, else run only if flags[g >> 1] == (g & 1).
+__host__ __device__ __forceinline__ bool guard_ok(const int* flags, int g) {
+    return g < 0 || flags[g >> 1] == (g & 1);
+}
 
 // Geometry of one band LU "unit": a SPIKE partition (kernels.cpp:29-42 layout:
 // rows = ubw+kl+1 packed rows per column, diagonal at packed row d = ubw) or a
@@ -33,6 +39,8 @@ struct PartDev {
     int pivoting;
     int fallback;    // pivoted-with-boosted-fallback (coupling blocks)
     int rowsT;       // row-major copy: row i holds (i, i-kl .. i+ubw) at [kl + c - i]
+    int guard;       // job guard for generic coupling units (-1: none)
+    int pad;
 };
 
 // Row-mapped view of a column-major buffer.  Logical row L maps to physical
@@ -54,6 +62,7 @@ struct SweepJob {
     int mode;
     int lo, hi;
     int c0, nc;  // column range (nc < 0: all call columns)
+    int guard;
 };
 
 enum CopyOp { CP_COPY = 0, CP_ADD = 1, CP_SUB = 2, CP_ZERO = 3 };
@@ -63,6 +72,7 @@ struct CopyJob {
     int L0, L1;  // logical rows [L0, L1) of both views
     int op;
     int c0, nc;  // nc < 0: call columns
+    int guard;
 };
 
 enum GemmOp { GM_SET = 0, GM_SUB = 1 };
@@ -75,7 +85,7 @@ struct GemmJob {
     int brow0, crow0;
     int r, kk, nc;  // nc < 0: call columns
     int op;
-    int pad;
+    int guard;
 };
 
 // Coupling construction for one pair of reduced units (factorize.cpp:94-101):
@@ -86,6 +96,8 @@ struct CouplingJob {
     int hL, hR;
     int part;
     int k;
+    int guard;  // flag index (pair)
+    int pad;
 };
 
 }  // namespace spk

@@ -51,6 +51,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
     const GemmJob& Jg = jobs[blockIdx.x];
+    if (!guard_ok(B.flags, Jg.guard)) return;
     const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
     const int jr = Jg.r, jkk = Jg.kk, transA = Jg.transA, op = Jg.op, brow0 = Jg.brow0, crow0 = Jg.crow0;
     const int tiles_r = (jr + TM - 1) / TM;

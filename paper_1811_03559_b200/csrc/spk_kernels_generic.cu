@@ -77,9 +77,10 @@ __global__ void k_band_lu(const int* __restrict__ units, const PartDev* __restri
                           double* __restrict__ fac, int* __restrict__ piv_pool,
                           const unsigned long long* __restrict__ amax_bits, double boost_eps,
                           int* __restrict__ boost_cnt, int* __restrict__ fell_back,
-                          int* __restrict__ status) {
+                          int* __restrict__ status, const int* __restrict__ flags) {
     const int u = units[blockIdx.x];
     const PartDev P = parts[u];
+    if (P.guard >= 0 && !guard_ok(flags, P.guard)) return;
     double* F = fac + P.fofs;
     int* piv = piv_pool + P.r0;
     const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
@@ -187,6 +188,7 @@ __global__ void k_sweep(const SweepJob* __restrict__ jobs, const PartDev* __rest
                         const double* __restrict__ fac, const int* __restrict__ piv_pool, Bufs B,
                         int ncols) {
     const SweepJob J = jobs[blockIdx.x];
+    if (!guard_ok(B.flags, J.guard)) return;
     const int wpb = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nc = J.nc >= 0 ? J.nc : ncols;
@@ -277,6 +279,7 @@ __global__ void k_sweep(const SweepJob* __restrict__ jobs, const PartDev* __rest
 // Row-mapped block copy / add / subtract / zero.
 __global__ void k_copy(const CopyJob* __restrict__ jobs, Bufs B, int ncols) {
     const CopyJob J = jobs[blockIdx.y];
+    if (!guard_ok(B.flags, J.guard)) return;
     const int nc = J.nc >= 0 ? J.nc : ncols;
     const int rowsn = J.L1 - J.L0;
     const long long total = (long long)rowsn * nc;
@@ -299,6 +302,7 @@ __global__ void k_copy(const CopyJob* __restrict__ jobs, Bufs B, int ncols) {
 // Small batched GEMM, 32x32 output tile per CTA (256 threads, 4 outputs each).
 __global__ void k_gemm(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
     const GemmJob J = jobs[blockIdx.x];
+    if (!guard_ok(B.flags, J.guard)) return;
     const int nc = J.nc >= 0 ? J.nc : ncols;
     const int tiles_r = (J.r + 31) / 32;
     const int tr = blockIdx.y % max(tiles_r, 1);
@@ -375,8 +379,9 @@ __global__ void k_corners(const double* __restrict__ band, long long n, int akl,
 __global__ void k_build_coupling(const CouplingJob* __restrict__ jobs,
                                  const PartDev* __restrict__ parts, const double* __restrict__ pool,
                                  double* __restrict__ fac, int* __restrict__ piv_pool,
-                                 unsigned long long* __restrict__ amax_bits) {
+                                 unsigned long long* __restrict__ amax_bits, const int* __restrict__ flags) {
     const CouplingJob J = jobs[blockIdx.y];
+    if (J.guard >= 0 && !guard_ok(flags, 2 * J.guard)) return;  // generic path: flag == 0
     const PartDev P = parts[J.part];
     const int k = J.k, nn = 2 * k;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nn; j += gridDim.x * blockDim.x)
@@ -471,10 +476,10 @@ void launch_fill_factors(const double* band, long long n, int akl, int aku, cons
 
 void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
                     const unsigned long long* amax, double boost_eps, int* boost_cnt,
-                    int* fell_back, int* status, cudaStream_t s) {
+                    int* fell_back, int* status, const int* flags, cudaStream_t s) {
     if (nunits <= 0) return;
     k_band_lu<<<nunits, 256, 0, s>>>(d_units, d_parts, fac, piv, amax, boost_eps, boost_cnt,
-                                     fell_back, status);
+                                     fell_back, status, flags);
     count_launch();
 }
 
@@ -514,10 +519,10 @@ void launch_corners(const double* band, long long n, int akl, int aku, const lon
 
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
                            const PartDev* d_parts, const double* pool, double* fac, int* piv,
-                           unsigned long long* amax, cudaStream_t s) {
+                           unsigned long long* amax, const int* flags, cudaStream_t s) {
     if (njobs <= 0) return;
     dim3 g(grid_for(max_elems, 256, 256), njobs);
-    k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, piv, amax);
+    k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, piv, amax, flags);
     count_launch();
 }
 

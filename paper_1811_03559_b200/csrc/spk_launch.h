@@ -14,7 +14,7 @@ void launch_fill_factors(const double* band, long long n, int akl, int aku, cons
                          cudaStream_t s);
 void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
                     const unsigned long long* amax, double boost_eps, int* boost_cnt,
-                    int* fell_back, int* status, cudaStream_t s);
+                    int* fell_back, int* status, const int* flags, cudaStream_t s);
 void launch_sweep(const SweepJob* d_jobs, int njobs, int max_nc, const PartDev* d_parts,
                   const double* fac, const int* piv, const Bufs& B, int ncols, cudaStream_t s);
 void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bufs& B, int ncols,
@@ -27,7 +27,12 @@ void launch_corners(const double* band, long long n, int akl, int aku, const lon
                     int p, int k, double* bhat, double* chat, cudaStream_t s);
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
                            const PartDev* d_parts, const double* pool, double* fac, int* piv,
-                           unsigned long long* amax, cudaStream_t s);
+                           unsigned long long* amax, const int* flags, cudaStream_t s);
+void launch_wcheck(const CouplingJob* d_jobs, int njobs, const double* pool, int* flags, cudaStream_t s);
+void launch_schur_init(const CouplingJob* d_jobs, int njobs, long long max_elems, const PartDev* d_parts,
+                       double* fac, int* piv, const int* flags, cudaStream_t s);
+void launch_dense_lu(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, double* fac, int* piv,
+                     int* flags, cudaStream_t s);
 void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,
                         long long ldx, int ncols, int transpose, double* Y, long long ldy,
                         cudaStream_t s);

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(640) k_sweep_fast(FastSweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
 
     const SweepJob J = A.jobs[blockIdx.x];
+    if (!guard_ok(A.B.flags, J.guard)) return;
     const PartDev P = A.parts[J.part];
     const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
     const int nwarps = blockDim.x >> 5;
