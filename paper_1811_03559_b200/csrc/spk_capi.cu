@@ -96,10 +96,12 @@ struct ProfRec {
 thread_local bool g_prof_on = false;
 thread_local std::vector<ProfRec> g_prof;
 thread_local std::vector<cudaEvent_t> g_evpool;
-constexpr int kNumClasses = 10;
-const char* kClassName[kNumClasses] = {"sweep",     "copy",      "gemm", "band_lu", "coupling",
-                                       "memset",    "memcpy_fx", "memcpy_fs", "fill_factors", "corners"};
-enum { PC_FILL = 8, PC_CORNERS = 9 };
+// one class per StageType (same order), then the factorization prologue
+constexpr int kNumClasses = 14;
+const char* kClassName[kNumClasses] = {"sweep",     "copy",       "gemm",         "band_lu",  "coupling",
+                                       "memset",    "memcpy_fx",  "memcpy_fs",    "transpose", "wcheck",
+                                       "schur_init", "dense_lu",  "fill_factors", "corners"};
+enum { PC_FILL = 12, PC_CORNERS = 13 };
 struct ProfAcc {
     double ms = 0, flops = 0, bytes = 0;
     long long launches = 0;
