@@ -135,6 +135,12 @@ spk_status spk_reduced_create(const double *vt, const double *vb, const double *
 spk_status spk_reduced_solve(const spk_reduced *r, int32_t transpose, double *z /* host 2pk x ncols */,
                              int32_t ncols, int64_t *couplings);
 int32_t spk_reduced_levels(const spk_reduced *r);
+/* The reduced-system solve of a factorization on its own (2pk tip block). */
+spk_status spk_fact_reduced_solve(const spk_fact *f, int32_t transpose, double *z, int32_t ncols,
+                                  int64_t *couplings);
+/* Test/debug hook: copy the packed LU pool (0), row-major copies (1) or 1/u_jj
+ * (2) to out (may be NULL); returns the element count. */
+int64_t spk_fact_dump(const spk_fact *f, int32_t which, double *out);
 int32_t spk_reduced_boost_warnings(const spk_reduced *r);
 void spk_reduced_destroy(spk_reduced *r);
 

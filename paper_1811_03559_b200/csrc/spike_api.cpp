@@ -1,0 +1,399 @@
+// spike_api.cpp — the reference's C++ API (namespace spike) over the C-ABI.
+//
+// Host-only glue: argument checks and exception types as in the reference
+// (SURVEY.md 8(b)), C-ABI calls for everything numerical, and host mirrors of
+// the factorization fields the reference's tests introspect.
+#include "../../include/spike/spike_b200.hpp"
+
+#include "../../include/spike_b200.h"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+namespace spike {
+
+namespace {
+
+[[noreturn]] void rethrow(spk_status st) {
+    const std::string msg = spk_last_error();
+    switch (st) {
+        case SPK_EINVAL: throw std::invalid_argument(msg);
+        case SPK_EDOMAIN: throw std::domain_error(msg);
+        case SPK_ERANGE: throw std::out_of_range(msg);
+        case SPK_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+void check(spk_status st) {
+    if (st != SPK_OK) rethrow(st);
+}
+
+std::vector<int32_t> kinds_of(const PartitionPlan& plan) {
+    std::vector<int32_t> k(plan.p, SPK_INNER_SINGLE);
+    for (int i = 0; i < plan.p && i < (int)plan.kinds.size(); ++i) k[i] = static_cast<int32_t>(plan.kinds[i]);
+    return k;
+}
+
+DenseBlock fetch_tip(spk_fact* f, int which, int i, int k) {
+    DenseBlock b(k, k);
+    check(spk_fact_tip(f, which, i, b.data.data()));
+    return b;
+}
+
+std::vector<int> level_units(int p) {
+    std::vector<int> u;
+    for (int x = p; x > 1; x = (x + 1) / 2) u.push_back(x);
+    return u;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ storage
+BandedMatrix::BandedMatrix(int n, int kl, int ku) : n_(n), kl_(kl), ku_(ku) {
+    if (n < 1) throw std::invalid_argument("BandedMatrix: n must be >= 1");
+    if (kl < 0 || ku < 0 || kl >= n || ku >= n) throw std::invalid_argument("BandedMatrix: need 0 <= kl,ku < n");
+    data_.assign(static_cast<std::size_t>(ld()) * n, 0.0);
+}
+
+BandedMatrix BandedMatrix::identity(int n) {
+    BandedMatrix a(n, 0, 0);
+    std::fill(a.data_.begin(), a.data_.end(), 1.0);
+    return a;
+}
+
+bool BandedMatrix::in_band(int i, int j) const {
+    return i >= 0 && j >= 0 && i < n_ && j < n_ && i - j <= kl_ && j - i <= ku_;
+}
+
+double BandedMatrix::at(int i, int j) const {
+    if (i < 0 || j < 0 || i >= n_ || j >= n_) throw std::out_of_range("BandedMatrix::at: index out of range");
+    return in_band(i, j) ? data_[static_cast<std::size_t>(j) * ld() + ku_ + i - j] : 0.0;
+}
+
+void BandedMatrix::set(int i, int j, double v) {
+    if (!in_band(i, j)) throw std::out_of_range("BandedMatrix::set: entry outside the band");
+    data_[static_cast<std::size_t>(j) * ld() + ku_ + i - j] = v;
+}
+
+DenseBlock::DenseBlock(int r, int c) : rows(r), cols(c) {
+    if (r < 0 || c < 0) throw std::invalid_argument("DenseBlock: negative shape");
+    data.assign(static_cast<std::size_t>(r) * c, 0.0);
+}
+MatView DenseBlock::view() { return {data.data(), rows, cols, rows}; }
+ConstMatView DenseBlock::view() const { return {data.data(), rows, cols, rows}; }
+MatView DenseBlock::block(int row0, int nrows) { return view().block(row0, nrows); }
+ConstMatView DenseBlock::block(int row0, int nrows) const { return view().block(row0, nrows); }
+
+DenseBlock copy_of(ConstMatView v) {
+    DenseBlock out(v.rows, v.cols);
+    assign(out.view(), v);
+    return out;
+}
+void assign(MatView dst, ConstMatView src) {
+    for (int j = 0; j < src.cols; ++j) std::memcpy(dst.col(j), src.col(j), sizeof(double) * src.rows);
+}
+void subtract_inplace(MatView dst, ConstMatView src) {
+    for (int j = 0; j < src.cols; ++j)
+        for (int i = 0; i < src.rows; ++i) dst.at(i, j) -= src.at(i, j);
+}
+void reverse_rows_inplace(MatView v) {
+    for (int j = 0; j < v.cols; ++j) std::reverse(v.col(j), v.col(j) + v.rows);
+}
+DenseBlock reversed_rows(ConstMatView v) {
+    DenseBlock out = copy_of(v);
+    reverse_rows_inplace(out.view());
+    return out;
+}
+void gemm_minus(MatView c, ConstMatView a, ConstMatView b) {
+    for (int j = 0; j < c.cols; ++j)
+        for (int l = 0; l < a.cols; ++l) {
+            const double s = b.at(l, j);
+            for (int i = 0; i < c.rows; ++i) c.at(i, j) -= s * a.at(i, l);
+        }
+}
+void gemm_minus_t(MatView c, ConstMatView a, ConstMatView b) {
+    for (int j = 0; j < c.cols; ++j)
+        for (int i = 0; i < c.rows; ++i) {
+            double s = 0.0;
+            for (int l = 0; l < a.rows; ++l) s += a.at(l, i) * b.at(l, j);
+            c.at(i, j) -= s;
+        }
+}
+
+// ------------------------------------------------------------------ planning
+int PartitionPlan::dual_count() const {
+    return static_cast<int>(std::count(kinds.begin(), kinds.end(), PartitionKind::InnerDual));
+}
+int PartitionPlan::single_count() const { return p - dual_count(); }
+
+PartitionPlan distribute_threads(int t, int cap_p) {
+    const int cap = std::max(2, 2 * t + 2);
+    std::vector<int32_t> kinds(cap);
+    int32_t p = 0, used = 0, idle = 0;
+    check(spk_distribute_threads(t, cap_p, &p, kinds.data(), cap, &used, &idle));
+    PartitionPlan plan;
+    plan.p = p;
+    for (int i = 0; i < p; ++i) plan.kinds.push_back(static_cast<PartitionKind>(kinds[i]));
+    plan.threads_used = used;
+    plan.idle_threads = idle;
+    return plan;
+}
+
+std::pair<double, double> compute_ratios(double k_const, int n_rhs, int k) {
+    if (k_const <= 0.0) throw std::invalid_argument("compute_ratios: K must be > 0");
+    if (k < 1) throw std::invalid_argument("compute_ratios: k must be >= 1");
+    if (n_rhs < 0) throw std::invalid_argument("compute_ratios: n_rhs must be >= 0");
+    double r12 = 0, r13 = 0;
+    spk_compute_ratios(k_const, n_rhs, k, &r12, &r13);
+    return {r12, r13};
+}
+
+std::vector<int> compute_sizes(int n, const PartitionPlan& skel, double r12, double r13, int min_single,
+                               int min_dual) {
+    std::vector<int32_t> kinds = kinds_of(skel);
+    std::vector<int64_t> sizes(skel.p);
+    check(spk_compute_sizes(n, skel.p, kinds.data(), r12, r13, min_single, min_dual, sizes.data()));
+    return std::vector<int>(sizes.begin(), sizes.end());
+}
+
+static PartitionPlan plan_from(int32_t p, const std::vector<int64_t>& b, const std::vector<int32_t>& k) {
+    PartitionPlan plan;
+    plan.p = p;
+    plan.bounds.assign(b.begin(), b.begin() + p + 1);
+    for (int i = 0; i < p; ++i) plan.kinds.push_back(static_cast<PartitionKind>(k[i]));
+    return plan;
+}
+
+PartitionPlan make_plan(int n, int kl, int ku, int t, double r12, double r13) {
+    const int cap = std::max(2, 2 * t + 2);
+    std::vector<int64_t> b(cap + 1);
+    std::vector<int32_t> k(cap);
+    int32_t p = 0, used = 0, idle = 0;
+    check(spk_make_plan(n, kl, ku, t, r12, r13, cap, &p, b.data(), k.data(), &used, &idle));
+    PartitionPlan plan = plan_from(p, b, k);
+    plan.threads_used = used;
+    plan.idle_threads = idle;
+    plan.r12 = r12;
+    plan.r13 = r13;
+    return plan;
+}
+
+PartitionPlan gpu_plan(int n, int kl, int ku, int nrhs, bool pivoting, int p_hint) {
+    const int cap = std::max(4096, 2 * p_hint + 2);
+    std::vector<int64_t> b(cap + 1);
+    std::vector<int32_t> k(cap);
+    int32_t p = 0;
+    check(spk_gpu_plan(n, kl, ku, nrhs, pivoting ? 1 : 0, p_hint, cap, &p, b.data(), k.data()));
+    PartitionPlan plan = plan_from(p, b, k);
+    plan.threads_used = p;
+    return plan;
+}
+
+// ------------------------------------------------------------------ factors
+SpikeFactorization factorize(const BandedMatrix& a, const PartitionPlan& plan, FactorOptions opts) {
+    if (plan.n() != a.n()) throw std::invalid_argument("factorize: plan does not match matrix");
+    for (int i = 0; i < plan.p; ++i)
+        if (plan.size(i) < 1) throw std::invalid_argument("factorize: empty partition");
+    std::vector<int64_t> bounds(plan.bounds.begin(), plan.bounds.end());
+    std::vector<int32_t> kinds = kinds_of(plan);
+    spk_plan sp{plan.p, bounds.data(), kinds.data()};
+    spk_factor_options so{opts.pivoting ? 1 : 0, opts.boost_eps};
+    spk_fact* h = nullptr;
+    check(spk_factorize(a.data().data(), SPK_MEM_HOST, a.n(), a.kl(), a.ku(), &sp, &so, nullptr, &h));
+    SpikeFactorization f;
+    f.handle = std::shared_ptr<void>(h, [](void* q) { spk_fact_destroy(static_cast<spk_fact*>(q)); });
+    f.plan = plan;
+    f.n = a.n();
+    f.kl = a.kl();
+    f.ku = a.ku();
+    f.k = std::max(a.kl(), a.ku());
+    f.options = opts;
+    int32_t nlev = 0, boost = 0, warn = 0;
+    check(spk_fact_info(h, nullptr, nullptr, nullptr, nullptr, nullptr, &nlev, &boost, &warn));
+    f.boost_count = boost;
+    std::vector<int64_t> sw(plan.p);
+    check(spk_fact_factor_sweeps(h, sw.data()));
+    f.factor_sweeps.assign(sw.begin(), sw.end());
+    std::vector<DenseBlock>* dst[6] = {&f.vt, &f.vb, &f.wt, &f.wb, &f.bhat, &f.chat};
+    for (int w = 0; w < 6; ++w)
+        for (int i = 0; i < plan.p; ++i) dst[w]->push_back(fetch_tip(h, w, i, f.k));
+    ReducedLevels& rl = f.levels;
+    rl.p = plan.p;
+    rl.k = f.k;
+    rl.boost_warnings = warn;
+    rl.device = f.handle;
+    for (int l = 0; l < nlev; ++l) {
+        const int units = spk_fact_units(h, l);
+        rl.v.emplace_back();
+        rl.w.emplace_back();
+        for (int u = 0; u < units; ++u)
+            for (int which = 0; which < 2; ++which) {
+                int32_t hh = 0;
+                check(spk_fact_level_spike(h, l, which, u, &hh, nullptr));
+                DenseBlock b(hh, f.k);
+                check(spk_fact_level_spike(h, l, which, u, &hh, b.data.data()));
+                (which == 0 ? rl.v : rl.w).back().push_back(std::move(b));
+            }
+        rl.pairs.emplace_back();
+        const int nn = 2 * f.k;
+        for (int a2 = 0; a2 < units / 2; ++a2) {
+            std::vector<double> lu(static_cast<std::size_t>(nn) * nn);
+            std::vector<int> piv(nn);
+            int32_t fb = 0;
+            check(spk_fact_coupling(h, l, a2, lu.data(), reinterpret_cast<int32_t*>(piv.data()), &fb));
+            rl.pairs.back().emplace_back(nn, std::move(lu), std::move(piv), fb == 0);
+        }
+    }
+    return f;
+}
+
+ReducedLevels reduce_factorize(const std::vector<DenseBlock>& vt, const std::vector<DenseBlock>& vb,
+                               const std::vector<DenseBlock>& wt, const std::vector<DenseBlock>& wb, int p, int k,
+                               double boost_eps, int) {
+    if (p < 1) throw std::invalid_argument("reduce_factorize: p must be >= 1");
+    const std::size_t kk = static_cast<std::size_t>(k) * k;
+    std::vector<double> packed[4];
+    const std::vector<DenseBlock>* src[4] = {&vt, &vb, &wt, &wb};
+    for (int w = 0; w < 4; ++w) {
+        packed[w].assign(kk * p + 1, 0.0);
+        for (int i = 0; i < p && i < (int)src[w]->size(); ++i)
+            if ((*src[w])[i].data.size() == kk) std::memcpy(&packed[w][kk * i], (*src[w])[i].data.data(), kk * 8);
+    }
+    spk_reduced* r = nullptr;
+    check(spk_reduced_create(packed[0].data(), packed[1].data(), packed[2].data(), packed[3].data(), p, k,
+                             boost_eps, &r));
+    ReducedLevels rl;
+    rl.p = p;
+    rl.k = k;
+    rl.standalone = true;
+    rl.device = std::shared_ptr<void>(r, [](void* q) { spk_reduced_destroy(static_cast<spk_reduced*>(q)); });
+    rl.boost_warnings = spk_reduced_boost_warnings(r);
+    if (k > 0)
+        for (int units : level_units(p)) rl.pairs.emplace_back(units / 2);
+    return rl;
+}
+
+// ------------------------------------------------------------------ solves
+static DenseBlock solve_impl(const SpikeFactorization& fact, const DenseBlock& f, SolveStats* stats,
+                             bool transpose) {
+    if (f.rows != fact.n)
+        throw std::invalid_argument(transpose ? "transpose_solve: F.rows must equal n" : "solve: F.rows must equal n");
+    DenseBlock x(fact.n, f.cols);
+    std::vector<int64_t> sw(fact.p());
+    spk_solve_stats st{sw.data(), 0};
+    check(spk_solve(static_cast<spk_fact*>(fact.handle.get()), transpose ? 1 : 0, f.data.data(), fact.n, f.cols,
+                    x.data.data(), fact.n, SPK_MEM_HOST, nullptr, &st));
+    if (stats) {
+        stats->partition_full_sweeps.assign(sw.begin(), sw.end());
+        stats->reduced_coupling_solves = st.reduced_coupling_solves;
+    }
+    return x;
+}
+
+DenseBlock solve(const SpikeFactorization& fact, const DenseBlock& f, SolveStats* stats) {
+    return solve_impl(fact, f, stats, false);
+}
+DenseBlock transpose_solve(const SpikeFactorization& fact, const DenseBlock& f, SolveStats* stats) {
+    return solve_impl(fact, f, stats, true);
+}
+
+static DenseBlock reduced_impl(const ReducedLevels& levels, const DenseBlock& y, long* couplings, bool transpose) {
+    if (y.rows != 2 * levels.p * levels.k)
+        throw std::invalid_argument(transpose ? "reduced_solve_transpose: tip block has wrong height"
+                                              : "reduced_solve: tip block has wrong height");
+    DenseBlock z = y;
+    int64_t c = 0;
+    if (levels.standalone) {
+        check(spk_reduced_solve(static_cast<spk_reduced*>(levels.device.get()), transpose ? 1 : 0, z.data.data(),
+                                z.cols, &c));
+    } else {
+        check(spk_fact_reduced_solve(static_cast<spk_fact*>(levels.device.get()), transpose ? 1 : 0, z.data.data(),
+                                     z.cols, &c));
+    }
+    if (couplings) *couplings += c;
+    return z;
+}
+
+DenseBlock reduced_solve(const ReducedLevels& levels, const DenseBlock& y, long* couplings, int) {
+    return reduced_impl(levels, y, couplings, false);
+}
+DenseBlock reduced_solve_transpose(const ReducedLevels& levels, const DenseBlock& g, long* couplings, int) {
+    return reduced_impl(levels, g, couplings, true);
+}
+
+// ------------------------------------------------------------------ band ops
+DenseBlock band_matmul(const BandedMatrix& a, const DenseBlock& x, bool transpose) {
+    if (x.rows != a.n()) throw std::invalid_argument("band_matmul: X.rows must equal n");
+    DenseBlock y(a.n(), x.cols);
+    if (x.cols)
+        check(spk_band_matmul(a.data().data(), a.n(), a.kl(), a.ku(), x.data.data(), a.n(), x.cols,
+                              transpose ? 1 : 0, y.data.data(), a.n(), SPK_MEM_HOST, nullptr));
+    return y;
+}
+
+double frobenius_norm(const DenseBlock& b) {
+    double s = 0.0;
+    for (double v : b.data) s += v * v;
+    return std::sqrt(s);
+}
+
+double relative_residual(const BandedMatrix& a, const DenseBlock& x, const DenseBlock& f, bool transpose) {
+    if (x.rows != a.n() || f.rows != a.n() || x.cols != f.cols)
+        throw std::invalid_argument("relative_residual: inconsistent shapes");
+    const double fn = frobenius_norm(f);
+    if (fn == 0.0) {
+        if (frobenius_norm(x) == 0.0) return 0.0;
+        throw std::domain_error("relative_residual: F is zero but X is not");
+    }
+    DenseBlock r = band_matmul(a, x, transpose);
+    for (std::size_t i = 0; i < r.data.size(); ++i) r.data[i] -= f.data[i];
+    return frobenius_norm(r) / fn;
+}
+
+double norm1(const BandedMatrix& a) {
+    double best = 0.0;
+    for (int j = 0; j < a.n(); ++j) {
+        double s = 0.0;
+        for (int q = 0; q < a.ld(); ++q) s += std::fabs(a.col(j)[q]);
+        best = std::max(best, s);
+    }
+    return best;
+}
+
+double max_abs(const BandedMatrix& a) {
+    double best = 0.0;
+    for (double v : a.data()) best = std::max(best, std::fabs(v));
+    return best;
+}
+
+RefineResult iterative_refine(const SpikeFactorization& fact, const BandedMatrix& a, const DenseBlock& f,
+                              const DenseBlock& x0, int max_iters, double tol, bool transpose) {
+    RefineResult res;
+    res.x = x0;
+    const double fnorm = frobenius_norm(f);
+    double prev = std::numeric_limits<double>::infinity();
+    for (int it = 0; it <= max_iters; ++it) {
+        DenseBlock r = band_matmul(a, res.x, transpose);
+        for (std::size_t i = 0; i < r.data.size(); ++i) r.data[i] = f.data[i] - r.data[i];
+        const double rn = frobenius_norm(r);
+        res.residual = fnorm == 0.0 ? (rn == 0.0 ? 0.0 : std::numeric_limits<double>::infinity()) : rn / fnorm;
+        res.iterations = it;
+        if (res.residual <= tol) {
+            res.converged = true;
+            return res;
+        }
+        if (it > 0 && res.residual * 1.1 > prev) {
+            res.stagnated = true;
+            return res;
+        }
+        if (it == max_iters) return res;
+        prev = res.residual;
+        DenseBlock d = transpose ? transpose_solve(fact, r) : solve(fact, r);
+        for (std::size_t i = 0; i < res.x.data.size(); ++i) res.x.data[i] += d.data[i];
+    }
+    return res;
+}
+
+}  // namespace spike

@@ -247,7 +247,7 @@ struct spk_fact {
     double* d_tfac = nullptr;
     double* d_dinv = nullptr;
     long long tfac_size = 0;
-    Program prog_factor, prog_fwd, prog_tr;
+    Program prog_factor, prog_fwd, prog_tr, prog_rfwd, prog_rtr;  // r*: reduced system only
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
     cudaStream_t stream = nullptr;
@@ -1274,9 +1274,16 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     ProgramBuilder pb;
     f.prog_fwd.clear();
     f.prog_tr.clear();
+    f.prog_rfwd.clear();
+    f.prog_rtr.clear();
     if (!f.reduced_only) {
         build_forward_program(f, pb);
         build_transpose_program(f, pb);
+        Builder bf{f, pb, f.prog_rfwd}, bt{f, pb, f.prog_rtr};
+        if (f.p > 1 && f.k > 0) {
+            build_reduced_solve(f, bf, false, 0);
+            build_reduced_solve(f, bt, true, 0);
+        }
     } else {
         Builder bf{f, pb, f.prog_fwd}, bt{f, pb, f.prog_tr};
         if (f.p > 1 && f.k > 0) {
@@ -1467,25 +1474,9 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
         // partitions do full sweeps in the D stage and the LU like everyone
         // else, so the CPU ratio model (partition.cpp:47-54) would make them
         // the critical path.
-        std::vector<double> w(pp, 1.0);
-        double tot = 0.0;
-        for (double x : w) tot += x;
-        for (int attempt = 0; attempt < 2; ++attempt) {
-            if (attempt == 1) {  // weighted sizes undercut the minimum: equal sizes
-                std::fill(w.begin(), w.end(), 1.0);
-                tot = pp;
-            }
-            bounds[0] = 0;
-            long long acc = 0;
-            bool ok = true;
-            for (int i = 0; i < pp; ++i) {
-                long long sz = (i == pp - 1) ? n - acc : (long long)std::llround(n * w[i] / tot);
-                acc += sz;
-                bounds[i + 1] = acc;
-                ok = ok && (sz >= min_part || pp == 1);
-            }
-            if (ok) break;
-        }
+        const long long base = n / pp, extra = n % pp;
+        bounds[0] = 0;
+        for (int i = 0; i < pp; ++i) bounds[i + 1] = bounds[i] + base + (i < extra ? 1 : 0);
         for (int i = 0; i < pp; ++i) {
             if (bounds[i + 1] - bounds[i] < min_part && pp > 1) fail(SPK_EDOMAIN, "gpu_plan: partition too small");
             kinds[i] = (i == 0 || i == pp - 1) ? SPK_FIRSTLAST : SPK_INNER_SINGLE;
@@ -1836,10 +1827,9 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
     });
 }
 
-spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z, int32_t ncols,
-                             int64_t* couplings) {
+static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t transpose, double* z, int32_t ncols,
+                                   int64_t* couplings) {
     return guarded([&] {
-        spk_fact& f = *r->f;
         if (couplings) *couplings += (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
         if (ncols == 0 || f.p < 2 || f.k == 0) return;
         cudaStream_t s = nullptr;
@@ -1854,12 +1844,22 @@ spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z,
         B.ld[B_AUX] = f.aux_rows;
         B.p[B_POOL] = f.d_pool;
         Exec ex{f, s, B, ncols};
-        ex.run(transpose ? f.prog_tr : f.prog_fwd, f.d_sblob);
+        ex.run(own_programs ? (transpose ? f.prog_tr : f.prog_fwd) : (transpose ? f.prog_rtr : f.prog_rfwd), f.d_sblob);
         ck(cudaMemcpyAsync(z, T, sizeof(double) * rows * ncols, cudaMemcpyDeviceToHost, s), "z download");
         ck(cudaFreeAsync(T, s), "free");
         ck(cudaFreeAsync(AUX, s), "free");
         ck(cudaStreamSynchronize(s), "reduced_solve");
     });
+}
+
+spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z, int32_t ncols,
+                             int64_t* couplings) {
+    return reduced_solve_on(*r->f, true, transpose, z, ncols, couplings);
+}
+
+spk_status spk_fact_reduced_solve(const spk_fact* f, int32_t transpose, double* z, int32_t ncols,
+                                  int64_t* couplings) {
+    return reduced_solve_on(const_cast<spk_fact&>(*f), false, transpose, z, ncols, couplings);
 }
 
 int32_t spk_reduced_levels(const spk_reduced* r) {

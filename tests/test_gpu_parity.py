@@ -327,3 +327,21 @@ def test_decoupled_boundaries_zero_tips(oracle, spk):
         assert np.abs(fact.wt[i]).max() == 0.0
     xo = oracle.oracle_solve(a.data, n, k, k, F)
     assert rel_componentwise(spk.solve(fact, F), xo) < 1e-12
+
+
+def test_cpp_dropin_api(spk, tmp_path):
+    """The reference-style C++ API (include/spike/*.hpp) against libspike_b200.so."""
+    import os
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cxx = shutil.which("g++")
+    if cxx is None:
+        pytest.skip("no host C++ compiler")
+    exe = tmp_path / "dropin_test"
+    libdir = os.path.dirname(spk.LIB_PATH)
+    subprocess.run([cxx, "-std=c++17", "-O1", os.path.join(root, "tests", "cpp", "dropin_test.cpp"),
+                    "-I", os.path.join(root, "include"), spk.LIB_PATH, f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "DROPIN PASS" in r.stdout, r.stdout + r.stderr
