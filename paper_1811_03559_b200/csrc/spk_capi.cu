@@ -10,6 +10,7 @@
 #include "../../include/spike_b200.h"
 #include "spk_launch.h"
 #include "spk_sweep_fast.cuh"
+#include "spk_sweep_dmma.cuh"
 
 namespace spk {
 struct FastLuArgs {
@@ -1023,6 +1024,34 @@ struct Exec {
 
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
         if (nc <= 0) return true;
+        static const bool no_dmma = getenv("SPK_NO_DMMA_SWEEP") && atoi(getenv("SPK_NO_DMMA_SWEEP"));
+        if (!no_dmma && !st.piv && nc >= 8 && st.kwmax <= 192) {
+            // blocked tensor-core sweep: 8 columns per warp, <= 16 warps per CTA,
+            // column groups balanced across CTAs
+            static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
+            int ntw = 0;
+            for (int t : ntws)
+                if (8 * (t - 1) >= st.kwmax) {
+                    ntw = t;
+                    break;
+                }
+            const int groups = (nc + 127) / 128;
+            const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
+            const int nwd = cols / 8;
+            const dim3 grid(st.njobs, (nc + cols - 1) / cols);
+            const size_t smem = dmma_sweep_smem(ntw, nwd);
+            FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
+            if (smem <= 227 * 1024) {
+                bool ok = false;
+                switch (st.mode) {
+                    case SW_FWD_L: ok = launch_sweep_dmma_fl(ntw, nwd, grid, smem, A, s); break;
+                    case SW_BWD_U: ok = launch_sweep_dmma_bu(ntw, nwd, grid, smem, A, s); break;
+                    case SW_FWD_UT: ok = launch_sweep_dmma_fut(ntw, nwd, grid, smem, A, s); break;
+                    default: ok = launch_sweep_dmma_blt(ntw, nwd, grid, smem, A, s); break;
+                }
+                if (ok) return true;
+            }
+        }
         int NC, nw;
         if (nc >= 64) {
             NC = 4;

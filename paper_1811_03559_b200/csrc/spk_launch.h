@@ -47,6 +47,10 @@ bool launch_sweep_fast_blt(int tr, int nc, bool piv, int nwarps, dim3 grid, size
                            cudaStream_t s);
 struct FastLuArgs;
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s);
+bool launch_sweep_dmma_fl(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
+bool launch_sweep_dmma_bu(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
+bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
+bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
 void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
                               double* tfac, double* dinv, cudaStream_t s);
 

@@ -1,0 +1,233 @@
+// spk_sweep_dmma.cuh — blocked triangular sweeps on the FP64 tensor cores.
+//
+// Same jobs and semantics as k_sweep_fast (non-pivoting modes), restructured
+// for DMMA (mma.sync.m8n8k4.f64): each warp owns 8 right-hand-side columns and
+// keeps the active band window as NTW 8x8 tiles in the accumulator (C
+// fragment) layout — lane l holds row l>>2, columns 2(l&3), 2(l&3)+1 of every
+// tile.  The sweep advances 8 rows per block:
+//   1. the pivot tile (rows 8b..8b+7) is solved in place: 8 in-tile steps of
+//      x_t = P_t (* 1/u for U sweeps); P_{t'} -= v_t[t'-t-1] x_t   (shuffles);
+//   2. its rows become the B operand (8 steps x 8 columns) and every other
+//      tile takes a rank-8 update  W_T -= A_T X  with A_T[r][t] = v_{8b+t}[r-t-1]
+//      — two DMMA per tile, A fragments loaded from a shared-memory block of
+//      factor vectors laid out [step][row] with a row stride = 8 (mod 16)
+//      doubles (conflict-free fragment loads);
+//   3. the solved tile is written back and its register slot recycled for the
+//      rows 8*NTW further on (staged one 32-row round ahead by cp.async).
+// Per 8 rows a warp issues 2(NTW-1) DMMA + 2(NTW-1) LDS + ~100 other
+// instructions against 8*8*(NTW-1)*8 FMAs, i.e. ~4x fewer issue slots and half
+// the shared-memory bytes per FMA of the per-row DFMA kernel.  Row interchanges
+// (pivoting) do not commute with the blocked update in gbtf2 storage, so the
+// pivoted forward sweep stays on k_sweep_fast.
+#pragma once
+
+#include "spk_device.cuh"
+#include "spk_sweep_fast.cuh"
+
+namespace spk {
+
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NTW>
+struct DmmaGeom {
+    static constexpr int KWT = 8 * (NTW - 1);                       // longest factor vector
+    static constexpr int SR = ((8 + KWT + 15) / 16) * 16 + 8;       // [step][row] stride, = 8 mod 16
+};
+
+inline size_t dmma_sweep_smem(int ntw, int nwarps) {
+    const int KWT = 8 * (ntw - 1);
+    const int SR = ((8 + KWT + 15) / 16) * 16 + 8;
+    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * nwarps * 8 * 8;
+    return 2 * per_stage + 64;
+}
+
+template <int NTW, int MODE>
+__global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
+    constexpr int SR = DmmaGeom<NTW>::SR;
+    constexpr int KWT = DmmaGeom<NTW>::KWT;
+    constexpr bool kAsc = (MODE == SW_FWD_L || MODE == SW_FWD_UT);
+    constexpr bool kDiag = (MODE == SW_BWD_U || MODE == SW_FWD_UT);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const SweepJob J = A.jobs[blockIdx.x];
+    if (!guard_ok(A.B.flags, J.guard)) return;
+    const PartDev P = A.parts[J.part];
+    const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
+    const int nwarps = blockDim.x >> 5;
+    const int ncta = nwarps * 8;
+    const int colbase = blockIdx.y * ncta;
+    if (colbase >= nc_total) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+
+    const int lo = J.lo;
+    const int hi = (MODE == SW_BWD_U) ? J.hi : P.m - 1;
+    const int nsteps = hi - lo + 1;
+    if (nsteps <= 0) return;
+
+    int kw;
+    const double* vbase;
+    long long vstride;
+    int vdir;
+    if (MODE == SW_FWD_L) {
+        kw = P.kl;
+        vbase = A.fac + P.fofs + P.d + 1;
+        vstride = P.rows;
+        vdir = 1;
+    } else if (MODE == SW_BWD_U) {
+        kw = P.ubw;
+        vbase = A.fac + P.fofs + P.d - 1;
+        vstride = P.rows;
+        vdir = -1;
+    } else if (MODE == SW_FWD_UT) {
+        kw = P.ubw;
+        vbase = A.tfac + P.tofs + P.kl + 1;
+        vstride = P.rowsT;
+        vdir = 1;
+    } else {
+        kw = P.kl;
+        vbase = A.tfac + P.tofs + P.kl - 1;
+        vstride = P.rowsT;
+        vdir = -1;
+    }
+
+    double* s_A = reinterpret_cast<double*>(smem_raw);      // [st][4 blocks][8 steps][SR rows]
+    double* s_dg = s_A + 2 * 4 * 8 * SR;                     // [st][32]
+    double* s_in = s_dg + 2 * 32;                            // [st][32 rows][ncta]
+
+    const View& v = J.v;
+    const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
+    double* const bbase = A.B.p[v.buf] + v.base;
+    auto phys = [&](int r) -> long long {
+        return v.rev ? (long long)(v.mrows - 1 - (r - v.off)) : (long long)(r - v.off);
+    };
+    auto rowof = [&](int u) -> int { return kAsc ? lo + u : hi - u; };
+
+    const int c0 = J.c0 + colbase;
+    const int ncta_valid = min(ncta, nc_total - colbase);
+    const int lc0 = warp * 8 + 2 * q;  // this lane's two columns (CTA-local)
+    const bool cv0 = lc0 < ncta_valid, cv1 = lc0 + 1 < ncta_valid;
+    double* const cp0 = bbase + (long long)(c0 + (cv0 ? lc0 : 0)) * ld;
+    double* const cp1 = bbase + (long long)(c0 + (cv1 ? lc0 + 1 : 0)) * ld;
+
+    auto load_round = [&](int R) {
+        const int st = R & 1;
+        const int u0 = 32 * R;
+        if (u0 < nsteps) {
+            double* dA = s_A + (size_t)st * 4 * 8 * SR;
+            for (int idx = threadIdx.x; idx < 4 * 8 * SR; idx += blockDim.x) {
+                const int bt = idx / SR, r = idx - bt * SR;  // bt = 8*bb + t
+                const int t = bt & 7;
+                const int u = u0 + bt;
+                const int dl = r - t - 1;
+                if (dl >= 0 && dl < kw && r < 8 + KWT && u < nsteps)
+                    cp_async8(dA + idx, vbase + (long long)rowof(u) * vstride + vdir * dl);
+                else
+                    dA[idx] = 0.0;
+            }
+            if (kDiag && threadIdx.x < 32) {
+                const int u = u0 + threadIdx.x;
+                if (u < nsteps) cp_async8(s_dg + st * 32 + threadIdx.x, A.dinv + P.r0 + rowof(u));
+            }
+            double* di = s_in + (size_t)st * 32 * ncta;
+            for (int idx = threadIdx.x; idx < 32 * ncta; idx += blockDim.x) {
+                const int t = idx & 31, col = idx >> 5;
+                const int uu = u0 + t + 8 * NTW;
+                double* dst = di + t * ncta + col;
+                if (uu < nsteps && col < ncta_valid)
+                    cp_async8(dst, bbase + phys(rowof(uu)) + (long long)(c0 + col) * ld);
+                else
+                    *dst = 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+
+    // window: tile slot T <-> rows [8T, 8T+8) of the sweep, initially T = 0..NTW-1
+    double Wt[NTW][2];
+#pragma unroll
+    for (int T = 0; T < NTW; ++T) {
+        const int u = 8 * T + g;
+        const bool ok = u < nsteps;
+        const long long pr = ok ? phys(rowof(u)) : 0;
+        Wt[T][0] = (ok && cv0) ? cp0[pr] : 0.0;
+        Wt[T][1] = (ok && cv1) ? cp1[pr] : 0.0;
+    }
+    load_round(0);
+
+    const int nblocks = (nsteps + 7) / 8;
+    for (int b0 = 0; b0 < nblocks; b0 += NTW) {
+#pragma unroll
+        for (int bi = 0; bi < NTW; ++bi) {
+            const int b = b0 + bi;
+            if (b < nblocks) {
+                if ((b & 3) == 0) {
+                    cp_async_wait<0>();
+                    __syncthreads();
+                    load_round((b >> 2) + 1);
+                }
+                const int st = (b >> 2) & 1, bb = b & 3;
+                const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
+                // 1. in-tile solve of the pivot tile (slot bi)
+                double p0 = Wt[bi][0], p1 = Wt[bi][1];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if (kDiag) {
+                        const double dg = s_dg[st * 32 + 8 * bb + t];
+                        if (g == t) {
+                            p0 *= dg;
+                            p1 *= dg;
+                        }
+                    }
+                    const double x0 = __shfl_sync(0xffffffffu, p0, 4 * t + q);
+                    const double x1 = __shfl_sync(0xffffffffu, p1, 4 * t + q);
+                    if (g > t) {
+                        const double l = Ab[t * SR + g];
+                        p0 = fma(-l, x0, p0);
+                        p1 = fma(-l, x1, p1);
+                    }
+                }
+                // 2. write back the 8 finished rows
+                {
+                    const int u = 8 * b + g;
+                    if (u < nsteps) {
+                        const long long pr = phys(rowof(u));
+                        if (cv0) cp0[pr] = p0;
+                        if (cv1) cp1[pr] = p1;
+                    }
+                }
+                // B fragments (-X): B[k][n] = X[4s+k][n], lane holds k = q, n = g
+                double nb[2];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const int src = 4 * (4 * s + q) + (g >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, p0, src);
+                    const double v1 = __shfl_sync(0xffffffffu, p1, src);
+                    nb[s] = -((g & 1) ? v1 : v0);
+                }
+                // 3. rank-8 update of the other NTW-1 tiles
+#pragma unroll
+                for (int i = 0; i < NTW - 1; ++i) {
+                    const int slot = (bi + 1 + i) % NTW;
+                    const int R0 = 8 * (1 + i);
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) {
+                        const double a = Ab[(4 * s + q) * SR + R0 + g];
+                        dmma_acc(Wt[slot][0], Wt[slot][1], a, nb[s]);
+                    }
+                }
+                // 4. recycle the pivot slot: rows 8(b+NTW)+g
+                const double* in = s_in + (size_t)st * 32 * ncta + (8 * bb + g) * ncta + lc0;
+                Wt[bi][0] = in[0];
+                Wt[bi][1] = in[1];
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+}  // namespace spk

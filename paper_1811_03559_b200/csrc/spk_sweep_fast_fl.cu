@@ -1,6 +1,8 @@
-// spk_sweep_fast_fl.cu — instantiations of k_sweep_fast for SW_FWD_L.
-// (split per mode so nvcc builds the templates in parallel)
+// spk_sweep_fast_fl.cu — instantiations of the sweep kernels for SW_FWD_L
+// (register-window DFMA: k_sweep_fast; blocked DMMA: k_sweep_dmma).
+// Split per mode so nvcc builds the templates in parallel.
 #include "spk_sweep_fast.cuh"
+#include "spk_sweep_dmma.cuh"
 #include "spk_launch.h"
 
 #include <cuda_runtime.h>
@@ -62,6 +64,27 @@ bool launch_sweep_fast_fl(int tr, int nc, bool piv, int nwarps, dim3 grid, size_
     if (!attr_done[piv][tr][nc]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done[piv][tr][nc] = true;
+    }
+    fn<<<grid, 32 * nwarps, smem, s>>>(A);
+    count_launch();
+    return true;
+}
+
+bool launch_sweep_dmma_fl(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s) {
+    void (*fn)(FastSweepArgs) = nullptr;
+    int slot = -1;
+    if (ntw == 3) { fn = k_sweep_dmma<3, SW_FWD_L>; slot = 0; }
+    if (ntw == 5) { fn = k_sweep_dmma<5, SW_FWD_L>; slot = 1; }
+    if (ntw == 9) { fn = k_sweep_dmma<9, SW_FWD_L>; slot = 2; }
+    if (ntw == 13) { fn = k_sweep_dmma<13, SW_FWD_L>; slot = 3; }
+    if (ntw == 17) { fn = k_sweep_dmma<17, SW_FWD_L>; slot = 4; }
+    if (ntw == 21) { fn = k_sweep_dmma<21, SW_FWD_L>; slot = 5; }
+    if (ntw == 25) { fn = k_sweep_dmma<25, SW_FWD_L>; slot = 6; }
+    if (!fn) return false;
+    static bool attr_done[7] = {};
+    if (!attr_done[slot]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_done[slot] = true;
     }
     fn<<<grid, 32 * nwarps, smem, s>>>(A);
     count_launch();
