@@ -41,7 +41,7 @@ struct DmmaGeom {
 inline size_t dmma_sweep_smem(int ntw, int nwarps) {
     const int KWT = 8 * (ntw - 1);
     const int SR = ((8 + KWT + 15) / 16) * 16 + 8;
-    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * nwarps * 8 * 8;
+    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * (nwarps * 8 + 1) * 8;
     return 2 * per_stage + 64;
 }
 
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
     const int nwarps = blockDim.x >> 5;
     const int ncta = nwarps * 8;
+    const int sin_ld = ncta + 1;
     const int colbase = blockIdx.y * ncta;
     if (colbase >= nc_total) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
 
     double* s_A = reinterpret_cast<double*>(smem_raw);      // [st][4 blocks][8 steps][SR rows]
     double* s_dg = s_A + 2 * 4 * 8 * SR;                     // [st][32]
-    double* s_in = s_dg + 2 * 32;                            // [st][32 rows][ncta]
+    double* s_in = s_dg + 2 * 32;                            // [st][32 rows][ncta+1] (odd stride)
 
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -133,11 +134,11 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
                 const int u = u0 + threadIdx.x;
                 if (u < nsteps) cp_async8(s_dg + st * 32 + threadIdx.x, A.dinv + P.r0 + rowof(u));
             }
-            double* di = s_in + (size_t)st * 32 * ncta;
+            double* di = s_in + (size_t)st * 32 * sin_ld;
             for (int idx = threadIdx.x; idx < 32 * ncta; idx += blockDim.x) {
                 const int t = idx & 31, col = idx >> 5;
                 const int uu = u0 + t + 8 * NTW;
-                double* dst = di + t * ncta + col;
+                double* dst = di + t * sin_ld + col;
                 if (uu < nsteps && col < ncta_valid)
                     cp_async8(dst, bbase + phys(rowof(uu)) + (long long)(c0 + col) * ld);
                 else
@@ -159,73 +160,73 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     }
     load_round(0);
 
+    // The tile registers rotate by one slot per block, so Wt[0] is always the
+    // pivot tile and Wt[i] holds rows [8i, 8i+8) past it: one loop body, no
+    // per-slot unrolling (the unrolled variant overflowed the instruction cache).
     const int nblocks = (nsteps + 7) / 8;
-    for (int b0 = 0; b0 < nblocks; b0 += NTW) {
+    for (int b = 0; b < nblocks; ++b) {
+        if ((b & 3) == 0) {
+            cp_async_wait<0>();
+            __syncthreads();
+            load_round((b >> 2) + 1);
+        }
+        const int st = (b >> 2) & 1, bb = b & 3;
+        const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
+        // 1. in-tile solve of the pivot tile
+        double p0 = Wt[0][0], p1 = Wt[0][1];
 #pragma unroll
-        for (int bi = 0; bi < NTW; ++bi) {
-            const int b = b0 + bi;
-            if (b < nblocks) {
-                if ((b & 3) == 0) {
-                    cp_async_wait<0>();
-                    __syncthreads();
-                    load_round((b >> 2) + 1);
+        for (int t = 0; t < 8; ++t) {
+            if (kDiag) {
+                const double dg = s_dg[st * 32 + 8 * bb + t];
+                if (g == t) {
+                    p0 *= dg;
+                    p1 *= dg;
                 }
-                const int st = (b >> 2) & 1, bb = b & 3;
-                const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
-                // 1. in-tile solve of the pivot tile (slot bi)
-                double p0 = Wt[bi][0], p1 = Wt[bi][1];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    if (kDiag) {
-                        const double dg = s_dg[st * 32 + 8 * bb + t];
-                        if (g == t) {
-                            p0 *= dg;
-                            p1 *= dg;
-                        }
-                    }
-                    const double x0 = __shfl_sync(0xffffffffu, p0, 4 * t + q);
-                    const double x1 = __shfl_sync(0xffffffffu, p1, 4 * t + q);
-                    if (g > t) {
-                        const double l = Ab[t * SR + g];
-                        p0 = fma(-l, x0, p0);
-                        p1 = fma(-l, x1, p1);
-                    }
-                }
-                // 2. write back the 8 finished rows
-                {
-                    const int u = 8 * b + g;
-                    if (u < nsteps) {
-                        const long long pr = phys(rowof(u));
-                        if (cv0) cp0[pr] = p0;
-                        if (cv1) cp1[pr] = p1;
-                    }
-                }
-                // B fragments (-X): B[k][n] = X[4s+k][n], lane holds k = q, n = g
-                double nb[2];
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int src = 4 * (4 * s + q) + (g >> 1);
-                    const double v0 = __shfl_sync(0xffffffffu, p0, src);
-                    const double v1 = __shfl_sync(0xffffffffu, p1, src);
-                    nb[s] = -((g & 1) ? v1 : v0);
-                }
-                // 3. rank-8 update of the other NTW-1 tiles
-#pragma unroll
-                for (int i = 0; i < NTW - 1; ++i) {
-                    const int slot = (bi + 1 + i) % NTW;
-                    const int R0 = 8 * (1 + i);
-#pragma unroll
-                    for (int s = 0; s < 2; ++s) {
-                        const double a = Ab[(4 * s + q) * SR + R0 + g];
-                        dmma_acc(Wt[slot][0], Wt[slot][1], a, nb[s]);
-                    }
-                }
-                // 4. recycle the pivot slot: rows 8(b+NTW)+g
-                const double* in = s_in + (size_t)st * 32 * ncta + (8 * bb + g) * ncta + lc0;
-                Wt[bi][0] = in[0];
-                Wt[bi][1] = in[1];
+            }
+            const double x0 = __shfl_sync(0xffffffffu, p0, 4 * t + q);
+            const double x1 = __shfl_sync(0xffffffffu, p1, 4 * t + q);
+            if (g > t) {
+                const double l = Ab[t * SR + g];
+                p0 = fma(-l, x0, p0);
+                p1 = fma(-l, x1, p1);
             }
         }
+        // B fragments (-X): B[k][n] = X[4s+k][n], lane holds k = q, n = g
+        double nb[2];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const int src = 4 * (4 * s2 + q) + (g >> 1);
+            const double v0 = __shfl_sync(0xffffffffu, p0, src);
+            const double v1 = __shfl_sync(0xffffffffu, p1, src);
+            nb[s2] = -((g & 1) ? v1 : v0);
+        }
+        // 2. rank-8 update of the other NTW-1 tiles (the next pivot tile first)
+#pragma unroll
+        for (int i = 1; i < NTW; ++i) {
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const double a = Ab[(4 * s2 + q) * SR + 8 * i + g];
+                dmma_acc(Wt[i][0], Wt[i][1], a, nb[s2]);
+            }
+        }
+        // 3. write back the 8 finished rows
+        {
+            const int u = 8 * b + g;
+            if (u < nsteps) {
+                const long long pr = phys(rowof(u));
+                if (cv0) cp0[pr] = p0;
+                if (cv1) cp1[pr] = p1;
+            }
+        }
+        // 4. rotate; the freed slot takes rows 8(b+NTW)+g
+#pragma unroll
+        for (int i = 0; i < NTW - 1; ++i) {
+            Wt[i][0] = Wt[i + 1][0];
+            Wt[i][1] = Wt[i + 1][1];
+        }
+        const double* in = s_in + (size_t)st * 32 * sin_ld + (8 * bb + g) * sin_ld + lc0;
+        Wt[NTW - 1][0] = in[0];
+        Wt[NTW - 1][1] = in[1];
     }
     cp_async_wait<0>();
 }
