@@ -27,7 +27,7 @@
 namespace spk {
 
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
@@ -35,13 +35,13 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
 template <int NTW>
 struct DmmaGeom {
     static constexpr int KWT = 8 * (NTW - 1);                       // longest factor vector
-    static constexpr int SR = ((8 + KWT + 15) / 16) * 16 + 8;       // [step][row] stride, = 8 mod 16
+    static constexpr int SR = ((8 + KWT + 15) / 16) * 16 + 4;       // [step][row] stride, = 4 mod 16
 };
 
 inline size_t dmma_sweep_smem(int ntw, int nwarps) {
     const int KWT = 8 * (ntw - 1);
-    const int SR = ((8 + KWT + 15) / 16) * 16 + 8;
-    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * (nwarps * 8 + 1) * 8;
+    const int SR = ((8 + KWT + 15) / 16) * 16 + 4;
+    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * (nwarps * 8 + 1) * 8 + 4 * 64 * 8;
     return 2 * per_stage + 64;
 }
 
@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     double* s_A = reinterpret_cast<double*>(smem_raw);      // [st][4 blocks][8 steps][SR rows]
     double* s_dg = s_A + 2 * 4 * 8 * SR;                     // [st][32]
     double* s_in = s_dg + 2 * 32;                            // [st][32 rows][ncta+1] (odd stride)
+    double* s_ti = s_in + 2 * 32 * (nwarps * 8 + 1);         // [st][4 blocks][8][8] inverse diagonal blocks
 
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -160,65 +161,98 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     }
     load_round(0);
 
+    // Per 8-row block the system is  P = M X  with M the 8x8 diagonal block of
+    // the triangular factor (M[r][t] = v_t[r-t-1] below, 1 or u_tt on the
+    // diagonal).  At each round start all threads form Tinv = M^-1 and fold it
+    // into the update operand, A'[t][r] = sum_s A[s][r] Tinv[s][t], so a block
+    // is just: X = Tinv P (2 DMMA, output), W_i -= A'_i P (2 DMMA per tile) —
+    // no serial in-tile solve on the critical path.
+    auto prep_round = [&](int st, int u0) {
+        double* Ar = s_A + (size_t)st * 4 * 8 * SR;
+        double* Ti = s_ti + (size_t)st * 4 * 64;
+        const double* dg = s_dg + st * 32;
+        // Tinv columns: thread (bb, c) solves M y = e_c by forward substitution
+        if (threadIdx.x < 32) {
+            const int bb = threadIdx.x >> 3, c = threadIdx.x & 7;
+            const double* Ab = Ar + (size_t)bb * 8 * SR;
+            double y[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double acc = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (t < r) acc -= Ab[t * SR + r] * y[t];
+                // diagonal: 1 for unit sweeps, u_tt = 1/dinv for U sweeps
+                y[r] = kDiag ? acc * dg[8 * bb + r] : acc;
+                if (u0 + 8 * bb + r >= nsteps) y[r] = 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) Ti[bb * 64 + r * 8 + c] = y[r];  // Tinv[r][c]
+        }
+        __syncthreads();
+        // A' rows 8..8+KWT of each block (in place)
+        for (int idx = threadIdx.x; idx < 4 * KWT; idx += blockDim.x) {
+            const int bb = idx / KWT, r = 8 + (idx - bb * KWT);
+            double* col = Ar + (size_t)bb * 8 * SR + r;
+            const double* T = Ti + bb * 64;
+            double a[8], o[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) a[t] = col[t * SR];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                double acc = 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < 8; ++s2) acc = fma(a[s2], T[s2 * 8 + t], acc);
+                o[t] = acc;
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) col[t * SR] = o[t];
+        }
+        __syncthreads();
+    };
+
     // The tile registers rotate by one slot per block, so Wt[0] is always the
-    // pivot tile and Wt[i] holds rows [8i, 8i+8) past it: one loop body, no
-    // per-slot unrolling (the unrolled variant overflowed the instruction cache).
+    // pivot tile and Wt[i] holds rows [8i, 8i+8) past it: one loop body.
     const int nblocks = (nsteps + 7) / 8;
     for (int b = 0; b < nblocks; ++b) {
-        if ((b & 3) == 0) {
+        const int st = (b >> 2) & 1, bb = b & 3;
+        if (bb == 0) {
             cp_async_wait<0>();
             __syncthreads();
+            prep_round(st, 8 * b);
             load_round((b >> 2) + 1);
         }
-        const int st = (b >> 2) & 1, bb = b & 3;
         const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
-        // 1. in-tile solve of the pivot tile
-        double p0 = Wt[0][0], p1 = Wt[0][1];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            if (kDiag) {
-                const double dg = s_dg[st * 32 + 8 * bb + t];
-                if (g == t) {
-                    p0 *= dg;
-                    p1 *= dg;
-                }
-            }
-            const double x0 = __shfl_sync(0xffffffffu, p0, 4 * t + q);
-            const double x1 = __shfl_sync(0xffffffffu, p1, 4 * t + q);
-            if (g > t) {
-                const double l = Ab[t * SR + g];
-                p0 = fma(-l, x0, p0);
-                p1 = fma(-l, x1, p1);
-            }
-        }
-        // B fragments (-X): B[k][n] = X[4s+k][n], lane holds k = q, n = g
-        double nb[2];
+        const double* T = s_ti + (size_t)(st * 4 + bb) * 64;
+        // P (C layout: row g, cols 2q..2q+1) -> B fragments: B[k][n] = P[4s+k][n]
+        double pb[2];
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
             const int src = 4 * (4 * s2 + q) + (g >> 1);
-            const double v0 = __shfl_sync(0xffffffffu, p0, src);
-            const double v1 = __shfl_sync(0xffffffffu, p1, src);
-            nb[s2] = -((g & 1) ? v1 : v0);
+            const double v0 = __shfl_sync(0xffffffffu, Wt[0][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
+            pb[s2] = (g & 1) ? v1 : v0;
         }
-        // 2. rank-8 update of the other NTW-1 tiles (the next pivot tile first)
+        // rank-8 update of the other NTW-1 tiles with A' (the next pivot first)
+        const double nb0 = -pb[0], nb1 = -pb[1];
 #pragma unroll
         for (int i = 1; i < NTW; ++i) {
-#pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const double a = Ab[(4 * s2 + q) * SR + 8 * i + g];
-                dmma_acc(Wt[i][0], Wt[i][1], a, nb[s2]);
-            }
+            dmma_acc(Wt[i][0], Wt[i][1], Ab[q * SR + 8 * i + g], nb0);
+            dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 + q) * SR + 8 * i + g], nb1);
         }
-        // 3. write back the 8 finished rows
+        // X = Tinv P : the 8 finished rows
+        double x0 = 0.0, x1 = 0.0;
+        dmma_acc(x0, x1, T[g * 8 + q], pb[0]);
+        dmma_acc(x0, x1, T[g * 8 + 4 + q], pb[1]);
         {
             const int u = 8 * b + g;
             if (u < nsteps) {
                 const long long pr = phys(rowof(u));
-                if (cv0) cp0[pr] = p0;
-                if (cv1) cp1[pr] = p1;
+                if (cv0) cp0[pr] = x0;
+                if (cv1) cp1[pr] = x1;
             }
         }
-        // 4. rotate; the freed slot takes rows 8(b+NTW)+g
+        // rotate; the freed slot takes rows 8(b+NTW)+g
 #pragma unroll
         for (int i = 0; i < NTW - 1; ++i) {
             Wt[i][0] = Wt[i + 1][0];
