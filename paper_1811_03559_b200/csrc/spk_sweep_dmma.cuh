@@ -163,10 +163,10 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
 
     // Per 8-row block the system is  P = M X  with M the 8x8 diagonal block of
     // the triangular factor (M[r][t] = v_t[r-t-1] below, 1 or u_tt on the
-    // diagonal).  At each round start all threads form Tinv = M^-1 and fold it
-    // into the update operand, A'[t][r] = sum_s A[s][r] Tinv[s][t], so a block
-    // is just: X = Tinv P (2 DMMA, output), W_i -= A'_i P (2 DMMA per tile) —
-    // no serial in-tile solve on the critical path.
+    // diagonal).  At each round start one warp forms Tinv = M^-1 for the
+    // round's 4 blocks, so a block is X = Tinv P (2 DMMA) followed by the
+    // rank-8 update W_i -= A_i X (2 DMMA per tile): a short shuffle/DMMA chain
+    // instead of an 8-step serial in-tile solve.
     auto prep_round = [&](int st, int u0) {
         double* Ar = s_A + (size_t)st * 4 * 8 * SR;
         double* Ti = s_ti + (size_t)st * 4 * 64;
@@ -188,25 +188,6 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
             }
 #pragma unroll
             for (int r = 0; r < 8; ++r) Ti[bb * 64 + r * 8 + c] = y[r];  // Tinv[r][c]
-        }
-        __syncthreads();
-        // A' rows 8..8+KWT of each block (in place)
-        for (int idx = threadIdx.x; idx < 4 * KWT; idx += blockDim.x) {
-            const int bb = idx / KWT, r = 8 + (idx - bb * KWT);
-            double* col = Ar + (size_t)bb * 8 * SR + r;
-            const double* T = Ti + bb * 64;
-            double a[8], o[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) a[t] = col[t * SR];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                double acc = 0.0;
-#pragma unroll
-                for (int s2 = 0; s2 < 8; ++s2) acc = fma(a[s2], T[s2 * 8 + t], acc);
-                o[t] = acc;
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t) col[t * SR] = o[t];
         }
         __syncthreads();
     };
@@ -233,17 +214,27 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
             const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
             pb[s2] = (g & 1) ? v1 : v0;
         }
-        // rank-8 update of the other NTW-1 tiles with A' (the next pivot first)
-        const double nb0 = -pb[0], nb1 = -pb[1];
-#pragma unroll
-        for (int i = 1; i < NTW; ++i) {
-            dmma_acc(Wt[i][0], Wt[i][1], Ab[q * SR + 8 * i + g], nb0);
-            dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 + q) * SR + 8 * i + g], nb1);
-        }
-        // X = Tinv P : the 8 finished rows
+        // X = Tinv P : the 8 finished rows (C layout)
         double x0 = 0.0, x1 = 0.0;
         dmma_acc(x0, x1, T[g * 8 + q], pb[0]);
         dmma_acc(x0, x1, T[g * 8 + 4 + q], pb[1]);
+        // X -> B fragments (negated)
+        double nb[2];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const int src = 4 * (4 * s2 + q) + (g >> 1);
+            const double v0 = __shfl_sync(0xffffffffu, x0, src);
+            const double v1 = __shfl_sync(0xffffffffu, x1, src);
+            nb[s2] = -((g & 1) ? v1 : v0);
+        }
+        // rank-8 update: the next pivot tile first, then k-slice-major so the
+        // two DMMAs of a tile are NTW-2 instructions apart
+        dmma_acc(Wt[1][0], Wt[1][1], Ab[q * SR + 8 + g], nb[0]);
+        dmma_acc(Wt[1][0], Wt[1][1], Ab[(4 + q) * SR + 8 + g], nb[1]);
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+            for (int i = 2; i < NTW; ++i) dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * i + g], nb[s2]);
         {
             const int u = 8 * b + g;
             if (u < nsteps) {
