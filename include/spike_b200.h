@@ -157,6 +157,11 @@ spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double *d_F
                             void *stream);
 /* Number of kernel launches issued by this library on the calling thread
  * since the last reset (instrumentation for bench.py's gpu_launches). */
+/* Device arena: freed factor/scratch blocks are cached for reuse by later calls
+ * (stream-ordered).  cached = bytes held; trim returns them to the driver. */
+int64_t spk_arena_cached(void);
+void spk_arena_trim(void);
+
 int64_t spk_launch_count(int32_t reset);
 
 /* Optional per-kernel-class CUDA-event timing (calling thread): launches are

@@ -37,6 +37,7 @@ struct FastLuArgs {
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -84,6 +85,24 @@ spk_status guarded(F&& f) {
 namespace spk {
 void count_launch(int n) { g_launches += n; }
 }  // namespace spk
+
+#include <chrono>
+namespace {
+// SPK_TRACE=1: host-side phase timestamps of factorize / solve on stderr
+struct Tracer {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    const char* what;
+    explicit Tracer(const char* w) : on(getenv("SPK_TRACE") && atoi(getenv("SPK_TRACE"))), what(w) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* phase) {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[spk %s] %-24s %9.3f ms\n", what, phase, ms);
+    }
+};
+}  // namespace
 
 // ---------------------------------------------------------------------------
 // optional per-kernel-class CUDA-event profiling (bench.py roofline):
@@ -218,6 +237,125 @@ struct Level {
 
 }  // namespace
 
+namespace {
+
+// Device arena: factorizations and solves allocate gigabytes of factor and
+// scratch storage per call.  Freed blocks go to a free list (exact size class,
+// 2 MiB granularity) with an event recorded on the freeing stream; a reuse on
+// another stream waits on that event, a reuse on the same stream is ordered by
+// the stream itself.  Growth uses cudaMalloc once; nothing is re-mapped on the
+// hot path (cudaMallocAsync re-mapped the pool on every factorization: ~22 ms
+// per C3 factorization).
+struct ArenaBlock {
+    void* p;
+    size_t bytes;
+    cudaStream_t stream;
+    cudaEvent_t ev;
+};
+
+struct Arena {
+    std::mutex mu;
+    std::vector<ArenaBlock> free_list;
+    size_t cached = 0;
+
+    static size_t round_up(size_t b) {
+        const size_t g = b >= (2u << 20) ? (2u << 20) : 256;
+        return (b + g - 1) / g * g;
+    }
+
+    void* alloc(size_t bytes, cudaStream_t s) {
+        bytes = round_up(bytes == 0 ? 1 : bytes);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            int best = -1;
+            for (int i = 0; i < (int)free_list.size(); ++i) {
+                const ArenaBlock& b = free_list[i];
+                if (b.bytes >= bytes && b.bytes <= bytes + bytes / 4 &&
+                    (best < 0 || b.bytes < free_list[best].bytes))
+                    best = i;
+            }
+            if (best >= 0) {
+                ArenaBlock b = free_list[best];
+                free_list.erase(free_list.begin() + best);
+                cached -= b.bytes;
+                if (b.stream != s) cudaStreamWaitEvent(s, b.ev, 0);
+                cudaEventDestroy(b.ev);
+                return b.p;
+            }
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            trim();  // give cached blocks back and retry once
+            ck(cudaMalloc(&p, bytes), "cudaMalloc");
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        sizes[p] = bytes;
+        return p;
+    }
+
+    void release(void* p, cudaStream_t s) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = sizes.find(p);
+        if (it == sizes.end()) return;
+        ArenaBlock b{p, it->second, s, nullptr};
+        cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
+        cudaEventRecord(b.ev, s);
+        free_list.push_back(b);
+        cached += b.bytes;
+        // Bound the cache: drop the oldest blocks beyond the cap (waits for
+        // their last use; only reached when shapes keep changing).
+        while (cached > cap() && free_list.size() > 1) {
+            ArenaBlock o = free_list.front();
+            free_list.erase(free_list.begin());
+            cudaEventSynchronize(o.ev);
+            cudaEventDestroy(o.ev);
+            sizes.erase(o.p);
+            cudaFree(o.p);
+            cached -= o.bytes;
+        }
+    }
+
+    static size_t cap() {
+        static size_t c = [] {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            return tot / 2;
+        }();
+        return c;
+    }
+
+    void trim() {
+        std::lock_guard<std::mutex> lk(mu);
+        for (ArenaBlock& b : free_list) {
+            cudaEventSynchronize(b.ev);
+            cudaEventDestroy(b.ev);
+            sizes.erase(b.p);
+            cudaFree(b.p);
+        }
+        free_list.clear();
+        cached = 0;
+    }
+
+    std::unordered_map<void*, size_t> sizes;
+};
+
+Arena& arena() {
+    static Arena* a = new Arena();  // leaked on purpose: no teardown-order issues at exit
+    return *a;
+}
+
+template <class T>
+T* dalloc(size_t count, cudaStream_t s) {
+    return static_cast<T*>(arena().alloc(sizeof(T) * (count == 0 ? 1 : count), s));
+}
+
+inline void dfree(void* p, cudaStream_t s) { arena().release(p, s); }
+
+}  // namespace
+
 struct spk_fact {
     long long n = 0;
     int kl = 0, ku = 0, k = 0, p = 0, piv_on = 0;
@@ -259,7 +397,7 @@ struct spk_fact {
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
                         (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags})
-            if (q) cudaFreeAsync(q, stream);
+            if (q) dfree(q, stream);
     }
 };
 
@@ -1165,38 +1303,6 @@ struct Exec {
     }
 };
 
-// Keep freed stream-ordered allocations in the device's default pool: with
-// the default release threshold (0) every synchronisation hands gigabytes of
-// factor/scratch memory back to the driver and the next factorization pays
-// to map it again.
-void keep_pool_memory() {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
-        unsigned long long thr = ~0ULL;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    });
-}
-
-template <class T>
-T* dalloc(size_t count, cudaStream_t s) {
-    void* p = nullptr;
-    keep_pool_memory();
-    if (count == 0) count = 1;
-    ck(cudaMallocAsync(&p, sizeof(T) * count, s), "cudaMallocAsync");
-    return static_cast<T*>(p);
-}
-
-template <class T>
-T* dalloc_sync(size_t count) {
-    void* p = nullptr;
-    if (count == 0) count = 1;
-    ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
-    return static_cast<T*>(p);
-}
 
 void validate_plan(long long n, const spk_plan* plan) {
     if (!plan || plan->p < 1 || !plan->bounds) fail(SPK_EINVAL, "factorize: invalid plan");
@@ -1208,6 +1314,7 @@ void validate_plan(long long n, const spk_plan* plan) {
 
 // Symbolic part: geometry, pool layout, programs, device allocations.
 void setup_fact(spk_fact& f, cudaStream_t s) {
+    Tracer tr("setup");
     const int p = f.p, k = f.k;
     const long long kk = (long long)k * k;
     f.parts.clear();
@@ -1248,8 +1355,10 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
                         std::min(f.parts[p - 1].m, k + (f.piv_on ? f.parts[p - 1].kl : 0)));
     f.tau_w = wmax;
     f.aux_rows = std::max<long long>((long long)std::max(p - 1, 0) * 2 * k + 2LL * wmax + 2LL * k, 1);
+    tr.mark("geometry");
     ProgramBuilder pb;
     build_factor_program(f, pb);
+    tr.mark("factor program");
     // device allocations (stream ordered)
     const int nparts = (int)f.parts.size();
     f.d_parts = dalloc<PartDev>(nparts, s);
@@ -1264,6 +1373,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     f.d_blob = dalloc<char>(pb.blob.size(), s);
     f.d_tfac = dalloc<double>(f.tfac_size, s);
     f.d_dinv = dalloc<double>(f.n, s);
+    tr.mark("allocations");
     f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
     ck(cudaMemsetAsync(f.d_flags, 0, sizeof(int) * std::max(f.npairs, 1), s), "memset");
     ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
@@ -1276,9 +1386,11 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     ck(cudaMemsetAsync(f.d_boost, 0, sizeof(int) * nparts, s), "memset");
     ck(cudaMemsetAsync(f.d_fell, 0, sizeof(int) * nparts, s), "memset");
     ck(cudaMemsetAsync(f.d_status, 0, sizeof(int), s), "memset");
+    tr.mark("uploads");
 }
 
 void finish_factor(spk_fact& f, cudaStream_t s) {
+    Tracer tr("finish");
     int status = 0;
     const int nparts = (int)f.parts.size();
     std::vector<int> boost(nparts), fell(nparts);
@@ -1286,6 +1398,7 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     ck(cudaMemcpyAsync(boost.data(), f.d_boost, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
     ck(cudaMemcpyAsync(fell.data(), f.d_fell, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
     ck(cudaStreamSynchronize(s), "factorize");
+    tr.mark("stream synced");
     ck(cudaGetLastError(), "factorize kernels");
     if (status == 2) fail(SPK_ESINGULAR, "lu_factor: exactly singular column in pivoting mode");
     f.boost_count = 0;
@@ -1368,6 +1481,10 @@ void spk_profile_reset(void) {
     prof_drain();
     for (auto& a : g_acc) a = ProfAcc{};
 }
+
+int64_t spk_arena_cached(void) { return (int64_t)arena().cached; }
+
+void spk_arena_trim(void) { arena().trim(); }
 
 int64_t spk_launch_count(int32_t reset) {
     const long long v = g_launches;
@@ -1534,7 +1651,9 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         f->kinds.assign(plan->p, SPK_INNER_SINGLE);
         if (plan->kinds) f->kinds.assign(plan->kinds, plan->kinds + plan->p);
         f->stream = s;
+        Tracer tr("factorize");
         setup_fact(*f, s);
+        tr.mark("setup (symbolic)");
         // band on device
         const long long ld = kl + ku + 1;
         const double* dband = band;
@@ -1570,10 +1689,12 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         ex.n = n;
         ex.band = dband;
         ex.run(f->prog_factor, f->d_blob);
-        if (fs) ck(cudaFreeAsync(fs, s), "free");
-        if (auxf) ck(cudaFreeAsync(auxf, s), "free");
-        if (tmp) ck(cudaFreeAsync(tmp, s), "free");
+        tr.mark("enqueued");
+        if (fs) dfree(fs, s);
+        if (auxf) dfree(auxf, s);
+        if (tmp) dfree(tmp, s);
         finish_factor(*f, s);
+        tr.mark("finished");
         *out = f.release();
     });
 }
@@ -1795,7 +1916,7 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
                                  cudaMemcpyDeviceToHost, s),
                "X download");
         for (double* q : {S, T, AUX, tF, tX})
-            if (q) ck(cudaFreeAsync(q, s), "free");
+            if (q) dfree(q, s);
         ck(cudaGetLastError(), "solve kernels");
         if (mem == SPK_MEM_HOST) ck(cudaStreamSynchronize(s), "solve");
     });
@@ -1849,7 +1970,7 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
             B.ld[B_AUX] = f.auxf_rows;
             Exec ex{f, s, B, k};
             ex.run(f.prog_factor, f.d_blob);
-            ck(cudaFreeAsync(auxf, s), "free");
+            dfree(auxf, s);
         }
         finish_factor(f, s);
         *out = r.release();
@@ -1875,8 +1996,8 @@ static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t trans
         Exec ex{f, s, B, ncols};
         ex.run(own_programs ? (transpose ? f.prog_tr : f.prog_fwd) : (transpose ? f.prog_rtr : f.prog_rfwd), f.d_sblob);
         ck(cudaMemcpyAsync(z, T, sizeof(double) * rows * ncols, cudaMemcpyDeviceToHost, s), "z download");
-        ck(cudaFreeAsync(T, s), "free");
-        ck(cudaFreeAsync(AUX, s), "free");
+        dfree(T, s);
+        dfree(AUX, s);
         ck(cudaStreamSynchronize(s), "reduced_solve");
     });
 }
@@ -1920,7 +2041,7 @@ spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku
         ck(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, dy, sizeof(double) * n, sizeof(double) * n, ncols,
                              cudaMemcpyDeviceToHost, s),
            "download");
-        for (double* q : {db, dx, dy}) ck(cudaFreeAsync(q, s), "free");
+        for (double* q : {db, dx, dy}) dfree(q, s);
         ck(cudaStreamSynchronize(s), "band_matmul");
     });
 }
