@@ -96,6 +96,41 @@ spk_status spk_factorize(const double *band, int32_t band_mem, int64_t n, int32_
                          spk_fact **out);
 void spk_fact_destroy(spk_fact *f);
 
+/* ---- multi-GPU slabs (no reference counterpart: the
+ * reference is single-node fork-join, parallel_util.hpp:13-45) ----
+ * Rows [R_g, R_g + n) of a global system factored on one GPU as its own SPIKE
+ * system whose edge partitions also carry the spikes that couple them to the
+ * neighbouring slabs; the local reduced hierarchy ends in one unit.
+ * band: packed columns [-k*open_left, n + k*open_right) of the slab, k =
+ * max(kl, ku) (k halo columns per open edge; device or host). */
+spk_status spk_factorize_slab(const double *band, int32_t band_mem, int64_t n, int32_t kl,
+                              int32_t ku, const spk_plan *plan, const spk_factor_options *opts,
+                              int32_t open_left, int32_t open_right, void *stream,
+                              spk_fact **out);
+/* bit 0: open left edge, bit 1: open right edge */
+int32_t spk_fact_open(const spk_fact *f);
+/* The slab unit's tips [vt; vb; wt; wb] (4 blocks of k*k column-major, device):
+ * top and bottom k rows of its V / W spikes over the slab's reduced rows;
+ * zero blocks where the edge is closed.  These are one "partition" of the
+ * slab-level reduced system (spk_reduced_create with p = number of slabs). */
+spk_status spk_fact_unit_tips(const spk_fact *f, double *d_tips, void *stream);
+
+/* Slab solve with exchange points (device buffers).  Forward: begin exports
+ * [y_top; y_bot] (2k x nrhs); the caller solves the slab-level reduced system
+ * and steps with [x_top of the right slab; x_bot of the left slab].
+ * Transpose: begin exports [chat_0^T tau_t; bhat_last^T tau_b] (2k x nrhs); step
+ * 1 imports [left slab's bhat^T tau_b; right slab's chat^T tau_t] and exports
+ * [t_top; t_bot; V_int^T t; W_int^T t] (4k x nrhs); step 2 imports [z_top; z_bot]
+ * of this slab from the slab-level transposed reduced solve and finishes X.
+ * Blocks are column-major with ld = their row count. */
+typedef struct spk_xsolve spk_xsolve;
+int32_t spk_xsolve_exchanges(const spk_fact *f, int32_t transpose);
+spk_status spk_xsolve_begin(const spk_fact *f, int32_t transpose, const double *d_F, int64_t ldf,
+                            int32_t nrhs, double *d_X, int64_t ldx, void *stream,
+                            double *d_export, spk_xsolve **out);
+spk_status spk_xsolve_step(spk_xsolve *x, const double *d_import, double *d_export);
+void spk_xsolve_end(spk_xsolve *x);
+
 /* Fields of SpikeFactorization (factorize.hpp:56-74).  Host mirrors copied on
  * demand; these synchronise the factorization's stream. */
 spk_status spk_fact_info(const spk_fact *f, int64_t *n, int32_t *kl, int32_t *ku, int32_t *k,
@@ -134,6 +169,9 @@ spk_status spk_reduced_create(const double *vt, const double *vb, const double *
                               spk_reduced **out);
 spk_status spk_reduced_solve(const spk_reduced *r, int32_t transpose, double *z /* host 2pk x ncols */,
                              int32_t ncols, int64_t *couplings);
+/* Same on a device block (2pk x ncols, ld 2pk), ordered on stream. */
+spk_status spk_reduced_solve_device(const spk_reduced *r, int32_t transpose, double *d_z,
+                                    int32_t ncols, void *stream);
 int32_t spk_reduced_levels(const spk_reduced *r);
 /* The reduced-system solve of a factorization on its own (2pk tip block). */
 spk_status spk_fact_reduced_solve(const spk_fact *f, int32_t transpose, double *z, int32_t ncols,
@@ -155,13 +193,21 @@ spk_status spk_generate_band(uint64_t seed, int64_t n, int32_t kl, int32_t ku, d
                              double *d_band, void *stream);
 spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double *d_F, int64_t ldf,
                             void *stream);
-/* Number of kernel launches issued by this library on the calling thread
- * since the last reset (instrumentation for bench.py's gpu_launches). */
+/* The same global matrix / RHS restricted to a slab: band columns
+ * [col0, col0 + ncols) of the n x n system (entries outside the matrix are
+ * zero, so halo columns past either end come out empty); F rows
+ * [row0, row0 + nrows). */
+spk_status spk_generate_band_cols(uint64_t seed, int64_t n, int32_t kl, int32_t ku, double dd,
+                                  int64_t col0, int64_t ncols, double *d_band, void *stream);
+spk_status spk_generate_rhs_rows(uint64_t seed, int64_t row0, int64_t nrows, int32_t ncols,
+                                 double *d_F, int64_t ldf, void *stream);
 /* Device arena: freed factor/scratch blocks are cached for reuse by later calls
  * (stream-ordered).  cached = bytes held; trim returns them to the driver. */
 int64_t spk_arena_cached(void);
 void spk_arena_trim(void);
 
+/* Number of kernel launches issued by this library on the calling thread
+ * since the last reset (instrumentation for bench.py's gpu_launches). */
 int64_t spk_launch_count(int32_t reset);
 
 /* Optional per-kernel-class CUDA-event timing (calling thread): launches are

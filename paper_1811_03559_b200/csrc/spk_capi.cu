@@ -181,7 +181,8 @@ namespace {
 
 enum StageType {
     ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS, ST_TRANSPOSE,
-    ST_WCHECK, ST_SCHUR_INIT, ST_DENSE_LU
+    ST_WCHECK, ST_SCHUR_INIT, ST_DENSE_LU,
+    ST_PHASE = 100  // exchange-point marker (no work, not profiled)
 };
 
 struct Stage {
@@ -359,6 +360,10 @@ inline void dfree(void* p, cudaStream_t s) { arena().release(p, s); }
 struct spk_fact {
     long long n = 0;
     int kl = 0, ku = 0, k = 0, p = 0, piv_on = 0;
+    // Slab of a multi-GPU system: an open edge couples to the neighbouring
+    // slab, so the edge partition carries that spike too and the local
+    // hierarchy ends in one unit with V (open right) / W (open left) spikes.
+    int open_l = 0, open_r = 0;
     double boost_eps = 0.0;
     bool reduced_only = false;
     std::vector<long long> bounds;
@@ -390,6 +395,14 @@ struct spk_fact {
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
     cudaStream_t stream = nullptr;
+
+    // closed-edge predicates (reference kinds: the first partition has no W,
+    // the last no V and is factored as UL)
+    bool first(int i) const { return i == 0 && !open_l; }
+    bool last(int i) const { return i == p - 1 && !open_r; }
+    bool open() const { return open_l || open_r; }
+    bool coupled() const { return k > 0 && (p > 1 || open()); }
+    int top_level() const { return levels.empty() ? -1 : (int)levels.size() - 1; }
 
     ~spk_fact() {
         // stream-ordered release on the factorization's stream (which must
@@ -431,7 +444,7 @@ PartDev make_part(long long r0, int m, int akl, int aku, int piv_on, int rev, in
 void build_levels(spk_fact& f, long long& pool_cursor) {
     const int p = f.p, k = f.k;
     f.levels.clear();
-    if (p < 2 || k == 0) return;
+    if (!f.coupled()) return;
     int L = 0;
     for (int u = p; u > 1; u = (u + 1) / 2) ++L;
     f.levels.resize(L + 1);
@@ -453,22 +466,23 @@ void build_levels(spk_fact& f, long long& pool_cursor) {
             }
         }
     }
-    // spike storage: level 0 holds [vt; vb] / [wt; wb]; level l+1 spikes exist
-    // where the reference forms them (factorize.cpp:104-115) plus carried units
-    for (int l = 0; l < L; ++l) {
+    // spike storage: level 0 holds [vt; vb] / [wt; wb].  A merged unit has a V
+    // spike when its right-most sub-unit has one and a W spike when its
+    // left-most has one (factorize.cpp:104-115 forms exactly those; carried
+    // odd units keep theirs).  Closed slabs: the top unit has neither.
+    for (int l = 0; l <= L; ++l) {
         Level& lv = f.levels[l];
         for (int a = 0; a < lv.units; ++a) {
             const long long sz = (long long)lv.uh[a] * k;
             bool hv = false, hw = false;
             if (l == 0) {
-                hv = a < lv.units - 1;
-                hw = a > 0;
+                hv = a < p - 1 || f.open_r;
+                hw = a > 0 || f.open_l;
             } else {
                 const Level& pv = f.levels[l - 1];
-                const bool carried = 2 * a + 1 >= pv.units;
-                hv = !carried && (2 * a + 1 < pv.units - 1);
-                hw = carried ? true : a > 0;
-                if (l == L) hv = hw = false;
+                const int right = 2 * a + 1 < pv.units ? 2 * a + 1 : 2 * a;
+                hv = pv.voff[right] >= 0;
+                hw = pv.woff[2 * a] >= 0;
             }
             if (hv) {
                 lv.voff[a] = pool_cursor;
@@ -629,6 +643,7 @@ struct Builder {
         prog.push_back(s);
     }
     void memcpy_fx() { prog.push_back(Stage{ST_MEMCPY_FX}); }
+    void phase() { prog.push_back(Stage{ST_PHASE}); }
     void memcpy_fs() { prog.push_back(Stage{ST_MEMCPY_FS}); }
 };
 
@@ -796,7 +811,7 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
         b.lu(units, true);  // register-window LU from the band, or fill + generic LU
         b.transpose_factors();
     }
-    if (p < 2 || k == 0) return;
+    if (!f.coupled()) return;
     if (!f.reduced_only) {
         // spike right-hand sides in FS (n x 2k): V = [0; bhat], W = [chat; 0]
         b.memset_buf(B_FS, 2 * k);
@@ -807,7 +822,7 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             const PartDev& P = f.parts[i];
             const int m = P.m;
             const long long r0 = f.bounds[i];
-            const bool first = i == 0, last = i == p - 1;
+            const bool first = f.first(i), last = f.last(i);  // open edges act as inner partitions
             const View fsv = view(B_FS, r0, 0, 0, m, n);
             const View fsr = view(B_FS, r0, P.rev, 0, m, n);
             const View fsw = view(B_FS, r0 + (long long)k * n, 0, 0, m, n);  // W columns
@@ -902,7 +917,6 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
         }
         b.cpl(cplG);
         b.lu(lus);
-        if (l + 1 == L) break;
         const Level& nx = f.levels[l + 1];
         std::vector<CopyJob> init;
         std::vector<PairZ> zs;
@@ -926,10 +940,18 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             }
         }
         if (lv.units % 2 == 1) {
+            // carried unit: its spikes move up unchanged
             const int h = lv.uh[lv.units - 1];
-            const View src = view(B_POOL, lv.woff[lv.units - 1], 0, 0, h, h);
-            const View dst = view(B_POOL, nx.woff[np], 0, 0, h, h);
-            init.push_back(cj(src, dst, 0, h, CP_COPY, 0, k));
+            if (lv.woff[lv.units - 1] >= 0) {
+                const View src = view(B_POOL, lv.woff[lv.units - 1], 0, 0, h, h);
+                const View dst = view(B_POOL, nx.woff[np], 0, 0, h, h);
+                init.push_back(cj(src, dst, 0, h, CP_COPY, 0, k));
+            }
+            if (lv.voff[lv.units - 1] >= 0) {
+                const View src = view(B_POOL, lv.voff[lv.units - 1], 0, 0, h, h);
+                const View dst = view(B_POOL, nx.voff[np], 0, 0, h, h);
+                init.push_back(cj(src, dst, 0, h, CP_COPY, 0, k));
+            }
         }
         b.copy(init);
         emit_pair_solves(b, zs, B_AUX, -1, k, false, k);
@@ -960,13 +982,27 @@ void build_reduced_solve(spk_fact& f, Builder& b, bool transpose, long long aux_
     }
 }
 
+// Slab exchange (open edges): T rows [0, k) / [H-k, H) are the slab's top and
+// bottom tips, H = 2pk; T has k halo rows on each side, [-k, 0) holding the
+// left neighbour's bottom tip and [H, H+k) the right neighbour's top tip.
+// Export / import blocks are column-major with ld = their row count.
+void emit_unit_correction(spk_fact& f, Builder& b) {
+    // y -= V_unit xi + W_unit eta over the slab's reduced rows (two stages:
+    // both update every row of T)
+    const Level& top = f.levels[f.top_level()];
+    const int H = top.uh[0], k = f.k;
+    const View tview = view(B_T, 0);
+    if (top.voff[0] >= 0) b.gemm({gj(view(B_POOL, top.voff[0], 0, 0, 0, H), 0, tview, H, tview, 0, H, k, GM_SUB)});
+    if (top.woff[0] >= 0) b.gemm({gj(view(B_POOL, top.woff[0], 0, 0, 0, H), 0, tview, -k, tview, 0, H, k, GM_SUB)});
+}
+
 void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
     Builder b{f, pb, f.prog_fwd};
     const int p = f.p, k = f.k;
     const long long kk = (long long)k * k;
     b.memcpy_fx();
     std::vector<SweepJob> s_fl, s_bu;
-    if (p == 1 || k == 0) {
+    if (!f.coupled()) {
         for (int i = 0; i < p; ++i) {
             const PartDev& P = f.parts[i];
             const View xv = view(B_X, f.bounds[i], P.rev, 0, P.m);
@@ -984,11 +1020,11 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
         const long long r0 = f.bounds[i];
         const View xv = view(B_X, r0, P.rev, 0, m);
         s_fl.push_back(sj(xv, i, SW_FWD_L, 0, 0));
-        if (i == 0) {
+        if (f.first(i)) {
             const View tv = view(B_T, k, 0, m - k, k);
             c_edge.push_back(cj(xv, tv, m - k, m));
             s_bu.push_back(sj(tv, i, SW_BWD_U, m - k, m - 1));
-        } else if (i == p - 1) {
+        } else if (f.last(i)) {
             const View tv = view(B_T, 2LL * i * k, 1, m - k, k);
             c_edge.push_back(cj(xv, tv, m - k, m));
             s_bu.push_back(sj(tv, i, SW_BWD_U, m - k, m - 1));
@@ -1003,6 +1039,18 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
     b.sweep(s_bu);
     b.copy(c_inner);
     build_reduced_solve(f, b, false, 0);
+    if (f.open()) {
+        // export [y_top; y_bot]; import [xi; eta] = [right neighbour's x_top;
+        // left neighbour's x_bot] from the slab-level reduced solve
+        const int H = 2 * p * k;
+        b.copy({cj(view(B_T, 0), view(B_XCH, 0), 0, k), cj(view(B_T, 0), view(B_XCH, 2 * k - H), H - k, H)});
+        b.phase();
+        std::vector<CopyJob> imp;
+        if (f.open_r) imp.push_back(cj(view(B_XIN, -H), view(B_T, 0), H, H + k));
+        if (f.open_l) imp.push_back(cj(view(B_XIN, 2 * k), view(B_T, 0), -k, 0));
+        b.copy(imp);
+        emit_unit_correction(f, b);
+    }
     // retrieval
     b.memset_buf(B_S);
     std::vector<GemmJob> g;
@@ -1018,9 +1066,9 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
         const View xv = view(B_X, r0, P.rev, 0, m);
         const View bh = view(B_POOL, f.off_bhat + i * kk, 0, 0, 0, k);
         const View ch = view(B_POOL, f.off_chat + i * kk, 0, 0, 0, k);
-        if (i < p - 1) g.push_back(gj(bh, 0, tview, 2 * (i + 1) * k, sv, m - k, k, k, GM_SET));
-        if (i > 0) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, sv, 0, k, k, GM_SET));
-        if (i == 0 || i == p - 1) {
+        if (!f.last(i)) g.push_back(gj(bh, 0, tview, 2 * (i + 1) * k, sv, m - k, k, k, GM_SET));
+        if (!f.first(i)) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, sv, 0, k, k, GM_SET));
+        if (f.first(i) || f.last(i)) {
             r_fl.push_back(sj(sr, i, SW_FWD_L, P.trunc, 0));
             r_sub.push_back(cj(sr, xv, P.trunc, m, CP_SUB));
             r_bu2.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
@@ -1043,7 +1091,7 @@ void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
     const int p = f.p, k = f.k;
     const long long kk = (long long)k * k;
     b.memcpy_fx();
-    if (p == 1 || k == 0) {
+    if (!f.coupled()) {
         std::vector<SweepJob> a, c;
         for (int i = 0; i < p; ++i) {
             const PartDev& P = f.parts[i];
@@ -1066,8 +1114,8 @@ void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
         const long long r0 = f.bounds[i];
         const View sv = view(B_S, r0, 0, 0, m);
         const View xv = view(B_X, r0, P.rev, 0, m);
-        if (i == 0 || i == p - 1) {
-            const bool last = i == p - 1;
+        if (f.first(i) || f.last(i)) {
+            const bool last = f.last(i);
             zero.push_back(cj(xv, xv, m - k, m, CP_ZERO));
             s_fut.push_back(sj(xv, i, SW_FWD_UT, 0, 0));
             const int w = std::min(m, k + (f.piv_on ? P.kl : 0));
@@ -1102,36 +1150,33 @@ void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
         gcopy.push_back(cj(fg, view(B_T, (2LL * i + 1) * k, 0, (int)(b1 - k), k), (int)(b1 - k), (int)b1));
     }
     const View tview = view(B_T, 0);
+    // where tau lives: the whole partition in S (inner), the tip rows in AUX
+    // (closed first: bottom, closed last: top, in reversed space)
+    auto tau_b = [&](int i) {  // view whose rows [m-k, m) are tau_b(i)
+        const PartDev& Q = f.parts[i];
+        if (f.first(i)) {
+            const int w = std::min(Q.m, k + (f.piv_on ? Q.kl : 0));
+            return view(B_AUX, red_rows, 0, Q.m - w, w);
+        }
+        return view(B_S, f.bounds[i], 0, 0, Q.m);
+    };
+    auto tau_t = [&](int i) {  // view whose rows [0, k) are tau_t(i)
+        const PartDev& Q = f.parts[i];
+        if (f.last(i)) {
+            const int w = std::min(Q.m, k + (f.piv_on ? Q.kl : 0));
+            return view(B_AUX, red_rows + f.tau_w, 1, 0, w);
+        }
+        return view(B_S, f.bounds[i], 0, 0, Q.m);
+    };
     for (int i = 1; i < p; ++i) {
         // tip_t(i) -= bhat_{i-1}^T tau_b(i-1)
-        const PartDev& Q = f.parts[i - 1];
-        const int mq = Q.m;
-        View tb;
-        int brow;
-        if (i - 1 == 0) {
-            const int w = std::min(mq, k + (f.piv_on ? Q.kl : 0));
-            tb = view(B_AUX, red_rows, 0, mq - w, w);
-            brow = mq - k;
-        } else {
-            tb = view(B_S, f.bounds[i - 1], 0, 0, mq);
-            brow = mq - k;
-        }
         const View bh = view(B_POOL, f.off_bhat + (i - 1) * kk, 0, 0, 0, k);
-        g.push_back(gj(bh, 1, tb, brow, tview, 2 * i * k, k, k, GM_SUB));
+        g.push_back(gj(bh, 1, tau_b(i - 1), f.parts[i - 1].m - k, tview, 2 * i * k, k, k, GM_SUB));
     }
     for (int i = 0; i + 1 < p; ++i) {
         // tip_b(i) -= chat_{i+1}^T tau_t(i+1)
-        const PartDev& Q = f.parts[i + 1];
-        const int mq = Q.m;
-        View tt;
-        if (i + 1 == p - 1) {
-            const int w = std::min(mq, k + (f.piv_on ? Q.kl : 0));
-            tt = view(B_AUX, red_rows + f.tau_w, 1, 0, w);
-        } else {
-            tt = view(B_S, f.bounds[i + 1], 0, 0, mq);
-        }
         const View ch = view(B_POOL, f.off_chat + (i + 1) * kk, 0, 0, 0, k);
-        g.push_back(gj(ch, 1, tt, 0, tview, (2 * i + 1) * k, k, k, GM_SUB));
+        g.push_back(gj(ch, 1, tau_t(i + 1), 0, tview, (2 * i + 1) * k, k, k, GM_SUB));
     }
     b.copy(zero);
     b.sweep(s_fut);
@@ -1140,6 +1185,42 @@ void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
     b.sweep(tau_blt);
     b.copy(gcopy);
     b.gemm(g);
+    if (f.open()) {
+        // exchange 1: the neighbours' G-tip terms across the slab edges.
+        // export [chat_0^T tau_t(0); bhat_{p-1}^T tau_b(p-1)], import
+        // [left neighbour's bhat^T tau_b; right neighbour's chat^T tau_t]
+        const int H = 2 * p * k;
+        b.memset_buf(B_XCH);
+        std::vector<GemmJob> ex;
+        if (f.open_l)
+            ex.push_back(gj(view(B_POOL, f.off_chat, 0, 0, 0, k), 1, tau_t(0), 0, view(B_XCH, 0), 0, k, k, GM_SET));
+        if (f.open_r)
+            ex.push_back(gj(view(B_POOL, f.off_bhat + (p - 1) * kk, 0, 0, 0, k), 1, tau_b(p - 1), f.parts[p - 1].m - k,
+                            view(B_XCH, 0), k, k, k, GM_SET));
+        b.gemm(ex);
+        b.phase();
+        std::vector<CopyJob> imp;
+        if (f.open_l) imp.push_back(cj(view(B_XIN, 0), tview, 0, k, CP_SUB));
+        if (f.open_r) imp.push_back(cj(view(B_XIN, 2 * k - H), tview, H - k, H, CP_SUB));
+        b.copy(imp);
+        // exchange 2: slab-level transposed reduced system.  export [t_top;
+        // t_bot; V_int^T t_int; W_int^T t_int], import [z_top; z_bot]
+        b.memset_buf(B_XCH);
+        b.copy({cj(tview, view(B_XCH, 0), 0, k), cj(tview, view(B_XCH, 2 * k - H), H - k, H)});
+        const Level& top = f.levels[f.top_level()];
+        std::vector<GemmJob> proj;
+        if (H > 2 * k) {
+            if (top.voff[0] >= 0)
+                proj.push_back(gj(view(B_POOL, top.voff[0] + k, 0, 0, 0, H), 1, tview, k, view(B_XCH, 0), 2 * k, k,
+                                  H - 2 * k, GM_SET));
+            if (top.woff[0] >= 0)
+                proj.push_back(gj(view(B_POOL, top.woff[0] + k, 0, 0, 0, H), 1, tview, k, view(B_XCH, 0), 3 * k, k,
+                                  H - 2 * k, GM_SET));
+        }
+        b.gemm(proj);
+        b.phase();
+        b.copy({cj(view(B_XIN, 0), tview, 0, k), cj(view(B_XIN, 2 * k - H), tview, H - k, H)});
+    }
     build_reduced_solve(f, b, true, 0);
     b.copy(d_copy);
     b.sweep(d_fut);
@@ -1213,8 +1294,16 @@ struct Exec {
         }
     }
 
-    void run(const Program& prog, const char* blob) {
+    // phase < 0: every stage; else only the stages between the phase-th and
+    // (phase+1)-th ST_PHASE markers (the exchange points of a slab solve)
+    void run(const Program& prog, const char* blob, int phase = -1) {
+        int cur = 0;
         for (const Stage& st : prog) {
+            if (st.t == ST_PHASE) {
+                ++cur;
+                continue;
+            }
+            if (phase >= 0 && cur != phase) continue;
             const char* jobs = blob + st.off;
             const double mult = st.max_nc < 0 ? ncols : 1.0;
             ProfScope ps((int)st.t, s, st.flops_per_col * mult, st.bytes_per_col * mult);
@@ -1322,7 +1411,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     if (!f.reduced_only) {
         for (int i = 0; i < p; ++i) {
             const int m = (int)(f.bounds[i + 1] - f.bounds[i]);
-            const int rev = (p > 1 && i == p - 1) ? 1 : 0;
+            const int rev = (f.coupled() && f.last(i)) ? 1 : 0;
             PartDev P = make_part(f.bounds[i], m, f.kl, f.ku, f.piv_on, rev, k);
             P.fofs = fac_cursor;
             fac_cursor += (long long)P.m * P.rows;
@@ -1331,7 +1420,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
             f.tfac_size += (long long)P.m * P.rowsT;
             f.parts.push_back(P);
         }
-        if (p > 1 && k > 0)
+        if (f.coupled())
             for (int i = 0; i < p; ++i)
                 if (f.parts[i].m < k)
                     fail(SPK_EINVAL, "factorize: partition smaller than the half-bandwidth");
@@ -1407,8 +1496,8 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     f.boost_warnings = 0;
     for (int i = f.p; i < nparts; ++i) f.boost_warnings += fell[i];
     f.factor_sweeps.assign(f.p, 0);
-    if (!f.reduced_only && f.p > 1 && f.k > 0)
-        for (int i = 1; i + 1 < f.p; ++i) f.factor_sweeps[i] = 3;
+    if (!f.reduced_only && f.coupled())
+        for (int i = 0; i < f.p; ++i) f.factor_sweeps[i] = (!f.first(i) && !f.last(i)) ? 3 : 0;
     // coupling paths are known now: compile the solve programs without guards
     f.flags.assign(std::max(f.npairs, 1), 0);
     if (f.npairs > 0)
@@ -1631,15 +1720,18 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
     });
 }
 
-spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
-                         const spk_plan* plan, const spk_factor_options* opts, void* stream,
-                         spk_fact** out) {
+static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
+                                 const spk_plan* plan, const spk_factor_options* opts, int open_l, int open_r,
+                                 void* stream, spk_fact** out) {
     return guarded([&] {
         *out = nullptr;
+        if (!out) fail(SPK_EINVAL, "factorize: null output");
         if (n < 1 || kl < 0 || ku < 0 || kl >= n || ku >= n) fail(SPK_EINVAL, "BandedMatrix: bad shape");
         validate_plan(n, plan);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         auto f = std::make_unique<spk_fact>();
+        f->open_l = open_l ? 1 : 0;
+        f->open_r = open_r ? 1 : 0;
         f->n = n;
         f->kl = kl;
         f->ku = ku;
@@ -1654,27 +1746,31 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         Tracer tr("factorize");
         setup_fact(*f, s);
         tr.mark("setup (symbolic)");
-        // band on device
+        // band on device; a slab's band starts k halo columns early when its
+        // left edge is open and carries k more when its right edge is
         const long long ld = kl + ku + 1;
+        const long long hl = (long long)f->k * f->open_l, hr = (long long)f->k * f->open_r;
         const double* dband = band;
         double* tmp = nullptr;
         if (band_mem == SPK_MEM_HOST) {
-            tmp = dalloc<double>(ld * n, s);
-            ck(cudaMemcpyAsync(tmp, band, sizeof(double) * ld * n, cudaMemcpyHostToDevice, s), "band upload");
+            tmp = dalloc<double>(ld * (n + hl + hr), s);
+            ck(cudaMemcpyAsync(tmp, band, sizeof(double) * ld * (n + hl + hr), cudaMemcpyHostToDevice, s),
+               "band upload");
             dband = tmp;
         }
+        dband += ld * hl;  // column 0 of the slab
         const int p = f->p;
         long long max_elems = 0;
         for (int i = 0; i < p; ++i) max_elems = std::max(max_elems, (long long)f->parts[i].m * f->parts[i].rows);
         (void)max_elems;
         {
             ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);
-            launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->d_pool + f->off_bhat,
+            launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->open_l, f->open_r, f->d_pool + f->off_bhat,
                            f->d_pool + f->off_chat, s);
         }
         double* fs = nullptr;
         double* auxf = nullptr;
-        if (p > 1 && f->k > 0) {
+        if (f->coupled()) {
             fs = dalloc<double>((size_t)n * 2 * f->k, s);
             auxf = dalloc<double>((size_t)f->auxf_rows * f->k, s);
         }
@@ -1698,6 +1794,44 @@ spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_
         *out = f.release();
     });
 }
+
+spk_status spk_factorize(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
+                         const spk_plan* plan, const spk_factor_options* opts, void* stream,
+                         spk_fact** out) {
+    return factorize_impl(band, band_mem, n, kl, ku, plan, opts, 0, 0, stream, out);
+}
+
+spk_status spk_factorize_slab(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
+                              const spk_plan* plan, const spk_factor_options* opts, int32_t open_left,
+                              int32_t open_right, void* stream, spk_fact** out) {
+    return factorize_impl(band, band_mem, n, kl, ku, plan, opts, open_left, open_right, stream, out);
+}
+
+spk_status spk_fact_unit_tips(const spk_fact* f, double* d_tips, void* stream) {
+    return guarded([&] {
+        const int k = f->k;
+        const long long kk = (long long)k * k;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (k == 0) return;
+        ck(cudaMemsetAsync(d_tips, 0, sizeof(double) * 4 * kk, s), "memset");
+        if (!f->coupled()) return;
+        const Level& top = f->levels[f->top_level()];
+        const long long H = top.uh[0];
+        const long long offs[2] = {top.voff[0], top.woff[0]};
+        for (int w = 0; w < 2; ++w) {
+            if (offs[w] < 0) continue;
+            // top rows [0, k) and bottom rows [H-k, H) of the unit spike (ld H)
+            ck(cudaMemcpy2DAsync(d_tips + (2 * w) * kk, sizeof(double) * k, f->d_pool + offs[w], sizeof(double) * H,
+                                 sizeof(double) * k, k, cudaMemcpyDeviceToDevice, s),
+               "unit tips");
+            ck(cudaMemcpy2DAsync(d_tips + (2 * w + 1) * kk, sizeof(double) * k, f->d_pool + offs[w] + H - k,
+                                 sizeof(double) * H, sizeof(double) * k, k, cudaMemcpyDeviceToDevice, s),
+               "unit tips");
+        }
+    });
+}
+
+int32_t spk_fact_open(const spk_fact* f) { return f->open_l | (f->open_r << 1); }
 
 void spk_fact_destroy(spk_fact* f) { delete f; }
 
@@ -1839,88 +1973,188 @@ spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu
     });
 }
 
+}  // extern "C"
+
+// One solve in flight: device buffers plus the program phase it stopped at.
+// A closed factorization runs every phase in one call; a slab runs up to each
+// exchange point and resumes when the neighbours' blocks are imported.
+struct spk_xsolve {
+    spk_fact* f = nullptr;
+    int transpose = 0, nrhs = 0, phase = 0, nphases = 1;
+    cudaStream_t s = nullptr;
+    double *S = nullptr, *T = nullptr, *AUX = nullptr, *tF = nullptr, *tX = nullptr;
+    double *XCH = nullptr, *XIN = nullptr;
+    Bufs B;
+
+    ~spk_xsolve() {
+        for (double* q : {S, T, AUX, tF, tX, XCH, XIN})
+            if (q) dfree(q, s);
+    }
+    const Program& prog() const { return transpose ? f->prog_tr : f->prog_fwd; }
+    // rows of the export block after phase q (column-major, ld = rows)
+    int export_rows(int q) const { return (transpose && q == 1) ? 4 * f->k : 2 * f->k; }
+    void run_phase() {
+        Exec ex{*f, s, B, nrhs};
+        ex.n = f->n;
+        if (phase + 1 < nphases) {
+            B.ld[B_XCH] = export_rows(phase);
+            ex.B.ld[B_XCH] = B.ld[B_XCH];
+        }
+        ex.run(prog(), f->d_sblob, f->open() ? phase : -1);
+        ++phase;
+    }
+};
+
+namespace {
+
+// Validates the call and sets up buffers; F/X device (or host with staging).
+std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf,
+                                       int32_t nrhs, double* X, int64_t ldx, int32_t mem, cudaStream_t s) {
+    spk_fact& f = const_cast<spk_fact&>(*fc);
+    const long long n = f.n;
+    auto x = std::make_unique<spk_xsolve>();
+    x->f = &f;
+    x->transpose = transpose;
+    x->nrhs = nrhs;
+    x->s = s;
+    x->nphases = f.open() ? (transpose ? 3 : 2) : 1;
+    const double* dF = F;
+    double* dX = X;
+    long long lf = ldf, lx = ldx;
+    if (mem == SPK_MEM_HOST) {
+        x->tF = dalloc<double>((size_t)n * nrhs, s);
+        x->tX = dalloc<double>((size_t)n * nrhs, s);
+        ck(cudaMemcpy2DAsync(x->tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
+                             cudaMemcpyHostToDevice, s),
+           "F upload");
+        dF = x->tF;
+        dX = x->tX;
+        lf = lx = n;
+    } else if (transpose) {
+        // the transpose program re-reads F after writing X: never alias
+        const char* f0 = (const char*)F;
+        const char* f1 = (const char*)(F + ldf * (nrhs - 1) + n);
+        const char* x0 = (const char*)X;
+        const char* x1 = (const char*)(X + ldx * (nrhs - 1) + n);
+        if (!(f1 <= x0 || x1 <= f0)) {
+            x->tF = dalloc<double>((size_t)n * nrhs, s);
+            ck(cudaMemcpy2DAsync(x->tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
+                                 cudaMemcpyDeviceToDevice, s),
+               "F copy");
+            dF = x->tF;
+            lf = n;
+        }
+    }
+    Bufs& B = x->B;
+    B = make_bufs(&f);
+    B.p[B_X] = dX;
+    B.ld[B_X] = lx;
+    B.p[B_F] = const_cast<double*>(dF);
+    B.ld[B_F] = lf;
+    if (f.coupled()) {
+        const long long H = 2LL * f.p * f.k, halo = f.open() ? f.k : 0;
+        x->S = dalloc<double>((size_t)n * nrhs, s);
+        x->T = dalloc<double>((size_t)(H + 2 * halo) * nrhs, s);
+        x->AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
+        if (f.open()) {
+            // dead tips of closed edges are read (times zero) by transposed
+            // pair solves: keep them finite
+            ck(cudaMemsetAsync(x->T, 0, sizeof(double) * (H + 2 * halo) * nrhs, s), "memset");
+            x->XCH = dalloc<double>((size_t)4 * f.k * nrhs, s);
+            x->XIN = dalloc<double>((size_t)2 * f.k * nrhs, s);
+        }
+        B.p[B_S] = x->S;
+        B.ld[B_S] = n;
+        B.p[B_T] = x->T + halo;
+        B.ld[B_T] = H + 2 * halo;
+        B.p[B_AUX] = x->AUX;
+        B.ld[B_AUX] = f.aux_rows;
+        B.p[B_XCH] = x->XCH;
+        B.ld[B_XCH] = 2 * f.k;
+        B.p[B_XIN] = x->XIN;
+        B.ld[B_XIN] = 2 * f.k;
+    }
+    B.p[B_POOL] = f.d_pool;
+    B.ld[B_POOL] = 1;
+    return x;
+}
+
+void fill_stats(const spk_fact& f, spk_solve_stats* stats) {
+    if (!stats) return;
+    if (stats->partition_full_sweeps)
+        for (int i = 0; i < f.p; ++i) {
+            const bool edge = f.first(i) || f.last(i);
+            stats->partition_full_sweeps[i] = !f.coupled() ? 2 : (edge ? 2 : 4);
+        }
+    stats->reduced_coupling_solves = f.coupled() ? f.p - 1 : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf, int32_t nrhs,
                      double* X, int64_t ldx, int32_t mem, void* stream, spk_solve_stats* stats) {
     return guarded([&] {
-        spk_fact& f = const_cast<spk_fact&>(*fc);
+        const spk_fact& f = *fc;
         const long long n = f.n;
         if (nrhs < 0) fail(SPK_EINVAL, "solve: negative nrhs");
         if (ldf < n || ldx < n) fail(SPK_EINVAL, transpose ? "transpose_solve: F.rows must equal n"
                                                            : "solve: F.rows must equal n");
-        if (stats) {
-            if (stats->partition_full_sweeps)
-                for (int i = 0; i < f.p; ++i) {
-                    const bool edge = f.p > 1 && (i == 0 || i == f.p - 1);
-                    stats->partition_full_sweeps[i] = f.p == 1 ? 2 : (f.k == 0 ? 2 : (edge ? 2 : 4));
-                }
-            stats->reduced_coupling_solves = (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
-        }
+        if (f.open()) fail(SPK_EINVAL, "solve: slab factorization (open edges) needs spk_xsolve_begin");
+        fill_stats(f, stats);
         if (nrhs == 0) return;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        const double* dF = F;
-        double* dX = X;
-        double* tF = nullptr;
-        double* tX = nullptr;
-        long long lf = ldf, lx = ldx;
-        if (mem == SPK_MEM_HOST) {
-            tF = dalloc<double>((size_t)n * nrhs, s);
-            tX = dalloc<double>((size_t)n * nrhs, s);
-            ck(cudaMemcpy2DAsync(tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
-                                 cudaMemcpyHostToDevice, s),
-               "F upload");
-            dF = tF;
-            dX = tX;
-            lf = lx = n;
-        } else if (transpose) {
-            // the transpose program re-reads F after writing X: never alias
-            const char* f0 = (const char*)F;
-            const char* f1 = (const char*)(F + ldf * (nrhs - 1) + n);
-            const char* x0 = (const char*)X;
-            const char* x1 = (const char*)(X + ldx * (nrhs - 1) + n);
-            if (!(f1 <= x0 || x1 <= f0)) {
-                tF = dalloc<double>((size_t)n * nrhs, s);
-                ck(cudaMemcpy2DAsync(tF, sizeof(double) * n, F, sizeof(double) * ldf, sizeof(double) * n, nrhs,
-                                     cudaMemcpyDeviceToDevice, s),
-                   "F copy");
-                dF = tF;
-                lf = n;
-            }
-        }
-        const bool coupled = f.p > 1 && f.k > 0;
-        double* S = nullptr;
-        double* T = nullptr;
-        double* AUX = nullptr;
-        if (coupled) {
-            S = dalloc<double>((size_t)n * nrhs, s);
-            T = dalloc<double>((size_t)2 * f.p * f.k * nrhs, s);
-            AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
-        }
-        Bufs B = make_bufs(&f);
-        B.p[B_X] = dX;
-        B.ld[B_X] = lx;
-        B.p[B_F] = const_cast<double*>(dF);
-        B.ld[B_F] = lf;
-        B.p[B_S] = S;
-        B.ld[B_S] = n;
-        B.p[B_T] = T;
-        B.ld[B_T] = 2LL * f.p * f.k;
-        B.p[B_AUX] = AUX;
-        B.ld[B_AUX] = f.aux_rows;
-        B.p[B_POOL] = f.d_pool;
-        B.ld[B_POOL] = 1;
-        Exec ex{f, s, B, nrhs};
-        ex.n = n;
-        ex.run(transpose ? f.prog_tr : f.prog_fwd, f.d_sblob);
+        auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, mem, s);
+        x->run_phase();
         if (mem == SPK_MEM_HOST)
-            ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, dX, sizeof(double) * n, sizeof(double) * n, nrhs,
+            ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, x->tX, sizeof(double) * n, sizeof(double) * n, nrhs,
                                  cudaMemcpyDeviceToHost, s),
                "X download");
-        for (double* q : {S, T, AUX, tF, tX})
-            if (q) dfree(q, s);
+        x.reset();
         ck(cudaGetLastError(), "solve kernels");
         if (mem == SPK_MEM_HOST) ck(cudaStreamSynchronize(s), "solve");
     });
 }
+
+int32_t spk_xsolve_exchanges(const spk_fact* f, int32_t transpose) {
+    return f->open() && f->coupled() ? (transpose ? 2 : 1) : 0;
+}
+
+spk_status spk_xsolve_begin(const spk_fact* f, int32_t transpose, const double* d_F, int64_t ldf, int32_t nrhs,
+                            double* d_X, int64_t ldx, void* stream, double* d_export, spk_xsolve** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (nrhs < 1) fail(SPK_EINVAL, "xsolve: nrhs must be positive");
+        if (ldf < f->n || ldx < f->n) fail(SPK_EINVAL, "xsolve: F.rows must equal n");
+        if (!f->open() || !f->coupled()) fail(SPK_EINVAL, "xsolve: not a slab factorization");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto x = open_solve(f, transpose, d_F, ldf, nrhs, d_X, ldx, SPK_MEM_DEVICE, s);
+        x->run_phase();
+        const long long rows = x->export_rows(0);
+        ck(cudaMemcpyAsync(d_export, x->XCH, sizeof(double) * rows * nrhs, cudaMemcpyDeviceToDevice, s), "export");
+        ck(cudaGetLastError(), "xsolve");
+        *out = x.release();
+    });
+}
+
+spk_status spk_xsolve_step(spk_xsolve* x, const double* d_import, double* d_export) {
+    return guarded([&] {
+        if (x->phase >= x->nphases) fail(SPK_EINVAL, "xsolve: solve already complete");
+        const long long k = x->f->k;
+        ck(cudaMemcpyAsync(x->XIN, d_import, sizeof(double) * 2 * k * x->nrhs, cudaMemcpyDeviceToDevice, x->s),
+           "import");
+        const int q = x->phase;
+        x->run_phase();
+        if (x->phase < x->nphases && d_export)
+            ck(cudaMemcpyAsync(d_export, x->XCH, sizeof(double) * x->export_rows(q) * x->nrhs,
+                               cudaMemcpyDeviceToDevice, x->s),
+               "export");
+        ck(cudaGetLastError(), "xsolve");
+    });
+}
+
+void spk_xsolve_end(spk_xsolve* x) { delete x; }
 
 spk_status spk_reduced_create(const double* vt, const double* vb, const double* wt, const double* wb, int32_t p,
                               int32_t k, double boost_eps, spk_reduced** out) {
@@ -1978,15 +2212,14 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
 }
 
 static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t transpose, double* z, int32_t ncols,
-                                   int64_t* couplings) {
+                                   int64_t* couplings, bool device = false, cudaStream_t s = nullptr) {
     return guarded([&] {
         if (couplings) *couplings += (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
         if (ncols == 0 || f.p < 2 || f.k == 0) return;
-        cudaStream_t s = nullptr;
         const long long rows = 2LL * f.p * f.k;
-        double* T = dalloc<double>((size_t)rows * ncols, s);
+        double* T = device ? z : dalloc<double>((size_t)rows * ncols, s);
         double* AUX = dalloc<double>((size_t)f.aux_rows * ncols, s);
-        ck(cudaMemcpyAsync(T, z, sizeof(double) * rows * ncols, cudaMemcpyHostToDevice, s), "z upload");
+        if (!device) ck(cudaMemcpyAsync(T, z, sizeof(double) * rows * ncols, cudaMemcpyHostToDevice, s), "z upload");
         Bufs B = make_bufs(&f);
         B.p[B_T] = T;
         B.ld[B_T] = rows;
@@ -1995,11 +2228,20 @@ static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t trans
         B.p[B_POOL] = f.d_pool;
         Exec ex{f, s, B, ncols};
         ex.run(own_programs ? (transpose ? f.prog_tr : f.prog_fwd) : (transpose ? f.prog_rtr : f.prog_rfwd), f.d_sblob);
+        dfree(AUX, s);
+        if (device) {
+            ck(cudaGetLastError(), "reduced_solve");
+            return;
+        }
         ck(cudaMemcpyAsync(z, T, sizeof(double) * rows * ncols, cudaMemcpyDeviceToHost, s), "z download");
         dfree(T, s);
-        dfree(AUX, s);
         ck(cudaStreamSynchronize(s), "reduced_solve");
     });
+}
+
+spk_status spk_reduced_solve_device(const spk_reduced* r, int32_t transpose, double* d_z, int32_t ncols,
+                                    void* stream) {
+    return reduced_solve_on(*r->f, true, transpose, d_z, ncols, nullptr, true, static_cast<cudaStream_t>(stream));
 }
 
 spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z, int32_t ncols,
@@ -2049,7 +2291,7 @@ spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku
 spk_status spk_generate_band(uint64_t seed, int64_t n, int32_t kl, int32_t ku, double dd, double* d_band,
                              void* stream) {
     return guarded([&] {
-        launch_generate_band(seed, n, kl, ku, dd, d_band, static_cast<cudaStream_t>(stream));
+        launch_generate_band(seed, n, kl, ku, dd, 0, n, d_band, static_cast<cudaStream_t>(stream));
         ck(cudaGetLastError(), "generate_band");
     });
 }
@@ -2057,7 +2299,25 @@ spk_status spk_generate_band(uint64_t seed, int64_t n, int32_t kl, int32_t ku, d
 spk_status spk_generate_rhs(uint64_t seed, int64_t n, int32_t ncols, double* d_F, int64_t ldf, void* stream) {
     return guarded([&] {
         if (ncols == 0) return;
-        launch_generate_rhs(seed, n, ncols, d_F, ldf, static_cast<cudaStream_t>(stream));
+        launch_generate_rhs(seed, 0, n, ncols, d_F, ldf, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "generate_rhs");
+    });
+}
+
+spk_status spk_generate_band_cols(uint64_t seed, int64_t n, int32_t kl, int32_t ku, double dd, int64_t col0,
+                                  int64_t ncols, double* d_band, void* stream) {
+    return guarded([&] {
+        if (ncols <= 0) return;
+        launch_generate_band(seed, n, kl, ku, dd, col0, ncols, d_band, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "generate_band");
+    });
+}
+
+spk_status spk_generate_rhs_rows(uint64_t seed, int64_t row0, int64_t nrows, int32_t ncols, double* d_F,
+                                 int64_t ldf, void* stream) {
+    return guarded([&] {
+        if (ncols == 0 || nrows <= 0) return;
+        launch_generate_rhs(seed, row0, nrows, ncols, d_F, ldf, static_cast<cudaStream_t>(stream));
         ck(cudaGetLastError(), "generate_rhs");
     });
 }

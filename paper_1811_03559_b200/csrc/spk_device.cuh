@@ -9,8 +9,9 @@
 
 namespace spk {
 
-constexpr int kMaxBufs = 8;
-enum BufId { B_X = 0, B_F = 1, B_S = 2, B_T = 3, B_AUX = 4, B_POOL = 5, B_FS = 6, B_FAC = 7 };
+constexpr int kMaxBufs = 10;
+// B_XCH / B_XIN: export / import blocks of a multi-GPU slab solve
+enum BufId { B_X = 0, B_F = 1, B_S = 2, B_T = 3, B_AUX = 4, B_POOL = 5, B_FS = 6, B_FAC = 7, B_XCH = 8, B_XIN = 9 };
 
 // Per call buffer table, passed by value.
 struct Bufs {

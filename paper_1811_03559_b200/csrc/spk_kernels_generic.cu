@@ -349,26 +349,30 @@ __global__ void k_gemm(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
 // k x k corner blocks at every partition boundary: bhat[i] = A[b-k:b, b:b+k],
 // chat[i+1] = A[b:b+k, b-k:b] (zero outside the band / matrix).
 __global__ void k_corners(const double* __restrict__ band, long long n, int akl, int aku,
-                          const long long* __restrict__ bounds, int p, int k,
+                          const long long* __restrict__ bounds, int p, int k, int open_l, int open_r,
                           double* __restrict__ bhat, double* __restrict__ chat) {
-    const int i = blockIdx.y;  // boundary after partition i
-    if (i + 1 >= p) return;
-    const long long b = bounds[i + 1];
+    // boundary j sits before partition j (row bounds[j]); j = 0 / j = p are the
+    // slab edges, coupled to a neighbouring slab through k halo columns when open
+    const int j = blockIdx.y;
+    const long long b = bounds[j];
+    const bool want_b = j >= 1 && (j < p || open_r);  // bhat[j-1]: rows above b, columns from b
+    const bool want_c = j < p && (j >= 1 || open_l);  // chat[j]:   rows from b, columns left of b
+    const long long jlo = open_l ? -(long long)k : 0, jhi = open_r ? n + k : n;
     const int ald = akl + aku + 1;
     const long long kk = (long long)k * k;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
         const int c = e / k, r = e - c * k;
-        {
+        if (want_b) {
             const long long gi = b - k + r, gj = b + c;
             double v = 0.0;
-            if (gi >= 0 && gj < n && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
-            bhat[i * kk + e] = v;
+            if (gi >= 0 && gj < jhi && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
+            bhat[(j - 1) * kk + e] = v;
         }
-        {
+        if (want_c) {
             const long long gi = b + r, gj = b - k + c;
             double v = 0.0;
-            if (gj >= 0 && gi < n && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
-            chat[(i + 1) * kk + e] = v;
+            if (gj >= jlo && gi < n && gi - gj <= akl && gj - gi <= aku) v = band[gj * ald + aku + gi - gj];
+            chat[j * kk + e] = v;
         }
     }
 }
@@ -510,10 +514,10 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const 
 }
 
 void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
-                    int p, int k, double* bhat, double* chat, cudaStream_t s) {
-    if (p < 2 || k == 0) return;
-    dim3 g(grid_for((long long)k * k, 256, 64), p);
-    k_corners<<<g, 256, 0, s>>>(band, n, akl, aku, d_bounds, p, k, bhat, chat);
+                    int p, int k, int open_l, int open_r, double* bhat, double* chat, cudaStream_t s) {
+    if ((p < 2 && !open_l && !open_r) || k == 0) return;
+    dim3 g(grid_for((long long)k * k, 256, 64), p + 1);
+    k_corners<<<g, 256, 0, s>>>(band, n, akl, aku, d_bounds, p, k, open_l, open_r, bhat, chat);
     count_launch();
 }
 

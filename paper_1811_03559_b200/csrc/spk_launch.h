@@ -24,7 +24,7 @@ void launch_gemm(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const 
 void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
                       cudaStream_t s);
 void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
-                    int p, int k, double* bhat, double* chat, cudaStream_t s);
+                    int p, int k, int open_l, int open_r, double* bhat, double* chat, cudaStream_t s);
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
                            const PartDev* d_parts, const double* pool, double* fac, int* piv,
                            unsigned long long* amax, const int* flags, cudaStream_t s);
@@ -54,9 +54,9 @@ bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const Fa
 void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
                               double* tfac, double* dinv, cudaStream_t s);
 
-void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd,
-                          double* band, cudaStream_t s);
-void launch_generate_rhs(unsigned long long seed, long long n, int ncols, double* F, long long ldf,
-                         cudaStream_t s);
+void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd, long long col0,
+                          long long ncols, double* band, cudaStream_t s);
+void launch_generate_rhs(unsigned long long seed, long long row0, long long nrows, int ncols, double* F,
+                         long long ldf, cudaStream_t s);
 
 }  // namespace spk

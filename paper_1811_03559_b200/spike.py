@@ -138,6 +138,27 @@ def lib():
         L.spk_generate_band.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
                                         C.c_void_p, C.c_void_p]
         L.spk_generate_rhs.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
+        L.spk_generate_band_cols.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                                             C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        L.spk_generate_rhs_rows.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
+                                            C.c_int64, C.c_void_p]
+        # multi-GPU slabs
+        L.spk_factorize_slab.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                         C.POINTER(_Plan), C.POINTER(_Opts), C.c_int32, C.c_int32,
+                                         C.c_void_p, C.POINTER(C.c_void_p)]
+        L.spk_fact_open.argtypes = [C.c_void_p]
+        L.spk_fact_open.restype = C.c_int32
+        L.spk_fact_unit_tips.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spk_xsolve_exchanges.argtypes = [C.c_void_p, C.c_int32]
+        L.spk_xsolve_exchanges.restype = C.c_int32
+        L.spk_xsolve_begin.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                       C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.spk_xsolve_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spk_xsolve_end.argtypes = [C.c_void_p]
+        L.spk_xsolve_end.restype = None
+        L.spk_reduced_solve_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
+        L.spk_arena_cached.restype = C.c_int64
+        L.spk_arena_trim.restype = None
         _lib = L
     return _lib
 
