@@ -10,6 +10,11 @@ higher is better, with time per step beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl ours|reference]
 
+N > 1 (torchrun, one process per GPU, NCCL): weak scaling -- ONE global
+system of N*n rows, each GPU factoring and solving its slab with the
+slab-level reduced system exchanged by all-gathers
+(paper_1811_03559_b200/distributed.py).
+
 Inputs are seeded synthetic data (include/spike_b200_gen.h), generated in HBM
 for the device-resident `value`, and in pinned host memory for `e2e`, which
 goes through the public C-ABI with host buffers (copies inside the timed
@@ -191,6 +196,181 @@ def impl_reference(args, cfg):
 # our arm
 
 
+def band_norm(band, chunk=1 << 20):
+    """max column abs-sum of the packed band (||A||_1) without a band-sized temporary."""
+    m = 0.0
+    for i in range(0, band.shape[0], chunk):
+        m = max(m, band[i:i + chunk].abs().sum(dim=1).max().item())
+    return m
+
+
+def profile_roofline(spk, cfg, steps, ms):
+    """Per-kernel-class device time inside the timed region -> roofline object
+    for the dominant class."""
+    import ctypes as C
+    prof = {}
+    ncls = spk.lib().spk_profile_classes()
+    spk.lib().spk_profile_read.restype = C.c_char_p
+    spk.lib().spk_profile_read.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    for c in range(ncls):
+        a, b, d, e = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+        name = spk.lib().spk_profile_read(c, C.byref(a), C.byref(b), C.byref(d), C.byref(e)).decode()
+        if e.value:
+            prof[name] = dict(ms=a.value / steps, flops=b.value / steps, bytes=d.value / steps,
+                              launches=e.value // steps)
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", dict(ms=1, flops=0, bytes=0, launches=1))
+    peaks = measured_peaks()
+    bound = cfg["bound"]
+    tms = top[1]["ms"]
+    if bound == "hbm":
+        ach = top[1]["bytes"] / (tms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
+        unit = "GB/s"
+    else:
+        ach = top[1]["flops"] / (tms * 1e-3) / 1e12
+        peak = FP64_PEAK_MEASURED
+        unit = "TFLOP/s"
+    return {"bound": bound, "kernel": top[0], "achieved": round(ach, 3), "peak": peak, "unit": unit,
+            "frac": round(ach / peak, 4), "traffic": None,
+            "kernel_share_of_step": round(tms / ms, 4),
+            "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm"
+                            else "tools/fp64_peak.cu measured DMMA/DFMA peak on this pool (B200)"),
+            "classes": {kk: {"ms": round(v["ms"], 4), "launches": v["launches"]} for kk, v in prof.items()}}
+
+
+def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
+    """N > 1: one global system of N*n rows (weak scaling: n rows per GPU),
+    each GPU factoring its slab (paper_1811_03559_b200/distributed.py); the
+    only collectives are the tip all-gathers of the slab-level reduced system."""
+    from paper_1811_03559_b200 import distributed as D
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    lib = spk.lib()
+    n_loc, k, nrhs = cfg["n"], cfg["k"], cfg["nrhs"]
+    n_glob = world * n_loc
+    rows = D.slab_rows(n_glob, world)
+    r0, r1 = rows[rank], rows[rank + 1]
+    n = r1 - r0
+    lh, rh = D.halo(rank, world, k)
+    ld = 2 * k + 1
+    band = torch.empty((n + lh + rh, ld), dtype=torch.float64, device=dev)  # slab + halo columns
+    F = torch.empty((nrhs, n), dtype=torch.float64, device=dev)
+    X = torch.empty_like(F)
+    XT = torch.empty_like(F)
+    spk.spike._check(lib.spk_generate_band_cols(SEED_A, n_glob, k, k, cfg["dd"], r0 - lh, n + lh + rh,
+                                                 band.data_ptr(), sptr))
+    spk.spike._check(lib.spk_generate_rhs_rows(SEED_A + 1, r0, n, nrhs, F.data_ptr(), n, sptr))
+    plan = spk.gpu_plan(n, k, k, nrhs, cfg["piv"], args.p)
+    opts = spk.FactorOptions(pivoting=cfg["piv"])
+
+    def step(band_t=band, F_t=F, X_t=X, XT_t=XT):
+        df = D.factorize_distributed(band_t.data_ptr(), n, k, k, plan, opts)
+        D.solve_distributed(df, F_t.data_ptr(), n, nrhs, X_t.data_ptr(), n, False)
+        if cfg["transpose"]:
+            D.solve_distributed(df, F_t.data_ptr(), n, nrhs, XT_t.data_ptr(), n, True)
+        return df
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard: backward error of this slab's rows of A X = F, with the
+    # neighbours' edge rows of X gathered into the halo
+    step()
+    edge = torch.cat([X[:, :k], X[:, n - k:]], dim=1).contiguous()
+    parts = [torch.empty_like(edge) for _ in range(world)]
+    dist.all_gather(parts, edge)
+    Xe = torch.zeros((nrhs, n + lh + rh), dtype=torch.float64, device=dev)
+    Xe[:, lh:lh + n] = X
+    if lh:
+        Xe[:, :k] = parts[rank - 1][:, k:]
+    if rh:
+        Xe[:, lh + n:] = parts[rank + 1][:, :k]
+    R = torch.empty_like(Xe)
+    lib.spk_band_matmul(band.data_ptr(), n + lh + rh, k, k, Xe.data_ptr(), n + lh + rh, nrhs, 0, R.data_ptr(),
+                        n + lh + rh, 1, sptr)
+    anorm = band_norm(band)
+    berr_t = ((R[:, lh:lh + n] - F).abs().amax(dim=1) / (anorm * X.abs().amax(dim=1))).max().reshape(1)
+    dist.all_reduce(berr_t, op=dist.ReduceOp.MAX)
+    berr = berr_t.item()
+    del R, Xe
+    torch.cuda.empty_cache()  # the library's own arena allocates next
+
+    dist.barrier()
+    torch.cuda.synchronize()
+    lib.spk_launch_count(1)
+    lib.spk_profile_reset()
+    lib.spk_profile_enable(1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    lib.spk_profile_enable(0)
+    launches = int(lib.spk_launch_count(1))
+    ms_t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = ms_t.item()
+    fl, useful = alg_flops(dict(cfg, n=n_glob))
+    value = fl / (ms * 1e-3) / 1e9
+    roofline = profile_roofline(spk, cfg, args.steps, ms)
+
+    e2e = None
+    if not args.no_e2e:
+        hband = band.cpu().pin_memory()
+        hF = F.cpu().pin_memory()
+        hX = torch.empty_like(hF).pin_memory()
+        hXT = torch.empty_like(hF).pin_memory()
+        del band, F, X, XT  # the e2e leg stages its own device copies
+        torch.cuda.empty_cache()
+        dband = torch.empty(hband.shape, dtype=torch.float64, device=dev)
+        dF, dX, dXT = (torch.empty(hF.shape, dtype=torch.float64, device=dev) for _ in range(3))
+
+        def e2e_step():
+            dband.copy_(hband, non_blocking=True)
+            dF.copy_(hF, non_blocking=True)
+            step(dband, dF, dX, dXT)
+            hX.copy_(dX, non_blocking=True)
+            if cfg["transpose"]:
+                hXT.copy_(dXT, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        ems_t = torch.tensor([(time.perf_counter() - t0) * 1e3 / e_steps], device=dev)
+        dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
+        ems = ems_t.item()
+        nsol = 2 if cfg["transpose"] else 1
+        e2e = {"value": round(fl / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(ems, 3),
+               "h2d_bytes_per_step": int(world * (hband.numel() + hF.numel()) * 8),
+               "d2h_bytes_per_step": int(world * nsol * hX.numel() * 8)}
+
+    if rank == 0:
+        line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h; each GPU "
+                        "generates its slab + halo columns in HBM)",
+                "config": {"workload": cfg["desc"] + f"; weak scaling: one global system of {world} x n rows",
+                           "n": n_glob, "n_per_gpu": n_loc, "kl": k, "ku": k, "nrhs": nrhs,
+                           "partitions_per_gpu": plan.p, "parallelism": f"slabs{world} (NCCL tip all-gathers)",
+                           "l2": "inputs larger than L2"},
+                "useful_gflops": round(useful / (ms * 1e-3) / 1e9, 3),
+                "backward_error": berr,
+                "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "impl": "ours"}
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
 def impl_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -202,9 +382,10 @@ def impl_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
+    if world > 1 or args.slabs:
+        dist.init_process_group("nccl", device_id=dev)
+        return impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
@@ -238,12 +419,11 @@ def impl_ours(args, cfg):
     R = torch.empty_like(F)
     lib = spk.lib()
     lib.spk_band_matmul(band.data_ptr(), n, k, k, X.data_ptr(), n, nrhs, 0, R.data_ptr(), n, 1, sptr)
-    anorm = band.abs().sum(dim=1).max().item()  # ||A||_1 (column sums) as the scale
+    anorm = band_norm(band)  # ||A||_1 (column sums) as the scale
     berr = ((R - F).abs().amax(dim=1) / (anorm * X.abs().amax(dim=1))).max().item()
     del fact, R
+    torch.cuda.empty_cache()  # the library's own arena allocates next
 
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     spk.lib().spk_launch_count(1)
     spk.lib().spk_profile_reset()
@@ -260,44 +440,11 @@ def impl_ours(args, cfg):
     spk.lib().spk_profile_enable(0)
     launches = int(spk.lib().spk_launch_count(1))
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
     fl, useful = alg_flops(cfg)
-    value = world * fl / (ms * 1e-3) / 1e9
+    value = fl / (ms * 1e-3) / 1e9
 
-    # per-kernel-class device time inside the timed region
-    import ctypes as C
-    prof = {}
-    ncls = spk.lib().spk_profile_classes()
-    spk.lib().spk_profile_read.restype = C.c_char_p
-    spk.lib().spk_profile_read.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                           C.POINTER(C.c_double), C.POINTER(C.c_int64)]
-    for c in range(ncls):
-        a, b, d, e = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
-        name = spk.lib().spk_profile_read(c, C.byref(a), C.byref(b), C.byref(d), C.byref(e)).decode()
-        if e.value:
-            prof[name] = dict(ms=a.value / args.steps, flops=b.value / args.steps, bytes=d.value / args.steps,
-                              launches=e.value // args.steps)
-    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", dict(ms=1, flops=0, bytes=0, launches=1))
-    peaks = measured_peaks()
-    bound = cfg["bound"]
-    tms = top[1]["ms"]
-    if bound == "hbm":
-        ach = top[1]["bytes"] / (tms * 1e-3) / 1e9
-        peak = peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)
-        unit = "GB/s"
-    else:
-        ach = top[1]["flops"] / (tms * 1e-3) / 1e12
-        peak = FP64_PEAK_MEASURED
-        unit = "TFLOP/s"
-    roofline = {"bound": bound, "kernel": top[0], "achieved": round(ach, 3), "peak": peak, "unit": unit,
-                "frac": round(ach / peak, 4), "traffic": None,
-                "kernel_share_of_step": round(tms / ms, 4),
-                "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm"
-                                else "tools/fp64_peak.cu measured DMMA/DFMA peak on this pool (B200)"),
-                "classes": {kk: {"ms": round(v["ms"], 4), "launches": v["launches"]} for kk, v in prof.items()}}
+    roofline = profile_roofline(spk, cfg, args.steps, ms)
+    l2_note = "inputs larger than L2" if flush is None else "L2 flushed between steps"
 
     # e2e through the public C-ABI with pinned host buffers
     e2e = None
@@ -306,6 +453,9 @@ def impl_ours(args, cfg):
         hF = F.cpu().pin_memory()
         hX = torch.empty_like(hF).pin_memory()
         hXT = torch.empty_like(hF).pin_memory()
+        # the e2e leg stages its own device copies: release the resident inputs
+        del band, F, X, XT, flush
+        torch.cuda.empty_cache()
 
         def e2e_step():
             fct = spk.lib()
@@ -321,27 +471,21 @@ def impl_ours(args, cfg):
 
         e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
         t0 = time.perf_counter()
         e_steps = max(1, min(args.steps, 5))
         for _ in range(e_steps):
             e2e_step()
         torch.cuda.synchronize()
         ems = (time.perf_counter() - t0) * 1e3 / e_steps
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
         nsol = 2 if cfg["transpose"] else 1
-        e2e = {"value": round(world * fl / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+        e2e = {"value": round(fl / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                "ms_per_step": round(ems, 3),
                "h2d_bytes_per_step": int(hband.numel() * 8 + nsol * hF.numel() * 8),
                "d2h_bytes_per_step": int(nsol * hX.numel() * 8)}
 
     # CPU baseline: the compiled reference on the box's host cores (rank 0, N=1)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if not args.no_cpu:
         try:
             from oracle.oracle import Reference
             if Reference.load() is not None:
@@ -357,20 +501,18 @@ def impl_ours(args, cfg):
             cpu = {"value": None, "error": str(ex)[:200]}
 
     if rank == 0:
-        line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": 1,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h; generated in HBM)",
                 "config": {"workload": cfg["desc"], "n": n, "kl": k, "ku": k, "nrhs": nrhs,
-                           "partitions": plan.p, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
-                           "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
-                "useful_gflops": round(world * useful / (ms * 1e-3) / 1e9, 3),
+                           "partitions": plan.p, "parallelism": "1gpu",
+                           "l2": l2_note},
+                "useful_gflops": round(useful / (ms * 1e-3) / 1e9, 3),
                 "backward_error": berr,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "impl": "ours"}
         print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
     return 0
 
 
@@ -384,6 +526,8 @@ def main():
     ap.add_argument("--p", type=int, default=0, help="force the partition count")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="multi-GPU slab path even at N=1 (under torchrun; N>1 always uses it)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     args.metric = "fp64 factor+solve GFLOP/s (SPIKE-algorithmic flops), " + CONFIGS[args.config]["desc"]

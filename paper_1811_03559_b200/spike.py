@@ -451,11 +451,29 @@ class _StandaloneReduced:
             pass
 
 
+class _FactHandle:
+    """Owns one spk_fact*.  Shared by a SpikeFactorization and its
+    ReducedLevels without a reference cycle, so dropping the factorization
+    frees its HBM immediately (not at the next cycle collection)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().spk_fact_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class SpikeFactorization:
     """Immutable device-resident SPIKE DS factorization (factorize.hpp:56-74).
     Host mirrors of the tips are fetched on first access."""
 
     def __init__(self, handle, plan: PartitionPlan, n, kl, ku, options: FactorOptions):
+        self._owner = _FactHandle(handle)
         self._h = handle
         self.plan = plan
         self.n, self.kl, self.ku = n, kl, ku
@@ -469,15 +487,7 @@ class SpikeFactorization:
         sw = (C.c_int64 * plan.p)()
         _check(lib().spk_fact_factor_sweeps(handle, sw))
         self.factor_sweeps = [int(x) for x in sw]
-        self.levels = ReducedLevels(self, handle, plan.p, self.k, standalone=False)
-
-    def __del__(self):
-        try:
-            if self._h:
-                lib().spk_fact_destroy(self._h)
-                self._h = None
-        except Exception:
-            pass
+        self.levels = ReducedLevels(self._owner, handle, plan.p, self.k, standalone=False)
 
     def p(self):
         return self.plan.p
