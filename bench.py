@@ -264,12 +264,14 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     plan = spk.gpu_plan(n, k, k, nrhs, cfg["piv"], args.p)
     opts = spk.FactorOptions(pivoting=cfg["piv"])
 
-    def step(band_t=band, F_t=F, X_t=X, XT_t=XT):
+    def run_step(band_t, F_t, X_t, XT_t):
         df = D.factorize_distributed(band_t.data_ptr(), n, k, k, plan, opts)
         D.solve_distributed(df, F_t.data_ptr(), n, nrhs, X_t.data_ptr(), n, False)
         if cfg["transpose"]:
             D.solve_distributed(df, F_t.data_ptr(), n, nrhs, XT_t.data_ptr(), n, True)
-        return df
+
+    def step():
+        run_step(band, F, X, XT)
 
     for _ in range(args.warmup):
         step()
@@ -323,15 +325,16 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
         hF = F.cpu().pin_memory()
         hX = torch.empty_like(hF).pin_memory()
         hXT = torch.empty_like(hF).pin_memory()
-        del band, F, X, XT  # the e2e leg stages its own device copies
+        del band, F, X, XT, step  # the e2e leg stages its own device copies
         torch.cuda.empty_cache()
+        lib.spk_arena_trim()
         dband = torch.empty(hband.shape, dtype=torch.float64, device=dev)
         dF, dX, dXT = (torch.empty(hF.shape, dtype=torch.float64, device=dev) for _ in range(3))
 
         def e2e_step():
             dband.copy_(hband, non_blocking=True)
             dF.copy_(hF, non_blocking=True)
-            step(dband, dF, dX, dXT)
+            run_step(dband, dF, dX, dXT)
             hX.copy_(dX, non_blocking=True)
             if cfg["transpose"]:
                 hXT.copy_(dXT, non_blocking=True)
@@ -454,8 +457,9 @@ def impl_ours(args, cfg):
         hX = torch.empty_like(hF).pin_memory()
         hXT = torch.empty_like(hF).pin_memory()
         # the e2e leg stages its own device copies: release the resident inputs
-        del band, F, X, XT, flush
+        del band, F, X, XT, flush, step
         torch.cuda.empty_cache()
+        lib.spk_arena_trim()
 
         def e2e_step():
             fct = spk.lib()

@@ -264,6 +264,11 @@ struct Arena {
         return (b + g - 1) / g * g;
     }
 
+    static bool tracing() {
+        static const bool t = getenv("SPK_TRACE") && atoi(getenv("SPK_TRACE")) > 1;
+        return t;
+    }
+
     void* alloc(size_t bytes, cudaStream_t s) {
         bytes = round_up(bytes == 0 ? 1 : bytes);
         {
@@ -281,11 +286,19 @@ struct Arena {
                 cached -= b.bytes;
                 if (b.stream != s) cudaStreamWaitEvent(s, b.ev, 0);
                 cudaEventDestroy(b.ev);
+                if (tracing() && bytes > (1u << 30))
+                    fprintf(stderr, "[spk arena] reuse %.3f GB for %.3f GB\n", b.bytes / 1e9, bytes / 1e9);
                 return b.p;
             }
         }
         void* p = nullptr;
         cudaError_t e = cudaMalloc(&p, bytes);
+        if (tracing()) {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            fprintf(stderr, "[spk arena] cudaMalloc %.3f GB (%s), cached %.3f GB, free %.3f GB\n", bytes / 1e9,
+                    e == cudaSuccess ? "ok" : "failed", cached / 1e9, fr / 1e9);
+        }
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             trim();  // give cached blocks back and retry once
@@ -306,8 +319,11 @@ struct Arena {
         cudaEventRecord(b.ev, s);
         free_list.push_back(b);
         cached += b.bytes;
-        // Bound the cache: drop the oldest blocks beyond the cap (waits for
-        // their last use; only reached when shapes keep changing).
+        if (tracing() && b.bytes > (1u << 30))
+            fprintf(stderr, "[spk arena] release %.3f GB, cached %.3f GB\n", b.bytes / 1e9, cached / 1e9);
+        // Bound the cache at 3/4 of HBM: drop the oldest blocks beyond it
+        // (waits for their last use; only reached when shapes keep changing;
+        // a failing cudaMalloc also trims).  C5 keeps ~104 GB cached.
         while (cached > cap() && free_list.size() > 1) {
             ArenaBlock o = free_list.front();
             free_list.erase(free_list.begin());
@@ -316,6 +332,7 @@ struct Arena {
             sizes.erase(o.p);
             cudaFree(o.p);
             cached -= o.bytes;
+            if (tracing()) fprintf(stderr, "[spk arena] evict %.3f GB\n", o.bytes / 1e9);
         }
     }
 
@@ -323,7 +340,7 @@ struct Arena {
         static size_t c = [] {
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
-            return tot / 2;
+            return tot / 4 * 3;
         }();
         return c;
     }
