@@ -28,6 +28,7 @@
 #include "spk_sweep_fast.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 
 namespace spk {
 
@@ -328,7 +329,511 @@ __global__ void __launch_bounds__(32 * NW, 1) k_band_lu_fast(FastLuArgs A) {
     for (int j = threadIdx.x; j < m; j += blockDim.x) A.piv[P.r0 + j] = j;
 }
 
+// ===========================================================================
+// Blocked variant on the FP64 tensor cores (kl, ku <= 128).
+//
+// Same factorization, 8 columns per step instead of 1.  The active window is
+// the 8 x 8 tiles of the rows and columns within the band of the current
+// 8-column panel: T = 8-blocks of max(kl, ku) + 1 column offsets and T-1 tile
+// rows below the panel, held in DMMA accumulator fragments, one warp per tile
+// row, indexed by column offset from the panel (registers rotate one tile per
+// step).  Step J (columns 8J .. 8J+7):
+//   1a. L21 = A21 U11^-1 for each tile row (DMMA with the inverse of the
+//       factored 8 x 8 diagonal block);
+//   1b. U12 = L11^-1 (A12 - L21' U12') per column offset: the panel row was
+//       published before its last (primed) rank-8 update, applied here;
+//   2.  the warp of the row right below the panel publishes its far tile, then
+//       updates the next diagonal tile and factors it (shuffles: LU with the
+//       boosting rule, L11^-1 and U11^-T in lockstep); every other warp applies
+//       the rank-8 update A22 -= L21 U12 (DMMA), shifts its row by one tile and
+//       takes the entering column block (cp.async staging, triple-buffered),
+//       the warp two rows below publishes its row as the panel row of step J+2,
+//       and the warp that took the entering row block last step reads it from
+//       staging inside its update; then the step's L columns / U rows go out in
+//       both packed layouts.
+// Tiles outside the band are exact zeros throughout, so no band tests sit in
+// the update.  Two CTA barriers per 8 columns (the register-window kernel above
+// needs one per column).  Multipliers equal the unblocked ones up to rounding
+// (l = a u_jj^-1 through the block inverse); boosting is decided exactly as
+// above (optimistic pass, re-run with the known threshold).  tools/lu_probe.cu
+// times the phases (the diagonal chain, latency-bound, sets the step time).
+__device__ __forceinline__ void lu_dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+template <int T>
+struct LuDmmaSmem {  // offsets in doubles
+    static constexpr int NW = T - 1;
+    static constexpr int D = 0;                  // [2][64] factored diagonal block, row-major
+    static constexpr int DINV = D + 128;         // [2][8]  1/u_jj
+    static constexpr int LI = DINV + 16;         // [2][64] L11^-1, A-fragment order
+    static constexpr int UI = LI + 128;          // [2][64] U11^-1, B-fragment order
+    static constexpr int PROW = UI + 128;        // [2][T][64] panel row of step J (parity J), accumulator order
+    static constexpr int SCR = PROW + 2 * 64 * T;  // [2][NW][64] per-warp scratch (1a, 1b)
+    static constexpr int L = SCR + 2 * 64 * NW;  // [2][T][64] -L21 by row offset, A-fragment order
+    static constexpr int U = L + 2 * 64 * T;     // [2][T][64] U12 by column offset, B-fragment order
+    static constexpr int ST = U + 2 * 64 * T;    // [3][2T][64] staging: T row tiles, T column tiles (by offset)
+    static constexpr int TOTAL = ST + 3 * 2 * T * 64;
+};
+
+#ifdef SPK_LU_PROFILE
+// tools/lu_probe.cu: per-phase clock totals of CTA 0 (lane 0 of each warp)
+__device__ unsigned long long g_lu_prof[8];
+#define LU_MARK(slot)                                                          \
+    do {                                                                       \
+        if (blockIdx.x == 0 && lane == 0) {                                    \
+            const long long now = clock64();                                  \
+            atomicAdd(&g_lu_prof[(slot)], (unsigned long long)(now - tprev)); \
+            tprev = now;                                                       \
+        }                                                                      \
+    } while (0)
+#else
+#define LU_MARK(slot) \
+    do {              \
+    } while (0)
+#endif
+
+// fragment orders: A (m x k, row-major): lane = m*4 + k%4, slice k/4;
+// B (k x n): lane = n*4 + k%4, slice k/4 -- one conflict-free 8-byte access each
+__device__ __forceinline__ int afrag(int m, int k) { return (k >> 2) * 32 + m * 4 + (k & 3); }
+__device__ __forceinline__ int bfrag(int k, int n) { return (k >> 2) * 32 + n * 4 + (k & 3); }
+
+template <int T>
+__global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) {
+    using S = LuDmmaSmem<T>;
+    constexpr int NW = T - 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sm = reinterpret_cast<double*>(smem_raw);
+    __shared__ double s_red[2 * 32];
+    __shared__ int s_cnt[32];
+
+    const int u = A.units[blockIdx.x];
+    const PartDev P = A.parts[u];
+    const int m = P.m, kl = P.kl, ku = P.ku, rows = P.rows, d = P.d, rowsT = P.rowsT;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = lane >> 2, q = lane & 3;  // accumulator fragment: row gi, columns 2q, 2q+1
+    const int ald = A.akl + A.aku + 1;
+    double* F = A.fac + P.fofs;
+    double* TF = A.tfac + P.tofs;
+    const int nblk = (m + 7) / 8;
+    const unsigned full = 0xffffffffu;
+    // LU-space (i, c) -> input band: base + sg * (c * (ald - 1) + i) (UL: reversed)
+    const double* bbase = A.band + (P.rev ? (long long)(P.r0 + m - 1) * ald + A.aku : (long long)P.r0 * ald + A.aku);
+    const long long sg = P.rev ? -1 : 1;
+    auto inband = [&](int i, int c) { return i < m && c < m && i - c <= kl && c - i <= ku; };
+    // LU-space entry; rows/columns past m continue as the identity
+    auto val = [&](int i, int c) -> double {
+        if (i >= 0 && c >= 0 && inband(i, c)) return bbase[sg * ((long long)c * (ald - 1) + i)];
+        return (i == c && i >= m) ? 1.0 : 0.0;
+    };
+
+    // staging for the recycle at step Jr: the entering block nb = Jr + T as a
+    // row (8 rows x the window columns 8(Jr+1) .., by column offset) and as a
+    // column (window rows 8(Jr+1) .. x 8 columns, by row offset); rows fastest
+    // within a band column, so the gathers coalesce.  Each thread's elements
+    // keep their band offset i - c and shared-memory slot from step to step and
+    // advance by 8 band columns: out-of-band slots are zeroed once, in-band
+    // ones are cp.async'd (identity past the partition end).
+    constexpr int NSE = (2 * 64 * T + 32 * NW - 1) / (32 * NW);
+    int se_off[NSE], se_i[NSE], se_c[NSE];
+    bool se_ok[NSE];
+#pragma unroll
+    for (int k = 0; k < NSE; ++k) {
+        const int idx = threadIdx.x + k * 32 * NW;
+        int i = 0, c = 0, off = -1;  // (i, c) at Jr = 0
+        if (idx < 64 * T) {
+            const int ci = idx >> 3, ii = idx & 7;
+            i = 8 * T + ii;
+            c = 8 + ci;
+            off = (ci >> 3) * 64 + ii * 8 + (ci & 7);
+        } else if (idx < 2 * 64 * T) {
+            const int e = idx - 64 * T, jj = e / (8 * T), ri = e - jj * 8 * T;
+            i = 8 + ri;
+            c = 8 * T + jj;
+            off = (T + (ri >> 3)) * 64 + (ri & 7) * 8 + jj;
+        }
+        se_off[k] = off;
+        se_i[k] = i;
+        se_c[k] = c;
+        se_ok[k] = off >= 0 && i - c <= kl && c - i <= ku;
+        if (off >= 0 && !se_ok[k])
+            for (int b = 0; b < 3; ++b) sm[S::ST + b * 2 * T * 64 + off] = 0.0;
+    }
+    auto stage_load = [&](int Jr) {
+        if (Jr < nblk) {
+            double* st = sm + S::ST + (Jr % 3) * 2 * T * 64;
+#pragma unroll
+            for (int k = 0; k < NSE; ++k) {
+                if (!se_ok[k]) continue;
+                const int i = se_i[k] + 8 * Jr, c = se_c[k] + 8 * Jr;
+                if (i < m && c < m) cp_async8(st + se_off[k], bbase + sg * ((long long)c * (ald - 1) + i));
+                else st[se_off[k]] = i == c ? 1.0 : 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+
+    double amax = 0.0, minpiv = 1.0 / 0.0;
+    int nboost = 0;
+    bool boost_mode = false;
+    double thresh = 0.0, bmag = 0.0;
+
+    // factor the diagonal block of step Jn held as an accumulator fragment;
+    // publish LU, 1/u_jj and both triangular inverses (buffer parity of Jn).
+    // One pass over the 8 pivots: the LU, X = L11^-1 (rows below pivot c take
+    // -l(gi, c) x row c) and Z = U11^-T (row c scales by 1/u_cc, rows below take
+    // -u(c, gi) x row c) advance in lockstep; U11^-1 = Z^T is stored transposed.
+    auto diag_factor = [&](double lu0, double lu1, int Jn) {
+        const int par = Jn & 1, j0n = 8 * Jn;
+        const int c0 = 2 * q, c1 = 2 * q + 1;
+        double x0 = gi == c0, x1 = gi == c1, z0 = x0, z1 = x1;
+        double dmine = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int src = c * 4 + (c >> 1);
+            double pv = __shfl_sync(full, (c & 1) ? lu1 : lu0, src);
+            const double lraw = __shfl_sync(full, (c & 1) ? lu1 : lu0, gi * 4 + (c >> 1));
+            const double u0 = __shfl_sync(full, lu0, c * 4 + q);
+            const double u1 = __shfl_sync(full, lu1, c * 4 + q);
+            const double ua = __shfl_sync(full, lu0, c * 4 + (gi >> 1));
+            const double ub = __shfl_sync(full, lu1, c * 4 + (gi >> 1));
+            const double xk0 = __shfl_sync(full, x0, c * 4 + q);
+            const double xk1 = __shfl_sync(full, x1, c * 4 + q);
+            if (j0n + c < m) {
+                minpiv = fmin(minpiv, fabs(pv));
+                if (boost_mode && fabs(pv) < thresh) {
+                    pv = pv == 0.0 ? bmag : copysign(bmag, pv);
+                    if (lane == 0) ++nboost;
+                }
+            }
+            // the (possibly boosted) pivot in place
+            lu0 = (gi == c && c0 == c) ? pv : lu0;
+            lu1 = (gi == c && c1 == c) ? pv : lu1;
+            // 1/u_cc: hardware estimate + two Newton steps (a zero pivot gives a
+            // non-finite inverse; the boosting re-run replaces it)
+            double inv;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(pv));
+            double e = fma(-pv, inv, 1.0);
+            inv = fma(inv, e, inv);
+            e = fma(-pv, inv, 1.0);
+            inv = fma(inv, e, inv);
+            dmine = lane == c ? inv : dmine;
+            const double lr = lraw * inv;
+            const bool below = gi > c;
+            const double n0 = fma(-lr, u0, lu0), n1 = fma(-lr, u1, lu1);
+            lu0 = below ? (c0 > c ? n0 : (c0 == c ? lr : lu0)) : lu0;
+            lu1 = below ? (c1 > c ? n1 : (c1 == c ? lr : lu1)) : lu1;
+            x0 = below ? fma(-lr, xk0, x0) : x0;
+            x1 = below ? fma(-lr, xk1, x1) : x1;
+            z0 = gi == c ? z0 * inv : z0;
+            z1 = gi == c ? z1 * inv : z1;
+            const double zc0 = __shfl_sync(full, z0, c * 4 + q);
+            const double zc1 = __shfl_sync(full, z1, c * 4 + q);
+            const double ucg = (gi & 1) ? ub : ua;
+            z0 = below ? fma(-ucg, zc0, z0) : z0;
+            z1 = below ? fma(-ucg, zc1, z1) : z1;
+        }
+        if (lane < 8) sm[S::DINV + par * 8 + lane] = dmine;
+        double* sD = sm + S::D + par * 64;
+        sD[gi * 8 + c0] = lu0;
+        sD[gi * 8 + c1] = lu1;
+        // L11^-1 (A-fragment order) and U11^-1 = Z^T (B-fragment order)
+        double* sLi = sm + S::LI + par * 64;
+        double* sUi = sm + S::UI + par * 64;
+        sLi[afrag(gi, c0)] = x0;
+        sLi[afrag(gi, c1)] = x1;
+        sUi[bfrag(c0, gi)] = z0;
+        sUi[bfrag(c1, gi)] = z1;
+    };
+
+    // positions of the packed layouts that no step writes must read as zero
+    for (int idx = threadIdx.x; idx < ku * ku; idx += blockDim.x) {
+        const int c = idx / ku, off = idx - c * ku + 1;
+        if (c < m && off > c) F[(long long)c * rows + d - off] = 0.0;
+    }
+    for (int idx = threadIdx.x; idx < kl * kl; idx += blockDim.x) {
+        const int r = idx / kl, off = idx - r * kl + 1;
+        if (r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
+    }
+
+    double2* prow = reinterpret_cast<double2*>(sm + S::PROW) + lane;  // + parity * T * 32 + offset * 32
+    double* scr = sm + S::SCR + w * 64;
+    double* scr2 = sm + S::SCR + (NW + w) * 64;
+    // transposed factor writes (row-major L rows, packed U columns): thread t
+    // owns one run of <= 8 entries; which of them lie in the band is fixed
+    const int tr_n = 15 + kl + ku;
+    unsigned tr_mask = 0;
+    if ((int)threadIdx.x < tr_n) {
+        const int t = threadIdx.x;
+        for (int qq = 0; qq < 8; ++qq) {
+            const bool in = t < 7 + kl ? (qq < t + 1 && t + 1 - qq <= kl) : (qq <= t - (7 + kl) && t - (7 + kl) - qq <= ku);
+            tr_mask |= (unsigned)in << qq;
+        }
+    }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        double acc[T][2];  // my tile row, by column offset from the panel
+        auto load_row = [&](int b) {  // row block b over column blocks 0..T-1
+#pragma unroll
+            for (int c = 0; c < T; ++c) {
+                const int i = 8 * b + gi, cc = 8 * c + 2 * q;
+                acc[c][0] = val(i, cc);
+                acc[c][1] = val(i, cc + 1);
+                if (i < m) amax = fmax(amax, fmax(fabs(acc[c][0]), fabs(acc[c][1])));
+            }
+        };
+        // step 0: warp 0 factors block row 0 and publishes it (nothing
+        // pending), warp 1 publishes block row 1 for step 1; warp w holds row
+        // block w+1 (row offset ro = ((w - J) mod NW) + 1)
+        if (w == 0) {
+            load_row(0);
+            diag_factor(acc[0][0], acc[0][1], 0);
+#pragma unroll
+            for (int c = 0; c < T; ++c) prow[c * 32] = make_double2(acc[c][0], acc[c][1]);
+        }
+        load_row(w + 1);
+        if (w == 0) {  // panel row of step 1 (block 1) at step-1 offsets, minus the far tile
+#pragma unroll
+            for (int c = 1; c < T; ++c) prow[(T + c - 1) * 32] = make_double2(acc[c][0], acc[c][1]);
+        }
+        stage_load(0);
+        __syncthreads();
+
+        int ro = w + 1;
+#ifdef SPK_LU_PROFILE
+        long long tprev = clock64();
+#endif
+        for (int J = 0; J < nblk; ++J) {
+            const int par = J & 1, j0 = 8 * J;
+            stage_load(J + 1);
+            LU_MARK(0);
+            double* sLc = sm + S::L + par * 64 * T;
+            double* sUc = sm + S::U + par * 64 * T;
+            const double* sLp = sm + S::L + (par ^ 1) * 64 * T;
+            const double* sUp = sm + S::U + (par ^ 1) * 64 * T;
+            // a warp that took the entering row block last step reads it from staging
+            const bool fresh = ro == NW && J > 0;
+            const double* stp = sm + S::ST + ((J + 2) % 3) * 2 * T * 64;  // staging of step J-1
+            // 1a. L21 of my tile row: (panel-column tile) x U11^-1
+            {
+                double a0 = acc[0][0], a1 = acc[0][1];
+                if (fresh) {
+                    const double2 v = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
+                    a0 = v.x;
+                    a1 = v.y;
+                }
+                scr[afrag(gi, 2 * q)] = a0;
+                scr[afrag(gi, 2 * q + 1)] = a1;
+                __syncwarp();
+                const double* sUi = sm + S::UI + par * 64;
+                double c0 = 0.0, c1 = 0.0;
+                lu_dmma(c0, c1, scr[lane], sUi[lane]);
+                lu_dmma(c0, c1, scr[32 + lane], sUi[32 + lane]);
+                sLc[ro * 64 + afrag(gi, 2 * q)] = -c0;
+                sLc[ro * 64 + afrag(gi, 2 * q + 1)] = -c1;
+            }
+            // 1b. U12 of column offset co = w+1: L11^-1 x (panel-row tile with the
+            // previous step's pending update -L21'[1] U12'[co+1] applied)
+            {
+                const int co = w + 1;
+                const double2 pv = prow[(par * T + co) * 32];
+                double c0 = pv.x, c1 = pv.y;
+                if (J > 0 && co + 1 < T) {
+                    lu_dmma(c0, c1, sLp[64 + lane], sUp[(co + 1) * 64 + lane]);
+                    lu_dmma(c0, c1, sLp[64 + 32 + lane], sUp[(co + 1) * 64 + 32 + lane]);
+                }
+                scr2[bfrag(gi, 2 * q)] = c0;
+                scr2[bfrag(gi, 2 * q + 1)] = c1;
+                __syncwarp();
+                const double* sLi = sm + S::LI + par * 64;
+                double u0 = 0.0, u1 = 0.0;
+                lu_dmma(u0, u1, sLi[lane], scr2[lane]);
+                lu_dmma(u0, u1, sLi[32 + lane], scr2[32 + lane]);
+                sUc[co * 64 + bfrag(gi, 2 * q)] = u0;
+                sUc[co * 64 + bfrag(gi, 2 * q + 1)] = u1;
+            }
+            LU_MARK(1);
+            cp_async_wait<1>();  // this step's staging (committed a step ago) has landed
+            __syncthreads();
+            LU_MARK(2);
+
+            const double* st = sm + S::ST + (J % 3) * 2 * T * 64;
+            if (ro == 1) {
+                // my row is the next panel row, already published one step ago
+                // (this step's update is applied by 1b of the next step) except
+                // its far tile, the entering column block; then update and factor
+                // the next diagonal tile.  Next step I take the entering row block.
+                const double2 cv = *reinterpret_cast<const double2*>(st + T * 64 + gi * 8 + 2 * q);
+                prow[((par ^ 1) * T + T - 1) * 32] = cv;
+                if (8 * (J + 1) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
+                double d0 = acc[1][0], d1 = acc[1][1];
+                LU_MARK(3);
+                lu_dmma(d0, d1, sLc[64 + lane], sUc[64 + lane]);
+                lu_dmma(d0, d1, sLc[64 + 32 + lane], sUc[64 + 32 + lane]);
+                diag_factor(d0, d1, J + 1);
+                LU_MARK(4);
+            }
+            if (ro != 1) {
+                // 2. trailing update of my tile row, shifted by one tile; the
+                // entering column block comes in at the far end
+                const double la0 = sLc[ro * 64 + lane], la1 = sLc[ro * 64 + 32 + lane];
+                if (fresh) {
+                    const bool live = 8 * (J - 1 + T) + gi < m;
+#pragma unroll
+                    for (int c = 1; c < T; ++c) {
+                        const double2 v = *reinterpret_cast<const double2*>(stp + c * 64 + gi * 8 + 2 * q);
+                        double t0 = v.x, t1 = v.y;
+                        if (live) amax = fmax(amax, fmax(fabs(t0), fabs(t1)));
+                        lu_dmma(t0, t1, la0, sUc[c * 64 + lane]);
+                        lu_dmma(t0, t1, la1, sUc[c * 64 + 32 + lane]);
+                        acc[c - 1][0] = t0;
+                        acc[c - 1][1] = t1;
+                    }
+                    const double2 v0 = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
+                    if (live) amax = fmax(amax, fmax(fabs(v0.x), fabs(v0.y)));
+                } else {
+#pragma unroll
+                    for (int c = 1; c < T; ++c) {
+                        lu_dmma(acc[c][0], acc[c][1], la0, sUc[c * 64 + lane]);
+                        lu_dmma(acc[c][0], acc[c][1], la1, sUc[c * 64 + 32 + lane]);
+                    }
+#pragma unroll
+                    for (int c = 0; c + 1 < T; ++c) {
+                        acc[c][0] = acc[c + 1][0];
+                        acc[c][1] = acc[c + 1][1];
+                    }
+                }
+                const double2 cv = *reinterpret_cast<const double2*>(st + (T + ro - 1) * 64 + gi * 8 + 2 * q);
+                acc[T - 1][0] = cv.x;
+                acc[T - 1][1] = cv.y;
+                if (8 * (J + ro) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
+                if (ro == 2) {
+                    // publish my row (next step's ro = 1) as the panel row of step J+2
+#pragma unroll
+                    for (int c = 1; c < T; ++c) prow[(par * T + c - 1) * 32] = make_double2(acc[c][0], acc[c][1]);
+                }
+                LU_MARK(5);
+            }
+            // write L columns j0.. and U rows j0.. (both packed layouts) and 1/u_jj
+            if (j0 < m) {
+                const double* sD = sm + S::D + par * 64;
+                // L columns (packed column-major) and U rows (row-major copy): one
+                // contiguous run per warp
+                for (int sgm = w; sgm < 16; sgm += NW) {
+                    const int qq = sgm & 7, c = j0 + qq;
+                    if (c >= m) continue;
+                    if (sgm < 8) {
+                        double* dst = F + (long long)c * rows + d;
+                        for (int off = lane + 1; off <= kl; off += 32) {
+                            const int rr = qq + off;
+                            const double v = rr < 8 ? sD[rr * 8 + qq] : -sLc[(rr >> 3) * 64 + afrag(rr & 7, qq)];
+                            dst[off] = c + off < m ? v : 0.0;
+                        }
+                    } else {
+                        double* dst = TF + (long long)c * rowsT + kl;
+                        for (int off = lane; off <= ku; off += 32) {
+                            const int cc = qq + off;
+                            const double v = cc < 8 ? sD[qq * 8 + cc] : sUc[(cc >> 3) * 64 + bfrag(qq, cc & 7)];
+                            dst[off] = c + off < m ? v : 0.0;
+                        }
+                    }
+                }
+                // L rows (row-major copy) and U columns (packed): one run of <= 8
+                // contiguous entries per thread
+                if ((int)threadIdx.x < tr_n) {
+                    const int t = threadIdx.x;
+                    const bool lrun = t < 7 + kl;
+                    const int x = lrun ? t + 1 : t - (7 + kl);  // rr (L row) or cc (U column)
+                    if (j0 + x < m) {
+                        double v[8];
+                        if (x < 8) {
+#pragma unroll
+                            for (int qq = 0; qq < 8; ++qq) v[qq] = lrun ? sD[x * 8 + qq] : sD[qq * 8 + x];
+                        } else {
+                            const double* src = (lrun ? sLc : sUc) + (x >> 3) * 64 + (x & 7) * 4;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const double2 p0 = *reinterpret_cast<const double2*>(src + 32 * h);
+                                const double2 p1 = *reinterpret_cast<const double2*>(src + 32 * h + 2);
+                                v[4 * h] = p0.x;
+                                v[4 * h + 1] = p0.y;
+                                v[4 * h + 2] = p1.x;
+                                v[4 * h + 3] = p1.y;
+                            }
+                            if (lrun)
+#pragma unroll
+                                for (int qq = 0; qq < 8; ++qq) v[qq] = -v[qq];
+                        }
+                        double* dst = lrun ? TF + (long long)(j0 + x) * rowsT + kl - x
+                                           : F + (long long)(j0 + x) * rows + d - x;
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq)
+                            if (((tr_mask >> qq) & 1) && j0 + qq < m) dst[qq] = v[qq];
+                    }
+                }
+                if (threadIdx.x < 8 && j0 + threadIdx.x < m)
+                    A.dinv[P.r0 + j0 + threadIdx.x] = sm[S::DINV + par * 8 + threadIdx.x];
+            }
+            LU_MARK(6);
+            ro = ro == 1 ? NW : ro - 1;
+            __syncthreads();
+            LU_MARK(7);
+        }
+        cp_async_wait<0>();
+        // optimistic boosting check: max|A_i| and min|u_jj| over the CTA
+        double am = amax, mp = minpiv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            am = fmax(am, __shfl_xor_sync(full, am, o));
+            mp = fmin(mp, __shfl_xor_sync(full, mp, o));
+        }
+        if (lane == 0) {
+            s_red[w] = am;
+            s_red[32 + w] = mp;
+        }
+        __syncthreads();
+        am = 0.0;
+        mp = 1.0 / 0.0;
+        for (int i = 0; i < NW; ++i) {
+            am = fmax(am, s_red[i]);
+            mp = fmin(mp, s_red[32 + i]);
+        }
+        __syncthreads();
+        const double scale = am == 0.0 ? 1.0 : am;
+        if (boost_mode || !(mp < DBL_EPSILON * scale)) break;
+        boost_mode = true;
+        thresh = DBL_EPSILON * scale;
+        bmag = A.boost_eps * scale;
+        nboost = 0;
+    }
+    if (lane == 0) s_cnt[w] = nboost;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nb = 0;
+        for (int i = 0; i < NW; ++i) nb += s_cnt[i];
+        if (nb) atomicAdd(&A.boost_cnt[u], nb);
+    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) A.piv[P.r0 + j] = j;
+}
+
+template <int T>
+static bool launch_lu_dmma(const int* d_units, int nunits, const FastLuArgs& A, cudaStream_t s) {
+    const size_t smem = sizeof(double) * LuDmmaSmem<T>::TOTAL;
+    cudaFuncSetAttribute(k_band_lu_dmma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_band_lu_dmma<T><<<nunits, 32 * (T - 1), smem, s>>>(A);
+    count_launch();
+    return true;
+}
+
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s) {
+    static const bool regwin = getenv("SPK_LU_REGWIN") && atoi(getenv("SPK_LU_REGWIN"));
+    if (!regwin && kmax >= 1) {
+        if (kmax <= 32) return launch_lu_dmma<5>(d_units, nunits, A, s);
+        if (kmax <= 64) return launch_lu_dmma<9>(d_units, nunits, A, s);
+        if (kmax <= 96) return launch_lu_dmma<13>(d_units, nunits, A, s);
+        if (kmax <= 128) return launch_lu_dmma<17>(d_units, nunits, A, s);
+    }
     void (*fn)(FastLuArgs) = nullptr;
     int nw = 0, K = 0;
     if (kmax <= 32) {
