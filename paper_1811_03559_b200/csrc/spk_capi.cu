@@ -1261,6 +1261,34 @@ struct Exec {
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
         if (nc <= 0) return true;
         static const bool no_dmma = getenv("SPK_NO_DMMA_SWEEP") && atoi(getenv("SPK_NO_DMMA_SWEEP"));
+        static const bool sweep_v1 = getenv("SPK_SWEEP_V1") && atoi(getenv("SPK_SWEEP_V1"));
+        // producer/consumer DMMA sweep (spk_sweep_dmma2.cuh): <= 14 compute warps
+        // (8 columns each) + 2 producer warps per CTA.  Taken when it needs no
+        // more column groups than the 16-warp kernel below (each group re-reads
+        // the factor) and keeps >= 6 compute warps busy (with fewer, one warp's
+        // dependency chain sets the pace and the synchronous kernel wins).
+        const int groups2 = (nc + 111) / 112, groups1 = (nc + 127) / 128;
+        const int cols2 = ((nc + groups2 - 1) / groups2 + 7) / 8 * 8;
+        if (!no_dmma && !sweep_v1 && !st.piv && nc >= 8 && st.kwmax <= 192 && groups2 == groups1 && cols2 >= 48) {
+            static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
+            int ntw = 0;
+            for (int t : ntws)
+                if (8 * (t - 1) >= st.kwmax) {
+                    ntw = t;
+                    break;
+                }
+            const int cols = cols2;
+            const dim3 grid(st.njobs, (nc + cols - 1) / cols);
+            FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
+            bool ok = false;
+            switch (st.mode) {
+                case SW_FWD_L: ok = launch_sweep_dmma2_fl(ntw, cols / 8, grid, A, s); break;
+                case SW_BWD_U: ok = launch_sweep_dmma2_bu(ntw, cols / 8, grid, A, s); break;
+                case SW_FWD_UT: ok = launch_sweep_dmma2_fut(ntw, cols / 8, grid, A, s); break;
+                default: ok = launch_sweep_dmma2_blt(ntw, cols / 8, grid, A, s); break;
+            }
+            if (ok) return true;
+        }
         if (!no_dmma && !st.piv && nc >= 8 && st.kwmax <= 192) {
             // blocked tensor-core sweep: 8 columns per warp, <= 16 warps per CTA,
             // column groups balanced across CTAs

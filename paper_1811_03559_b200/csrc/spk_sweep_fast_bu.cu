@@ -3,6 +3,7 @@
 // Split per mode so nvcc builds the templates in parallel.
 #include "spk_sweep_fast.cuh"
 #include "spk_sweep_dmma.cuh"
+#include "spk_sweep_dmma2.cuh"
 #include "spk_launch.h"
 
 #include <cuda_runtime.h>
@@ -63,6 +64,29 @@ bool launch_sweep_dmma_bu(int ntw, int nwarps, dim3 grid, size_t smem, const Fas
         attr_done[slot] = true;
     }
     fn<<<grid, 32 * nwarps, smem, s>>>(A);
+    count_launch();
+    return true;
+}
+
+bool launch_sweep_dmma2_bu(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s) {
+    void (*fn)(FastSweepArgs) = nullptr;
+    int slot = -1;
+    if (ntw == 3) { fn = k_sweep_dmma2<3, SW_BWD_U>; slot = 0; }
+    if (ntw == 5) { fn = k_sweep_dmma2<5, SW_BWD_U>; slot = 1; }
+    if (ntw == 9) { fn = k_sweep_dmma2<9, SW_BWD_U>; slot = 2; }
+    if (ntw == 13) { fn = k_sweep_dmma2<13, SW_BWD_U>; slot = 3; }
+    if (ntw == 17) { fn = k_sweep_dmma2<17, SW_BWD_U>; slot = 4; }
+    if (ntw == 21) { fn = k_sweep_dmma2<21, SW_BWD_U>; slot = 5; }
+    if (ntw == 25) { fn = k_sweep_dmma2<25, SW_BWD_U>; slot = 6; }
+    if (!fn) return false;
+    const size_t smem = dmma2_sweep_smem(ntw);
+    if (smem > 227 * 1024) return false;
+    static bool attr_done[7] = {};
+    if (!attr_done[slot]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_done[slot] = true;
+    }
+    fn<<<grid, 32 * (ncw + kDmma2Producers), smem, s>>>(A);
     count_launch();
     return true;
 }
