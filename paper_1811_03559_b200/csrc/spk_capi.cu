@@ -192,6 +192,7 @@ struct Stage {
     int max_nc = 0;  // sweep/gemm: max explicit columns; -1: call columns
     long long max_elems = 0;
     int max_r = 0;
+    int max_kk = 0;  // gemm: longest inner dimension (split-K choice)
     int buf = 0;  // memset target
     int cols = -1;  // memset columns (-1: call columns)
     // algorithmic work per call column (explicit-column stages: per launch)
@@ -617,6 +618,7 @@ struct Builder {
         }
         s.max_r = mr;
         s.max_nc = mnc;
+        for (auto& j : jobs) s.max_kk = std::max(s.max_kk, j.kk);
         for (auto& j : jobs) {
             const double nc = j.nc < 0 ? 1.0 : j.nc;
             s.flops_per_col += 2.0 * j.r * j.kk * nc;
@@ -1375,8 +1377,18 @@ struct Exec {
                 case ST_GEMM: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
                     static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
-                    if (generic_only) launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
-                    else launch_gemm_dmma((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                    if (generic_only) {
+                        launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                    } else {
+                        const int ns = gemm_splitk_factor(st.njobs, st.max_r, nc, st.max_kk);
+                        if (ns > 1) {
+                            double* ws = dalloc<double>(gemm_splitk_workspace(st.njobs, st.max_r, nc, ns), s);
+                            launch_gemm_dmma((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s, ws, ns);
+                            dfree(ws, s);
+                        } else {
+                            launch_gemm_dmma((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
+                        }
+                    }
                     break;
                 }
                 case ST_LU: {

@@ -11,6 +11,8 @@
 // 4 warps each owning a 32x32 sub-tile = 4x4 DMMA accumulators; A and B
 // chunks are staged through shared memory (cp.async, double-buffered).
 #include "spk_device.cuh"
+
+#include <algorithm>
 #include "spk_launch.h"
 #include "spk_sweep_fast.cuh"
 
@@ -49,7 +51,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 }  // namespace
 
-__global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols) {
+// Split-K (ws != nullptr): blockIdx.z takes K range [z*ks, (z+1)*ks) and writes
+// its partial tile to ws[((job * tiles + tile) * nsplit + z) * TM*TN]; the
+// reduction kernel sums the splits in order (deterministic, no atomics).
+__global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
+                                                   double* __restrict__ ws, int nsplit, int tiles_max) {
     const GemmJob& Jg = jobs[blockIdx.x];
     if (!guard_ok(B.flags, Jg.guard)) return;
     const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
@@ -66,6 +72,13 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
     const int g = lane >> 2, q = lane & 3;
     const int row0 = tr * TM, col0 = tc * TN;
 
+    // K range of this CTA (whole K unless split)
+    int kbeg = 0, kend = jkk;
+    if (ws) {
+        const int ks = ((jkk + nsplit - 1) / nsplit + TK - 1) / TK * TK;
+        kbeg = blockIdx.z * ks;
+        kend = min(jkk, kbeg + ks);
+    }
     auto stage = [=](int buf, int k0) {
         // A tile: TM x TK, element (i, l) of opA(A)
         for (int idx = tid; idx < TM * TK; idx += 128) {
@@ -79,7 +92,7 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
             }
             double* dst = &sA[buf][i * SA + l];
             const int gi = row0 + i, gl = k0 + l;
-            if (gi < jr && gl < jkk) {
+            if (gi < jr && gl < kend) {
                 const double* src = transA ? va.at(gl, gi) : va.at(gi, gl);
                 cp_async8(dst, src);
             } else {
@@ -91,7 +104,7 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
             const int l = idx % TK, c = idx / TK;
             double* dst = &sB[buf][c * SB + l];
             const int gl = k0 + l, gc = col0 + c;
-            if (gl < jkk && gc < nc) cp_async8(dst, vb.at(brow0 + gl, gc));
+            if (gl < kend && gc < nc) cp_async8(dst, vb.at(brow0 + gl, gc));
             else *dst = 0.0;
         }
         cp_async_commit();
@@ -103,12 +116,12 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-    const int nk = (jkk + TK - 1) / TK;
-    stage(0, 0);
+    const int nk = kend > kbeg ? (kend - kbeg + TK - 1) / TK : 0;
+    if (nk > 0) stage(0, kbeg);
     for (int kc = 0; kc < nk; ++kc) {
         const int buf = kc & 1;
         if (kc + 1 < nk) {
-            stage(buf ^ 1, (kc + 1) * TK);
+            stage(buf ^ 1, kbeg + (kc + 1) * TK);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -130,6 +143,16 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
         }
         __syncthreads();
     }
+    if (ws) {
+        double* part = ws + (((size_t)blockIdx.x * tiles_max + blockIdx.y) * nsplit + blockIdx.z) * (TM * TN);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                *reinterpret_cast<double2*>(part + (wm + 8 * a + g) * TN + wn + 8 * b + 2 * q) =
+                    make_double2(acc[a][b][0], acc[a][b][1]);
+        return;
+    }
     // epilogue: C[row, col] with row = wm+8a+g, col = wn+8b+2q+{0,1}
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -148,12 +171,60 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
     }
 }
 
+// split-K reduction: C (=|-=) sum_z ws[..z..] for each job tile, in split order
+__global__ void __launch_bounds__(256) k_gemm_splitk_reduce(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
+                                                            const double* __restrict__ ws, int nsplit,
+                                                            int tiles_max) {
+    const GemmJob& Jg = jobs[blockIdx.x];
+    if (!guard_ok(B.flags, Jg.guard)) return;
+    const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
+    const int jr = Jg.r;
+    const int tiles_r = (jr + TM - 1) / TM;
+    const int tr = blockIdx.y % tiles_r, tc = blockIdx.y / tiles_r;
+    if (tc * TN >= nc || jr <= 0) return;
+    const RV vc = resolve(B, Jg.c);
+    const double* part = ws + ((size_t)blockIdx.x * tiles_max + blockIdx.y) * nsplit * (TM * TN);
+    for (int e = threadIdx.x; e < TM * TN; e += blockDim.x) {
+        const int i = tr * TM + (e & (TM - 1)), c = tc * TN + (e / TM);
+        if (i >= jr || c >= nc) continue;
+        const int loc = (e & (TM - 1)) * TN + e / TM;
+        double sum = 0.0;
+        for (int z = 0; z < nsplit; ++z) sum += part[(size_t)z * (TM * TN) + loc];
+        double* dst = vc.at(Jg.crow0 + i, c);
+        if (Jg.op == GM_SET) *dst = sum;
+        else *dst -= sum;
+    }
+}
+
+int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk) {
+    // few output tiles over a long K (the transposed reduced-system updates):
+    // spread K over CTAs, ~512 per split, enough CTAs for the SMs
+    const long long tiles = (long long)njobs * ((max_r + TM - 1) / TM) * ((max_nc + TN - 1) / TN);
+    if (max_kk < 1024 || tiles >= 296) return 1;
+    int ns = (max_kk + 511) / 512;
+    ns = (int)std::min<long long>(ns, (592 + tiles - 1) / tiles);
+    return std::max(1, std::min(ns, 64));
+}
+
+size_t gemm_splitk_workspace(int njobs, int max_r, int max_nc, int nsplit) {
+    const size_t tiles = (size_t)((max_r + TM - 1) / TM) * ((max_nc + TN - 1) / TN);
+    return (size_t)njobs * tiles * nsplit * TM * TN;
+}
+
 void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
-                      cudaStream_t s) {
+                      cudaStream_t s, double* ws, int nsplit) {
     if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
     const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
+    if (ws && nsplit > 1) {
+        dim3 g(njobs, tr * tc, nsplit);
+        k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
+        dim3 gr(njobs, tr * tc);
+        k_gemm_splitk_reduce<<<gr, 256, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
+        count_launch(2);
+        return;
+    }
     dim3 g(njobs, tr * tc);
-    k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols);
+    k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols, nullptr, 1, tr * tc);
     count_launch();
 }
 
