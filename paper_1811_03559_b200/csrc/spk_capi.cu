@@ -2136,6 +2136,71 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     return x;
 }
 
+// Host-buffer solve, pipelined over right-hand-side column chunks: uploads
+// run ahead on one copy stream, downloads follow on another, so PCIe in both
+// directions overlaps the solve of the neighbouring chunks (columns are
+// independent; each chunk runs the full program on its columns).
+struct CopyStreams {
+    cudaStream_t up = nullptr, down = nullptr;
+    int dev = -1;
+};
+CopyStreams& copy_streams() {
+    static thread_local CopyStreams cs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cs.dev != dev) {
+        ck(cudaStreamCreateWithFlags(&cs.up, cudaStreamNonBlocking), "copy stream");
+        ck(cudaStreamCreateWithFlags(&cs.down, cudaStreamNonBlocking), "copy stream");
+        cs.dev = dev;
+    }
+    return cs;
+}
+
+void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf, int32_t nrhs,
+                          double* X, int64_t ldx, cudaStream_t s) {
+    const long long n = fc->n;
+    CopyStreams& cs = copy_streams();
+    // two chunks: each still fills the sweep kernels (column groups of 80 at
+    // C3); more, narrower chunks cost more compute than the copies they hide
+    const int chunk = std::max(16, ((nrhs + 1) / 2 + 7) / 8 * 8);
+    const int nch = (nrhs + chunk - 1) / chunk;
+    double* dF = dalloc<double>((size_t)n * nrhs, s);
+    double* dX = dalloc<double>((size_t)n * nrhs, s);
+    std::vector<cudaEvent_t> ev(3 * nch + 1);
+    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    // the buffers come from the arena in stream order on s: uploads wait for that
+    ck(cudaEventRecord(ev[3 * nch], s), "event");
+    ck(cudaStreamWaitEvent(cs.up, ev[3 * nch], 0), "wait");
+    for (int c = 0; c < nch; ++c) {
+        const int c0 = c * chunk, nc = std::min(chunk, nrhs - c0);
+        ck(cudaMemcpy2DAsync(dF + (size_t)c0 * n, sizeof(double) * n, F + (size_t)c0 * ldf, sizeof(double) * ldf,
+                             sizeof(double) * n, nc, cudaMemcpyHostToDevice, cs.up),
+           "F upload");
+        ck(cudaEventRecord(ev[c], cs.up), "event");
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int c0 = c * chunk, nc = std::min(chunk, nrhs - c0);
+        ck(cudaStreamWaitEvent(s, ev[c], 0), "wait");
+        {
+            auto x = open_solve(fc, transpose, dF + (size_t)c0 * n, n, nc, dX + (size_t)c0 * n, n, SPK_MEM_DEVICE, s);
+            x->run_phase();
+        }
+        ck(cudaEventRecord(ev[nch + c], s), "event");
+        ck(cudaStreamWaitEvent(cs.down, ev[nch + c], 0), "wait");
+        ck(cudaMemcpy2DAsync(X + (size_t)c0 * ldx, sizeof(double) * ldx, dX + (size_t)c0 * n, sizeof(double) * n,
+                             sizeof(double) * n, nc, cudaMemcpyDeviceToHost, cs.down),
+           "X download");
+        ck(cudaEventRecord(ev[2 * nch + c], cs.down), "event");
+    }
+    // downloads done before the buffers go back to the arena on s
+    ck(cudaStreamWaitEvent(s, ev[3 * nch - 1], 0), "wait");
+    dfree(dF, s);
+    dfree(dX, s);
+    ck(cudaGetLastError(), "solve kernels");
+    ck(cudaStreamSynchronize(s), "solve");
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
 void fill_stats(const spk_fact& f, spk_solve_stats* stats) {
     if (!stats) return;
     if (stats->partition_full_sweeps)
@@ -2162,6 +2227,10 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
         fill_stats(f, stats);
         if (nrhs == 0) return;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (mem == SPK_MEM_HOST && nrhs >= 32) {
+            solve_host_pipelined(fc, transpose, F, ldf, nrhs, X, ldx, s);
+            return;
+        }
         auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, mem, s);
         x->run_phase();
         if (mem == SPK_MEM_HOST)
