@@ -235,6 +235,7 @@ struct Level {
     std::vector<int> pair_part;         // PartDev index per pair: generic 2k coupling unit
     std::vector<int> spart;             // PartDev index per pair: k x k Schur-complement unit
     std::vector<int> gidx;              // flag index per pair (1 = Schur path, 0 = generic)
+    std::vector<long long> sinv;        // pool offset of S^-1 (k x k, ld k) per pair, Schur path
 };
 
 }  // namespace
@@ -720,6 +721,7 @@ GemmJob gj(View a, int transA, View b, int brow0, View c, int crow0, int r, int 
 // `path` bit 0 emits the generic jobs, bit 1 the Schur jobs; when both are
 // emitted (factor time, before the path is known) the jobs carry guards.
 struct PairZ {
+    long long sinv;  // pool offset of S^-1 (Schur unit)
     int spart;  // Schur unit
     int gidx;   // flag index of the pair
     int pair_part;
@@ -740,9 +742,9 @@ Jb guarded_job(Jb j, const PairZ& z, int want) {
 void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long long redld,
                       int ncols_explicit, bool transpose, int k) {
     if (zs.empty()) return;
-    std::vector<CopyJob> gather, scatter;
-    std::vector<SweepJob> s1, s2, t1, t2;
-    std::vector<GemmJob> g, ga, gb, gd, ge;
+    std::vector<CopyJob> gather, scatter, gsc;
+    std::vector<SweepJob> s1, s2;
+    std::vector<GemmJob> g, ga, gb, gd, ge, gs;
     const int nc = ncols_explicit;
     for (const PairZ& z : zs) {
         const View zv = view(z.zbuf, z.zbase, 0, 0, 0, z.zld);
@@ -773,10 +775,13 @@ void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long
             const View Wk = view(B_POOL, z.wr_off + k, 0, 0, 0, hR);       // wr[k:hR]
             const View V = view(B_POOL, z.vl_off + hL - k, 0, 0, 0, hL);   // vl[hL-k:hL]
             const View Vt = view(B_POOL, z.vl_off, 0, 0, 0, hL);           // vl[0:hL-k]
+            // z2 = S^-1 z2 (S^-T z2): GEMM into the pair's red region, copied back
+            const View Si = view(B_POOL, z.sinv, 0, 0, 0, k);
+            const View red = view(redbuf, z.red_row, 0, 0, 2 * k, redld);
+            gs.push_back(guarded_job(gj(Si, transpose ? 1 : 0, zv, hL, red, 0, k, k, GM_SET, nc), z, 1));
+            gsc.push_back(guarded_job(cj(red, z2, 0, k, CP_COPY, 0, nc), z, 1));
             if (!transpose) {
                 ga.push_back(guarded_job(gj(W, 0, zv, hL - k, zv, hL, k, k, GM_SUB, nc), z, 1));
-                t1.push_back(guarded_job(sj(z2, z.spart, SW_FWD_L, 0, 0, 0, nc), z, 1));
-                t2.push_back(guarded_job(sj(z2, z.spart, SW_BWD_U, 0, k - 1, 0, nc), z, 1));
                 gd.push_back(guarded_job(gj(V, 0, zv, hL, zv, hL - k, k, k, GM_SUB, nc), z, 1));
                 if (hL - k > 0) ge.push_back(guarded_job(gj(Vt, 0, zv, hL, zv, 0, hL - k, k, GM_SUB, nc), z, 1));
                 if (hR - k > 0) ge.push_back(guarded_job(gj(Wk, 0, zv, hL - k, zv, hL + k, hR - k, k, GM_SUB, nc), z, 1));
@@ -784,8 +789,6 @@ void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long
                 if (hR - k > 0) ga.push_back(guarded_job(gj(Wk, 1, zv, hL + k, zv, hL - k, k, hR - k, GM_SUB, nc), z, 1));
                 if (hL - k > 0) ga.push_back(guarded_job(gj(Vt, 1, zv, 0, zv, hL, k, hL - k, GM_SUB, nc), z, 1));
                 gb.push_back(guarded_job(gj(V, 1, zv, hL - k, zv, hL, k, k, GM_SUB, nc), z, 1));
-                t1.push_back(guarded_job(sj(z2, z.spart, SW_FWD_UT, 0, 0, 0, nc), z, 1));
-                t2.push_back(guarded_job(sj(z2, z.spart, SW_BWD_LT, 0, 0, 0, nc), z, 1));
                 ge.push_back(guarded_job(gj(W, 1, zv, hL, zv, hL - k, k, k, GM_SUB, nc), z, 1));
             }
         }
@@ -805,15 +808,15 @@ void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long
     // Schur path
     if (!transpose) {
         b.gemm(ga);
-        b.sweep(t1);
-        b.sweep(t2);
+        b.gemm(gs);
+        b.copy(gsc);
         b.gemm(gd);
         b.gemm(ge);
     } else {
         b.gemm(ga);
         b.gemm(gb);
-        b.sweep(t1);
-        b.sweep(t2);
+        b.gemm(gs);
+        b.copy(gsc);
         b.gemm(ge);
     }
 }
@@ -933,6 +936,24 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             b.cjobs(ST_SCHUR_INIT, cplS);
             b.gemm(sgemm);
             b.cjobs(ST_DENSE_LU, cplS);
+            // S^-1 = U_S^-1 L_S^-1 P_S: identity columns through the factored unit
+            std::vector<CopyJob> ident;
+            std::vector<SweepJob> sfl, sbu;
+            for (int a = 0; a < np; ++a) {
+                const View Si = view(B_POOL, lv.sinv[a], 0, 0, k, k);
+                CopyJob cjb = cj(Si, Si, 0, k, CP_IDENT, 0, k);
+                cjb.guard = 2 * lv.gidx[a] + 1;
+                ident.push_back(cjb);
+                SweepJob a1 = sj(Si, lv.spart[a], SW_FWD_L, 0, 0, 0, k);
+                a1.guard = 2 * lv.gidx[a] + 1;
+                sfl.push_back(a1);
+                SweepJob a2 = sj(Si, lv.spart[a], SW_BWD_U, 0, k - 1, 0, k);
+                a2.guard = 2 * lv.gidx[a] + 1;
+                sbu.push_back(a2);
+            }
+            b.copy(ident);
+            b.sweep(sfl);
+            b.sweep(sbu);
         }
         b.cpl(cplG);
         b.lu(lus);
@@ -945,16 +966,16 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
                 const View src = view(B_POOL, lv.voff[2 * a + 1], 0, hL, hR, hR);
                 const View dst = view(B_POOL, nx.voff[a], 0, 0, H, H);
                 init.push_back(cj(src, dst, hL, H, CP_COPY, 0, k));
-                zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
-                                   hL, hR, B_POOL, nx.voff[a], H, red_cursor, both});
+                zs.push_back(PairZ{lv.sinv[a], lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a],
+                                   lv.woff[2 * a + 1], hL, hR, B_POOL, nx.voff[a], H, red_cursor, both});
                 red_cursor += 2 * k;
             }
             if (nx.woff[a] >= 0) {
                 const View src = view(B_POOL, lv.woff[2 * a], 0, 0, hL, hL);
                 const View dst = view(B_POOL, nx.woff[a], 0, 0, H, H);
                 init.push_back(cj(src, dst, 0, hL, CP_COPY, 0, k));
-                zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
-                                   hL, hR, B_POOL, nx.woff[a], H, red_cursor, both});
+                zs.push_back(PairZ{lv.sinv[a], lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a],
+                                   lv.woff[2 * a + 1], hL, hR, B_POOL, nx.woff[a], H, red_cursor, both});
                 red_cursor += 2 * k;
             }
         }
@@ -994,8 +1015,8 @@ void build_reduced_solve(spk_fact& f, Builder& b, bool transpose, long long aux_
         const Level& lv = f.levels[l];
         std::vector<PairZ> zs;
         for (int a = 0; a < lv.units / 2; ++a)
-            zs.push_back(PairZ{lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a], lv.woff[2 * a + 1],
-                               lv.uh[2 * a], lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
+            zs.push_back(PairZ{lv.sinv[a], lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a],
+                               lv.woff[2 * a + 1], lv.uh[2 * a], lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
                                level_base[l] + 2LL * k * a, f.flags[lv.gidx[a]] ? 2 : 1});
         emit_pair_solves(b, zs, B_AUX, -1, -1, transpose, k);
     }
@@ -1491,6 +1512,15 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     pool += kk * p;
     build_levels(f, pool);
     add_couplings(f, fac_cursor);
+    // explicit S^-1 per pair (Schur path): pair solves apply it as one GEMM
+    for (size_t l = 0; l + 1 < f.levels.size(); ++l) {
+        Level& lv = f.levels[l];
+        lv.sinv.assign(lv.units / 2, -1);
+        for (int a = 0; a < lv.units / 2; ++a) {
+            lv.sinv[a] = pool;
+            pool += kk;
+        }
+    }
     f.pool_size = pool;
     f.fac_size = fac_cursor;
     f.piv_size = f.n + (long long)(f.parts.size() - p) * 2 * k + 1;

@@ -66,7 +66,7 @@ struct SweepJob {
     int guard;
 };
 
-enum CopyOp { CP_COPY = 0, CP_ADD = 1, CP_SUB = 2, CP_ZERO = 3 };
+enum CopyOp { CP_COPY = 0, CP_ADD = 1, CP_SUB = 2, CP_ZERO = 3, CP_IDENT = 4 };  // IDENT: dst = (L - L0 == c)
 
 struct CopyJob {
     View src, dst;

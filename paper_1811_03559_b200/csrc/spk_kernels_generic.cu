@@ -293,6 +293,7 @@ __global__ void k_copy(const CopyJob* __restrict__ jobs, Bufs B, int ncols) {
             case CP_COPY: dst = vat(B, J.src, L, c); break;
             case CP_ADD: dst += vat(B, J.src, L, c); break;
             case CP_SUB: dst -= vat(B, J.src, L, c); break;
+            case CP_IDENT: dst = (L - J.L0 == c) ? 1.0 : 0.0; break;
             default: dst = 0.0; break;
         }
     }
