@@ -1459,10 +1459,7 @@ struct Exec {
                 case ST_MEMCPY_FS: {
                     double* dst = st.t == ST_MEMCPY_FX ? B.p[B_X] : B.p[B_S];
                     const long long ldd = st.t == ST_MEMCPY_FX ? B.ld[B_X] : B.ld[B_S];
-                    if (ncols > 0 && dst != B.p[B_F])
-                        ck(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, B.p[B_F], sizeof(double) * B.ld[B_F],
-                                             sizeof(double) * n, ncols, cudaMemcpyDeviceToDevice, s),
-                           "memcpy F");
+                    if (ncols > 0 && dst != B.p[B_F]) launch_copy_cols(B.p[B_F], B.ld[B_F], dst, ldd, n, ncols, s);
                     break;
                 }
             }

@@ -17,6 +17,7 @@
 #include "spk_device.cuh"
 #include "spk_launch.h"
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -297,6 +298,41 @@ __global__ void k_copy(const CopyJob* __restrict__ jobs, Bufs B, int ncols) {
             default: dst = 0.0; break;
         }
     }
+}
+
+// Column block copy dst(:, c) = src(:, c), rows [0, n): the F -> X / F -> S
+// staging of the solve programs.  All SMs, 16-byte accesses where both
+// columns are 16-byte aligned (a D2D cudaMemcpy2DAsync ran at ~1 TB/s).
+__global__ void k_copy_cols(const double* __restrict__ src, long long lds, double* __restrict__ dst, long long ldd,
+                            long long n, int ncols) {
+    for (int c = blockIdx.y; c < ncols; c += gridDim.y) {
+        const double* sc = src + (long long)c * lds;
+        double* dc = dst + (long long)c * ldd;
+        const bool vec = ((reinterpret_cast<uintptr_t>(sc) | reinterpret_cast<uintptr_t>(dc)) & 15) == 0;
+        if (vec) {
+            const long long n2 = n >> 1;
+            const double2* s2 = reinterpret_cast<const double2*>(sc);
+            double2* d2 = reinterpret_cast<double2*>(dc);
+            for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2;
+                 e += (long long)gridDim.x * blockDim.x)
+                d2[e] = s2[e];
+            if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) dc[n - 1] = sc[n - 1];
+        } else {
+            for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+                 e += (long long)gridDim.x * blockDim.x)
+                dc[e] = sc[e];
+        }
+    }
+}
+
+void launch_copy_cols(const double* src, long long lds, double* dst, long long ldd, long long n, int ncols,
+                      cudaStream_t s) {
+    if (ncols <= 0 || n <= 0) return;
+    const long long per_col = (n + 511) / 512;
+    const int gx = (int)std::min<long long>(std::max<long long>(1, per_col / 4), 148 * 8);
+    const int gy = std::max(1, std::min(ncols, 148 * 8 / std::max(1, gx) + 1));
+    k_copy_cols<<<dim3(gx, gy), 256, 0, s>>>(src, lds, dst, ldd, n, ncols);
+    count_launch();
 }
 
 // ---------------------------------------------------------------------------

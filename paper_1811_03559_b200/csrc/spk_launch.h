@@ -25,6 +25,8 @@ void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, c
                       cudaStream_t s, double* ws = nullptr, int nsplit = 1);
 int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk);
 size_t gemm_splitk_workspace(int njobs, int max_r, int max_nc, int nsplit);
+void launch_copy_cols(const double* src, long long lds, double* dst, long long ldd, long long n, int ncols,
+                      cudaStream_t s);
 void launch_corners(const double* band, long long n, int akl, int aku, const long long* d_bounds,
                     int p, int k, int open_l, int open_r, double* bhat, double* chat, cudaStream_t s);
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--p", type=int, default=0)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--prof", action="store_true", help="print per-class device times")
+    ap.add_argument("--factor-only", action="store_true", help="no solves")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     n, k, r = a.n, a.k, a.nrhs
@@ -45,8 +46,9 @@ def main():
         fact = spk.factorize_device(band.data_ptr(), n, k, k, plan, opts, s)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        spk.solve_device(fact, F.data_ptr(), n, r, X.data_ptr(), n, False, s)
-        if a.transpose:
+        if not a.factor_only:
+            spk.solve_device(fact, F.data_ptr(), n, r, X.data_ptr(), n, False, s)
+        if a.transpose and not a.factor_only:
             spk.solve_device(fact, F.data_ptr(), n, r, X.data_ptr(), n, True, s)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
@@ -63,7 +65,7 @@ def main():
             name = L.spk_profile_read(c, C.byref(ms), C.byref(fl), C.byref(by), C.byref(ln)).decode()
             if ln.value:
                 print(f"  {name:12s} {ms.value / a.reps:9.3f} ms  {ln.value // a.reps:4d} launches  "
-                      f"{fl.value / max(ms.value, 1e-9) / 1e9:8.1f} GF/s  {by.value / max(ms.value, 1e-9) / 1e6:8.1f} GB/s")
+                      f"{fl.value / max(ms.value, 1e-9) / 1e9:8.1f} TF/s  {by.value / max(ms.value, 1e-9) / 1e6:8.1f} GB/s")
 
 
 if __name__ == "__main__":
