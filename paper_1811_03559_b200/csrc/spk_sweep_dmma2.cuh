@@ -283,6 +283,17 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
             qv[j][1] = qv[j + 1][1];
         }
         rhs(8 * (b + 1 + NTW + LA - 1) + g, qv[LA - 1][0], qv[LA - 1][1]);
+        {
+            // L2 prefetch of the rows the queue takes PF blocks later: the
+            // register queue alone (LA blocks) is shorter than HBM latency
+            constexpr int PF = 8;
+            const int u = 8 * (b + 1 + NTW + LA - 1 + PF) + g;
+            if (u < nsteps) {
+                const long long pr = phys(rowof(u));
+                if (cv0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp0 + pr));
+                if (cv1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp1 + pr));
+            }
+        }
     }
 }
 
