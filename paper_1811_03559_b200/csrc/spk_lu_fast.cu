@@ -363,7 +363,7 @@ __device__ __forceinline__ void lu_dmma(double& d0, double& d1, double a, double
         : "d"(a), "d"(b));
 }
 
-template <int T>
+template <int T, int TR>
 struct LuDmmaSmem {  // offsets in doubles
     static constexpr int NW = T - 1;
     static constexpr int D = 0;                  // [2][64] factored diagonal block, row-major
@@ -371,11 +371,12 @@ struct LuDmmaSmem {  // offsets in doubles
     static constexpr int LI = DINV + 16;         // [2][64] L11^-1, A-fragment order
     static constexpr int UI = LI + 128;          // [2][64] U11^-1, B-fragment order
     static constexpr int PROW = UI + 128;        // [2][T][64] panel row of step J (parity J), accumulator order
-    static constexpr int SCR = PROW + 2 * 64 * T;  // [2][NW][64] per-warp scratch (1a, 1b)
-    static constexpr int L = SCR + 2 * 64 * NW;  // [2][T][64] -L21 by row offset, A-fragment order
+    static constexpr int L = PROW + 2 * 64 * T;  // [2][T][64] -L21 by row offset, A-fragment order
     static constexpr int U = L + 2 * 64 * T;     // [2][T][64] U12 by column offset, B-fragment order
-    static constexpr int ST = U + 2 * 64 * T;    // [3][2T][64] staging: T row tiles, T column tiles (by offset)
-    static constexpr int TOTAL = ST + 3 * 2 * T * 64;
+    static constexpr int ST = U + 2 * 64 * T;    // staging: [2][T][64] column tiles, then [2][T][64] row tiles
+    static constexpr int NS = T - TR;            // column offsets held in shared memory per tile row
+    static constexpr int WIN = ST + 4 * T * 64;  // [NW][NS][32] double2, circular by step
+    static constexpr int TOTAL = WIN + NW * NS * 64;
 };
 
 #ifdef SPK_LU_PROFILE
@@ -400,9 +401,14 @@ __device__ unsigned long long g_lu_prof[8];
 __device__ __forceinline__ int afrag(int m, int k) { return (k >> 2) * 32 + m * 4 + (k & 3); }
 __device__ __forceinline__ int bfrag(int k, int n) { return (k >> 2) * 32 + n * 4 + (k & 3); }
 
-template <int T>
+// Column offsets < TR of a tile row live in registers; offsets TR..T-1 in a
+// per-warp circular shared-memory window (slot (J + o - TR) mod (T-TR) at step
+// J), so the per-step rotation moves one tile in and one out.  T = 21 (k <=
+// 160) needs it: 20 warps leave 96 registers per thread.
+template <int T, int TR>
 __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) {
-    using S = LuDmmaSmem<T>;
+    using S = LuDmmaSmem<T, TR>;
+    constexpr int NS = T - TR;
     constexpr int NW = T - 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* sm = reinterpret_cast<double*>(smem_raw);
@@ -430,49 +436,42 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
     };
 
     // staging for the recycle at step Jr: the entering block nb = Jr + T as a
-    // row (8 rows x the window columns 8(Jr+1) .., by column offset) and as a
-    // column (window rows 8(Jr+1) .. x 8 columns, by row offset); rows fastest
-    // within a band column, so the gathers coalesce.  Each thread's elements
-    // keep their band offset i - c and shared-memory slot from step to step and
-    // advance by 8 band columns: out-of-band slots are zeroed once, in-band
-    // ones are cp.async'd (identity past the partition end).
-    constexpr int NSE = (2 * 64 * T + 32 * NW - 1) / (32 * NW);
-    int se_off[NSE], se_i[NSE], se_c[NSE];
-    bool se_ok[NSE];
-#pragma unroll
-    for (int k = 0; k < NSE; ++k) {
-        const int idx = threadIdx.x + k * 32 * NW;
-        int i = 0, c = 0, off = -1;  // (i, c) at Jr = 0
+    // column (window rows 8(Jr+1) .. x 8 columns, by row offset; read at step Jr)
+    // and as a row (8 rows x the window columns 8(Jr+1) .., by column offset;
+    // read at step Jr+1 by the warp taking it).  Column tiles of step J+1 and
+    // row tiles of step J are issued at the start of step J (double buffers:
+    // nobody reads the buffer being refilled).  Rows fastest within a band
+    // column, so the gathers coalesce; out-of-band slots are fixed, zeroed once.
+    auto stage_elem = [&](int idx, int Jr, int& i, int& c, int& off) {  // idx < 64T: column tiles
         if (idx < 64 * T) {
-            const int ci = idx >> 3, ii = idx & 7;
-            i = 8 * T + ii;
-            c = 8 + ci;
-            off = (ci >> 3) * 64 + ii * 8 + (ci & 7);
-        } else if (idx < 2 * 64 * T) {
-            const int e = idx - 64 * T, jj = e / (8 * T), ri = e - jj * 8 * T;
-            i = 8 + ri;
-            c = 8 * T + jj;
-            off = (T + (ri >> 3)) * 64 + (ri & 7) * 8 + jj;
+            const int jj = idx / (8 * T), ri = idx - jj * 8 * T;
+            i = 8 * (Jr + 1) + ri;
+            c = 8 * (Jr + T) + jj;
+            off = (Jr & 1) * T * 64 + (ri >> 3) * 64 + (ri & 7) * 8 + jj;
+        } else {
+            const int e = idx - 64 * T, ci = e >> 3, ii = e & 7;
+            i = 8 * (Jr + T) + ii;
+            c = 8 * (Jr + 1) + ci;
+            off = 2 * T * 64 + (Jr & 1) * T * 64 + (ci >> 3) * 64 + ii * 8 + (ci & 7);
         }
-        se_off[k] = off;
-        se_i[k] = i;
-        se_c[k] = c;
-        se_ok[k] = off >= 0 && i - c <= kl && c - i <= ku;
-        if (off >= 0 && !se_ok[k])
-            for (int b = 0; b < 3; ++b) sm[S::ST + b * 2 * T * 64 + off] = 0.0;
-    }
-    auto stage_load = [&](int Jr) {
-        if (Jr < nblk) {
-            double* st = sm + S::ST + (Jr % 3) * 2 * T * 64;
-#pragma unroll
-            for (int k = 0; k < NSE; ++k) {
-                if (!se_ok[k]) continue;
-                const int i = se_i[k] + 8 * Jr, c = se_c[k] + 8 * Jr;
-                if (i < m && c < m) cp_async8(st + se_off[k], bbase + sg * ((long long)c * (ald - 1) + i));
-                else st[se_off[k]] = i == c ? 1.0 : 0.0;
+    };
+    for (int idx = threadIdx.x; idx < 2 * 64 * T; idx += blockDim.x)
+        for (int b2 = 0; b2 < 2; ++b2) {
+            int i, c, off;
+            stage_elem(idx, b2, i, c, off);
+            if (i - c > kl || c - i > ku) sm[S::ST + off] = 0.0;
+        }
+    auto stage_load = [&](int Jr, bool rows) {
+        if (Jr >= 0 && Jr < nblk) {
+            const int lo = rows ? 64 * T : 0;
+            for (int idx = lo + threadIdx.x; idx < lo + 64 * T; idx += blockDim.x) {
+                int i, c, off;
+                stage_elem(idx, Jr, i, c, off);
+                if (i - c > kl || c - i > ku) continue;  // zero, never loaded
+                if (i < m && c < m) cp_async8(sm + S::ST + off, bbase + sg * ((long long)c * (ald - 1) + i));
+                else sm[S::ST + off] = i == c ? 1.0 : 0.0;
             }
         }
-        cp_async_commit();
     };
 
     double amax = 0.0, minpiv = 1.0 / 0.0;
@@ -559,8 +558,7 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
     }
 
     double2* prow = reinterpret_cast<double2*>(sm + S::PROW) + lane;  // + parity * T * 32 + offset * 32
-    double* scr = sm + S::SCR + w * 64;
-    double* scr2 = sm + S::SCR + (NW + w) * 64;
+    double2* win = reinterpret_cast<double2*>(sm + S::WIN) + (size_t)w * NS * 32 + lane;
     // transposed factor writes (row-major L rows, packed U columns): thread t
     // owns one run of <= 8 entries; which of them lie in the band is fixed
     const int tr_n = 15 + kl + ku;
@@ -573,14 +571,38 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
         }
     }
     for (int attempt = 0; attempt < 2; ++attempt) {
-        double acc[T][2];  // my tile row, by column offset from the panel
-        auto load_row = [&](int b) {  // row block b over column blocks 0..T-1
+        double acc[TR][2];  // my tile row, by column offset from the panel (offsets < TR)
+        // offset c of my row as seen at step J: registers or window slot
+        auto slot = [&](int J, int c) {
+            int sl = (J % NS) + c - TR;
+            if (sl >= NS) sl -= NS;
+            return sl;
+        };
+        auto get = [&](int J, int c, double& t0, double& t1) {
+            if (c < TR) {
+                t0 = acc[c < TR ? c : 0][0];
+                t1 = acc[c < TR ? c : 0][1];
+            } else {
+                const double2 v = win[slot(J, c) * 32];
+                t0 = v.x;
+                t1 = v.y;
+            }
+        };
+        auto put = [&](int J, int c, double t0, double t1) {
+            if (c < TR) {
+                acc[c < TR ? c : 0][0] = t0;
+                acc[c < TR ? c : 0][1] = t1;
+            } else {
+                win[slot(J, c) * 32] = make_double2(t0, t1);
+            }
+        };
+        auto load_row = [&](int b) {  // row block b over column blocks 0..T-1 (step 0 offsets)
 #pragma unroll
             for (int c = 0; c < T; ++c) {
                 const int i = 8 * b + gi, cc = 8 * c + 2 * q;
-                acc[c][0] = val(i, cc);
-                acc[c][1] = val(i, cc + 1);
-                if (i < m) amax = fmax(amax, fmax(fabs(acc[c][0]), fabs(acc[c][1])));
+                const double v0 = val(i, cc), v1 = val(i, cc + 1);
+                put(0, c, v0, v1);
+                if (i < m) amax = fmax(amax, fmax(fabs(v0), fabs(v1)));
             }
         };
         // step 0: warp 0 factors block row 0 and publishes it (nothing
@@ -590,14 +612,23 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
             load_row(0);
             diag_factor(acc[0][0], acc[0][1], 0);
 #pragma unroll
-            for (int c = 0; c < T; ++c) prow[c * 32] = make_double2(acc[c][0], acc[c][1]);
+            for (int c = 0; c < T; ++c) {
+                double t0, t1;
+                get(0, c, t0, t1);
+                prow[c * 32] = make_double2(t0, t1);
+            }
         }
         load_row(w + 1);
         if (w == 0) {  // panel row of step 1 (block 1) at step-1 offsets, minus the far tile
 #pragma unroll
-            for (int c = 1; c < T; ++c) prow[(T + c - 1) * 32] = make_double2(acc[c][0], acc[c][1]);
+            for (int c = 1; c < T; ++c) {
+                double t0, t1;
+                get(0, c, t0, t1);
+                prow[(T + c - 1) * 32] = make_double2(t0, t1);
+            }
         }
-        stage_load(0);
+        stage_load(0, false);
+        cp_async_commit();
         __syncthreads();
 
         int ro = w + 1;
@@ -606,7 +637,9 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
 #endif
         for (int J = 0; J < nblk; ++J) {
             const int par = J & 1, j0 = 8 * J;
-            stage_load(J + 1);
+            stage_load(J + 1, false);
+            stage_load(J, true);
+            cp_async_commit();
             LU_MARK(0);
             double* sLc = sm + S::L + par * 64 * T;
             double* sUc = sm + S::U + par * 64 * T;
@@ -614,7 +647,7 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
             const double* sUp = sm + S::U + (par ^ 1) * 64 * T;
             // a warp that took the entering row block last step reads it from staging
             const bool fresh = ro == NW && J > 0;
-            const double* stp = sm + S::ST + ((J + 2) % 3) * 2 * T * 64;  // staging of step J-1
+            const double* stp = sm + S::ST + 2 * T * 64 + ((J + 1) & 1) * T * 64;  // row tiles of step J-1
             // 1a. L21 of my tile row: (panel-column tile) x U11^-1
             {
                 double a0 = acc[0][0], a1 = acc[0][1];
@@ -623,13 +656,19 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                     a0 = v.x;
                     a1 = v.y;
                 }
-                scr[afrag(gi, 2 * q)] = a0;
-                scr[afrag(gi, 2 * q + 1)] = a1;
-                __syncwarp();
+                // accumulator -> A fragments: A[gi][q + 4 ks] sits in lane gi*4 + 2ks + q/2
+                double af[2];
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int src = gi * 4 + 2 * ks + (q >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, a0, src);
+                    const double v1 = __shfl_sync(0xffffffffu, a1, src);
+                    af[ks] = (q & 1) ? v1 : v0;
+                }
                 const double* sUi = sm + S::UI + par * 64;
                 double c0 = 0.0, c1 = 0.0;
-                lu_dmma(c0, c1, scr[lane], sUi[lane]);
-                lu_dmma(c0, c1, scr[32 + lane], sUi[32 + lane]);
+                lu_dmma(c0, c1, af[0], sUi[lane]);
+                lu_dmma(c0, c1, af[1], sUi[32 + lane]);
                 sLc[ro * 64 + afrag(gi, 2 * q)] = -c0;
                 sLc[ro * 64 + afrag(gi, 2 * q + 1)] = -c1;
             }
@@ -643,13 +682,19 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                     lu_dmma(c0, c1, sLp[64 + lane], sUp[(co + 1) * 64 + lane]);
                     lu_dmma(c0, c1, sLp[64 + 32 + lane], sUp[(co + 1) * 64 + 32 + lane]);
                 }
-                scr2[bfrag(gi, 2 * q)] = c0;
-                scr2[bfrag(gi, 2 * q + 1)] = c1;
-                __syncwarp();
+                // accumulator -> B fragments: B[q + 4 ks][gi] sits in lane (q + 4ks)*4 + gi/2
+                double bf[2];
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int src = (q + 4 * ks) * 4 + (gi >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, c0, src);
+                    const double v1 = __shfl_sync(0xffffffffu, c1, src);
+                    bf[ks] = (gi & 1) ? v1 : v0;
+                }
                 const double* sLi = sm + S::LI + par * 64;
                 double u0 = 0.0, u1 = 0.0;
-                lu_dmma(u0, u1, sLi[lane], scr2[lane]);
-                lu_dmma(u0, u1, sLi[32 + lane], scr2[32 + lane]);
+                lu_dmma(u0, u1, sLi[lane], bf[0]);
+                lu_dmma(u0, u1, sLi[32 + lane], bf[1]);
                 sUc[co * 64 + bfrag(gi, 2 * q)] = u0;
                 sUc[co * 64 + bfrag(gi, 2 * q + 1)] = u1;
             }
@@ -658,13 +703,13 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
             __syncthreads();
             LU_MARK(2);
 
-            const double* st = sm + S::ST + (J % 3) * 2 * T * 64;
+            const double* stc = sm + S::ST + (J & 1) * T * 64;  // column tiles of step J (by row offset - 1)
             if (ro == 1) {
                 // my row is the next panel row, already published one step ago
                 // (this step's update is applied by 1b of the next step) except
                 // its far tile, the entering column block; then update and factor
                 // the next diagonal tile.  Next step I take the entering row block.
-                const double2 cv = *reinterpret_cast<const double2*>(st + T * 64 + gi * 8 + 2 * q);
+                const double2 cv = *reinterpret_cast<const double2*>(stc + gi * 8 + 2 * q);
                 prow[((par ^ 1) * T + T - 1) * 32] = cv;
                 if (8 * (J + 1) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
                 double d0 = acc[1][0], d1 = acc[1][1];
@@ -687,31 +732,49 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                         if (live) amax = fmax(amax, fmax(fabs(t0), fabs(t1)));
                         lu_dmma(t0, t1, la0, sUc[c * 64 + lane]);
                         lu_dmma(t0, t1, la1, sUc[c * 64 + 32 + lane]);
-                        acc[c - 1][0] = t0;
-                        acc[c - 1][1] = t1;
+                        put(J + 1, c - 1, t0, t1);
                     }
                     const double2 v0 = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
                     if (live) amax = fmax(amax, fmax(fabs(v0.x), fabs(v0.y)));
                 } else {
 #pragma unroll
                     for (int c = 1; c < T; ++c) {
-                        lu_dmma(acc[c][0], acc[c][1], la0, sUc[c * 64 + lane]);
-                        lu_dmma(acc[c][0], acc[c][1], la1, sUc[c * 64 + 32 + lane]);
+                        if (c < TR) {
+                            lu_dmma(acc[c < TR ? c : 0][0], acc[c < TR ? c : 0][1], la0, sUc[c * 64 + lane]);
+                            lu_dmma(acc[c < TR ? c : 0][0], acc[c < TR ? c : 0][1], la1, sUc[c * 64 + 32 + lane]);
+                        } else {
+                            double t0, t1;
+                            get(J, c, t0, t1);
+                            lu_dmma(t0, t1, la0, sUc[c * 64 + lane]);
+                            lu_dmma(t0, t1, la1, sUc[c * 64 + 32 + lane]);
+                            put(J, c, t0, t1);
+                        }
                     }
+                    // shift by one tile: registers move down, the window slot of
+                    // offset TR comes into the last register (and is refilled below)
 #pragma unroll
-                    for (int c = 0; c + 1 < T; ++c) {
+                    for (int c = 0; c + 1 < TR; ++c) {
                         acc[c][0] = acc[c + 1][0];
                         acc[c][1] = acc[c + 1][1];
                     }
+                    if (TR < T) {
+                        double t0, t1;
+                        get(J, TR, t0, t1);
+                        acc[TR - 1][0] = t0;
+                        acc[TR - 1][1] = t1;
+                    }
                 }
-                const double2 cv = *reinterpret_cast<const double2*>(st + (T + ro - 1) * 64 + gi * 8 + 2 * q);
-                acc[T - 1][0] = cv.x;
-                acc[T - 1][1] = cv.y;
+                const double2 cv = *reinterpret_cast<const double2*>(stc + (ro - 1) * 64 + gi * 8 + 2 * q);
+                put(J + 1, T - 1, cv.x, cv.y);
                 if (8 * (J + ro) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
                 if (ro == 2) {
                     // publish my row (next step's ro = 1) as the panel row of step J+2
 #pragma unroll
-                    for (int c = 1; c < T; ++c) prow[(par * T + c - 1) * 32] = make_double2(acc[c][0], acc[c][1]);
+                    for (int c = 1; c < T; ++c) {
+                        double t0, t1;
+                        get(J + 1, c, t0, t1);
+                        prow[(par * T + c - 1) * 32] = make_double2(t0, t1);
+                    }
                 }
                 LU_MARK(5);
             }
@@ -817,11 +880,12 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
     for (int j = threadIdx.x; j < m; j += blockDim.x) A.piv[P.r0 + j] = j;
 }
 
-template <int T>
+template <int T, int TR>
 static bool launch_lu_dmma(const int* d_units, int nunits, const FastLuArgs& A, cudaStream_t s) {
-    const size_t smem = sizeof(double) * LuDmmaSmem<T>::TOTAL;
-    cudaFuncSetAttribute(k_band_lu_dmma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_band_lu_dmma<T><<<nunits, 32 * (T - 1), smem, s>>>(A);
+    const size_t smem = sizeof(double) * LuDmmaSmem<T, TR>::TOTAL;
+    if (smem > 227 * 1024) return false;
+    cudaFuncSetAttribute(k_band_lu_dmma<T, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_band_lu_dmma<T, TR><<<nunits, 32 * (T - 1), smem, s>>>(A);
     count_launch();
     return true;
 }
@@ -829,10 +893,11 @@ static bool launch_lu_dmma(const int* d_units, int nunits, const FastLuArgs& A, 
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s) {
     static const bool regwin = getenv("SPK_LU_REGWIN") && atoi(getenv("SPK_LU_REGWIN"));
     if (!regwin && kmax >= 1) {
-        if (kmax <= 32) return launch_lu_dmma<5>(d_units, nunits, A, s);
-        if (kmax <= 64) return launch_lu_dmma<9>(d_units, nunits, A, s);
-        if (kmax <= 96) return launch_lu_dmma<13>(d_units, nunits, A, s);
-        if (kmax <= 128) return launch_lu_dmma<17>(d_units, nunits, A, s);
+        if (kmax <= 32) return launch_lu_dmma<5, 5>(d_units, nunits, A, s);
+        if (kmax <= 64) return launch_lu_dmma<9, 9>(d_units, nunits, A, s);
+        if (kmax <= 96) return launch_lu_dmma<13, 13>(d_units, nunits, A, s);
+        if (kmax <= 128) return launch_lu_dmma<17, 17>(d_units, nunits, A, s);
+        if (kmax <= 160) return launch_lu_dmma<21, 12>(d_units, nunits, A, s);
     }
     void (*fn)(FastLuArgs) = nullptr;
     int nw = 0, K = 0;
