@@ -65,13 +65,14 @@ __global__ void __launch_bounds__(512) k_dense_lu(const CouplingJob* __restrict_
     if (flags[J.guard] != 1) return;
     const PartDev P = parts[J.part];
     const int n = P.m;
-    extern __shared__ double sm[];  // n x n column-major, ld n
+    extern __shared__ double sm[];  // n x n column-major, ld n+1 (odd: the row swap is conflict-free)
     __shared__ int s_ip, s_fail;
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
     double* F = fac + P.fofs;
+    const int ls = n + 1;
     for (int e = tid; e < n * n; e += T) {
         const int c = e / n, r = e - c * n;
-        sm[e] = F[(long long)c * P.rows + P.d + r - c];
+        sm[c * ls + r] = F[(long long)c * P.rows + P.d + r - c];
     }
     __syncthreads();
     int* piv = piv_pool + P.r0;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(512) k_dense_lu(const CouplingJob* __restrict_
             double best = -1.0;
             int bi = j;
             for (int r = j + lane; r < n; r += 32) {
-                const double a = fabs(sm[j * n + r]);
+                const double a = fabs(sm[j * ls + r]);
                 if (a > best) {
                     best = a;
                     bi = r;
@@ -109,26 +110,29 @@ __global__ void __launch_bounds__(512) k_dense_lu(const CouplingJob* __restrict_
         if (tid == 0) piv[j] = ip;
         if (ip != j)
             for (int c = j + tid; c < n; c += T) {
-                const double t = sm[c * n + j];
-                sm[c * n + j] = sm[c * n + ip];
-                sm[c * n + ip] = t;
+                const double t = sm[c * ls + j];
+                sm[c * ls + j] = sm[c * ls + ip];
+                sm[c * ls + ip] = t;
             }
         __syncthreads();
-        const double inv = 1.0 / sm[j * n + j];
-        for (int r = j + 1 + tid; r < n; r += T) sm[j * n + r] *= inv;
+        const double inv = 1.0 / sm[j * ls + j];
+        for (int r = j + 1 + tid; r < n; r += T) sm[j * ls + r] *= inv;
         __syncthreads();
-        const int rem = n - 1 - j;
-        for (int e = tid; e < rem * rem; e += T) {
-            const int cc = e / rem, r = e - cc * rem;
-            const int c = j + 1 + cc;
-            const double ajc = sm[c * n + j];
-            if (ajc != 0.0) sm[c * n + j + 1 + r] -= ajc * sm[j * n + j + 1 + r];
+        // rank-1 update: warp -> columns, lane -> consecutive rows (no index
+        // divisions, conflict-free); zero a(j, c) skipped as in kernels.cpp:108
+        const int nw = T >> 5, wid = tid >> 5;
+        for (int c = j + 1 + wid; c < n; c += nw) {
+            const double ajc = sm[c * ls + j];
+            if (ajc == 0.0) continue;
+            double* col = sm + (size_t)c * ls;
+            const double* lj = sm + (size_t)j * ls;
+            for (int r = j + 1 + lane; r < n; r += 32) col[r] -= ajc * lj[r];
         }
         __syncthreads();
     }
     for (int e = tid; e < n * n; e += T) {
         const int c = e / n, r = e - c * n;
-        F[(long long)c * P.rows + P.d + r - c] = sm[e];
+        F[(long long)c * P.rows + P.d + r - c] = sm[c * ls + r];
     }
 }
 
@@ -149,7 +153,7 @@ void launch_schur_init(const CouplingJob* d_jobs, int njobs, long long max_elems
 void launch_dense_lu(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, double* fac, int* piv,
                      int* flags, cudaStream_t s) {
     if (njobs <= 0) return;
-    const size_t smem = (size_t)n * n * 8;
+    const size_t smem = (size_t)n * (n + 1) * 8;
     cudaFuncSetAttribute(k_dense_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_dense_lu<<<njobs, 512, smem, s>>>(d_jobs, d_parts, fac, piv, flags);
     count_launch();
