@@ -301,8 +301,6 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     dist.barrier()
     torch.cuda.synchronize()
     lib.spk_launch_count(1)
-    lib.spk_profile_reset()
-    lib.spk_profile_enable(1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         for i in range(args.steps):
@@ -310,14 +308,18 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    lib.spk_profile_enable(0)
     launches = int(lib.spk_launch_count(1))
     ms_t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device=dev)
     dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = ms_t.item()
     fl, useful = alg_flops(dict(cfg, n=n_glob))
     value = fl / (ms * 1e-3) / 1e9
-    roofline = profile_roofline(spk, cfg, args.steps, ms)
+    lib.spk_profile_reset()
+    lib.spk_profile_enable(1)
+    step()
+    torch.cuda.synchronize()
+    lib.spk_profile_enable(0)
+    roofline = profile_roofline(spk, cfg, 1, ms)
 
     e2e = None
     if not args.no_e2e:
@@ -429,8 +431,6 @@ def impl_ours(args, cfg):
 
     torch.cuda.synchronize()
     spk.lib().spk_launch_count(1)
-    spk.lib().spk_profile_reset()
-    spk.lib().spk_profile_enable(1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -440,13 +440,23 @@ def impl_ours(args, cfg):
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    spk.lib().spk_profile_enable(0)
     launches = int(spk.lib().spk_launch_count(1))
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     fl, useful = alg_flops(cfg)
     value = fl / (ms * 1e-3) / 1e9
 
-    roofline = profile_roofline(spk, cfg, args.steps, ms)
+    # per-kernel-class device time from separate profiled steps (the per-launch
+    # events would inflate the timed ones)
+    spk.lib().spk_profile_reset()
+    spk.lib().spk_profile_enable(1)
+    nprof = 2
+    for _ in range(nprof):
+        if flush is not None:
+            flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    spk.lib().spk_profile_enable(0)
+    roofline = profile_roofline(spk, cfg, nprof, ms)
     l2_note = "inputs larger than L2" if flush is None else "L2 flushed between steps"
 
     # e2e through the public C-ABI with pinned host buffers

@@ -36,6 +36,7 @@ struct FastLuArgs {
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <stdexcept>
@@ -411,6 +412,7 @@ struct spk_fact {
     double* d_dinv = nullptr;
     long long tfac_size = 0;
     Program prog_factor, prog_fwd, prog_tr, prog_rfwd, prog_rtr;  // r*: reduced system only
+    std::shared_ptr<struct Symbolic> sym;  // cached geometry + programs (shared by equal factorizations)
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
     cudaStream_t stream = nullptr;
@@ -1476,11 +1478,81 @@ void validate_plan(long long n, const spk_plan* plan) {
         if (plan->bounds[i + 1] - plan->bounds[i] < 1) fail(SPK_EINVAL, "factorize: empty partition");
 }
 
-// Symbolic part: geometry, pool layout, programs, device allocations.
+}  // namespace
+
+// Symbolic state of a factorization: everything that depends only on the
+// shape, the plan and the options (geometry, pool layout, compiled programs),
+// shared by repeated factorizations of the same structure.  Solve programs are
+// cached per vector of coupling-path flags.  (Host program construction is
+// ~8 ms at p = 1184: most of C1's factorization before this cache.)
+struct SolveProgs {
+    Program fwd, tr, rfwd, rtr;
+    std::vector<char> blob;
+};
+struct Symbolic {
+    std::vector<PartDev> parts;
+    std::vector<Level> levels;
+    long long off_bhat = 0, off_chat = 0, pool_size = 0, fac_size = 0, piv_size = 0, tfac_size = 0;
+    long long aux_rows = 0, auxf_rows = 0;
+    int tau_w = 0, npairs = 0;
+    Program prog_factor;
+    std::vector<char> blob;
+    std::map<std::vector<int>, SolveProgs> solves;
+};
+
+namespace {
+
+struct SymCache {
+    std::mutex mu;
+    std::map<std::string, std::shared_ptr<Symbolic>> map;
+};
+SymCache& sym_cache() {
+    static SymCache* c = new SymCache();
+    return *c;
+}
+std::string sym_key(const spk_fact& f) {
+    std::string key;
+    auto put = [&](long long v) { key.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
+    for (long long v : {f.n, (long long)f.kl, (long long)f.ku, (long long)f.k, (long long)f.p, (long long)f.piv_on,
+                        (long long)f.open_l, (long long)f.open_r, (long long)f.reduced_only})
+        put(v);
+    for (long long b : f.bounds) put(b);
+    return key;
+}
+
+void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob);
+
+// Symbolic part: geometry, pool layout, programs (cached), device allocations.
 void setup_fact(spk_fact& f, cudaStream_t s) {
     Tracer tr("setup");
     const int p = f.p, k = f.k;
     const long long kk = (long long)k * k;
+    const std::string key = sym_key(f);
+    {
+        SymCache& c = sym_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.map.find(key);
+        if (it != c.map.end()) f.sym = it->second;
+    }
+    if (f.sym) {
+        const Symbolic& y = *f.sym;
+        f.parts = y.parts;
+        f.levels = y.levels;
+        f.off_bhat = y.off_bhat;
+        f.off_chat = y.off_chat;
+        f.pool_size = y.pool_size;
+        f.fac_size = y.fac_size;
+        f.piv_size = y.piv_size;
+        f.tfac_size = y.tfac_size;
+        f.aux_rows = y.aux_rows;
+        f.auxf_rows = y.auxf_rows;
+        f.tau_w = y.tau_w;
+        f.npairs = y.npairs;
+        f.prog_factor = y.prog_factor;
+        tr.mark("symbolic (cached)");
+        alloc_fact(f, s, y.blob);
+        return;
+    }
     f.parts.clear();
     long long fac_cursor = 0;
     if (!f.reduced_only) {
@@ -1532,7 +1604,35 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     ProgramBuilder pb;
     build_factor_program(f, pb);
     tr.mark("factor program");
-    // device allocations (stream ordered)
+    auto y = std::make_shared<Symbolic>();
+    y->parts = f.parts;
+    y->levels = f.levels;
+    y->off_bhat = f.off_bhat;
+    y->off_chat = f.off_chat;
+    y->pool_size = f.pool_size;
+    y->fac_size = f.fac_size;
+    y->piv_size = f.piv_size;
+    y->tfac_size = f.tfac_size;
+    y->aux_rows = f.aux_rows;
+    y->auxf_rows = f.auxf_rows;
+    y->tau_w = f.tau_w;
+    y->npairs = f.npairs;
+    y->prog_factor = f.prog_factor;
+    y->blob = std::move(pb.blob);
+    {
+        SymCache& c = sym_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.map.size() >= 32) c.map.clear();  // bounded: shapes rarely vary that much
+        c.map[key] = y;
+    }
+    f.sym = y;
+    alloc_fact(f, s, y->blob);
+}
+
+// device allocations (stream ordered) and uploads of the symbolic state
+void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
+    Tracer tr("alloc");
+    const int p = f.p;
     const int nparts = (int)f.parts.size();
     f.d_parts = dalloc<PartDev>(nparts, s);
     f.d_fac = dalloc<double>(f.fac_size, s);
@@ -1543,7 +1643,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     f.d_boost = dalloc<int>(nparts, s);
     f.d_fell = dalloc<int>(nparts, s);
     f.d_status = dalloc<int>(1, s);
-    f.d_blob = dalloc<char>(pb.blob.size(), s);
+    f.d_blob = dalloc<char>(std::max<size_t>(blob.size(), 1), s);
     f.d_tfac = dalloc<double>(f.tfac_size, s);
     f.d_dinv = dalloc<double>(f.n, s);
     tr.mark("allocations");
@@ -1552,8 +1652,8 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
     ck(cudaMemcpyAsync(f.d_bounds, f.bounds.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s),
        "upload");
-    if (!pb.blob.empty())
-        ck(cudaMemcpyAsync(f.d_blob, pb.blob.data(), pb.blob.size(), cudaMemcpyHostToDevice, s), "upload");
+    if (!blob.empty())
+        ck(cudaMemcpyAsync(f.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s), "upload");
     ck(cudaMemsetAsync(f.d_pool, 0, sizeof(double) * f.pool_size, s), "memset");
     ck(cudaMemsetAsync(f.d_amax, 0, sizeof(unsigned long long) * nparts, s), "memset");
     ck(cudaMemsetAsync(f.d_boost, 0, sizeof(int) * nparts, s), "memset");
@@ -1586,6 +1686,22 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     f.flags.assign(std::max(f.npairs, 1), 0);
     if (f.npairs > 0)
         ck(cudaMemcpy(f.flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost), "flags");
+    if (f.sym) {
+        SymCache& c = sym_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = f.sym->solves.find(f.flags);
+        if (it != f.sym->solves.end()) {
+            const SolveProgs& sp = it->second;
+            f.prog_fwd = sp.fwd;
+            f.prog_tr = sp.tr;
+            f.prog_rfwd = sp.rfwd;
+            f.prog_rtr = sp.rtr;
+            f.d_sblob = dalloc<char>(std::max<size_t>(sp.blob.size(), 1), s);
+            if (!sp.blob.empty())
+                ck(cudaMemcpyAsync(f.d_sblob, sp.blob.data(), sp.blob.size(), cudaMemcpyHostToDevice, s), "upload");
+            return;
+        }
+    }
     ProgramBuilder pb;
     f.prog_fwd.clear();
     f.prog_tr.clear();
@@ -1606,9 +1722,20 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
             build_reduced_solve(f, bt, true, 0);
         }
     }
-    f.d_sblob = dalloc<char>(pb.blob.size(), s);
+    f.d_sblob = dalloc<char>(std::max<size_t>(pb.blob.size(), 1), s);
     if (!pb.blob.empty())
         ck(cudaMemcpyAsync(f.d_sblob, pb.blob.data(), pb.blob.size(), cudaMemcpyHostToDevice, s), "upload");
+    if (f.sym) {
+        SymCache& c = sym_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (f.sym->solves.size() >= 8) f.sym->solves.clear();
+        SolveProgs& sp = f.sym->solves[f.flags];
+        sp.fwd = f.prog_fwd;
+        sp.tr = f.prog_tr;
+        sp.rfwd = f.prog_rfwd;
+        sp.rtr = f.prog_rtr;
+        sp.blob = std::move(pb.blob);
+    }
 }
 
 Bufs make_bufs(const spk_fact* f = nullptr) {
