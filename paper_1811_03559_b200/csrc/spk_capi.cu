@@ -25,6 +25,15 @@ struct FastLuArgs {
     double boost_eps;
     int* boost_cnt;
 };
+struct PivLuArgs {  // spk_lu_fast.cu
+    const int* units;
+    const PartDev* parts;
+    const double* band;
+    int akl, aku;
+    double* fac;
+    int* piv;
+    int* status;
+};
 }  // namespace spk
 
 #include <cuda_runtime.h>
@@ -1425,6 +1434,12 @@ struct Exec {
                                 lu_fast_done = true;
                                 break;
                             }
+                        }
+                        if (f.piv_on && !generic_only) {
+                            // pivoted: shared-memory window kernel (factor + pivots; the
+                            // transpose stage then builds the row-major copy and 1/u_jj)
+                            PivLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac, f.d_piv, f.d_status};
+                            if (launch_band_lu_piv((const int*)jobs, st.njobs, f.kl, f.ku, A, s)) break;
                         }
                         long long max_elems = 0;
                         for (int i = 0; i < f.p; ++i)

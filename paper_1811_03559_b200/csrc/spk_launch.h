@@ -51,6 +51,8 @@ bool launch_sweep_fast_blt(int tr, int nc, bool piv, int nwarps, dim3 grid, size
                            cudaStream_t s);
 struct FastLuArgs;
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s);
+struct PivLuArgs;
+bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_bu(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_fut(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);

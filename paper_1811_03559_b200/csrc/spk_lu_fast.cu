@@ -27,6 +27,7 @@
 #include "spk_launch.h"
 #include "spk_sweep_fast.cuh"
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -886,6 +887,210 @@ static bool launch_lu_dmma(const int* d_units, int nunits, const FastLuArgs& A, 
     if (smem > 227 * 1024) return false;
     cudaFuncSetAttribute(k_band_lu_dmma<T, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_band_lu_dmma<T, TR><<<nunits, 32 * (T - 1), smem, s>>>(A);
+    count_launch();
+    return true;
+}
+
+// ===========================================================================
+// Partial-pivoting band LU (gbtf2 semantics, kernels.cpp:79-118 pivoting
+// branch), one CTA per partition, active window in shared memory.
+//
+// Step j touches rows j..j+kl and columns j..j+ubw (ubw = kl+ku): that window
+// is kept circularly (row r in row slot r mod (kl+1), column c in column slot
+// c mod (ubw+1)).  Three CTA barriers per column: (1) warp argmax of |a(r, j)|
+// (first index on ties) -> pivot; (2) interchange rows j and ip in columns >=
+// j, multipliers l = a(:, j) / a(ip, j) and the pivot row u copied aside;
+// (3) rank-1 update a(r, c) -= l(r) u(c) (skipped where u(c) == 0, as the
+// reference does), the finished L column / U row go to the packed factor, and
+// the slots of column j and row j take the entering column j+ubw+1 and row
+// j+kl+1 (raw band values: no earlier step touched them), staged by cp.async
+// one step ahead.  An exactly zero pivot column sets status 2 (the
+// reference's runtime_error).  tfac / 1/u_jj follow from the transpose stage.
+struct PivLuArgs {
+    const int* units;
+    const PartDev* parts;
+    const double* band;
+    int akl, aku;
+    double* fac;
+    int* piv;
+    int* status;
+};
+
+__global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
+    extern __shared__ __align__(16) double psm[];
+    const int u = A.units[blockIdx.x];
+    const PartDev P = A.parts[u];
+    const int m = P.m, kl = P.kl, ku = P.ku, ubw = P.ubw, d = P.d, rows = P.rows;
+    const int NR = kl + 1, NC = ubw + 1, LDW = NR + (NR % 2 == 0 ? 1 : 0);  // odd column stride
+    double* W = psm;                     // [NC][LDW]
+    double* s_l = W + (size_t)NC * LDW;  // [NR] multipliers of the step (row slot order)
+    double* s_u = s_l + NR;              // [NC] pivot row (column slot order)
+    double* s_st = s_u + NC;             // [2][NR + NC] staging: entering column, entering row
+    __shared__ int s_ip, s_fail;
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = T >> 5;
+    const int ald = A.akl + A.aku + 1;
+    double* F = A.fac + P.fofs;
+    int* piv = A.piv + P.r0;
+    const double* bbase = A.band + (P.rev ? (long long)(P.r0 + m - 1) * ald + A.aku : (long long)P.r0 * ald + A.aku);
+    const long long sg = P.rev ? -1 : 1;
+    auto aval_ptr = [&](int i, int c) -> const double* {
+        if (i < 0 || c < 0 || i >= m || c >= m || i - c > kl || c - i > ku) return nullptr;
+        return bbase + sg * ((long long)c * (ald - 1) + i);
+    };
+    // staging for step js (entering column js+ubw+1 rows js+1..js+kl+1, entering
+    // row js+kl+1 columns js+1..js+ubw+1)
+    auto stage = [&](int js) {
+        double* st = s_st + (js & 1) * (NR + NC);
+        for (int e = tid; e < NR + NC; e += T) {
+            int i, c;
+            if (e < NR) {
+                i = js + 1 + e;
+                c = js + ubw + 1;
+            } else {
+                i = js + kl + 1;
+                c = js + 1 + (e - NR);
+            }
+            const double* p = aval_ptr(i, c);
+            if (p) cp_async8(st + e, p);
+            else st[e] = 0.0;
+        }
+        cp_async_commit();
+    };
+    // zero the packed positions no step writes (above row 0)
+    for (int idx = tid; idx < ubw * ubw; idx += T) {
+        const int c = idx / ubw, off = idx - c * ubw + 1;
+        if (c < m && off > c) F[(long long)c * rows + d - off] = 0.0;
+    }
+    // initial window: rows 0..kl, columns 0..ubw
+    for (int e = tid; e < NC * NR; e += T) {
+        const int c = e / NR, r = e - c * NR;
+        const double* p = aval_ptr(r, c);
+        W[(size_t)c * LDW + r] = p ? *p : 0.0;
+    }
+    stage(0);
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+        const int rl = min(kl, m - 1 - j);    // rows below the pivot
+        const int ce = min(ubw, m - 1 - j);   // columns right of the pivot
+        const int cs = j % NC;
+        // (1) pivot: max |a(r, j)|, r = j..j+rl, first index on ties
+        if (wid == 0) {
+            double best = -1.0;
+            int bi = j;
+            int slot = (j + lane) % NR;
+            const int step = 32 % NR;
+            for (int r = j + lane; r <= j + rl; r += 32) {
+                const double a = fabs(W[(size_t)cs * LDW + slot]);
+                if (a > best) {
+                    best = a;
+                    bi = r;
+                }
+                slot += step;
+                if (slot >= NR) slot -= NR;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_ip = bi;
+                s_fail = !(best > 0.0);
+            }
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) atomicMax(A.status, 2);
+            return;
+        }
+        const int ip = s_ip, sj = j % NR, sp = ip % NR;
+        // (2) interchange rows j, ip in columns j..j+ce; pivot row aside; multipliers
+        for (int cc = tid; cc <= ce; cc += T) {
+            int csl = cs + cc;
+            if (csl >= NC) csl -= NC;  // cc < T = 512 may exceed NC: reduce fully
+            while (csl >= NC) csl -= NC;
+            double* col = W + (size_t)csl * LDW;
+            const double vj = col[sj], vp = col[sp];
+            col[sj] = vp;
+            col[sp] = vj;
+            s_u[cc] = vp;
+        }
+        if (tid == 0) piv[j] = ip;
+        __syncthreads();
+        {
+            const double inv = 1.0 / s_u[0];
+            double* colj = W + (size_t)cs * LDW;
+            for (int r = 1 + tid; r <= rl; r += T) {
+                int sl = sj + r;
+                while (sl >= NR) sl -= NR;
+                const double l = colj[sl] * inv;
+                colj[sl] = l;
+                s_l[r] = l;
+            }
+        }
+        cp_async_wait<0>();  // this step's staging (issued a step ago), visible after the barrier
+        __syncthreads();
+        // (3) rank-1 update (warp -> columns, lane -> rows); outputs; refill
+        {
+            int sl0 = sj + 1 + lane;  // row slot of row j+1+lane
+            while (sl0 >= NR) sl0 -= NR;
+            const int rstep = 32 % NR;
+            int csl = cs + 1 + wid;  // column slot of column j+1+wid
+            while (csl >= NC) csl -= NC;
+            const int cstep = nw % NC;
+            for (int cc = 1 + wid; cc <= ce; cc += nw) {
+                const double uc = s_u[cc];
+                double* col = W + (size_t)csl * LDW;
+                csl += cstep;
+                if (csl >= NC) csl -= NC;
+                if (uc == 0.0) continue;
+                int sl = sl0;
+                for (int r = 1 + lane; r <= rl; r += 32) {
+                    double& a = col[sl];
+                    a = fma(-s_l[r], uc, a);
+                    sl += rstep;
+                    if (sl >= NR) sl -= NR;
+                }
+            }
+        }
+        // packed factor: L column j (rows j+1..j+kl, zero past m), U row j
+        for (int r = 1 + tid; r <= kl; r += T) F[(long long)j * rows + d + r] = r <= rl ? s_l[r] : 0.0;
+        for (int cc = tid; cc <= ubw; cc += T)
+            if (j + cc < m) F[(long long)(j + cc) * rows + d - cc] = cc <= ce ? s_u[cc] : 0.0;
+        // entering column / row into the slots of column j and row j
+        {
+            const double* st = s_st + (j & 1) * (NR + NC);
+            // column j+ubw+1 into slot cs: rows j+1..j+kl+1 -> row slots
+            for (int e = tid; e < NR; e += T) {
+                int sl = sj + 1 + e;
+                while (sl >= NR) sl -= NR;
+                W[(size_t)cs * LDW + sl] = st[e];
+            }
+            // row j+kl+1 into row slot sj: columns j+1..j+ubw (the corner column
+            // j+ubw+1 came with the column above)
+            for (int e = tid; e < NC - 1; e += T) {
+                int csl = cs + 1 + e;
+                while (csl >= NC) csl -= NC;
+                W[(size_t)csl * LDW + sj] = st[NR + e];
+            }
+        }
+        __syncthreads();
+        stage(j + 1);
+    }
+    cp_async_wait<0>();
+}
+
+bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s) {
+    // the reversed (UL) partition swaps kl and ku: size for the larger window
+    const int ubw = kl + ku, NR = std::max(kl, ku) + 1, NC = ubw + 1, LDW = NR + (NR % 2 == 0 ? 1 : 0);
+    const size_t smem = sizeof(double) * ((size_t)NC * LDW + NR + NC + 2 * (NR + NC));
+    if (smem > 200 * 1024) return false;
+    cudaFuncSetAttribute(k_band_lu_piv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_band_lu_piv<<<nunits, 512, smem, s>>>(A);
     count_launch();
     return true;
 }
