@@ -916,7 +916,7 @@ struct PivLuArgs {
     int* status;
 };
 
-__global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
+__global__ void __launch_bounds__(256, 2) k_band_lu_piv(PivLuArgs A) {
     extern __shared__ __align__(16) double psm[];
     const int u = A.units[blockIdx.x];
     const PartDev P = A.parts[u];
@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
     double* W = psm;                     // [NC][LDW]
     double* s_l = W + (size_t)NC * LDW;  // [NR] multipliers of the step (row slot order)
     double* s_u = s_l + NR;              // [NC] pivot row (column slot order)
-    double* s_st = s_u + NC;             // [2][NR + NC] staging: entering column, entering row
+    double* s_st = s_u + NC;             // [4][NR + NC] staging ring: entering column, entering row
     __shared__ int s_ip, s_fail;
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = T >> 5;
     const int ald = A.akl + A.aku + 1;
@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
     // staging for step js (entering column js+ubw+1 rows js+1..js+kl+1, entering
     // row js+kl+1 columns js+1..js+ubw+1)
     auto stage = [&](int js) {
-        double* st = s_st + (js & 1) * (NR + NC);
+        double* st = s_st + (js & 3) * (NR + NC);
         for (int e = tid; e < NR + NC; e += T) {
             int i, c;
             if (e < NR) {
@@ -967,7 +967,9 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
         const double* p = aval_ptr(r, c);
         W[(size_t)c * LDW + r] = p ? *p : 0.0;
     }
-    stage(0);
+    stage(0);  // three steps ahead: HBM latency exceeds a step
+    stage(1);
+    stage(2);
     __syncthreads();
     for (int j = 0; j < m; ++j) {
         const int rl = min(kl, m - 1 - j);    // rows below the pivot
@@ -1032,7 +1034,7 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
                 s_l[r] = l;
             }
         }
-        cp_async_wait<0>();  // this step's staging (issued a step ago), visible after the barrier
+        cp_async_wait<2>();  // this step's staging (issued three steps ago), visible after the barrier
         __syncthreads();
         // (3) rank-1 update (warp -> columns, lane -> rows); outputs; refill
         {
@@ -1063,7 +1065,7 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
             if (j + cc < m) F[(long long)(j + cc) * rows + d - cc] = cc <= ce ? s_u[cc] : 0.0;
         // entering column / row into the slots of column j and row j
         {
-            const double* st = s_st + (j & 1) * (NR + NC);
+            const double* st = s_st + (j & 3) * (NR + NC);
             // column j+ubw+1 into slot cs: rows j+1..j+kl+1 -> row slots
             for (int e = tid; e < NR; e += T) {
                 int sl = sj + 1 + e;
@@ -1079,7 +1081,7 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
             }
         }
         __syncthreads();
-        stage(j + 1);
+        stage(j + 3);
     }
     cp_async_wait<0>();
 }
@@ -1087,10 +1089,10 @@ __global__ void __launch_bounds__(512, 1) k_band_lu_piv(PivLuArgs A) {
 bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s) {
     // the reversed (UL) partition swaps kl and ku: size for the larger window
     const int ubw = kl + ku, NR = std::max(kl, ku) + 1, NC = ubw + 1, LDW = NR + (NR % 2 == 0 ? 1 : 0);
-    const size_t smem = sizeof(double) * ((size_t)NC * LDW + NR + NC + 2 * (NR + NC));
+    const size_t smem = sizeof(double) * ((size_t)NC * LDW + NR + NC + 4 * (NR + NC));
     if (smem > 200 * 1024) return false;
     cudaFuncSetAttribute(k_band_lu_piv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_band_lu_piv<<<nunits, 512, smem, s>>>(A);
+    k_band_lu_piv<<<nunits, 256, smem, s>>>(A);  // 2 CTAs per SM (registers)
     count_launch();
     return true;
 }
