@@ -1301,9 +1301,11 @@ struct Exec {
         // more column groups than the 16-warp kernel below (each group re-reads
         // the factor) and keeps >= 6 compute warps busy (with fewer, one warp's
         // dependency chain sets the pace and the synchronous kernel wins).
+        static const bool sweep_v2 = getenv("SPK_SWEEP_V2") && atoi(getenv("SPK_SWEEP_V2"));
         const int groups2 = (nc + 111) / 112, groups1 = (nc + 127) / 128;
         const int cols2 = ((nc + groups2 - 1) / groups2 + 7) / 8 * 8;
-        if (!no_dmma && !sweep_v1 && !st.piv && nc >= 8 && st.kwmax <= 192 && groups2 == groups1 && cols2 >= 48) {
+        if (!no_dmma && !sweep_v1 && !st.piv && nc >= 8 && st.kwmax <= 192 &&
+            (sweep_v2 || (groups2 == groups1 && cols2 >= 48))) {
             static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
@@ -1323,9 +1325,12 @@ struct Exec {
             }
             if (ok) return true;
         }
-        if (!no_dmma && !st.piv && nc >= 8 && st.kwmax <= 192) {
+        if (!no_dmma && !st.piv && st.kwmax <= 192) {
             // blocked tensor-core sweep: 8 columns per warp, <= 16 warps per CTA,
-            // column groups balanced across CTAs
+            // column groups balanced across CTAs.  Narrow solves (nc < 8) run
+            // padded to one warp: the chain per 8-row block (~4 DMMA latencies)
+            // beats the per-row chain of the DFMA kernel ~10x, and the tensor
+            // pipe has room for the padding
             static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
