@@ -1924,11 +1924,14 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
             // one partition per SM for wide bands (the sweep kernels then split
             // the right-hand sides across SMs); more for narrow bands, where a
             // partition's column chain is short per step.
+            // Narrow solves (nrhs <= 64) on wide bands get two partitions per SM:
+            // their sweeps are latency-bound at <= 8 warps per partition (C5:
+            // 238 -> 216 ms per step); wide ones fill an SM per partition (C3:
+            // p = 296 would cost 9 ms).
             const int sms = 148;
-            if (k >= 96) pp = sms;
+            if (k >= 96) pp = nrhs <= 64 ? 2 * sms : sms;
             else if (k >= 32) pp = 2 * sms;
             else pp = 8 * sms;
-            (void)nrhs;
             (void)pivoting;
         }
         pp = (int)std::max<long long>(1, std::min<long long>(pp, n / std::max<long long>(min_part, 1)));
