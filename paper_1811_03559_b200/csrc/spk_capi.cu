@@ -211,6 +211,8 @@ struct Stage {
     // a SPIKE partition it supports
     bool fast = false;
     int mode = 0, kwmax = 0, tr = 0, piv = 0;
+    // sweeps on short units: shared-memory staged kernel (k_sweep_small)
+    int small_ch = 0, small_rows = 0;
     bool partitions = false;  // ST_LU over SPIKE partitions (fill from the input band)
 };
 
@@ -594,6 +596,23 @@ struct Builder {
         }
         const int tr = (kwneed + 31) / 32;
         if (tr > 8) fast = false;
+        // staged rows per job (the rows k_sweep touches) and factor entries per row
+        int srows = 0, sbw = 0;
+        for (auto& j : jobs) {
+            const PartDev& P = f.parts[j.part];
+            int a = j.lo, e = P.m, bw = P.kl;
+            if (j.mode == SW_BWD_U || j.mode == SW_FWD_UT) {
+                a = std::max(j.lo - P.ubw, j.v.off);
+                bw = P.ubw;
+            }
+            if (j.mode == SW_BWD_U) e = j.hi + 1;
+            srows = std::max(srows, e - a);
+            sbw = std::max(sbw, bw);
+        }
+        if (srows <= 1024 && sbw <= 320) {
+            s.small_rows = std::max(srows, 1);
+            s.small_ch = std::max(1, (sbw + 31) / 32);
+        }
         s.fast = fast;
         s.mode = jobs[0].mode;
         s.kwmax = kwmax;
@@ -646,6 +665,7 @@ struct Builder {
         s.off = pb.push(units);
         for (int u : units) {
             const PartDev& P = f.parts[u];
+            s.max_r = std::max(s.max_r, P.m);
             s.flops_per_col += 2.0 * P.m * P.kl * P.ubw;
             s.bytes_per_col += 16.0 * P.m * P.rows;
         }
@@ -1105,8 +1125,8 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
     // retrieval
     b.memset_buf(B_S);
     std::vector<GemmJob> g;
-    std::vector<SweepJob> r_fl, r_bu, r_bu2;
-    std::vector<CopyJob> r_sub;
+    std::vector<SweepJob> r_fl, r_bu;
+    std::vector<CopyJob> r_sub_edge, r_sub_inner;
     const View tview = view(B_T, 0);
     for (int i = 0; i < p; ++i) {
         const PartDev& P = f.parts[i];
@@ -1121,19 +1141,22 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
         if (!f.first(i)) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, sv, 0, k, k, GM_SET));
         if (f.first(i) || f.last(i)) {
             r_fl.push_back(sj(sr, i, SW_FWD_L, P.trunc, 0));
-            r_sub.push_back(cj(sr, xv, P.trunc, m, CP_SUB));
-            r_bu2.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
+            r_sub_edge.push_back(cj(sr, xv, P.trunc, m, CP_SUB));
+            r_bu.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
         } else {
             r_fl.push_back(sj(sv, i, SW_FWD_L, 0, 0));
             r_bu.push_back(sj(sv, i, SW_BWD_U, 0, m - 1));
-            r_sub.push_back(cj(sv, xv, 0, m, CP_SUB));
+            r_sub_inner.push_back(cj(sv, xv, 0, m, CP_SUB));
         }
     }
+    // edges subtract their truncated forward sweep first, so their full
+    // backward sweep (on X) shares one launch with the inner partitions'
+    // (on S) instead of running as a 2-job tail after it
     b.gemm(g);
     b.sweep(r_fl);
+    b.copy(r_sub_edge);
     b.sweep(r_bu);
-    b.copy(r_sub);
-    b.sweep(r_bu2);
+    b.copy(r_sub_inner);
 }
 
 // transpose solve program (solve.cpp:225-380)
@@ -1231,9 +1254,9 @@ void build_transpose_program(spk_fact& f, ProgramBuilder& pb) {
     }
     b.copy(zero);
     b.sweep(s_fut);
-    b.sweep(s_blt);
     b.copy(tau_copy);
-    b.sweep(tau_blt);
+    for (const SweepJob& j : tau_blt) s_blt.push_back(j);  // one launch with the inner sweeps
+    b.sweep(s_blt);
     b.copy(gcopy);
     b.gemm(g);
     if (f.open()) {
@@ -1395,6 +1418,11 @@ struct Exec {
                 case ST_SWEEP: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
                     if (st.fast && run_fast_sweep(st, (const SweepJob*)jobs, nc)) break;
+                    static const bool no_small = getenv("SPK_SWEEP_SMALL") && !atoi(getenv("SPK_SWEEP_SMALL"));
+                    if (st.small_ch > 0 && !no_small &&
+                        launch_sweep_small((const SweepJob*)jobs, st.njobs, nc, st.small_ch, st.small_rows, f.d_parts,
+                                           f.d_fac, f.d_piv, B, ncols, s))
+                        break;
                     launch_sweep((const SweepJob*)jobs, st.njobs, nc, f.d_parts, f.d_fac, f.d_piv, B,
                                  ncols, s);
                     break;
@@ -1451,6 +1479,13 @@ struct Exec {
                             max_elems = std::max(max_elems, (long long)f.parts[i].m * f.parts[i].rows);
                         launch_fill_factors(band, n, f.kl, f.ku, f.d_parts, f.p, max_elems, f.d_fac, f.d_piv,
                                             f.d_amax, s);
+                    }
+                    {
+                        static const bool no_small = getenv("SPK_LU_SMALL") && !atoi(getenv("SPK_LU_SMALL"));
+                        if (!no_small && launch_band_lu_small((const int*)jobs, st.njobs, st.max_r, f.d_parts,
+                                                              f.d_fac, f.d_piv, f.d_amax, f.boost_eps, f.d_boost,
+                                                              f.d_fell, f.d_status, f.d_flags, s))
+                            break;
                     }
                     launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
                                    f.boost_eps, f.d_boost, f.d_fell, f.d_status, f.d_flags, s);

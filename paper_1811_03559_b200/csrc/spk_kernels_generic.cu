@@ -184,6 +184,166 @@ __global__ void k_band_lu(const int* __restrict__ units, const PartDev* __restri
 }
 
 // ---------------------------------------------------------------------------
+// k_band_lu for short units (m <= 160: the 2k coupling units of the reduced
+// hierarchy, tiny partitions): the unit is staged densely in shared memory
+// (column-major, ld m+1) and factored there with the exact conventions and
+// arithmetic of k_band_lu -- first-max pivot over kl+1 candidates, row swap
+// over columns [j, j+ubw] (multipliers of earlier columns stay put, gbtf2
+// style), boost when not pivoting, restart without pivoting from the backup
+// on an exactly zero column -- then written back to the band layout.  Warp w
+// updates columns j+1+w, j+1+w+W, ...; lane l owns rows j+1+l+32q and keeps
+// their multipliers in registers, so the scaling needs no extra barrier.
+constexpr int kLuSmallMaxM = 160;
+constexpr int kLuSmallThreads = 256;
+
+__global__ void __launch_bounds__(kLuSmallThreads) k_band_lu_small(
+    const int* __restrict__ units, const PartDev* __restrict__ parts, double* __restrict__ fac,
+    int* __restrict__ piv_pool, const unsigned long long* __restrict__ amax_bits, double boost_eps,
+    int* __restrict__ boost_cnt, int* __restrict__ fell_back, int* __restrict__ status,
+    const int* __restrict__ flags) {
+    extern __shared__ double sa[];
+    const int u = units[blockIdx.x];
+    const PartDev P = parts[u];
+    if (P.guard >= 0 && !guard_ok(flags, P.guard)) return;
+    double* F = fac + P.fofs;
+    int* piv = piv_pool + P.r0;
+    const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
+    const int ld = m + 1;
+    const double amax = __longlong_as_double((long long)amax_bits[u]);
+    const double scale = amax == 0.0 ? 1.0 : amax;
+    const double thresh = DBL_EPSILON * scale, bmag = boost_eps * scale;
+    __shared__ int s_ip, s_fail;
+    int pivoting = P.pivoting;
+    int nboost = 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = kLuSmallThreads / 32;
+    auto in_band = [&](int i, int c) { return i - c <= kl && c - i <= ubw; };
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const double* src = attempt == 0 ? F : fac + P.bofs;
+        for (int e = tid; e < m * m; e += kLuSmallThreads) {
+            const int c = e / m, i = e - c * m;
+            sa[c * ld + i] = in_band(i, c) ? src[(long long)c * rows + d + i - c] : 0.0;
+        }
+        if (attempt == 1) {
+            pivoting = 0;
+            nboost = 0;
+        }
+        __syncthreads();
+        bool failed = false;
+        for (int j = 0; j < m; ++j) {
+            double* cj = sa + j * ld;
+            const int rl = min(kl, m - 1 - j);
+            if (pivoting) {
+                if (warp == 0) {
+                    double best = -1.0;
+                    int bi = 0;
+                    for (int r = lane; r <= rl; r += 32) {
+                        const double a = fabs(cj[j + r]);
+                        if (a > best) {
+                            best = a;
+                            bi = r;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        if (ob > best || (ob == best && oi < bi)) {
+                            best = ob;
+                            bi = oi;
+                        }
+                    }
+                    if (lane == 0) {
+                        s_ip = j + bi;
+                        s_fail = (best == 0.0);
+                    }
+                }
+                __syncthreads();
+                if (s_fail) {
+                    failed = true;
+                    break;
+                }
+                const int ip = s_ip;
+                if (tid == 0) piv[j] = ip;
+                if (ip != j) {
+                    const int ce = min(m - 1, j + ubw);
+                    for (int c = j + tid; c <= ce; c += kLuSmallThreads) {
+                        double* cc = sa + c * ld;
+                        const double t = cc[j];
+                        cc[j] = cc[ip];
+                        cc[ip] = t;
+                    }
+                }
+                __syncthreads();
+            } else {
+                if (tid == 0) {
+                    piv[j] = j;
+                    if (fabs(cj[j]) < thresh) {
+                        cj[j] = cj[j] == 0.0 ? bmag : copysign(bmag, cj[j]);
+                        ++nboost;
+                    }
+                }
+                __syncthreads();
+            }
+            if (rl == 0) continue;
+            const double inv = 1.0 / cj[j];
+            double l[kLuSmallMaxM / 32];
+#pragma unroll
+            for (int q = 0; q < kLuSmallMaxM / 32; ++q) {
+                const int r = lane + 32 * q;
+                l[q] = r < rl ? cj[j + 1 + r] * inv : 0.0;
+            }
+            const int ce = min(m - 1, j + ubw);
+            for (int c = j + 1 + warp; c <= ce; c += W) {
+                double* col = sa + c * ld;
+                const double ajc = col[j];
+                if (ajc != 0.0) {
+#pragma unroll
+                    for (int q = 0; q < kLuSmallMaxM / 32; ++q) {
+                        const int r = lane + 32 * q;
+                        if (r < rl) col[j + 1 + r] -= ajc * l[q];
+                    }
+                }
+            }
+            __syncthreads();
+            // column j is not read again: publish its multipliers
+            if (warp == 0) {
+#pragma unroll
+                for (int q = 0; q < kLuSmallMaxM / 32; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r < rl) cj[j + 1 + r] = l[q];
+                }
+            }
+        }
+        if (!failed) break;
+        if (!P.fallback) {
+            if (tid == 0) atomicExch(status, 2);
+            return;
+        }
+        if (tid == 0 && fell_back) fell_back[u] = 1;
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += kLuSmallThreads) {
+        const int c = e / m, i = e - c * m;
+        if (in_band(i, c)) F[(long long)c * rows + d + i - c] = sa[c * ld + i];
+    }
+    if (tid == 0 && nboost) atomicAdd(&boost_cnt[u], nboost);
+}
+
+bool launch_band_lu_small(const int* d_units, int nunits, int max_m, const PartDev* d_parts, double* fac,
+                          int* piv, const unsigned long long* amax, double boost_eps, int* boost_cnt,
+                          int* fell_back, int* status, const int* flags, cudaStream_t s) {
+    if (nunits <= 0) return true;
+    if (max_m > kLuSmallMaxM) return false;
+    const size_t smem = (size_t)max_m * (max_m + 1) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_band_lu_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_band_lu_small<<<nunits, kLuSmallThreads, smem, s>>>(d_units, d_parts, fac, piv, amax, boost_eps, boost_cnt,
+                                                          fell_back, status, flags);
+    count_launch();
+    return true;
+}
+
+// ---------------------------------------------------------------------------
 // Triangular sweeps, one warp per (job, right-hand-side column).
 __global__ void k_sweep(const SweepJob* __restrict__ jobs, const PartDev* __restrict__ parts,
                         const double* __restrict__ fac, const int* __restrict__ piv_pool, Bufs B,
@@ -274,6 +434,230 @@ __global__ void k_sweep(const SweepJob* __restrict__ jobs, const PartDev* __rest
             }
             break;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Short-unit sweeps (coupling units, S^-1 formation, transpose tau tails): the
+// same four recurrences as k_sweep, one warp per column, but the column's
+// touched rows [a, b) live in shared memory and each row's factor entries
+// (and pivot) are prefetched kSmallD rows ahead into a register ring, so a row
+// costs one shared-memory round trip instead of several dependent L2 ones.
+// Arithmetic order matches k_sweep exactly.
+constexpr int kSmallWpb = 4;
+constexpr int kSmallD = 4;
+
+__device__ __forceinline__ void small_range(const SweepJob& J, const PartDev& P, int& a, int& b) {
+    switch (J.mode) {
+        case SW_BWD_U: a = max(J.lo - P.ubw, J.v.off); b = J.hi + 1; break;
+        case SW_FWD_UT: a = max(J.lo - P.ubw, J.v.off); b = P.m; break;
+        default: a = J.lo; b = P.m; break;
+    }
+}
+
+template <int CH>
+__global__ void __launch_bounds__(32 * kSmallWpb) k_sweep_small(const SweepJob* __restrict__ jobs,
+                                                                const PartDev* __restrict__ parts,
+                                                                const double* __restrict__ fac,
+                                                                const int* __restrict__ piv_pool, Bufs B,
+                                                                int ncols, int maxr) {
+    extern __shared__ double sm_small[];
+    const SweepJob J = jobs[blockIdx.x];
+    if (!guard_ok(B.flags, J.guard)) return;
+    const int lane = threadIdx.x & 31;
+    const int nc = J.nc >= 0 ? J.nc : ncols;
+    const int cl = blockIdx.y * kSmallWpb + (threadIdx.x >> 5);
+    if (cl >= nc) return;
+    const int c = J.c0 + cl;
+    const PartDev P = parts[J.part];
+    const double* F = fac + P.fofs;
+    const int* piv = piv_pool + P.r0;
+    const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
+    const bool pivoting = P.pivoting;
+    const View& v = J.v;
+    int a, b;
+    small_range(J, P, a, b);
+    double* x = sm_small + (size_t)(threadIdx.x >> 5) * maxr - a;  // x[L], L in [a, b)
+    for (int L = a + lane; L < b; L += 32) x[L] = vat(B, v, L, c);
+    __syncwarp();
+    double ring[kSmallD][CH], dg[kSmallD];
+    int pr[kSmallD];
+    switch (J.mode) {
+        case SW_FWD_L: {
+            auto load = [&](int j, double* e, int& pv) {
+                if (j >= m) return;
+                const int rl = min(kl, m - 1 - j);
+                const double* lj = F + (long long)j * rows + d + 1;
+#pragma unroll
+                for (int q = 0; q < CH; ++q) e[q] = lane + 32 * q < rl ? lj[lane + 32 * q] : 0.0;
+                pv = pivoting ? piv[j] : j;
+            };
+#pragma unroll
+            for (int t = 0; t < kSmallD; ++t) load(J.lo + t, ring[t], pr[t]);
+            for (int j0 = J.lo; j0 < m; j0 += kSmallD) {
+#pragma unroll
+                for (int t = 0; t < kSmallD; ++t) {
+                    const int j = j0 + t;
+                    if (j >= m) break;
+                    if (pr[t] != j) {
+                        if (lane == 0) {
+                            const double tmp = x[j];
+                            x[j] = x[pr[t]];
+                            x[pr[t]] = tmp;
+                        }
+                        __syncwarp();
+                    }
+                    const int rl = min(kl, m - 1 - j);
+                    if (rl > 0) {
+                        const double bj = x[j];
+                        if (bj != 0.0) {
+#pragma unroll
+                            for (int q = 0; q < CH; ++q)
+                                if (lane + 32 * q < rl) x[j + 1 + lane + 32 * q] -= bj * ring[t][q];
+                        }
+                        __syncwarp();
+                    }
+                    load(j + kSmallD, ring[t], pr[t]);
+                }
+            }
+            break;
+        }
+        case SW_BWD_U: {
+            auto load = [&](int j, double* e, double& dj) {
+                if (j < J.lo) return;
+                const double* cj = F + (long long)j * rows;
+                const int r0 = max(j - ubw, v.off);
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int r = r0 + lane + 32 * q;
+                    e[q] = r < j ? cj[d + r - j] : 0.0;
+                }
+                dj = cj[d];
+            };
+#pragma unroll
+            for (int t = 0; t < kSmallD; ++t) load(J.hi - t, ring[t], dg[t]);
+            for (int j0 = J.hi; j0 >= J.lo; j0 -= kSmallD) {
+#pragma unroll
+                for (int t = 0; t < kSmallD; ++t) {
+                    const int j = j0 - t;
+                    if (j < J.lo) break;
+                    const double z = x[j] / dg[t];
+                    __syncwarp();
+                    if (lane == 0) x[j] = z;
+                    const int r0 = max(j - ubw, v.off);
+                    if (z != 0.0) {
+#pragma unroll
+                        for (int q = 0; q < CH; ++q) {
+                            const int r = r0 + lane + 32 * q;
+                            if (r < j) x[r] -= z * ring[t][q];
+                        }
+                    }
+                    __syncwarp();
+                    load(j - kSmallD, ring[t], dg[t]);
+                }
+            }
+            break;
+        }
+        case SW_FWD_UT: {
+            auto load = [&](int i, double* e, double& di) {
+                if (i >= m) return;
+                const double* ci = F + (long long)i * rows;
+                const int q0 = max(i - ubw, v.off);
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int r = q0 + lane + 32 * q;
+                    e[q] = r < i ? ci[d + r - i] : 0.0;
+                }
+                di = ci[d];
+            };
+#pragma unroll
+            for (int t = 0; t < kSmallD; ++t) load(J.lo + t, ring[t], dg[t]);
+            for (int i0 = J.lo; i0 < m; i0 += kSmallD) {
+#pragma unroll
+                for (int t = 0; t < kSmallD; ++t) {
+                    const int i = i0 + t;
+                    if (i >= m) break;
+                    const int q0 = max(i - ubw, v.off);
+                    double part = 0.0;
+#pragma unroll
+                    for (int q = 0; q < CH; ++q) {
+                        const int r = q0 + lane + 32 * q;
+                        if (r < i) part += ring[t][q] * x[r];
+                    }
+                    const double sum = warp_sum(part);
+                    if (lane == 0) x[i] = (x[i] - sum) / dg[t];
+                    __syncwarp();
+                    load(i + kSmallD, ring[t], dg[t]);
+                }
+            }
+            break;
+        }
+        case SW_BWD_LT: {
+            auto load = [&](int i, double* e, int& pv) {
+                if (i < J.lo) return;
+                const int rl = min(kl, m - 1 - i);
+                const double* li = F + (long long)i * rows + d + 1;
+#pragma unroll
+                for (int q = 0; q < CH; ++q) e[q] = lane + 32 * q < rl ? li[lane + 32 * q] : 0.0;
+                pv = pivoting ? piv[i] : i;
+            };
+#pragma unroll
+            for (int t = 0; t < kSmallD; ++t) load(m - 1 - t, ring[t], pr[t]);
+            for (int i0 = m - 1; i0 >= J.lo; i0 -= kSmallD) {
+#pragma unroll
+                for (int t = 0; t < kSmallD; ++t) {
+                    const int i = i0 - t;
+                    if (i < J.lo) break;
+                    const int rl = min(kl, m - 1 - i);
+                    if (rl > 0) {
+                        double part = 0.0;
+#pragma unroll
+                        for (int q = 0; q < CH; ++q)
+                            if (lane + 32 * q < rl) part += ring[t][q] * x[i + 1 + lane + 32 * q];
+                        const double sum = warp_sum(part);
+                        if (lane == 0) x[i] -= sum;
+                    }
+                    __syncwarp();
+                    if (pr[t] != i) {
+                        if (lane == 0) {
+                            const double tmp = x[i];
+                            x[i] = x[pr[t]];
+                            x[pr[t]] = tmp;
+                        }
+                        __syncwarp();
+                    }
+                    load(i - kSmallD, ring[t], pr[t]);
+                }
+            }
+            break;
+        }
+    }
+    __syncwarp();
+    for (int L = a + lane; L < b; L += 32) vat(B, v, L, c) = x[L];
+}
+
+bool launch_sweep_small(const SweepJob* d_jobs, int njobs, int max_nc, int chunks, int maxr,
+                        const PartDev* d_parts, const double* fac, const int* piv, const Bufs& B, int ncols,
+                        cudaStream_t s) {
+    if (njobs <= 0 || max_nc <= 0) return true;
+    const dim3 g(njobs, (max_nc + kSmallWpb - 1) / kSmallWpb);
+    const size_t smem = (size_t)kSmallWpb * maxr * sizeof(double);
+    if (smem > 227 * 1024) return false;
+#define SPK_SMALL(CH)                                                                                    \
+    {                                                                                                   \
+        if (smem > 48 * 1024)                                                                           \
+            cudaFuncSetAttribute(k_sweep_small<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_sweep_small<CH><<<g, 32 * kSmallWpb, smem, s>>>(d_jobs, d_parts, fac, piv, B, ncols, maxr);   \
+        count_launch();                                                                                 \
+        return true;                                                                                    \
+    }
+    if (chunks <= 1) SPK_SMALL(1)
+    if (chunks <= 2) SPK_SMALL(2)
+    if (chunks <= 3) SPK_SMALL(3)
+    if (chunks <= 5) SPK_SMALL(5)
+    if (chunks <= 8) SPK_SMALL(8)
+    if (chunks <= 10) SPK_SMALL(10)
+#undef SPK_SMALL
+    return false;
 }
 
 // ---------------------------------------------------------------------------

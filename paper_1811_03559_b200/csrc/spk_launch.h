@@ -15,6 +15,16 @@ void launch_fill_factors(const double* band, long long n, int akl, int aku, cons
 void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, double* fac, int* piv,
                     const unsigned long long* amax, double boost_eps, int* boost_cnt,
                     int* fell_back, int* status, const int* flags, cudaStream_t s);
+// units with m <= 160 factored in shared memory (spk_kernels_generic.cu);
+// false when a unit is larger (caller falls back to launch_band_lu)
+bool launch_band_lu_small(const int* d_units, int nunits, int max_m, const PartDev* d_parts, double* fac,
+                          int* piv, const unsigned long long* amax, double boost_eps, int* boost_cnt,
+                          int* fell_back, int* status, const int* flags, cudaStream_t s);
+// short units staged in shared memory (spk_kernels_generic.cu); false when
+// the shape is not covered (caller falls back to launch_sweep)
+bool launch_sweep_small(const SweepJob* d_jobs, int njobs, int max_nc, int chunks, int maxr,
+                        const PartDev* d_parts, const double* fac, const int* piv, const Bufs& B, int ncols,
+                        cudaStream_t s);
 void launch_sweep(const SweepJob* d_jobs, int njobs, int max_nc, const PartDev* d_parts,
                   const double* fac, const int* piv, const Bufs& B, int ncols, cudaStream_t s);
 void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bufs& B, int ncols,
