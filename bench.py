@@ -482,6 +482,8 @@ def impl_ours(args, cfg):
             if cfg["transpose"]:
                 spk.spike._check(fct.spk_solve(h, 1, hF.data_ptr(), n, nrhs, hXT.data_ptr(), n, 0, sptr, None))
             fct.spk_fact_destroy(h)
+            # host X / X^T complete (stream-ordered host solves): no overlap across steps
+            spk.spike._check(fct.spk_stream_sync(sptr))
 
         e2e_step()
         torch.cuda.synchronize()

@@ -90,11 +90,22 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
                         int32_t p_hint, int32_t cap, int32_t *p, int64_t *bounds,
                         int32_t *kinds);
 
-/* ---- factorization ---- */
+/* ---- factorization ----
+ * Stream-ordered: returns once the factorization is enqueued on `stream` (a
+ * host band is uploaded first).  Its host-side completion -- the exactly
+ * singular pivot check of factorize.cpp:133-257 / kernels.cpp:94-101, boost
+ * counts, the coupling paths -- happens at the first call that consumes the
+ * factorization (spk_solve, spk_xsolve_begin, spk_fact_*), which reports
+ * SPK_ESINGULAR there, or explicitly with spk_fact_sync (what the reference's
+ * throwing factorize() maps to). */
 spk_status spk_factorize(const double *band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
                          const spk_plan *plan, const spk_factor_options *opts, void *stream,
                          spk_fact **out);
+/* waits for the factorization and reports its status (SPK_ESINGULAR) */
+spk_status spk_fact_sync(const spk_fact *f);
 void spk_fact_destroy(spk_fact *f);
+/* cudaStreamSynchronize(stream): completes stream-ordered host-memory solves */
+spk_status spk_stream_sync(void *stream);
 
 /* ---- multi-GPU slabs (no reference counterpart: the
  * reference is single-node fork-join, parallel_util.hpp:13-45) ----
@@ -157,7 +168,11 @@ typedef struct spk_solve_stats {
 } spk_solve_stats;
 
 /* X := A^-1 F (transpose=0) or A^-T F (transpose=1); F, X column-major with
- * leading dimensions ldf, ldx >= n.  X may alias F. */
+ * leading dimensions ldf, ldx >= n.  X may alias F.  mem = SPK_MEM_HOST with
+ * nrhs >= 32 (pinned buffers) is pipelined over column chunks and
+ * stream-ordered: uploads start at once (under a still running factorization),
+ * the call returns without waiting, and X is complete once `stream` is
+ * synchronised (spk_stream_sync).  Smaller host solves complete before return. */
 spk_status spk_solve(const spk_fact *f, int32_t transpose, const double *F, int64_t ldf,
                      int32_t nrhs, double *X, int64_t ldx, int32_t mem, void *stream,
                      spk_solve_stats *stats);

@@ -191,7 +191,7 @@ namespace {
 
 enum StageType {
     ST_SWEEP, ST_COPY, ST_GEMM, ST_LU, ST_CPL, ST_MEMSET, ST_MEMCPY_FX, ST_MEMCPY_FS, ST_TRANSPOSE,
-    ST_WCHECK, ST_SCHUR_INIT, ST_DENSE_LU,
+    ST_WCHECK, ST_SCHUR_INIT, ST_SCHUR_INV,
     ST_PHASE = 100  // exchange-point marker (no work, not profiled)
 };
 
@@ -287,13 +287,23 @@ struct Arena {
         bytes = round_up(bytes == 0 ? 1 : bytes);
         {
             std::lock_guard<std::mutex> lk(mu);
+            // best fit, preferring blocks already free for this stream (released
+            // on it, or their last use finished): a block still in flight on
+            // another stream would order this stream behind that work.  A
+            // large in-flight block is left alone and a new one allocated.
             int best = -1;
+            bool best_ready = false;
             for (int i = 0; i < (int)free_list.size(); ++i) {
                 const ArenaBlock& b = free_list[i];
-                if (b.bytes >= bytes && b.bytes <= bytes + bytes / 4 &&
-                    (best < 0 || b.bytes < free_list[best].bytes))
+                if (b.bytes < bytes || b.bytes > bytes + bytes / 4) continue;
+                const bool ready = b.stream == s || cudaEventQuery(b.ev) == cudaSuccess;
+                if (best < 0 || (ready && !best_ready) || (ready == best_ready && b.bytes < free_list[best].bytes)) {
                     best = i;
+                    best_ready = ready;
+                }
             }
+            (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady
+            if (best >= 0 && !best_ready && bytes >= (64u << 20)) best = -1;
             if (best >= 0) {
                 ArenaBlock b = free_list[best];
                 free_list.erase(free_list.begin() + best);
@@ -427,6 +437,12 @@ struct spk_fact {
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
     cudaStream_t stream = nullptr;
+    // spk_factorize returns once the work is enqueued; the host-side finish
+    // (status, boost counts, coupling paths -> solve programs) runs at the
+    // first call that needs it (ensure_finished)
+    bool pending = false;
+    cudaEvent_t upload_ev = nullptr;  // host band upload done (orders later host-solve uploads after it)
+    char* d_sblob_prev = nullptr;     // guarded solve jobs used while pending
 
     // closed-edge predicates (reference kinds: the first partition has no W,
     // the last no V and is factored as UL)
@@ -441,8 +457,9 @@ struct spk_fact {
         // outlive it); no device-wide synchronisation
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
-                        (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags})
+                        (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags, (void*)d_sblob_prev})
             if (q) dfree(q, stream);
+        if (upload_ev) cudaEventDestroy(upload_ev);
     }
 };
 
@@ -947,6 +964,7 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             c.k = k;
             c.guard = lv.gidx[a];
             c.pad = 0;
+            c.aux = -1;
             c.part = lv.pair_part[a];
             cplG.push_back(c);
             lus.push_back(lv.pair_part[a]);
@@ -966,25 +984,8 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             b.cjobs(ST_WCHECK, cplS);
             b.cjobs(ST_SCHUR_INIT, cplS);
             b.gemm(sgemm);
-            b.cjobs(ST_DENSE_LU, cplS);
-            // S^-1 = U_S^-1 L_S^-1 P_S: identity columns through the factored unit
-            std::vector<CopyJob> ident;
-            std::vector<SweepJob> sfl, sbu;
-            for (int a = 0; a < np; ++a) {
-                const View Si = view(B_POOL, lv.sinv[a], 0, 0, k, k);
-                CopyJob cjb = cj(Si, Si, 0, k, CP_IDENT, 0, k);
-                cjb.guard = 2 * lv.gidx[a] + 1;
-                ident.push_back(cjb);
-                SweepJob a1 = sj(Si, lv.spart[a], SW_FWD_L, 0, 0, 0, k);
-                a1.guard = 2 * lv.gidx[a] + 1;
-                sfl.push_back(a1);
-                SweepJob a2 = sj(Si, lv.spart[a], SW_BWD_U, 0, k - 1, 0, k);
-                a2.guard = 2 * lv.gidx[a] + 1;
-                sbu.push_back(a2);
-            }
-            b.copy(ident);
-            b.sweep(sfl);
-            b.sweep(sbu);
+            for (int a = 0; a < np; ++a) cplS[a].aux = lv.sinv[a];
+            b.cjobs(ST_SCHUR_INV, cplS);  // S^-1 into the pool (S stays in the factor pool)
         }
         b.cpl(cplG);
         b.lu(lus);
@@ -1048,7 +1049,9 @@ void build_reduced_solve(spk_fact& f, Builder& b, bool transpose, long long aux_
         for (int a = 0; a < lv.units / 2; ++a)
             zs.push_back(PairZ{lv.sinv[a], lv.spart[a], lv.gidx[a], lv.pair_part[a], lv.voff[2 * a],
                                lv.woff[2 * a + 1], lv.uh[2 * a], lv.uh[2 * a + 1], B_T, (long long)lv.uoff[2 * a], -1,
-                               level_base[l] + 2LL * k * a, f.flags[lv.gidx[a]] ? 2 : 1});
+                               level_base[l] + 2LL * k * a,
+                               // paths unknown (factorization still running): both, device-guarded
+                               f.flags.empty() ? (k <= 160 ? 3 : 1) : (f.flags[lv.gidx[a]] ? 2 : 1)});
         emit_pair_solves(b, zs, B_AUX, -1, -1, transpose, k);
     }
 }
@@ -1502,9 +1505,10 @@ struct Exec {
                     launch_schur_init((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts, f.d_fac,
                                       f.d_piv, f.d_flags, s);
                     break;
-                case ST_DENSE_LU:
-                    launch_dense_lu((const CouplingJob*)jobs, st.njobs, f.k, f.d_parts, f.d_fac, f.d_piv,
-                                    f.d_flags, s);
+                case ST_SCHUR_INV:
+                    if (!launch_schur_inverse((const CouplingJob*)jobs, st.njobs, f.k, f.d_parts, f.d_fac, f.d_pool,
+                                              f.d_flags, s))
+                        fail(SPK_EINVAL, "schur inverse: k > 160");
                     break;
                 case ST_MEMSET: {
                     const int nc = st.cols < 0 ? ncols : st.cols;
@@ -1717,6 +1721,8 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     tr.mark("uploads");
 }
 
+void build_solve_programs(spk_fact& f, cudaStream_t s);
+
 void finish_factor(spk_fact& f, cudaStream_t s) {
     Tracer tr("finish");
     int status = 0;
@@ -1741,6 +1747,19 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     f.flags.assign(std::max(f.npairs, 1), 0);
     if (f.npairs > 0)
         ck(cudaMemcpy(f.flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost), "flags");
+    build_solve_programs(f, s);
+}
+
+// Solve programs for f.flags (the per-pair coupling paths), or -- flags empty,
+// factorization still running -- with both paths emitted and device-guarded.
+// Cached per flag pattern in the symbolic.
+void build_solve_programs(spk_fact& f, cudaStream_t s) {
+    if (f.d_sblob) {
+        // solves already enqueued may still read the previous jobs: kept to the end
+        if (f.d_sblob_prev) dfree(f.d_sblob_prev, f.stream);
+        f.d_sblob_prev = f.d_sblob;
+        f.d_sblob = nullptr;
+    }
     if (f.sym) {
         SymCache& c = sym_cache();
         std::lock_guard<std::mutex> lk(c.mu);
@@ -1791,6 +1810,15 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
         sp.rtr = f.prog_rtr;
         sp.blob = std::move(pb.blob);
     }
+}
+
+// the deferred host-side finish of a factorization (stream-ordered
+// spk_factorize): synchronises its stream, reports an exactly singular pivot
+void ensure_finished(const spk_fact* fc) {
+    if (!fc || !fc->pending) return;
+    spk_fact& f = const_cast<spk_fact&>(*fc);
+    f.pending = false;
+    finish_factor(f, f.stream);
 }
 
 Bufs make_bufs(const spk_fact* f = nullptr) {
@@ -2014,6 +2042,10 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         f->stream = s;
         Tracer tr("factorize");
         setup_fact(*f, s);
+        // until the factorization is finished (ensure_finished) solves run
+        // device-guarded programs; built and uploaded here, ahead of the work
+        f->flags.clear();
+        build_solve_programs(*f, s);
         tr.mark("setup (symbolic)");
         // band on device; a slab's band starts k halo columns early when its
         // left edge is open and carries k more when its right edge is
@@ -2025,6 +2057,8 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
             tmp = dalloc<double>(ld * (n + hl + hr), s);
             ck(cudaMemcpyAsync(tmp, band, sizeof(double) * ld * (n + hl + hr), cudaMemcpyHostToDevice, s),
                "band upload");
+            ck(cudaEventCreateWithFlags(&f->upload_ev, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(f->upload_ev, s), "event");
             dband = tmp;
         }
         dband += ld * hl;  // column 0 of the slab
@@ -2058,8 +2092,7 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         if (fs) dfree(fs, s);
         if (auxf) dfree(auxf, s);
         if (tmp) dfree(tmp, s);
-        finish_factor(*f, s);
-        tr.mark("finished");
+        f->pending = true;  // finished lazily (ensure_finished)
         *out = f.release();
     });
 }
@@ -2078,6 +2111,7 @@ spk_status spk_factorize_slab(const double* band, int32_t band_mem, int64_t n, i
 
 spk_status spk_fact_unit_tips(const spk_fact* f, double* d_tips, void* stream) {
     return guarded([&] {
+        ensure_finished(f);
         const int k = f->k;
         const long long kk = (long long)k * k;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -2104,9 +2138,18 @@ int32_t spk_fact_open(const spk_fact* f) { return f->open_l | (f->open_r << 1); 
 
 void spk_fact_destroy(spk_fact* f) { delete f; }
 
+spk_status spk_fact_sync(const spk_fact* f) {
+    return guarded([&] { ensure_finished(f); });
+}
+
+spk_status spk_stream_sync(void* stream) {
+    return guarded([&] { ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "stream sync"); });
+}
+
 spk_status spk_fact_info(const spk_fact* f, int64_t* n, int32_t* kl, int32_t* ku, int32_t* k, int32_t* p,
                          int32_t* levels, int32_t* boost_count, int32_t* boost_warnings) {
     return guarded([&] {
+        ensure_finished(f);
         if (n) *n = f->n;
         if (kl) *kl = f->kl;
         if (ku) *ku = f->ku;
@@ -2123,11 +2166,13 @@ spk_status spk_fact_bounds(const spk_fact* f, int64_t* bounds) {
 }
 
 spk_status spk_fact_factor_sweeps(const spk_fact* f, int64_t* sweeps) {
-    return guarded([&] { std::copy(f->factor_sweeps.begin(), f->factor_sweeps.end(), sweeps); });
+    return guarded([&] {
+        ensure_finished(f); std::copy(f->factor_sweeps.begin(), f->factor_sweeps.end(), sweeps); });
 }
 
 spk_status spk_fact_tip(const spk_fact* f, int32_t which, int32_t i, double* out) {
     return guarded([&] {
+        ensure_finished(f);
         const int k = f->k, p = f->p;
         if (i < 0 || i >= p || which < 0 || which > 5) fail(SPK_ERANGE, "fact_tip: index out of range");
         const long long kk = (long long)k * k;
@@ -2153,6 +2198,10 @@ int64_t spk_fact_dump(const spk_fact* f, int32_t which, double* out) {
     // debug/test hook: 0 packed LU pool, 1 row-major copies, 2 1/u_jj
     const long long sz = which == 0 ? f->fac_size : which == 1 ? f->tfac_size : f->n;
     const double* src = which == 0 ? f->d_fac : which == 1 ? f->d_tfac : f->d_dinv;
+    try {
+        ensure_finished(f);
+    } catch (...) {
+    }
     if (out) cudaMemcpy(out, src, sizeof(double) * sz, cudaMemcpyDeviceToHost);
     return sz;
 }
@@ -2165,6 +2214,7 @@ int32_t spk_fact_units(const spk_fact* f, int32_t l) {
 spk_status spk_fact_level_spike(const spk_fact* f, int32_t l, int32_t which, int32_t u, int32_t* h,
                                 double* out) {
     return guarded([&] {
+        ensure_finished(f);
         if (l < 0 || l + 1 >= (int)f->levels.size()) fail(SPK_ERANGE, "level_spike: level out of range");
         const Level& lv = f->levels[l];
         if (u < 0 || u >= lv.units) fail(SPK_ERANGE, "level_spike: unit out of range");
@@ -2183,6 +2233,7 @@ spk_status spk_fact_level_spike(const spk_fact* f, int32_t l, int32_t which, int
 spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu, int32_t* piv,
                              int32_t* fell_back) {
     return guarded([&] {
+        ensure_finished(f);
         if (l < 0 || l + 1 >= (int)f->levels.size()) fail(SPK_ERANGE, "coupling: level out of range");
         const Level& lv = f->levels[l];
         if (a < 0 || a >= (int)lv.pair_part.size()) fail(SPK_ERANGE, "coupling: pair out of range");
@@ -2214,8 +2265,47 @@ spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu
             }
             return;
         }
-        // Schur path: [[I, 0], [W, L_S]] [[I, V], [0, U_S]] with rows k.. permuted by P_S
-        unpack(f->parts[lv.spart[a]], dense, pv);
+        // Schur path: [[I, 0], [W, L_S]] [[I, V], [0, U_S]] with rows k.. permuted by P_S.
+        // The factorization keeps S itself (the solves use S^-1): factor a
+        // scratch copy with the gbtf2-convention dense LU on demand.
+        {
+            PartDev S = f->parts[lv.spart[a]];
+            const size_t fsz = (size_t)S.m * S.rows;
+            double* d_s = nullptr;
+            int* d_i = nullptr;
+            void* d_meta = nullptr;
+            ck(cudaMalloc(&d_s, sizeof(double) * fsz), "coupling");
+            ck(cudaMalloc(&d_i, sizeof(int) * (S.m + 1)), "coupling");
+            ck(cudaMalloc(&d_meta, sizeof(PartDev) + sizeof(CouplingJob)), "coupling");
+            ck(cudaMemcpy(d_s, f->d_fac + S.fofs, sizeof(double) * fsz, cudaMemcpyDeviceToDevice), "coupling");
+            S.fofs = 0;
+            S.r0 = 0;
+            CouplingJob J{};
+            J.part = 0;
+            J.k = k;
+            J.guard = S.m;  // flag slot after the pivots
+            const int one = 1;
+            ck(cudaMemcpy(d_i + S.m, &one, sizeof(int), cudaMemcpyHostToDevice), "coupling");
+            ck(cudaMemcpy(d_meta, &S, sizeof(PartDev), cudaMemcpyHostToDevice), "coupling");
+            ck(cudaMemcpy((char*)d_meta + sizeof(PartDev), &J, sizeof(CouplingJob), cudaMemcpyHostToDevice),
+               "coupling");
+            launch_dense_lu((const CouplingJob*)((char*)d_meta + sizeof(PartDev)), 1, S.m, (const PartDev*)d_meta, d_s,
+                            d_i, d_i, 0);
+            ck(cudaDeviceSynchronize(), "coupling");
+            std::vector<double> band(fsz);
+            ck(cudaMemcpy(band.data(), d_s, sizeof(double) * fsz, cudaMemcpyDeviceToHost), "coupling");
+            pv.resize(S.m);
+            ck(cudaMemcpy(pv.data(), d_i, sizeof(int) * S.m, cudaMemcpyDeviceToHost), "coupling");
+            cudaFree(d_s);
+            cudaFree(d_i);
+            cudaFree(d_meta);
+            dense.assign((size_t)S.m * S.m, 0.0);
+            for (int j = 0; j < S.m; ++j)
+                for (int i = 0; i < S.m; ++i) {
+                    const int q = S.d + i - j;
+                    dense[(size_t)j * S.m + i] = (q >= 0 && q < S.rows) ? band[(size_t)j * S.rows + q] : 0.0;
+                }
+        }
         const int hL = lv.uh[2 * a], hR = lv.uh[2 * a + 1];
         std::vector<double> vl((size_t)hL * k), wr((size_t)hR * k);
         ck(cudaMemcpy(vl.data(), f->d_pool + lv.voff[2 * a], sizeof(double) * vl.size(), cudaMemcpyDeviceToHost),
@@ -2372,17 +2462,18 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
                           double* X, int64_t ldx, cudaStream_t s) {
     const long long n = fc->n;
     CopyStreams& cs = copy_streams();
-    // two chunks: each still fills the sweep kernels (column groups of 80 at
-    // C3); more, narrower chunks cost more compute than the copies they hide
-    const int chunk = std::max(16, ((nrhs + 1) / 2 + 7) / 8 * 8);
+    // three column chunks: enough to hide the solve behind PCIe in both
+    // directions while each chunk still fills the sweep kernels
+    static const int want = getenv("SPK_HOST_CHUNKS") ? std::max(1, atoi(getenv("SPK_HOST_CHUNKS"))) : 3;
+    const int chunk = std::max(16, ((nrhs + want - 1) / want + 7) / 8 * 8);
     const int nch = (nrhs + chunk - 1) / chunk;
-    double* dF = dalloc<double>((size_t)n * nrhs, s);
-    double* dX = dalloc<double>((size_t)n * nrhs, s);
-    std::vector<cudaEvent_t> ev(3 * nch + 1);
+    // F's staging buffer belongs to the upload stream, so the uploads start
+    // at once -- under a still running factorization (stream-ordered
+    // spk_factorize) or the previous call's downloads
+    double* dF = dalloc<double>((size_t)n * nrhs, cs.up);
+    if (fc->upload_ev) ck(cudaStreamWaitEvent(cs.up, fc->upload_ev, 0), "wait");  // PCIe: the band first
+    std::vector<cudaEvent_t> ev(3 * nch);
     for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    // the buffers come from the arena in stream order on s: uploads wait for that
-    ck(cudaEventRecord(ev[3 * nch], s), "event");
-    ck(cudaStreamWaitEvent(cs.up, ev[3 * nch], 0), "wait");
     for (int c = 0; c < nch; ++c) {
         const int c0 = c * chunk, nc = std::min(chunk, nrhs - c0);
         ck(cudaMemcpy2DAsync(dF + (size_t)c0 * n, sizeof(double) * n, F + (size_t)c0 * ldf, sizeof(double) * ldf,
@@ -2390,6 +2481,9 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
            "F upload");
         ck(cudaEventRecord(ev[c], cs.up), "event");
     }
+    // no host wait: while the factorization is pending its solve programs are
+    // device-guarded on the coupling paths
+    double* dX = dalloc<double>((size_t)n * nrhs, s);
     for (int c = 0; c < nch; ++c) {
         const int c0 = c * chunk, nc = std::min(chunk, nrhs - c0);
         ck(cudaStreamWaitEvent(s, ev[c], 0), "wait");
@@ -2404,12 +2498,12 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
            "X download");
         ck(cudaEventRecord(ev[2 * nch + c], cs.down), "event");
     }
-    // downloads done before the buffers go back to the arena on s
+    dfree(dF, s);  // last read by the solve on s
+    // stream-ordered completion: s (and whoever synchronises it) is ordered
+    // after the downloads; the host is not blocked
     ck(cudaStreamWaitEvent(s, ev[3 * nch - 1], 0), "wait");
-    dfree(dF, s);
     dfree(dX, s);
     ck(cudaGetLastError(), "solve kernels");
-    ck(cudaStreamSynchronize(s), "solve");
     for (auto& e : ev) cudaEventDestroy(e);
 }
 
@@ -2443,6 +2537,7 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
             solve_host_pipelined(fc, transpose, F, ldf, nrhs, X, ldx, s);
             return;
         }
+        ensure_finished(fc);
         auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, mem, s);
         x->run_phase();
         if (mem == SPK_MEM_HOST)
@@ -2462,6 +2557,7 @@ int32_t spk_xsolve_exchanges(const spk_fact* f, int32_t transpose) {
 spk_status spk_xsolve_begin(const spk_fact* f, int32_t transpose, const double* d_F, int64_t ldf, int32_t nrhs,
                             double* d_X, int64_t ldx, void* stream, double* d_export, spk_xsolve** out) {
     return guarded([&] {
+        ensure_finished(f);
         *out = nullptr;
         if (nrhs < 1) fail(SPK_EINVAL, "xsolve: nrhs must be positive");
         if (ldf < f->n || ldx < f->n) fail(SPK_EINVAL, "xsolve: F.rows must equal n");
@@ -2589,6 +2685,8 @@ spk_status spk_reduced_solve(const spk_reduced* r, int32_t transpose, double* z,
 
 spk_status spk_fact_reduced_solve(const spk_fact* f, int32_t transpose, double* z, int32_t ncols,
                                   int64_t* couplings) {
+    const spk_status st = guarded([&] { ensure_finished(f); });
+    if (st != SPK_OK) return st;
     return reduced_solve_on(const_cast<spk_fact&>(*f), false, transpose, z, ncols, couplings);
 }
 

@@ -10,10 +10,13 @@
 //   k_wcheck      flag[pair] = max|W| <= 1            (else: generic 2k path)
 //   k_schur_init  S storage := I (dense k x k kept as a full band, so the band
 //                 sweep kernels solve with it)      ; then S -= W V on DMMA
+//   k_schur_inverse  S^-1 by register-resident Gauss-Jordan with partial
+//                 pivoting (the solves apply it as a GEMM); an exactly zero
+//                 pivot column clears the flag so the generic path reproduces
+//                 the reference's boosted fallback.
 //   k_dense_lu    partial-pivot LU of S in shared memory, LAPACK/gbtf2 row
-//                 interchange convention (earlier L columns not swapped), one
-//                 CTA per pair; an exactly zero column clears the flag so the
-//                 generic path reproduces the reference's boosted fallback.
+//                 interchange convention (earlier L columns not swapped): the
+//                 P_S S = L_S U_S factors spk_fact_coupling reports.
 #include "spk_device.cuh"
 #include "spk_launch.h"
 
@@ -134,6 +137,170 @@ __global__ void __launch_bounds__(512) k_dense_lu(const CouplingJob* __restrict_
         const int c = e / n, r = e - c * n;
         F[(long long)c * P.rows + P.d + r - c] = sm[c * ls + r];
     }
+}
+
+// S^-1 of the k x k Schur units by in-place Gauss-Jordan with partial
+// pivoting, register resident: thread (warp w of 8, lane l) holds S(r, c) for
+// r = l + 32a, c = w + 8b.  Step j: the owner warp of column j (w = j % 8)
+// picks the pivot among the rows not yet used (max |s(r, j)|, first index on
+// ties: the same choice as the row-interchange LU), publishes the column and
+// the pivot through shared memory (double-buffered, one CTA barrier per
+// step); every warp takes the pivot row of its own columns by warp shuffle
+// and updates in registers:
+//   row ip:  s(ip, c) /= p, s(ip, j) = 1/p;  others: s(r, c) -= s(r, j) s(ip, c)/p,
+//   s(r, j) = -s(r, j)/p.
+// Pivot rows are never moved, so the result M is the inverse up to the
+// pivot order: S^-1(q(r), perm(c)) = M(r, c), perm(j) = pivot row of step j,
+// q = perm^-1.  An exactly zero pivot column clears the flag (generic 2k path,
+// like k_dense_lu).  S itself stays in the factor pool (spk_fact_coupling
+// factors it on demand).
+template <int RA, int CB, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) k_schur_inverse(const CouplingJob* __restrict__ jobs,
+                                                           const PartDev* __restrict__ parts,
+                                                           const double* __restrict__ fac,
+                                                           double* __restrict__ pool, int* __restrict__ flags) {
+    constexpr int NR = 32 * RA;
+    __shared__ double s_col[2][NR];
+    __shared__ double s_inv[2];
+    __shared__ int s_ip[2];
+    __shared__ int s_perm[NR], s_q[NR];
+    __shared__ double s_row[NW][CB];
+    const CouplingJob J = jobs[blockIdx.x];
+    if (flags[J.guard] != 1) return;
+    const PartDev P = parts[J.part];
+    const int n = P.m;
+    const double* F = fac + P.fofs;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double a[RA][CB];
+#pragma unroll
+    for (int ra = 0; ra < RA; ++ra)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+            const int r = lane + 32 * ra, c = w + NW * cb;
+            a[ra][cb] = (r < n && c < n) ? F[(long long)c * P.rows + P.d + r - c] : 0.0;
+        }
+    unsigned used = 0;
+#pragma unroll
+    for (int ra = 0; ra < RA; ++ra)
+        if (lane + 32 * ra >= n) used |= 1u << ra;
+    // Register chunks are only ever selected by warp- or block-uniform indices
+    // (column chunk jb of the owner warp, row chunk ia of the pivot), so the
+    // selections compile to uniform branches, never to runtime-indexed
+    // registers (which would be demoted to local memory).
+    auto publish = [&](int j) {  // owner warp of column j
+        const int jb = j / NW, buf = j & 1;
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb)
+            if (cb == jb)
+#pragma unroll
+                for (int ra = 0; ra < RA; ++ra) s_col[buf][lane + 32 * ra] = a[ra][cb];
+        __syncwarp();
+        double best = -1.0, bv = 0.0;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) {
+            const double v = s_col[buf][lane + 32 * ra];
+            if (!((used >> ra) & 1u) && fabs(v) > best) {
+                best = fabs(v);
+                bv = v;
+                bi = lane + 32 * ra;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_ip[buf] = best > 0.0 ? bi : -1;
+            s_inv[buf] = 1.0 / bv;
+        }
+    };
+    if (w == 0) publish(0);
+    for (int j = 0; j < n; ++j) {
+        __syncthreads();
+        const int buf = j & 1;
+        const int ip = s_ip[buf];
+        if (ip < 0) {
+            if (threadIdx.x == 0) flags[J.guard] = 0;
+            return;
+        }
+        const double inv = s_inv[buf];
+        if (threadIdx.x == 0) s_perm[j] = ip;
+        const int ia = ip >> 5, il = ip & 31;
+        // pivot row of this warp's columns, scaled, from its holder lane
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra)
+            if (ra == ia) {
+                if (lane == il) {
+#pragma unroll
+                    for (int cb = 0; cb < CB; ++cb) s_row[w][cb] = a[ra][cb] * inv;
+                }
+                if (lane == il) used |= 1u << ra;
+            }
+        __syncwarp();
+        double f[RA];
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) f[ra] = s_col[buf][lane + 32 * ra];
+        // rank-1 elimination on every element (pivot row and column j are
+        // rewritten below)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+            const double u = s_row[w][cb];
+#pragma unroll
+            for (int ra = 0; ra < RA; ++ra) a[ra][cb] = fma(-f[ra], u, a[ra][cb]);
+        }
+        if (w == j % NW) {  // column j := -s(r, j) / p
+            const int jb = j / NW;
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb)
+                if (cb == jb)
+#pragma unroll
+                    for (int ra = 0; ra < RA; ++ra) a[ra][cb] = -f[ra] * inv;
+        }
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra)  // pivot row := s(ip, c) / p, s(ip, j) = 1/p
+            if (ra == ia && lane == il) {
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) a[ra][cb] = (w + NW * cb == j) ? inv : s_row[w][cb];
+            }
+        if (j + 1 < n && w == (j + 1) % NW) publish(j + 1);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) s_q[s_perm[j]] = j;
+    __syncthreads();
+    double* out = pool + J.aux;
+#pragma unroll
+    for (int ra = 0; ra < RA; ++ra)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+            const int r = lane + 32 * ra, c = w + NW * cb;
+            if (r < n && c < n) out[(long long)s_perm[c] * n + s_q[r]] = a[ra][cb];
+        }
+}
+
+bool launch_schur_inverse(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, const double* fac,
+                          double* pool, int* flags, cudaStream_t s) {
+    if (njobs <= 0) return true;
+#define SPK_SINV(RA, CB)                                                                            \
+    if (n <= 32 * RA && n <= 8 * CB) {                                                              \
+        k_schur_inverse<RA, CB, 8><<<njobs, 256, 0, s>>>(d_jobs, d_parts, fac, pool, flags);      \
+        count_launch();                                                                             \
+        return true;                                                                                \
+    }
+    SPK_SINV(1, 4)
+    SPK_SINV(2, 8)
+    SPK_SINV(3, 12)
+    SPK_SINV(4, 16)
+    SPK_SINV(5, 20)
+#undef SPK_SINV
+    return false;
 }
 
 void launch_wcheck(const CouplingJob* d_jobs, int njobs, const double* pool, int* flags, cudaStream_t s) {

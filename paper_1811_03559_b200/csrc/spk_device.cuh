@@ -99,6 +99,7 @@ struct CouplingJob {
     int k;
     int guard;  // flag index (pair)
     int pad;
+    long long aux;  // ST_SCHUR_INV: pool offset of S^-1 (k x k, ld k)
 };
 
 }  // namespace spk

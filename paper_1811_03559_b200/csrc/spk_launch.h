@@ -45,6 +45,8 @@ void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_e
 void launch_wcheck(const CouplingJob* d_jobs, int njobs, const double* pool, int* flags, cudaStream_t s);
 void launch_schur_init(const CouplingJob* d_jobs, int njobs, long long max_elems, const PartDev* d_parts,
                        double* fac, int* piv, const int* flags, cudaStream_t s);
+bool launch_schur_inverse(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, const double* fac,
+                          double* pool, int* flags, cudaStream_t s);
 void launch_dense_lu(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, double* fac, int* piv,
                      int* flags, cudaStream_t s);
 void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,

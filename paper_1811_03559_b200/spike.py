@@ -114,6 +114,10 @@ def lib():
                                     C.POINTER(C.c_void_p)]
         L.spk_fact_destroy.argtypes = [C.c_void_p]
         L.spk_fact_destroy.restype = None
+        L.spk_fact_sync.argtypes = [C.c_void_p]
+        L.spk_fact_sync.restype = C.c_int32
+        L.spk_stream_sync.argtypes = [C.c_void_p]
+        L.spk_stream_sync.restype = C.c_int32
         L.spk_fact_info.argtypes = [C.c_void_p, _i64p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]
         L.spk_fact_bounds.argtypes = [C.c_void_p, _i64p]
         L.spk_fact_factor_sweeps.argtypes = [C.c_void_p, _i64p]
@@ -532,7 +536,9 @@ def factorize(a: BandedMatrix, plan: PartitionPlan, opts: Optional[FactorOptions
     h = C.c_void_p()
     _check(lib().spk_factorize(a.data.ctypes.data, 0, a.n, a.kl, a.ku, C.byref(st), C.byref(o), stream,
                                C.byref(h)))
-    return SpikeFactorization(h.value, plan, a.n, a.kl, a.ku, opts)
+    fact = SpikeFactorization(h.value, plan, a.n, a.kl, a.ku, opts)
+    _check(lib().spk_fact_sync(fact._h))  # factorize() raises like the reference (SingularMatrix)
+    return fact
 
 
 def factorize_device(band_ptr: int, n: int, kl: int, ku: int, plan: PartitionPlan,
@@ -544,7 +550,9 @@ def factorize_device(band_ptr: int, n: int, kl: int, ku: int, plan: PartitionPla
     h = C.c_void_p()
     _check(lib().spk_factorize(C.c_void_p(band_ptr), 1, n, kl, ku, C.byref(st), C.byref(o), stream,
                                C.byref(h)))
-    return SpikeFactorization(h.value, plan, n, kl, ku, opts)
+    fact = SpikeFactorization(h.value, plan, n, kl, ku, opts)
+    _check(lib().spk_fact_sync(fact._h))
+    return fact
 
 
 # ----------------------------------------------------------------------------
@@ -573,6 +581,7 @@ def _solve(fact: SpikeFactorization, f, transpose: bool, stats: Optional[SolveSt
     else:
         _check(lib().spk_solve(fact._h, int(transpose), f.ctypes.data, fact.n, nrhs, x.ctypes.data, fact.n,
                                0, None, C.byref(st)))
+        _check(lib().spk_stream_sync(None))  # X is complete once the stream is
     if stats is not None:
         stats.partition_full_sweeps = [int(v) for v in sw]
         stats.reduced_coupling_solves = int(st.reduced_coupling_solves)

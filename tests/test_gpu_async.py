@@ -1,0 +1,119 @@
+"""Stream-ordered C-ABI and the generic coupling path.
+
+* spk_factorize returns once enqueued; a host-memory spk_solve issued right
+  after it runs the device-guarded solve programs (coupling paths decided on
+  the device) and returns before X lands; spk_stream_sync completes it.  The
+  result must equal the synchronous path's (unguarded programs) bit for bit.
+* Reduced systems whose W blocks exceed 1 in magnitude take the generic 2k
+  coupling path (pivoted coupling LU, reference factorize.cpp:94-102) instead
+  of the Schur complement; checked against a dense solve.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_componentwise
+
+pytestmark = pytest.mark.gpu
+
+
+def _reduced_dense(vt, vb, wt, wb, p, k):
+    N = 2 * p * k
+    red = np.eye(N)
+    for i in range(p):
+        if i + 1 < p:
+            red[2 * i * k:(2 * i + 1) * k, 2 * (i + 1) * k:(2 * i + 3) * k] = vt[i]
+            red[(2 * i + 1) * k:(2 * i + 2) * k, 2 * (i + 1) * k:(2 * i + 3) * k] = vb[i]
+        if i > 0:
+            red[2 * i * k:(2 * i + 1) * k, (2 * i - 1) * k:2 * i * k] = wt[i]
+            red[(2 * i + 1) * k:(2 * i + 2) * k, (2 * i - 1) * k:2 * i * k] = wb[i]
+    return red
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("k", [1, 3, 8])
+@pytest.mark.parametrize("scale", [0.4, 3.0])
+def test_reduced_generic_and_schur_paths(spk, p, k, scale):
+    """scale 3: |W| > 1 in most pairs (generic path); 0.4: Schur path."""
+    rng = np.random.default_rng(900 + 31 * p + k + int(10 * scale))
+    vt, vb, wt, wb = [[scale * (rng.random((k, k)) - 0.5) for _ in range(p)] for _ in range(4)]
+    red = _reduced_dense(vt, vb, wt, wb, p, k)
+    if np.linalg.cond(red) > 1e8:
+        pytest.skip("ill-conditioned draw")
+    rl = spk.reduce_factorize(vt, vb, wt, wb, p, k)
+    y = rng.random((2 * p * k, 3))
+    x = spk.reduced_solve(rl, y, [])
+    xt = spk.reduced_solve_transpose(rl, y, [])
+    tol = 1e-13 * max(1.0, np.linalg.cond(red))
+    assert rel_componentwise(x, np.linalg.solve(red, y)) <= tol
+    assert rel_componentwise(xt, np.linalg.solve(red.T, y)) <= tol
+
+
+CASES = [
+    # n, k, nrhs, p, dd, piv
+    (20000, 8, 40, 9, 1.3, False),
+    (20000, 5, 33, 6, 1.2, True),
+    (12000, 6, 48, 7, 0.6, True),  # not dominant: generic coupling pairs
+    (30000, 40, 64, 5, 1.5, False),
+]
+
+
+@pytest.mark.parametrize("n,k,nrhs,p,dd,piv", CASES)
+def test_stream_ordered_host_solve_matches_sync(oracle, spk, n, k, nrhs, p, dd, piv):
+    L = spk.lib()
+    band = oracle.generate_band(4000 + n + k, n, k, k, dd)
+    F = np.asfortranarray(oracle.generate_rhs(4001 + n, n, nrhs))
+    plan = spk.gpu_plan(n, k, k, nrhs, piv, p)
+    opts = spk.FactorOptions(pivoting=piv)
+    # synchronous reference: the Python API (factorize waits, unguarded programs)
+    a = spk.BandedMatrix(n, k, k, band)
+    fact = spk.factorize(a, plan, opts)
+    want = {False: spk.solve(fact, F), True: spk.transpose_solve(fact, F)}
+    # stream-ordered raw C-ABI with pinned host buffers
+    hband = torch.from_numpy(np.ascontiguousarray(band)).pin_memory()
+    hF = torch.from_numpy(np.ascontiguousarray(F.T)).pin_memory()  # column-major n x nrhs
+    hX = {tr: torch.full_like(hF, float("nan")).pin_memory() for tr in (False, True)}
+    st, keep = spk.spike._plan_struct(plan)
+    o = spk.spike._Opts(int(piv), opts.boost_eps)
+    h = C.c_void_p()
+    spk.spike._check(L.spk_factorize(C.c_void_p(hband.data_ptr()), 0, n, k, k, C.byref(st), C.byref(o), None,
+                                     C.byref(h)))
+    try:
+        for tr in (False, True):
+            spk.spike._check(L.spk_solve(h, int(tr), C.c_void_p(hF.data_ptr()), n, nrhs,
+                                         C.c_void_p(hX[tr].data_ptr()), n, 0, None, None))
+        spk.spike._check(L.spk_stream_sync(None))
+        spk.spike._check(L.spk_fact_sync(h))
+    finally:
+        L.spk_fact_destroy(h)
+    for tr in (False, True):
+        got = hX[tr].numpy().T
+        assert np.array_equal(got, want[tr]), (tr, rel_componentwise(got, want[tr]))
+
+
+def test_singular_reported_by_fact_sync(spk):
+    """Pivoting mode, exactly zero column: the stream-ordered factorization
+    reports SPK_ESINGULAR at spk_fact_sync (the reference throws at factorize);
+    the raw C-ABI call itself returns once enqueued."""
+    n, k = 4000, 3
+    a = spk.BandedMatrix(n, k, k)
+    for i in range(n):
+        a.set(i, i, 2.0)
+    for i in range(1234 - k, 1234 + k + 1):
+        a.set(i, 1234, 0.0)
+    plan = spk.gpu_plan(n, k, k, 1, True, 4)
+    with pytest.raises(RuntimeError):
+        spk.factorize(a, plan, spk.FactorOptions(pivoting=True))
+    L = spk.lib()
+    st, keep = spk.spike._plan_struct(plan)
+    o = spk.spike._Opts(1, spk.FactorOptions().boost_eps)
+    h = C.c_void_p()
+    band = np.ascontiguousarray(a.data)
+    spk.spike._check(L.spk_factorize(C.c_void_p(band.ctypes.data), 0, n, k, k, C.byref(st), C.byref(o), None,
+                                     C.byref(h)))
+    try:
+        assert L.spk_fact_sync(h) != 0
+    finally:
+        L.spk_fact_destroy(h)
