@@ -231,8 +231,19 @@ def profile_roofline(spk, cfg, steps, ms):
         ach = top[1]["flops"] / (tms * 1e-3) / 1e12
         peak = FP64_PEAK_MEASURED
         unit = "TFLOP/s"
+    # DRAM bytes per launch of that kernel class from the committed ncu capture
+    # (profiles/traffic.json), when one exists for this workload
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+        ent = tj.get(cfg["desc"].split()[0], {}).get(top[0])
+        if ent:
+            traffic = (ent["bytes_per_launch"], ent["kernel"] + "; " + ent["source"])
+    except (OSError, ValueError):
+        pass
     return {"bound": bound, "kernel": top[0], "achieved": round(ach, 3), "peak": peak, "unit": unit,
-            "frac": round(ach / peak, 4), "traffic": None,
+            "frac": round(ach / peak, 4), "traffic": traffic[0] if traffic else None,
+            "traffic_unit": "bytes per launch (dram read + write)", "traffic_source": traffic[1] if traffic else None,
             "kernel_share_of_step": round(tms / ms, 4),
             "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if bound == "hbm"
                             else "tools/fp64_peak.cu measured DMMA/DFMA peak on this pool (B200)"),
