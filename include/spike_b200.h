@@ -177,6 +177,40 @@ spk_status spk_solve(const spk_fact *f, int32_t transpose, const double *F, int6
                      int32_t nrhs, double *X, int64_t ldx, int32_t mem, void *stream,
                      spk_solve_stats *stats);
 
+/* ---- verification and refinement on the device ----
+ * All blocks are device pointers (column-major, leading dimensions >= n);
+ * only per-column scalars come back to the host. */
+/* R = F - op(A) X (band_ops.cpp:11-37 band_matmul, the residual of
+ * band_ops.cpp:45-57); d_R may be NULL (not stored).  out (host, 4*ncols):
+ * per column c {||r_c||_2^2, ||f_c||_2^2, max|r_c|, max|x_c|}, deterministic. */
+spk_status spk_residual_device(const double *d_band, int64_t n, int32_t kl, int32_t ku, const double *d_X,
+                               int64_t ldx, const double *d_F, int64_t ldf, int32_t ncols,
+                               int32_t transpose, double *d_R, int64_t ldr, void *stream, double *out);
+/* out (host, 3): ||A||_1, ||A||_inf, max|a_ij| (band_ops.cpp:59-69 norm1 / max_abs) */
+spk_status spk_band_norms_device(const double *d_band, int64_t n, int32_t kl, int32_t ku, void *stream,
+                                 double *out);
+/* RefineResult (solve.hpp:38-44) without x: X is refined in place */
+typedef struct spk_refine_result {
+    int32_t iterations;
+    int32_t converged;
+    int32_t stagnated;
+    double residual;
+} spk_refine_result;
+/* iterative_refine (solve.cpp:404-432, solve.hpp:49-51) on the device: residual
+ * r = F - op(A) X on the tensor cores, ||r||_F / ||F||_F to the host, correction
+ * solve with the factorization, X += d; stops at tol, at max_iters, or when the
+ * residual shrinks by less than 1.1x (stagnated).  band is A, packed
+ * ((kl+ku+1) x n); X holds x0 on entry and the refined x on return.  mem:
+ * SPK_MEM_DEVICE (all device pointers) or SPK_MEM_HOST (staged; the loop still
+ * runs on the device).  Completes before returning. */
+spk_status spk_refine(const spk_fact *f, const double *band, const double *F, int64_t ldf, int32_t nrhs,
+                      double *X, int64_t ldx, int32_t transpose, int32_t max_iters, double tol, int32_t mem,
+                      void *stream, spk_refine_result *res);
+/* Hager's 1-norm condition estimate ||A||_1 * est(||A^-1||_1) (oracle.cpp:132-166,
+ * condition_estimate_1norm) with the factorization's forward/transpose solves;
+ * band on the device or the host (mem). */
+spk_status spk_condest_1norm(const spk_fact *f, const double *band, int32_t mem, void *stream, double *cond);
+
 /* ---- reduced system on its own (reduce_factorize / reduced_solve) ----
  * vt, vb, wt, wb: p blocks of k*k column-major each (host). */
 spk_status spk_reduced_create(const double *vt, const double *vb, const double *wt,

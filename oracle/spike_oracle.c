@@ -1142,9 +1142,10 @@ double orc_backward_error_inf(const double *band, int n, int kl, int ku, const d
     double *r = (double *)malloc(sizeof(double) * (size_t)n * (nc > 0 ? nc : 1));
     orc_band_matmul(band, n, kl, ku, X, nc, transpose, r);
     double anorm = 0.0; /* ||A||_inf (or ||A^T||_inf = ||A||_1) */
+    const int lo = transpose ? ku : kl, hi = transpose ? kl : ku; /* row i of op(A): j in [i-lo, i+hi] */
     for (int i = 0; i < n; ++i) {
         double s = 0.0;
-        for (int j = imax(0, i - kl); j <= imin(n - 1, i + ku); ++j)
+        for (int j = imax(0, i - lo); j <= imin(n - 1, i + hi); ++j)
             s += fabs(transpose ? band_at(band, n, kl, ku, j, i) : band_at(band, n, kl, ku, i, j));
         anorm = fmax(anorm, s);
     }

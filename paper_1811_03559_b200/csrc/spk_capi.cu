@@ -2703,7 +2703,7 @@ spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         if (ncols == 0) return;
         if (mem == SPK_MEM_DEVICE) {
-            launch_band_matmul(band, n, kl, ku, X, ldx, ncols, transpose, Y, ldy, s);
+            launch_band_mm(band, n, kl, ku, X, ldx, ncols, transpose, nullptr, 0, Y, ldy, s);
             ck(cudaGetLastError(), "band_matmul");
             return;
         }
@@ -2715,12 +2715,234 @@ spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku
         ck(cudaMemcpy2DAsync(dx, sizeof(double) * n, X, sizeof(double) * ldx, sizeof(double) * n, ncols,
                              cudaMemcpyHostToDevice, s),
            "upload");
-        launch_band_matmul(db, n, kl, ku, dx, n, ncols, transpose, dy, n, s);
+        launch_band_mm(db, n, kl, ku, dx, n, ncols, transpose, nullptr, 0, dy, n, s);
         ck(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, dy, sizeof(double) * n, sizeof(double) * n, ncols,
                              cudaMemcpyDeviceToHost, s),
            "download");
         for (double* q : {db, dx, dy}) dfree(q, s);
         ck(cudaStreamSynchronize(s), "band_matmul");
+    });
+}
+
+// ---------------------------------------------------------------------------
+// verification and refinement on the device
+}  // extern "C"
+
+namespace {
+
+// per-column {sum|x|, sum x^2, max|x|} of an n x ncols device block, to the host
+std::vector<double> col_stats_host(const double* X, long long ldx, long long n, int ncols, cudaStream_t s) {
+    std::vector<double> h((size_t)3 * ncols);
+    if (ncols <= 0) return h;
+    const int nblk = col_stats_blocks(n);
+    double* part = dalloc<double>((size_t)3 * nblk * ncols, s);
+    double* out = dalloc<double>((size_t)3 * ncols, s);
+    launch_col_stats(X, ldx, n, ncols, part, out, s);
+    ck(cudaGetLastError(), "col_stats");
+    ck(cudaMemcpyAsync(h.data(), out, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s), "col_stats");
+    ck(cudaStreamSynchronize(s), "col_stats");
+    dfree(part, s);
+    dfree(out, s);
+    return h;
+}
+
+void device_solve(const spk_fact* fc, int transpose, const double* F, long long ldf, int nrhs, double* X,
+                  long long ldx, cudaStream_t s) {
+    ensure_finished(fc);
+    auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, SPK_MEM_DEVICE, s);
+    x->run_phase();
+}
+
+}  // namespace
+
+extern "C" {
+
+spk_status spk_residual_device(const double* d_band, int64_t n, int32_t kl, int32_t ku, const double* d_X,
+                               int64_t ldx, const double* d_F, int64_t ldf, int32_t ncols, int32_t transpose,
+                               double* d_R, int64_t ldr, void* stream, double* out) {
+    return guarded([&] {
+        if (n < 1 || kl < 0 || ku < 0) fail(SPK_EINVAL, "residual: bad shape");
+        if (ldx < n || ldf < n || (d_R && ldr < n)) fail(SPK_EINVAL, "residual: X.rows must equal n");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (ncols <= 0) return;
+        double* R = d_R;
+        long long lr = ldr;
+        if (!R) {
+            R = dalloc<double>((size_t)n * ncols, s);
+            lr = n;
+        }
+        launch_band_mm(d_band, n, kl, ku, d_X, ldx, ncols, transpose, d_F, ldf, R, lr, s);
+        ck(cudaGetLastError(), "residual");
+        const std::vector<double> sr = col_stats_host(R, lr, n, ncols, s);
+        const std::vector<double> sf = col_stats_host(d_F, ldf, n, ncols, s);
+        const std::vector<double> sx = col_stats_host(d_X, ldx, n, ncols, s);
+        if (!d_R) dfree(R, s);
+        for (int c = 0; c < ncols; ++c) {
+            out[4 * c + 0] = sr[3 * c + 1];
+            out[4 * c + 1] = sf[3 * c + 1];
+            out[4 * c + 2] = sr[3 * c + 2];
+            out[4 * c + 3] = sx[3 * c + 2];
+        }
+    });
+}
+
+spk_status spk_band_norms_device(const double* d_band, int64_t n, int32_t kl, int32_t ku, void* stream,
+                                 double* out) {
+    return guarded([&] {
+        if (n < 1 || kl < 0 || ku < 0) fail(SPK_EINVAL, "band_norms: bad shape");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        unsigned long long* d = dalloc<unsigned long long>(3, s);
+        ck(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), s), "band_norms");
+        launch_band_norms(d_band, n, kl, ku, d, s);
+        ck(cudaGetLastError(), "band_norms");
+        unsigned long long h[3];
+        ck(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s), "band_norms");
+        ck(cudaStreamSynchronize(s), "band_norms");
+        dfree(d, s);
+        for (int i = 0; i < 3; ++i) out[i] = __builtin_bit_cast(double, h[i]);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+void refine_on_device(const spk_fact* fc, const double* d_band, const double* d_F, int64_t ldf, int32_t nrhs,
+                      double* d_X, int64_t ldx, int32_t transpose, int32_t max_iters, double tol, cudaStream_t s,
+                      spk_refine_result* res) {
+        const spk_fact& f = *fc;
+        const long long n = f.n;
+        *res = spk_refine_result{0, 0, 0, 0.0};
+        // ||F||_F (band_ops.cpp frobenius_norm), column sums of squares in order
+        double fn2 = 0.0;
+        {
+            const std::vector<double> sf = col_stats_host(d_F, ldf, n, nrhs, s);
+            for (int c = 0; c < nrhs; ++c) fn2 += sf[3 * c + 1];
+        }
+        const double fnorm = std::sqrt(fn2);
+        double* R = dalloc<double>((size_t)n * std::max(nrhs, 1), s);
+        double prev = INFINITY;
+        for (int it = 0; it <= max_iters; ++it) {
+            // r = f - op(A) x  (solve.cpp:412-413)
+            if (nrhs > 0) launch_band_mm(d_band, n, f.kl, f.ku, d_X, ldx, nrhs, transpose, d_F, ldf, R, n, s);
+            ck(cudaGetLastError(), "iterative_refine");
+            double rn2 = 0.0;
+            const std::vector<double> sr = col_stats_host(R, n, n, nrhs, s);
+            for (int c = 0; c < nrhs; ++c) rn2 += sr[3 * c + 1];
+            const double rn = std::sqrt(rn2);
+            res->residual = fnorm == 0.0 ? (rn == 0.0 ? 0.0 : INFINITY) : rn / fnorm;
+            res->iterations = it;
+            if (res->residual <= tol) {
+                res->converged = 1;
+                break;
+            }
+            if (it > 0 && res->residual * 1.1 > prev) {
+                res->stagnated = 1;
+                break;
+            }
+            if (it == max_iters) break;
+            prev = res->residual;
+            // d = op(A)^-1 r in place; x += d  (solve.cpp:427-429)
+            device_solve(fc, transpose, R, n, nrhs, R, n, s);
+            launch_axpy(d_X, ldx, R, n, n, nrhs, s);
+            ck(cudaGetLastError(), "iterative_refine");
+        }
+        dfree(R, s);
+}
+
+// a host band / block staged on the device (arena), or the caller's device pointer
+struct Staged {
+    double* p = nullptr;
+    bool own = false;
+    cudaStream_t s = nullptr;
+    Staged(const double* src, long long rows, long long ld, int cols, int mem, cudaStream_t st) : s(st) {
+        if (mem == SPK_MEM_DEVICE) {
+            p = const_cast<double*>(src);
+            return;
+        }
+        own = true;
+        p = dalloc<double>((size_t)rows * std::max(cols, 1), s);
+        if (cols > 0)
+            ck(cudaMemcpy2DAsync(p, sizeof(double) * rows, src, sizeof(double) * ld, sizeof(double) * rows, cols,
+                                 cudaMemcpyHostToDevice, s),
+               "upload");
+    }
+    ~Staged() {
+        if (own) dfree(p, s);
+    }
+};
+}  // namespace
+
+extern "C" {
+
+spk_status spk_refine(const spk_fact* fc, const double* band, const double* F, int64_t ldf, int32_t nrhs, double* X,
+                      int64_t ldx, int32_t transpose, int32_t max_iters, double tol, int32_t mem, void* stream,
+                      spk_refine_result* res) {
+    return guarded([&] {
+        const spk_fact& f = *fc;
+        const long long n = f.n;
+        if (ldf < n || ldx < n) fail(SPK_EINVAL, "iterative_refine: F.rows must equal n");
+        if (f.open()) fail(SPK_EINVAL, "iterative_refine: slab factorization");
+        if (nrhs < 0 || max_iters < 0) fail(SPK_EINVAL, "iterative_refine: negative nrhs or max_iters");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const long long ld = f.kl + f.ku + 1;
+        Staged b(band, ld * n, ld * n, 1, mem, s), fs(F, n, ldf, nrhs, mem, s), xs(X, n, ldx, nrhs, mem, s);
+        const long long lf = mem == SPK_MEM_DEVICE ? ldf : n, lx = mem == SPK_MEM_DEVICE ? ldx : n;
+        refine_on_device(fc, b.p, fs.p, lf, nrhs, xs.p, lx, transpose, max_iters, tol, s, res);
+        if (mem != SPK_MEM_DEVICE && nrhs > 0)
+            ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, xs.p, sizeof(double) * n, sizeof(double) * n, nrhs,
+                                 cudaMemcpyDeviceToHost, s),
+               "download");
+        ck(cudaStreamSynchronize(s), "iterative_refine");
+    });
+}
+
+spk_status spk_condest_1norm(const spk_fact* fc, const double* band, int32_t mem, void* stream, double* cond) {
+    return guarded([&] {
+        const spk_fact& f = *fc;
+        const long long n = f.n;
+        if (f.open()) fail(SPK_EINVAL, "condition_estimate: slab factorization");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const long long ld = f.kl + f.ku + 1;
+        Staged b(band, ld * n, ld * n, 1, mem, s);
+        const double* d_band = b.p;
+        double norms[3];
+        spk_status st = spk_band_norms_device(d_band, n, f.kl, f.ku, stream, norms);
+        if (st != SPK_OK) fail(st, g_err.c_str());
+        double* x = dalloc<double>((size_t)n, s);
+        double* y = dalloc<double>((size_t)n, s);
+        double* xi = dalloc<double>((size_t)n, s);
+        const int nblk = dot_argmax_blocks(n);
+        double* part = dalloc<double>((size_t)3 * nblk, s);
+        std::vector<double> hp((size_t)3 * nblk);
+        launch_fill(x, n, 1.0 / n, s);
+        double est = 0.0;
+        // Hager / Higham 1-norm estimator, oracle.cpp:132-166: at most 6 steps
+        for (int it = 0; it < 6; ++it) {
+            device_solve(fc, 0, x, n, 1, y, n, s);
+            const std::vector<double> sy = col_stats_host(y, n, n, 1, s);
+            est = std::max(est, sy[0]);
+            launch_sign(y, xi, n, s);
+            device_solve(fc, 1, xi, n, 1, xi, n, s);
+            launch_dot_argmax(xi, x, n, part, s);
+            ck(cudaGetLastError(), "condition_estimate");
+            ck(cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s),
+               "condition_estimate");
+            ck(cudaStreamSynchronize(s), "condition_estimate");
+            double zdx = 0.0, zmax = -1.0;
+            long long jmax = 0;
+            for (int b = 0; b < nblk; ++b) {  // blocks in index order: first max wins
+                zdx += hp[3 * b];
+                if (hp[3 * b + 1] > zmax) {
+                    zmax = hp[3 * b + 1];
+                    jmax = (long long)hp[3 * b + 2];
+                }
+            }
+            if (zmax <= zdx) break;
+            launch_unit(x, n, jmax, s);
+        }
+        for (double* q : {x, y, xi, part}) dfree(q, s);
+        ck(cudaStreamSynchronize(s), "condition_estimate");
+        *cond = est * norms[0];
     });
 }
 

@@ -49,6 +49,19 @@ bool launch_schur_inverse(const CouplingJob* d_jobs, int njobs, int n, const Par
                           double* pool, int* flags, cudaStream_t s);
 void launch_dense_lu(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, double* fac, int* piv,
                      int* flags, cudaStream_t s);
+// spk_verify.cu: verification and refinement kernels
+void launch_band_mm(const double* band, long long n, int kl, int ku, const double* X, long long ldx, int ncols,
+                    int transpose, const double* F, long long ldf, double* Y, long long ldy, cudaStream_t s);
+int col_stats_blocks(long long n);
+void launch_col_stats(const double* X, long long ldx, long long n, int ncols, double* part, double* out,
+                      cudaStream_t s);
+void launch_band_norms(const double* band, long long n, int kl, int ku, unsigned long long* out, cudaStream_t s);
+void launch_axpy(double* X, long long ldx, const double* D, long long ldd, long long n, int ncols, cudaStream_t s);
+void launch_sign(const double* y, double* xi, long long n, cudaStream_t s);
+int dot_argmax_blocks(long long n);
+void launch_dot_argmax(const double* z, const double* x, long long n, double* part, cudaStream_t s);
+void launch_unit(double* x, long long n, long long j, cudaStream_t s);
+void launch_fill(double* x, long long n, double v, cudaStream_t s);
 void launch_band_matmul(const double* band, long long n, int kl, int ku, const double* X,
                         long long ldx, int ncols, int transpose, double* Y, long long ldy,
                         cudaStream_t s);

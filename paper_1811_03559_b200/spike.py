@@ -114,6 +114,18 @@ def lib():
                                     C.POINTER(C.c_void_p)]
         L.spk_fact_destroy.argtypes = [C.c_void_p]
         L.spk_fact_destroy.restype = None
+        L.spk_residual_device.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.POINTER(C.c_double)]
+        L.spk_residual_device.restype = C.c_int32
+        L.spk_band_norms_device.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                            C.POINTER(C.c_double)]
+        L.spk_band_norms_device.restype = C.c_int32
+        L.spk_refine.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                 C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.POINTER(_RefineC)]
+        L.spk_refine.restype = C.c_int32
+        L.spk_condest_1norm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double)]
+        L.spk_condest_1norm.restype = C.c_int32
         L.spk_fact_sync.argtypes = [C.c_void_p]
         L.spk_fact_sync.restype = C.c_int32
         L.spk_stream_sync.argtypes = [C.c_void_p]
@@ -688,6 +700,11 @@ def max_abs(a: BandedMatrix) -> float:
     return float(np.abs(a.data).max())
 
 
+class _RefineC(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("stagnated", C.c_int32),
+                ("residual", C.c_double)]
+
+
 @dataclass
 class RefineResult:
     x: np.ndarray
@@ -699,29 +716,69 @@ class RefineResult:
 
 def iterative_refine(fact: SpikeFactorization, a: BandedMatrix, f, x0, max_iters: int, tol: float,
                      transpose: bool = False) -> RefineResult:
-    """Residual-correction refinement (solve.cpp:404-432): residual A x on the GPU,
-    correction solve on the GPU factorization."""
+    """Residual-correction refinement (solve.cpp:404-432), the whole loop on the
+    GPU (spk_refine): residual on the tensor cores, correction solves with the
+    factorization, only ||r||_F crossing to the host per iteration."""
     f = _as_block(f)
-    res = RefineResult(x=_as_block(x0).copy(order="F"))
-    fnorm = frobenius_norm(f)
-    prev = math.inf
-    for it in range(max_iters + 1):
-        r = f - band_matmul(a, res.x, transpose)
-        rn = frobenius_norm(r)
-        res.residual = (0.0 if rn == 0.0 else math.inf) if fnorm == 0.0 else rn / fnorm
-        res.iterations = it
-        if res.residual <= tol:
-            res.converged = True
-            return res
-        if it > 0 and res.residual * 1.1 > prev:
-            res.stagnated = True
-            return res
-        if it == max_iters:
-            return res
-        prev = res.residual
-        d = transpose_solve(fact, r) if transpose else solve(fact, r)
-        res.x = res.x + d
-    return res
+    x = _as_block(x0).copy(order="F")
+    if f.shape != x.shape or f.shape[0] != fact.n or a.n != fact.n:
+        raise InvalidArgument("iterative_refine: F.rows must equal n")
+    out = _RefineC()
+    _check(lib().spk_refine(fact._h, a.data.ctypes.data, f.ctypes.data, fact.n, f.shape[1], x.ctypes.data,
+                            fact.n, int(transpose), int(max_iters), float(tol), 0, None, C.byref(out)))
+    return RefineResult(x=x, iterations=int(out.iterations), residual=float(out.residual),
+                        converged=bool(out.converged), stagnated=bool(out.stagnated))
+
+
+def refine_device(fact: SpikeFactorization, band_ptr: int, f_ptr: int, ldf: int, nrhs: int, x_ptr: int, ldx: int,
+                  max_iters: int, tol: float, transpose: bool = False, stream: int = 0) -> RefineResult:
+    """iterative_refine on device buffers: X (x0 on entry) is refined in place."""
+    out = _RefineC()
+    _check(lib().spk_refine(fact._h, C.c_void_p(band_ptr), C.c_void_p(f_ptr), ldf, nrhs, C.c_void_p(x_ptr), ldx,
+                            int(transpose), int(max_iters), float(tol), 1, stream, C.byref(out)))
+    return RefineResult(x=None, iterations=int(out.iterations), residual=float(out.residual),
+                        converged=bool(out.converged), stagnated=bool(out.stagnated))
+
+
+# Hager's estimator: the reference's condition_estimate_1norm (src/oracle.cpp:132-166)
+def condition_estimate_1norm(fact: SpikeFactorization, a: BandedMatrix) -> float:
+    """Hager's kappa_1 estimate (condition_estimate_1norm) with the GPU factorization's solves."""
+    cond = C.c_double()
+    _check(lib().spk_condest_1norm(fact._h, a.data.ctypes.data, 0, None, C.byref(cond)))
+    return float(cond.value)
+
+
+def condition_estimate_device(fact: SpikeFactorization, band_ptr: int, stream: int = 0) -> float:
+    cond = C.c_double()
+    _check(lib().spk_condest_1norm(fact._h, C.c_void_p(band_ptr), 1, stream, C.byref(cond)))
+    return float(cond.value)
+
+
+def residual_device(band_ptr: int, n: int, kl: int, ku: int, x_ptr: int, ldx: int, f_ptr: int, ldf: int,
+                    ncols: int, transpose: bool = False, r_ptr: int = 0, ldr: int = 0, stream: int = 0) -> np.ndarray:
+    """R = F - op(A) X on device buffers; returns per column
+    [||r||_2^2, ||f||_2^2, max|r|, max|x|] (ncols x 4)."""
+    out = np.zeros((max(ncols, 1), 4))
+    _check(lib().spk_residual_device(C.c_void_p(band_ptr), n, kl, ku, C.c_void_p(x_ptr), ldx, C.c_void_p(f_ptr),
+                                     ldf, ncols, int(transpose), C.c_void_p(r_ptr or None), ldr or n, stream,
+                                     out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out[:ncols]
+
+
+def band_norms_device(band_ptr: int, n: int, kl: int, ku: int, stream: int = 0):
+    """(||A||_1, ||A||_inf, max|a_ij|) of a device band."""
+    out = (C.c_double * 3)()
+    _check(lib().spk_band_norms_device(C.c_void_p(band_ptr), n, kl, ku, stream, out))
+    return float(out[0]), float(out[1]), float(out[2])
+
+
+def backward_error_device(band_ptr: int, n: int, kl: int, ku: int, x_ptr: int, ldx: int, f_ptr: int, ldf: int,
+                          ncols: int, transpose: bool = False, stream: int = 0) -> float:
+    """Normwise backward error max_c ||r_c||_inf / (||op(A)||_inf ||x_c||_inf)."""
+    st = residual_device(band_ptr, n, kl, ku, x_ptr, ldx, f_ptr, ldf, ncols, transpose, stream=stream)
+    n1, ninf, _ = band_norms_device(band_ptr, n, kl, ku, stream)
+    an = n1 if transpose else ninf
+    return float(max((r[2] / (an * r[3]) if r[3] > 0 else (0.0 if r[2] == 0 else math.inf)) for r in st)) if ncols else 0.0
 
 
 # ----------------------------------------------------------------------------
