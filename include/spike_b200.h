@@ -45,7 +45,8 @@ typedef enum spk_status {
     SPK_ECUDA = 4,     /* CUDA runtime failure                          */
     SPK_ENOMEM = 5,    /* device allocation failure                     */
     SPK_ENCCL = 6,     /* collective failure                            */
-    SPK_ERANGE = 7     /* std::out_of_range                             */
+    SPK_ERANGE = 7,    /* std::out_of_range                             */
+    SPK_EIO = 8        /* std::runtime_error (file open / format, band_io.cpp) */
 } spk_status;
 
 enum { SPK_MEM_HOST = 0, SPK_MEM_DEVICE = 1 };
@@ -210,6 +211,24 @@ spk_status spk_refine(const spk_fact *f, const double *band, const double *F, in
  * condition_estimate_1norm) with the factorization's forward/transpose solves;
  * band on the device or the host (mem). */
 spk_status spk_condest_1norm(const spk_fact *f, const double *band, int32_t mem, void *stream, double *cond);
+
+/* ---- .spkb band files (band_io.cpp:98-143 read_spkb / write_matrix; SURVEY.md
+ * section 8(f) row 3) ----
+ * Format: "SPKB", then n, kl, ku as little-endian int64, then the packed band
+ * (kl+ku+1 little-endian doubles per column, columns 0..n-1), i.e. exactly the
+ * BandedMatrix / spk_factorize layout.  Errors: SPK_EIO with the reference's
+ * messages ("bad SPKB magic", "bad SPKB dimensions", "SPKB file truncated",
+ * "cannot open <path>"). */
+spk_status spk_spkb_header(const char *path, int64_t *n, int32_t *kl, int32_t *ku);
+/* Columns [col0, col0+ncols) of the packed band into dst ((kl+ku+1) x ncols).
+ * mem = SPK_MEM_DEVICE streams the file through pinned buffers straight into
+ * HBM (file reads overlap the uploads; a slab loads its own column window with
+ * its halos); SPK_MEM_HOST reads into host memory.  Completes before return. */
+spk_status spk_spkb_load(const char *path, int64_t col0, int64_t ncols, double *dst, int32_t mem,
+                         void *stream);
+/* Write a packed band (device or host memory) as .spkb. */
+spk_status spk_spkb_store(const char *path, const double *band, int64_t n, int32_t kl, int32_t ku,
+                          int32_t mem, void *stream);
 
 /* ---- reduced system on its own (reduce_factorize / reduced_solve) ----
  * vt, vb, wt, wb: p blocks of k*k column-major each (host). */

@@ -249,9 +249,26 @@ class Reference:
         L.ref_time_path.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
                                     C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _ip]
         L.ref_hw_threads.restype = C.c_int
+        L.ref_write_spkb.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
+        L.ref_read_spkb.argtypes = [C.c_char_p, _ip, _ip, _ip, _dp]
 
     def err(self):
         return self.L.ref_last_error().decode()
+
+    def write_spkb(self, band, n, kl, ku, path):
+        """band_io.cpp write_matrix(..., MatrixFormat::Spkb)"""
+        band = np.ascontiguousarray(band, dtype=np.float64)
+        if self.L.ref_write_spkb(_d(band), n, kl, ku, path.encode()):
+            raise RuntimeError(self.err())
+
+    def read_spkb(self, path):
+        """band_io.cpp read_matrix on a .spkb file -> (n, kl, ku, band)"""
+        n, kl, ku = C.c_int(), C.c_int(), C.c_int()
+        if self.L.ref_read_spkb(path.encode(), C.byref(n), C.byref(kl), C.byref(ku), None):
+            raise RuntimeError(self.err())
+        band = np.zeros((n.value, kl.value + ku.value + 1))
+        self.L.ref_read_spkb(path.encode(), C.byref(n), C.byref(kl), C.byref(ku), _d(band))
+        return n.value, kl.value, ku.value, band
 
     def make_plan(self, n, kl, ku, t, r12, r13):
         cap = 4096

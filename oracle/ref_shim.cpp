@@ -6,6 +6,7 @@
 // golden fixtures under tests/golden/ that pin oracle/spike_oracle.c, and
 // (b) by bench.py --impl reference / cpu_baseline to time the reference's own
 // CPU path (spike::make_plan -> factorize -> solve / transpose_solve).
+#include "spike/band_io.hpp"
 #include "spike/band_ops.hpp"
 #include "spike/factorize.hpp"
 #include "spike/oracle.hpp"
@@ -234,6 +235,21 @@ int ref_time_path(const double* band, int n, int kl, int ku, const double* F, in
             *t_tsolve = std::chrono::duration<double>(clk::now() - t3).count();
             if (XT) std::memcpy(XT, xt.data.data(), sizeof(double) * xt.data.size());
         }
+    });
+}
+
+// band_io.cpp: the reference's own .spkb writer / reader (golden fixtures)
+int ref_write_spkb(const double* band, int n, int kl, int ku, const char* path) {
+    return guarded([&] { write_matrix(band_from(band, n, kl, ku), path, MatrixFormat::Spkb); });
+}
+
+int ref_read_spkb(const char* path, int* n, int* kl, int* ku, double* out) {
+    return guarded([&] {
+        BandedMatrix a = read_matrix(path);
+        *n = a.n();
+        *kl = a.kl();
+        *ku = a.ku();
+        if (out) std::memcpy(out, a.data().data(), sizeof(double) * a.data().size());
     });
 }
 

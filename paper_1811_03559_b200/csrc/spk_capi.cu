@@ -38,6 +38,10 @@ struct PivLuArgs {  // spk_lu_fast.cu
 
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cfloat>
@@ -2943,6 +2947,182 @@ spk_status spk_condest_1norm(const spk_fact* fc, const double* band, int32_t mem
         for (double* q : {x, y, xi, part}) dfree(q, s);
         ck(cudaStreamSynchronize(s), "condition_estimate");
         *cond = est * norms[0];
+    });
+}
+
+// ---------------------------------------------------------------------------
+// .spkb files (band_io.cpp:98-143)
+}  // extern "C"
+
+namespace {
+
+constexpr long long kSpkbHeader = 4 + 3 * 8;
+
+struct Fd {
+    int fd = -1;
+    ~Fd() {
+        if (fd >= 0) close(fd);
+    }
+};
+
+void full_pread(int fd, void* dst, size_t bytes, long long off, const char* what) {
+    char* p = static_cast<char*>(dst);
+    while (bytes > 0) {
+        const ssize_t r = pread(fd, p, bytes, off);
+        if (r <= 0) fail(SPK_EIO, what);
+        p += r;
+        bytes -= (size_t)r;
+        off += r;
+    }
+}
+
+void full_write(int fd, const void* src, size_t bytes, const std::string& path) {
+    const char* p = static_cast<const char*>(src);
+    while (bytes > 0) {
+        const ssize_t r = write(fd, p, bytes);
+        if (r <= 0) fail(SPK_EIO, "write to " + path + " failed");
+        p += r;
+        bytes -= (size_t)r;
+    }
+}
+
+// header + size check; little-endian host (x86-64 / aarch64) assumed, like the
+// reference's get_i64 / get_f64 byte order
+void spkb_open(const char* path, Fd& f, long long& n, int& kl, int& ku) {
+    static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "spkb: little-endian host");
+    f.fd = open(path, O_RDONLY);
+    if (f.fd < 0) fail(SPK_EIO, std::string("cannot open ") + path);
+    char head[kSpkbHeader];
+    struct stat st;
+    if (fstat(f.fd, &st) != 0) fail(SPK_EIO, std::string("cannot open ") + path);
+    if (st.st_size < 4 || pread(f.fd, head, 4, 0) != 4 || std::memcmp(head, "SPKB", 4) != 0)
+        fail(SPK_EIO, "bad SPKB magic");
+    if (st.st_size < kSpkbHeader) fail(SPK_EIO, "SPKB file truncated");
+    full_pread(f.fd, head, kSpkbHeader, 0, "SPKB file truncated");
+    int64_t v[3];
+    std::memcpy(v, head + 4, sizeof(v));
+    if (v[0] < 1 || v[1] < 0 || v[2] < 0 || v[1] >= v[0] || v[2] >= v[0]) fail(SPK_EIO, "bad SPKB dimensions");
+    n = v[0];
+    kl = (int)v[1];
+    ku = (int)v[2];
+    if ((long long)st.st_size < kSpkbHeader + 8LL * (kl + ku + 1) * n) fail(SPK_EIO, "SPKB file truncated");
+}
+
+// two pinned staging buffers, cached per thread (pinned allocation is slow)
+struct Staging {
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+};
+Staging& staging(size_t want) {
+    static thread_local Staging st;
+    if (st.bytes < want) {
+        for (int i = 0; i < 2; ++i) {
+            if (st.buf[i]) cudaFreeHost(st.buf[i]);
+            if (st.ev[i]) cudaEventDestroy(st.ev[i]);
+            ck(cudaHostAlloc(&st.buf[i], want, cudaHostAllocDefault), "pinned staging");
+            ck(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming), "event");
+        }
+        st.bytes = want;
+    }
+    return st;
+}
+
+size_t spkb_chunk_bytes() {
+    static const size_t c = getenv("SPK_SPKB_CHUNK") ? std::max<size_t>(8, strtoull(getenv("SPK_SPKB_CHUNK"), 0, 10))
+                                                     : (size_t)64 << 20;
+    return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+spk_status spk_spkb_header(const char* path, int64_t* n, int32_t* kl, int32_t* ku) {
+    return guarded([&] {
+        Fd f;
+        long long nn;
+        int a, b;
+        spkb_open(path, f, nn, a, b);
+        *n = nn;
+        *kl = a;
+        *ku = b;
+    });
+}
+
+spk_status spk_spkb_load(const char* path, int64_t col0, int64_t ncols, double* dst, int32_t mem, void* stream) {
+    return guarded([&] {
+        Fd f;
+        long long n;
+        int kl, ku;
+        spkb_open(path, f, n, kl, ku);
+        if (col0 < 0 || ncols < 0 || col0 + ncols > n) fail(SPK_ERANGE, "spkb_load: column window out of range");
+        const long long ld = kl + ku + 1;
+        const long long off = kSpkbHeader + 8LL * ld * col0;
+        const size_t total = (size_t)(8LL * ld * ncols);
+        if (total == 0) return;
+        if (mem != SPK_MEM_DEVICE) {
+            full_pread(f.fd, dst, total, off, "SPKB file truncated");
+            return;
+        }
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t chunk = std::min(total, spkb_chunk_bytes());
+        Staging& st = staging(chunk);
+        size_t done = 0;
+        for (int c = 0; done < total; ++c) {
+            const int b = c & 1;
+            const size_t len = std::min(chunk, total - done);
+            if (c >= 2) ck(cudaEventSynchronize(st.ev[b]), "spkb_load");  // buffer b's previous upload
+            full_pread(f.fd, st.buf[b], len, off + (long long)done, "SPKB file truncated");
+            ck(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + done, st.buf[b], len, cudaMemcpyHostToDevice, s),
+               "spkb upload");
+            ck(cudaEventRecord(st.ev[b], s), "event");
+            done += len;
+        }
+        ck(cudaStreamSynchronize(s), "spkb_load");
+    });
+}
+
+spk_status spk_spkb_store(const char* path, const double* band, int64_t n, int32_t kl, int32_t ku, int32_t mem,
+                          void* stream) {
+    return guarded([&] {
+        if (n < 1 || kl < 0 || ku < 0 || kl >= n || ku >= n) fail(SPK_EINVAL, "BandedMatrix: bad shape");
+        Fd f;
+        f.fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (f.fd < 0) fail(SPK_EIO, std::string("cannot open ") + path + " for writing");
+        char head[kSpkbHeader];
+        std::memcpy(head, "SPKB", 4);
+        const int64_t v[3] = {n, kl, ku};
+        std::memcpy(head + 4, v, sizeof(v));
+        const std::string p(path);
+        full_write(f.fd, head, kSpkbHeader, p);
+        const size_t total = (size_t)(8LL * (kl + ku + 1) * n);
+        if (mem != SPK_MEM_DEVICE) {
+            full_write(f.fd, band, total, p);
+            return;
+        }
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t chunk = std::min(total, spkb_chunk_bytes());
+        Staging& st = staging(chunk);
+        // download chunk c+1 while chunk c is written
+        size_t issued = 0, written = 0;
+        size_t len[2] = {0, 0};
+        auto issue = [&](int b) {
+            len[b] = std::min(chunk, total - issued);
+            ck(cudaMemcpyAsync(st.buf[b], reinterpret_cast<const char*>(band) + issued, len[b],
+                               cudaMemcpyDeviceToHost, s),
+               "spkb download");
+            ck(cudaEventRecord(st.ev[b], s), "event");
+            issued += len[b];
+        };
+        issue(0);
+        for (int c = 0; written < total; ++c) {
+            const int b = c & 1;
+            if (issued < total) issue(b ^ 1);
+            ck(cudaEventSynchronize(st.ev[b]), "spkb_store");
+            full_write(f.fd, st.buf[b], len[b], p);
+            written += len[b];
+        }
     });
 }
 

@@ -54,6 +54,22 @@ def halo(rank: int, world: int, k: int):
     return (k if rank > 0 else 0), (k if rank < world - 1 else 0)
 
 
+def load_slab_band(path, rank: int, world: int, device=None, stream: int = 0):
+    """This rank's slab of a .spkb band straight into HBM (spk_spkb_load): the
+    packed columns [R_g - left halo, R_{g+1} + right halo), i.e. the band
+    spk_factorize_slab takes; no other rank's rows are read.  Returns
+    (tensor (ncols, kl+ku+1), (n, kl, ku), left halo)."""
+    n, kl, ku = _spk.spkb_header(path)
+    k = max(kl, ku)
+    rows = slab_rows(n, world)
+    lh, rh = halo(rank, world, k)
+    c0 = rows[rank] - lh
+    nc = rows[rank + 1] - rows[rank] + lh + rh
+    t = torch.empty((nc, kl + ku + 1), dtype=torch.float64, device=device or torch.device("cuda"))
+    _spk.load_spkb_device(path, t.data_ptr(), c0, nc, stream)
+    return t, (n, kl, ku), lh
+
+
 # ----------------------------------------------------------------------------
 # slab-level reduced-system assembly (pure tensor code: device or CPU)
 def gather_tips_host(gathered: torch.Tensor, k: int):

@@ -62,8 +62,12 @@ class OutOfRange(IndexError):
     """std::out_of_range"""
 
 
+class FileFormatError(RuntimeError):
+    """std::runtime_error from band_io.cpp (cannot open, bad SPKB magic / dimensions, truncated)."""
+
+
 _STATUS = {1: InvalidArgument, 2: SingularError, 3: DomainError, 4: CudaError, 5: MemoryError,
-           6: CudaError, 7: OutOfRange}
+           6: CudaError, 7: OutOfRange, 8: FileFormatError}
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -126,6 +130,13 @@ def lib():
         L.spk_refine.restype = C.c_int32
         L.spk_condest_1norm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double)]
         L.spk_condest_1norm.restype = C.c_int32
+        L.spk_spkb_header.argtypes = [C.c_char_p, _i64p, _i32p, _i32p]
+        L.spk_spkb_header.restype = C.c_int32
+        L.spk_spkb_load.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]
+        L.spk_spkb_load.restype = C.c_int32
+        L.spk_spkb_store.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                     C.c_void_p]
+        L.spk_spkb_store.restype = C.c_int32
         L.spk_fact_sync.argtypes = [C.c_void_p]
         L.spk_fact_sync.restype = C.c_int32
         L.spk_stream_sync.argtypes = [C.c_void_p]
@@ -779,6 +790,58 @@ def backward_error_device(band_ptr: int, n: int, kl: int, ku: int, x_ptr: int, l
     n1, ninf, _ = band_norms_device(band_ptr, n, kl, ku, stream)
     an = n1 if transpose else ninf
     return float(max((r[2] / (an * r[3]) if r[3] > 0 else (0.0 if r[2] == 0 else math.inf)) for r in st)) if ncols else 0.0
+
+
+# ----------------------------------------------------------------------------
+# .spkb band files (band_io.hpp / band_io.cpp:98-143)
+
+
+def _path(p) -> bytes:
+    return os.fsencode(p)
+
+
+def spkb_header(path):
+    """(n, kl, ku) of a .spkb file."""
+    n, kl, ku = C.c_int64(), C.c_int32(), C.c_int32()
+    _check(lib().spk_spkb_header(_path(path), C.byref(n), C.byref(kl), C.byref(ku)))
+    return int(n.value), int(kl.value), int(ku.value)
+
+
+def read_spkb(path) -> BandedMatrix:
+    """read_matrix on a .spkb file (band_io.cpp:98-110, :145-155)."""
+    n, kl, ku = spkb_header(path)
+    data = np.zeros((n, kl + ku + 1))
+    _check(lib().spk_spkb_load(_path(path), 0, n, data.ctypes.data, 0, None))
+    return BandedMatrix(n, kl, ku, data)
+
+
+def read_matrix(path) -> BandedMatrix:
+    """band_io.cpp:145-155 for the binary format (MatrixMarket text is out of scope)."""
+    with open(path, "rb") as fh:
+        head = fh.read(4)
+    if not head:
+        raise FileFormatError("empty matrix file")
+    if head != b"SPKB":
+        raise FileFormatError("MatrixMarket input is not supported; convert to .spkb")
+    return read_spkb(path)
+
+
+def write_spkb(a: BandedMatrix, path) -> None:
+    """write_matrix(a, path, MatrixFormat::Spkb) (band_io.cpp:114-122)."""
+    _check(lib().spk_spkb_store(_path(path), a.data.ctypes.data, a.n, a.kl, a.ku, 0, None))
+
+
+def load_spkb_device(path, dst_ptr: int, col0: int = 0, ncols: Optional[int] = None, stream: int = 0):
+    """Columns [col0, col0+ncols) of a .spkb band straight into HBM (a slab's
+    window with its halo columns); returns (n, kl, ku) of the file."""
+    n, kl, ku = spkb_header(path)
+    ncols = n - col0 if ncols is None else ncols
+    _check(lib().spk_spkb_load(_path(path), col0, ncols, C.c_void_p(dst_ptr), 1, stream))
+    return n, kl, ku
+
+
+def store_spkb_device(path, band_ptr: int, n: int, kl: int, ku: int, stream: int = 0) -> None:
+    _check(lib().spk_spkb_store(_path(path), C.c_void_p(band_ptr), n, kl, ku, 1, stream))
 
 
 # ----------------------------------------------------------------------------

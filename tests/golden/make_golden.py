@@ -96,6 +96,23 @@ def main():
     out["plans"] = np.array(plans, dtype=np.int64)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     print("wrote", os.path.join(HERE, "golden.npz"))
+    write_spkb_fixtures(ref, o)
+
+
+# .spkb files written by the reference's own band_io.cpp (write_matrix,
+# MatrixFormat::Spkb): the byte-level contract of spk_spkb_load / _store
+SPKB_CASES = [("ref_n300_kl3_ku5.spkb", 300, 3, 5, 1.5), ("ref_n1_kl0_ku0.spkb", 1, 0, 0, 2.0),
+              ("ref_n257_kl16_ku2.spkb", 257, 16, 2, 1.2)]
+
+
+def write_spkb_fixtures(ref, o):
+    for (fname, n, kl, ku, dd) in SPKB_CASES:
+        band = o.generate_band(SEED + n, n, kl, ku, dd)
+        path = os.path.join(HERE, fname)
+        ref.write_spkb(band, n, kl, ku, path)
+        rn, rkl, rku, back = ref.read_spkb(path)
+        assert (rn, rkl, rku) == (n, kl, ku) and np.array_equal(back, band)
+        print("wrote", path)
 
 
 if __name__ == "__main__":

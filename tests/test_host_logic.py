@@ -117,13 +117,13 @@ def test_banded_matrix_mirror(spk):
 
 def test_no_cpu_fallback_without_library(monkeypatch, tmp_path):
     """The product path fails loudly when the CUDA library is missing."""
-    import importlib
     import paper_1811_03559_b200.spike as sp
     monkeypatch.setattr(sp, "LIB_PATH", str(tmp_path / "missing.so"))
     monkeypatch.setattr(sp, "_lib", None)
     with pytest.raises(ImportError):
         sp.lib()
-    importlib.reload(sp)
+    # monkeypatch restores LIB_PATH and _lib (no module reload: that would
+    # re-create the exception classes other tests match against)
 
 
 def test_product_does_not_import_oracle():
