@@ -91,6 +91,31 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
                         int32_t p_hint, int32_t cap, int32_t *p, int64_t *bounds,
                         int32_t *kinds);
 
+/* ---- K calibration and ratio planning on the GPU (partition.cpp:120-170,
+ * partition.hpp:58-74) ---- */
+typedef struct spk_calibration {
+    double k;              /* median over reps of t_solve(nrhs = k_sample) / t_factor */
+    double factor_seconds; /* mean, one partition factorized on the GPU */
+    double solve_seconds;  /* mean, its two-sweep solve */
+    int32_t timer_warning; /* total sample < 10 ms (the reference's rule) */
+} spk_calibration;
+/* calibrate_k on the device: one non-pivoting partition of n_sample rows
+ * (n_sample <= 0: 200 * k_sample) and bandwidth k_sample, CUDA-event timed. */
+spk_status spk_calibrate_k(int64_t n_sample, int32_t k_sample, int32_t reps, void *stream,
+                           spk_calibration *out);
+/* default_k_cache_path (copied into buf, NUL-terminated): $SPIKE_K_CACHE or
+ * "spike_k.cache"; write/read_k_cache in the reference's "K <value>" format.
+ * spk_read_k_cache sets *found = 0 when the file or the key is missing. */
+spk_status spk_default_k_cache_path(char *buf, int32_t cap);
+spk_status spk_write_k_cache(const char *path, double k);
+spk_status spk_read_k_cache(const char *path, double *k, int32_t *found);
+/* spk_gpu_plan with explicit first/last partitions r13 x the inner size
+ * (the reference's R13, partition.cpp:47-54; r12 has no GPU counterpart:
+ * dual partitions factor like single ones). */
+spk_status spk_gpu_plan_ratio(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t pivoting,
+                              int32_t p_hint, double r13, int32_t cap, int32_t *p, int64_t *bounds,
+                              int32_t *kinds);
+
 /* ---- factorization ----
  * Stream-ordered: returns once the factorization is enqueued on `stream` (a
  * host band is uploaded first).  Its host-side completion -- the exactly

@@ -2021,6 +2021,122 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
     });
 }
 
+spk_status spk_gpu_plan_ratio(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t pivoting, int32_t p_hint,
+                              double r13, int32_t cap, int32_t* p, int64_t* bounds, int32_t* kinds) {
+    return guarded([&] {
+        if (!(r13 > 0.0)) fail(SPK_EDOMAIN, "gpu_plan_ratio: r13 must be positive");
+        spk_status st = spk_gpu_plan(n, kl, ku, nrhs, pivoting, p_hint, cap, p, bounds, kinds);
+        if (st != SPK_OK) fail(st, g_err.c_str());
+        const int pp = *p;
+        if (pp < 3) return;  // both partitions first/last: equal halves (as compute_sizes)
+        // first/last = r13 * inner (compute_sizes, partition.cpp:47-76, without dual partitions)
+        const int k = std::max(kl, ku);
+        const long long min_part = std::max<long long>(2LL * k + 1, 1);
+        const double inner = (double)n / (pp - 2 + 2.0 * r13);
+        const long long fl = std::max<long long>(std::llround(r13 * inner), min_part);
+        const long long rest = n - 2 * fl, ni = pp - 2;
+        if (rest < ni * min_part) fail(SPK_EDOMAIN, "gpu_plan_ratio: partition too small");
+        const long long base = rest / ni, extra = rest % ni;
+        bounds[0] = 0;
+        bounds[1] = fl;
+        for (int i = 1; i < pp - 1; ++i) bounds[i + 1] = bounds[i] + base + (i - 1 < extra ? 1 : 0);
+        bounds[pp] = n;
+        for (int i = 0; i < pp; ++i)
+            if (bounds[i + 1] - bounds[i] < min_part) fail(SPK_EDOMAIN, "gpu_plan_ratio: partition too small");
+    });
+}
+
+spk_status spk_default_k_cache_path(char* buf, int32_t cap) {
+    return guarded([&] {
+        const char* env = getenv("SPIKE_K_CACHE");
+        const std::string path = env ? env : "spike_k.cache";  // partition.cpp:149-152
+        if ((int)path.size() + 1 > cap) fail(SPK_EINVAL, "k_cache_path: buffer too small");
+        std::memcpy(buf, path.c_str(), path.size() + 1);
+    });
+}
+
+spk_status spk_write_k_cache(const char* path, double k) {
+    return guarded([&] {
+        FILE* fp = fopen(path, "w");
+        if (!fp) fail(SPK_EIO, std::string("cannot write calibration cache ") + path);
+        fprintf(fp, "K %.17g\n", k);  // os.precision(17); os << "K " << k (partition.cpp:154-159)
+        fclose(fp);
+    });
+}
+
+spk_status spk_read_k_cache(const char* path, double* k, int32_t* found) {
+    return guarded([&] {
+        *found = 0;
+        FILE* fp = fopen(path, "r");
+        if (!fp) return;
+        char key[256];
+        double v = 0.0;
+        while (fscanf(fp, "%255s %lf", key, &v) == 2)  // partition.cpp:161-169: first "K" wins
+            if (std::strcmp(key, "K") == 0) {
+                *k = v;
+                *found = 1;
+                break;
+            }
+        fclose(fp);
+    });
+}
+
+spk_status spk_calibrate_k(int64_t n_sample, int32_t k_sample, int32_t reps, void* stream, spk_calibration* out) {
+    return guarded([&] {
+        if (k_sample < 1) fail(SPK_EINVAL, "calibrate_k: k_sample must be >= 1");
+        if (n_sample <= 0) n_sample = 200LL * k_sample;
+        if (k_sample >= n_sample) fail(SPK_EINVAL, "calibrate_k: k_sample must be < n_sample");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const long long n = n_sample, ld = 2LL * k_sample + 1;
+        double* band = dalloc<double>((size_t)(ld * n), s);
+        double* F = dalloc<double>((size_t)(n * k_sample), s);
+        double* X = dalloc<double>((size_t)(n * k_sample), s);
+        launch_generate_band(1234, n, k_sample, k_sample, 1.5, 0, n, band, s);
+        launch_generate_rhs(5678, 0, n, k_sample, F, n, s);
+        ck(cudaGetLastError(), "calibrate_k");
+        // one partition: the serial LU and two-sweep solve of partition.cpp:131-135
+        int64_t bnds[2] = {0, n};
+        int32_t kind = SPK_FIRSTLAST;
+        spk_plan plan{1, bnds, &kind};
+        spk_factor_options opts{0, 0.0};
+        cudaEvent_t e[3];
+        for (auto& x : e) ck(cudaEventCreate(&x), "event");
+        std::vector<double> ratios;
+        double tf_total = 0.0, ts_total = 0.0;
+        const int R = std::max(reps, 1);
+        for (int rep = 0; rep < R + 1; ++rep) {  // rep 0 warms up (symbolic cache, arena)
+            spk_fact* f = nullptr;
+            ck(cudaEventRecord(e[0], s), "event");
+            spk_status st = spk_factorize(band, SPK_MEM_DEVICE, n, k_sample, k_sample, &plan, &opts, s, &f);
+            if (st != SPK_OK) fail(st, g_err.c_str());
+            ck(cudaEventRecord(e[1], s), "event");
+            st = spk_solve(f, 0, F, n, k_sample, X, n, SPK_MEM_DEVICE, s, nullptr);
+            if (st != SPK_OK) {
+                spk_fact_destroy(f);
+                fail(st, g_err.c_str());
+            }
+            ck(cudaEventRecord(e[2], s), "event");
+            ck(cudaEventSynchronize(e[2]), "calibrate_k");
+            spk_fact_destroy(f);
+            if (rep == 0) continue;
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, e[0], e[1]);
+            cudaEventElapsedTime(&b, e[1], e[2]);
+            const double tf = a * 1e-3, ts = b * 1e-3;
+            tf_total += tf;
+            ts_total += ts;
+            ratios.push_back(ts / std::max(tf, 1e-12));
+        }
+        for (auto& x : e) cudaEventDestroy(x);
+        for (double* q : {band, F, X}) dfree(q, s);
+        std::sort(ratios.begin(), ratios.end());
+        out->k = ratios[ratios.size() / 2];
+        out->factor_seconds = tf_total / R;
+        out->solve_seconds = ts_total / R;
+        out->timer_warning = (tf_total + ts_total) < 0.010;
+    });
+}
+
 static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n, int32_t kl, int32_t ku,
                                  const spk_plan* plan, const spk_factor_options* opts, int open_l, int open_r,
                                  void* stream, spk_fact** out) {

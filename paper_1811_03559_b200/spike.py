@@ -130,6 +130,17 @@ def lib():
         L.spk_refine.restype = C.c_int32
         L.spk_condest_1norm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double)]
         L.spk_condest_1norm.restype = C.c_int32
+        L.spk_gpu_plan_ratio.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_double, C.c_int32, _i32p, _i64p, _i32p]
+        L.spk_gpu_plan_ratio.restype = C.c_int32
+        L.spk_calibrate_k.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(_CalibC)]
+        L.spk_calibrate_k.restype = C.c_int32
+        L.spk_default_k_cache_path.argtypes = [C.c_char_p, C.c_int32]
+        L.spk_default_k_cache_path.restype = C.c_int32
+        L.spk_write_k_cache.argtypes = [C.c_char_p, C.c_double]
+        L.spk_write_k_cache.restype = C.c_int32
+        L.spk_read_k_cache.argtypes = [C.c_char_p, C.POINTER(C.c_double), _i32p]
+        L.spk_read_k_cache.restype = C.c_int32
         L.spk_spkb_header.argtypes = [C.c_char_p, _i64p, _i32p, _i32p]
         L.spk_spkb_header.restype = C.c_int32
         L.spk_spkb_load.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]
@@ -348,16 +359,62 @@ def make_plan(n: int, kl: int, ku: int, t: int, r12: float, r13: float) -> Parti
                          threads_used=tu.value, idle_threads=idle.value, r12=r12, r13=r13)
 
 
-def gpu_plan(n: int, kl: int, ku: int, nrhs: int = 1, pivoting: bool = False, p: int = 0) -> PartitionPlan:
-    """B200 planner: any p >= 1 (not only powers of two), partitions mapped onto SMs."""
+def gpu_plan(n: int, kl: int, ku: int, nrhs: int = 1, pivoting: bool = False, p: int = 0,
+             r13: Optional[float] = None) -> PartitionPlan:
+    """B200 planner: any p >= 1 (not only powers of two), partitions mapped onto SMs;
+    equal partitions, or first/last = r13 x inner (the reference's R13) when given."""
     cap = max(4096, 2 * p + 2)
     pp = C.c_int32()
     bounds = (C.c_int64 * (cap + 1))()
     kinds = (C.c_int32 * cap)()
-    _check(lib().spk_gpu_plan(n, kl, ku, nrhs, int(pivoting), p, cap, C.byref(pp), bounds, kinds))
+    if r13 is None:
+        _check(lib().spk_gpu_plan(n, kl, ku, nrhs, int(pivoting), p, cap, C.byref(pp), bounds, kinds))
+    else:
+        _check(lib().spk_gpu_plan_ratio(n, kl, ku, nrhs, int(pivoting), p, float(r13), cap, C.byref(pp), bounds,
+                                        kinds))
     return PartitionPlan(p=pp.value, bounds=list(bounds[:pp.value + 1]),
                          kinds=[PartitionKind(kinds[i]) for i in range(pp.value)],
                          threads_used=pp.value, idle_threads=0)
+
+
+# ----------------------------------------------------------------------------
+# K calibration (partition.hpp:58-74, partition.cpp:120-170) on the GPU
+
+
+class _CalibC(C.Structure):
+    _fields_ = [("k", C.c_double), ("factor_seconds", C.c_double), ("solve_seconds", C.c_double),
+                ("timer_warning", C.c_int32)]
+
+
+@dataclass
+class CalibrationResult:
+    k: float = 1.0
+    factor_seconds: float = 0.0
+    solve_seconds: float = 0.0
+    timer_warning: bool = False
+
+
+def calibrate_k(n_sample: int = 0, k_sample: int = 16, reps: int = 5, stream: int = 0) -> CalibrationResult:
+    """K = median t_solve(nrhs = k) / t_factor of one partition, timed on the GPU."""
+    out = _CalibC()
+    _check(lib().spk_calibrate_k(n_sample, k_sample, reps, stream, C.byref(out)))
+    return CalibrationResult(out.k, out.factor_seconds, out.solve_seconds, bool(out.timer_warning))
+
+
+def default_k_cache_path() -> str:
+    buf = C.create_string_buffer(4096)
+    _check(lib().spk_default_k_cache_path(buf, 4096))
+    return os.fsdecode(buf.value)
+
+
+def write_k_cache(path, k: float) -> None:
+    _check(lib().spk_write_k_cache(os.fsencode(path), float(k)))
+
+
+def read_k_cache(path) -> Optional[float]:
+    v, found = C.c_double(), C.c_int32()
+    _check(lib().spk_read_k_cache(os.fsencode(path), C.byref(v), C.byref(found)))
+    return float(v.value) if found.value else None
 
 
 # ----------------------------------------------------------------------------
