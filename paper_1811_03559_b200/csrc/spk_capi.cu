@@ -1503,7 +1503,7 @@ struct Exec {
                                           f.d_pool, f.d_fac, f.d_piv, f.d_amax, f.d_flags, s);
                     break;
                 case ST_WCHECK:
-                    launch_wcheck((const CouplingJob*)jobs, st.njobs, f.d_pool, f.d_flags, s);
+                    launch_wcheck((const CouplingJob*)jobs, st.njobs, f.k, f.d_pool, f.d_flags, s);
                     break;
                 case ST_SCHUR_INIT:
                     launch_schur_init((const CouplingJob*)jobs, st.njobs, st.max_elems, f.d_parts, f.d_fac,

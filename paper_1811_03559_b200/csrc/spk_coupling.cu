@@ -20,26 +20,31 @@
 #include "spk_device.cuh"
 #include "spk_launch.h"
 
+#include <algorithm>
 #include <cfloat>
 
 namespace spk {
 
-// flag[g] = (max |W| <= 1) for the top k x k tip of wr (h x k, ld h)
-__global__ void k_wcheck(const CouplingJob* __restrict__ jobs, const double* __restrict__ pool,
-                         int* __restrict__ flags) {
+// flag[g] = (max |W| <= 1) for the top k x k tip of wr (h x k, ld h).  The
+// pair's k columns are split over gridDim.y CTAs (warp per column, lanes over
+// rows); flags were set to 1 by k_wcheck_init, and any CTA seeing |w| > 1
+// writes 0 (idempotent: deterministic).
+__global__ void k_wcheck_init(const CouplingJob* __restrict__ jobs, int njobs, int* __restrict__ flags) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < njobs) flags[jobs[a].guard] = 1;
+}
+
+__global__ void __launch_bounds__(256) k_wcheck(const CouplingJob* __restrict__ jobs,
+                                                const double* __restrict__ pool, int* __restrict__ flags) {
     const CouplingJob J = jobs[blockIdx.x];
     const int k = J.k;
-    __shared__ int bad;
-    if (threadIdx.x == 0) bad = 0;
-    __syncthreads();
-    int mybad = 0;
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-        const int c = e / k, r = e - c * k;
-        if (fabs(pool[J.wr_off + (long long)c * J.hR + r]) > 1.0) mybad = 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    int bad = 0;
+    for (int c = blockIdx.y * W + warp; c < k; c += gridDim.y * W) {
+        const double* col = pool + J.wr_off + (long long)c * J.hR;
+        for (int r = lane; r < k; r += 32) bad |= fabs(col[r]) > 1.0;
     }
-    if (mybad) atomicOr(&bad, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) flags[J.guard] = bad ? 0 : 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) flags[J.guard] = 0;
 }
 
 // S unit storage (dense k x k as a full band: rows 2k-1, diagonal row k-1) := I
@@ -303,9 +308,12 @@ bool launch_schur_inverse(const CouplingJob* d_jobs, int njobs, int n, const Par
     return false;
 }
 
-void launch_wcheck(const CouplingJob* d_jobs, int njobs, const double* pool, int* flags, cudaStream_t s) {
+void launch_wcheck(const CouplingJob* d_jobs, int njobs, int k, const double* pool, int* flags, cudaStream_t s) {
     if (njobs <= 0) return;
-    k_wcheck<<<njobs, 256, 0, s>>>(d_jobs, pool, flags);
+    k_wcheck_init<<<(njobs + 127) / 128, 128, 0, s>>>(d_jobs, njobs, flags);
+    count_launch();
+    const int ycta = std::max(1, std::min((k + 7) / 8, 16));  // <= 8 columns per CTA
+    k_wcheck<<<dim3(njobs, ycta), 256, 0, s>>>(d_jobs, pool, flags);
     count_launch();
 }
 

@@ -54,7 +54,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Split-K (ws != nullptr): blockIdx.z takes K range [z*ks, (z+1)*ks) and writes
 // its partial tile to ws[((job * tiles + tile) * nsplit + z) * TM*TN]; the
 // reduction kernel sums the splits in order (deterministic, no atomics).
-__global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
+__global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
                                                    double* __restrict__ ws, int nsplit, int tiles_max) {
     const GemmJob& Jg = jobs[blockIdx.x];
     if (!guard_ok(B.flags, Jg.guard)) return;
@@ -144,56 +144,74 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(const GemmJob* __restrict__ j
         __syncthreads();
     }
     if (ws) {
-        double* part = ws + (((size_t)blockIdx.x * tiles_max + blockIdx.y) * nsplit + blockIdx.z) * (TM * TN);
+        // split-K: every split stores its partial tile; the last split to
+        // arrive (per-tile counter) sums them in split order -- deterministic --
+        // and applies the epilogue, then re-arms the counter
+        const size_t tile_id = (size_t)blockIdx.x * tiles_max + blockIdx.y;
+        double* tile = ws + tile_id * nsplit * (TM * TN);
+        double* part = tile + (size_t)blockIdx.z * (TM * TN);
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b)
                 *reinterpret_cast<double2*>(part + (wm + 8 * a + g) * TN + wn + 8 * b + 2 * q) =
                     make_double2(acc[a][b][0], acc[a][b][1]);
-        return;
-    }
-    // epilogue: C[row, col] with row = wm+8a+g, col = wn+8b+2q+{0,1}
+        __threadfence();
+        __syncthreads();
+        __shared__ int s_last;
+        if (tid == 0) {
+            int* cnt = reinterpret_cast<int*>(ws + (size_t)gridDim.x * tiles_max * nsplit * (TM * TN)) + tile_id;
+            s_last = atomicAdd(cnt, 1) == nsplit - 1;
+            if (s_last) *cnt = 0;
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // this thread's fragment positions again, summed over the splits in
+        // order (all 32 loads of a split in flight), then the epilogue below
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int i = row0 + wm + 8 * a + g;
-        if (i >= jr) continue;
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int z = 0; z < nsplit; ++z) {
+            const double* pz = tile + (size_t)z * (TM * TN);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const double2 v = __ldcg(reinterpret_cast<const double2*>(pz + (wm + 8 * a + g) * TN + wn + 8 * b + 2 * q));
+                    acc[a][b][0] += v.x;
+                    acc[a][b][1] += v.y;
+                }
+        }
+    }
+    // epilogue: C[row, col] with row = wm+8a+g, col = wn+8b+2q+{0,1}.  All of
+    // C's old values are loaded before the first store: interleaved
+    // load-subtract-store through computed pointers would serialise on
+    // possible aliasing, one memory latency per element.
+    // element (i0 + 8a, c0 + 8b + e) of C sits at P0 + 8a*sr + (8b+e)*ld
+    const int i0 = row0 + wm + g, c0 = col0 + wn + 2 * q;
+    const long long ld = vc.ld;
+    const int sr = vc.rev ? -1 : 1;
+    double* const P0 = vc.p + (vc.rev ? (vc.mrows - 1 - (crow0 + i0 - vc.off)) : (crow0 + i0 - vc.off)) +
+                       (long long)c0 * ld;
+    if (op != GM_SET) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (i0 + 8 * a < jr && c0 + 8 * b + e < nc)
+                        acc[a][b][e] = P0[8 * a * sr + (8 * b + e) * ld] - acc[a][b][e];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int c = col0 + wn + 8 * b + 2 * q + e;
-                if (c >= nc) continue;
-                double* dst = vc.at(crow0 + i, c);
-                if (op == GM_SET) *dst = acc[a][b][e];
-                else *dst -= acc[a][b][e];
-            }
-    }
-}
-
-// split-K reduction: C (=|-=) sum_z ws[..z..] for each job tile, in split order
-__global__ void __launch_bounds__(256) k_gemm_splitk_reduce(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
-                                                            const double* __restrict__ ws, int nsplit,
-                                                            int tiles_max) {
-    const GemmJob& Jg = jobs[blockIdx.x];
-    if (!guard_ok(B.flags, Jg.guard)) return;
-    const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
-    const int jr = Jg.r;
-    const int tiles_r = (jr + TM - 1) / TM;
-    const int tr = blockIdx.y % tiles_r, tc = blockIdx.y / tiles_r;
-    if (tc * TN >= nc || jr <= 0) return;
-    const RV vc = resolve(B, Jg.c);
-    const double* part = ws + ((size_t)blockIdx.x * tiles_max + blockIdx.y) * nsplit * (TM * TN);
-    for (int e = threadIdx.x; e < TM * TN; e += blockDim.x) {
-        const int i = tr * TM + (e & (TM - 1)), c = tc * TN + (e / TM);
-        if (i >= jr || c >= nc) continue;
-        const int loc = (e & (TM - 1)) * TN + e / TM;
-        double sum = 0.0;
-        for (int z = 0; z < nsplit; ++z) sum += part[(size_t)z * (TM * TN) + loc];
-        double* dst = vc.at(Jg.crow0 + i, c);
-        if (Jg.op == GM_SET) *dst = sum;
-        else *dst -= sum;
-    }
+            for (int e = 0; e < 2; ++e)
+                if (i0 + 8 * a < jr && c0 + 8 * b + e < nc) P0[8 * a * sr + (8 * b + e) * ld] = acc[a][b][e];
 }
 
 int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk) {
@@ -206,9 +224,10 @@ int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk) {
     return std::max(1, std::min(ns, 64));
 }
 
+// doubles: partial tiles, then one int counter per output tile
 size_t gemm_splitk_workspace(int njobs, int max_r, int max_nc, int nsplit) {
     const size_t tiles = (size_t)((max_r + TM - 1) / TM) * ((max_nc + TN - 1) / TN);
-    return (size_t)njobs * tiles * nsplit * TM * TN;
+    return (size_t)njobs * tiles * nsplit * TM * TN + ((size_t)njobs * tiles + 1) / 2;
 }
 
 void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
@@ -216,11 +235,11 @@ void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, c
     if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
     const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
     if (ws && nsplit > 1) {
+        const size_t tiles = (size_t)njobs * tr * tc;
+        cudaMemsetAsync(ws + tiles * nsplit * TM * TN, 0, sizeof(int) * tiles, s);  // split counters
         dim3 g(njobs, tr * tc, nsplit);
         k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
-        dim3 gr(njobs, tr * tc);
-        k_gemm_splitk_reduce<<<gr, 256, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
-        count_launch(2);
+        count_launch();
         return;
     }
     dim3 g(njobs, tr * tc);

@@ -42,7 +42,7 @@ void launch_corners(const double* band, long long n, int akl, int aku, const lon
 void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_elems,
                            const PartDev* d_parts, const double* pool, double* fac, int* piv,
                            unsigned long long* amax, const int* flags, cudaStream_t s);
-void launch_wcheck(const CouplingJob* d_jobs, int njobs, const double* pool, int* flags, cudaStream_t s);
+void launch_wcheck(const CouplingJob* d_jobs, int njobs, int k, const double* pool, int* flags, cudaStream_t s);
 void launch_schur_init(const CouplingJob* d_jobs, int njobs, long long max_elems, const PartDev* d_parts,
                        double* fac, int* piv, const int* flags, cudaStream_t s);
 bool launch_schur_inverse(const CouplingJob* d_jobs, int njobs, int n, const PartDev* d_parts, const double* fac,
