@@ -21,6 +21,8 @@
 #include <memory>
 #include <stdexcept>
 #include <utility>
+#include <optional>
+#include <string>
 #include <vector>
 
 namespace spike {
@@ -223,5 +225,29 @@ double relative_residual(const BandedMatrix& a, const DenseBlock& x, const Dense
 double frobenius_norm(const DenseBlock& b);
 double norm1(const BandedMatrix& a);
 double max_abs(const BandedMatrix& a);
+// Hager's kappa_1 estimate (oracle.hpp condition_estimate_1norm) computed with
+// the factorization's GPU solves instead of a serial banded GE
+double condition_estimate_1norm(const SpikeFactorization& fact, const BandedMatrix& a);
+
+// ---------------------------------------------------------------- band_io.hpp
+// .spkb binary files (band_io.cpp:98-143); MatrixMarket text is not supported
+// by the GPU library and throws std::runtime_error.
+enum class MatrixFormat { MatrixMarket, Spkb };
+void write_matrix(const BandedMatrix& a, const std::string& path, MatrixFormat fmt);
+BandedMatrix read_matrix(const std::string& path, std::optional<int> expected_kl = std::nullopt,
+                         std::optional<int> expected_ku = std::nullopt);
+
+// ---------------------------------------------------------------- K calibration (partition.hpp:58-74)
+struct CalibrationResult {
+    double k = 1.0;
+    double factor_seconds = 0.0;
+    double solve_seconds = 0.0;
+    bool timer_warning = false;
+};
+// timed on the GPU: one partition's factorization and its two-sweep solve
+CalibrationResult calibrate_k(int n_sample, int k_sample, int reps = 5);
+std::string default_k_cache_path();
+void write_k_cache(const std::string& path, double k);
+std::optional<double> read_k_cache(const std::string& path);
 
 }  // namespace spike

@@ -368,32 +368,65 @@ double max_abs(const BandedMatrix& a) {
     return best;
 }
 
+// solve.cpp:404-432, the loop on the device (spk_refine): residual on the
+// tensor cores, correction solves, only ||r||_F / ||F||_F per iteration to the host
 RefineResult iterative_refine(const SpikeFactorization& fact, const BandedMatrix& a, const DenseBlock& f,
                               const DenseBlock& x0, int max_iters, double tol, bool transpose) {
+    if (f.rows != a.n() || x0.rows != f.rows || x0.cols != f.cols)
+        throw std::invalid_argument("iterative_refine: F.rows must equal n");
     RefineResult res;
     res.x = x0;
-    const double fnorm = frobenius_norm(f);
-    double prev = std::numeric_limits<double>::infinity();
-    for (int it = 0; it <= max_iters; ++it) {
-        DenseBlock r = band_matmul(a, res.x, transpose);
-        for (std::size_t i = 0; i < r.data.size(); ++i) r.data[i] = f.data[i] - r.data[i];
-        const double rn = frobenius_norm(r);
-        res.residual = fnorm == 0.0 ? (rn == 0.0 ? 0.0 : std::numeric_limits<double>::infinity()) : rn / fnorm;
-        res.iterations = it;
-        if (res.residual <= tol) {
-            res.converged = true;
-            return res;
-        }
-        if (it > 0 && res.residual * 1.1 > prev) {
-            res.stagnated = true;
-            return res;
-        }
-        if (it == max_iters) return res;
-        prev = res.residual;
-        DenseBlock d = transpose ? transpose_solve(fact, r) : solve(fact, r);
-        for (std::size_t i = 0; i < res.x.data.size(); ++i) res.x.data[i] += d.data[i];
-    }
+    spk_refine_result r{};
+    check(spk_refine(static_cast<spk_fact*>(fact.handle.get()), a.data().data(), f.data.data(), f.rows, f.cols, res.x.data.data(), res.x.rows,
+                     transpose ? 1 : 0, max_iters, tol, SPK_MEM_HOST, nullptr, &r));
+    res.iterations = r.iterations;
+    res.residual = r.residual;
+    res.converged = r.converged != 0;
+    res.stagnated = r.stagnated != 0;
     return res;
+}
+
+double condition_estimate_1norm(const SpikeFactorization& fact, const BandedMatrix& a) {
+    double c = 0.0;
+    check(spk_condest_1norm(static_cast<spk_fact*>(fact.handle.get()), a.data().data(), SPK_MEM_HOST, nullptr, &c));
+    return c;
+}
+
+void write_matrix(const BandedMatrix& a, const std::string& path, MatrixFormat fmt) {
+    if (fmt != MatrixFormat::Spkb) throw std::runtime_error("write_matrix: only the SPKB format is supported");
+    check(spk_spkb_store(path.c_str(), a.data().data(), a.n(), a.kl(), a.ku(), SPK_MEM_HOST, nullptr));
+}
+
+BandedMatrix read_matrix(const std::string& path, std::optional<int> expected_kl, std::optional<int> expected_ku) {
+    int64_t n = 0;
+    int32_t kl = 0, ku = 0;
+    check(spk_spkb_header(path.c_str(), &n, &kl, &ku));
+    if ((expected_kl && *expected_kl != kl) || (expected_ku && *expected_ku != ku))
+        throw std::runtime_error("SPKB bandwidths differ from the expected ones");
+    BandedMatrix a(static_cast<int>(n), kl, ku);
+    check(spk_spkb_load(path.c_str(), 0, n, a.data().data(), SPK_MEM_HOST, nullptr));
+    return a;
+}
+
+CalibrationResult calibrate_k(int n_sample, int k_sample, int reps) {
+    spk_calibration c{};
+    check(spk_calibrate_k(n_sample, k_sample, reps, nullptr, &c));
+    return CalibrationResult{c.k, c.factor_seconds, c.solve_seconds, c.timer_warning != 0};
+}
+
+std::string default_k_cache_path() {
+    char buf[4096];
+    check(spk_default_k_cache_path(buf, sizeof buf));
+    return buf;
+}
+
+void write_k_cache(const std::string& path, double k) { check(spk_write_k_cache(path.c_str(), k)); }
+
+std::optional<double> read_k_cache(const std::string& path) {
+    double k = 0.0;
+    int32_t found = 0;
+    check(spk_read_k_cache(path.c_str(), &k, &found));
+    return found ? std::optional<double>(k) : std::nullopt;
 }
 
 }  // namespace spike

@@ -2,6 +2,7 @@
 // library: same calls and checks as the reference suites
 // (proj/tests/test_solve_stage.cpp, test_factor_ds.cpp), written here as a
 // plain main() (the reference's doctest header is not vendored).
+#include "spike/band_io.hpp"
 #include "spike/factorize.hpp"
 #include "spike/partition.hpp"
 #include "spike/solve.hpp"
@@ -10,6 +11,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 using namespace spike;
@@ -166,6 +168,36 @@ int main() {
         RefineResult r = iterative_refine(fact, a, f, DenseBlock(n, 2), 5, 1e-12);
         CHECK(r.converged);
         CHECK(relative_residual(a, r.x, f) <= 1e-12);
+    }
+    {  // band_io.hpp: .spkb round trip through the reference's write_matrix / read_matrix
+        const int n = 300, kl = 3, ku = 5;
+        BandedMatrix a = make_dd(n, kl, ku, 1.5, 123);
+        const std::string path = "dropin_tmp.spkb";
+        write_matrix(a, path, MatrixFormat::Spkb);
+        BandedMatrix b = read_matrix(path);
+        CHECK(b.n() == n && b.kl() == kl && b.ku() == ku && b.data() == a.data());
+        bool threw = false;
+        try {
+            read_matrix(path, 4, 5);
+        } catch (const std::runtime_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+        std::remove(path.c_str());
+    }
+    {  // partition.hpp calibration and its cache; oracle.hpp condition estimate
+        CalibrationResult c = calibrate_k(20000, 8, 3);
+        CHECK(c.k > 0.0 && c.factor_seconds > 0.0 && c.solve_seconds > 0.0);
+        const std::string path = "dropin_k.cache";
+        write_k_cache(path, c.k);
+        CHECK(read_k_cache(path).value_or(-1.0) == c.k);
+        std::remove(path.c_str());
+        CHECK(!read_k_cache("no_such_k.cache").has_value());
+        const int n = 400, k = 3;
+        BandedMatrix a = make_dd(n, k, k, 1.2, 131);
+        SpikeFactorization fact = factorize(a, gpu_plan(n, k, k, 1, false, 4));
+        const double cond = condition_estimate_1norm(fact, a);
+        CHECK(cond >= 1.0 && std::isfinite(cond));
     }
     std::printf(failures ? "DROPIN FAIL %d\n" : "DROPIN PASS\n", failures);
     return failures ? 1 : 0;
