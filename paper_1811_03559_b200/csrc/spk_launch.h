@@ -76,6 +76,18 @@ bool launch_sweep_fast_blt(int tr, int nc, bool piv, int nwarps, dim3 grid, size
                            cudaStream_t s);
 struct FastLuArgs;
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s);
+// blocked pivoted band LU on the tensor cores (spk_lu_piv_dmma.cu); false
+// when the band is wider than its tile windows (kl+ku > 192)
+struct PivDmmaArgs {
+    const int* units;
+    const PartDev* parts;
+    const double* band;
+    int akl, aku;
+    double* fac;
+    int* piv;
+    int* status;
+};
+bool launch_band_lu_piv_dmma(int nunits, int kl, int ku, const PivDmmaArgs& A, cudaStream_t s);
 struct PivLuArgs;
 bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
