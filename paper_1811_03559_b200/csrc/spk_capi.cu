@@ -1477,10 +1477,13 @@ struct Exec {
                         }
                         static const bool piv_old = getenv("SPK_LU_PIV_OLD") && atoi(getenv("SPK_LU_PIV_OLD"));
                         if (f.piv_on && !generic_only && !piv_old) {
-                            // pivoted: blocked DMMA kernel (factor + pivots; the transpose
-                            // stage then builds the row-major copy and 1/u_jj)
-                            PivDmmaArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac, f.d_piv, f.d_status};
-                            if (launch_band_lu_piv_dmma(st.njobs, f.kl, f.ku, A, s)) break;
+                            // pivoted: blocked DMMA kernel (factor, pivots, row-major copy, 1/u_jj)
+                            PivDmmaArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac,
+                                          f.d_tfac, f.d_dinv, f.d_piv, f.d_status};
+                            if (launch_band_lu_piv_dmma(st.njobs, f.kl, f.ku, A, s)) {
+                                lu_fast_done = true;  // it writes the row-major copy and 1/u_jj too
+                                break;
+                            }
                         }
                         if (f.piv_on && !generic_only) {
                             // pivoted: shared-memory window kernel (factor + pivots; the

@@ -84,6 +84,8 @@ struct PivDmmaArgs {
     const double* band;
     int akl, aku;
     double* fac;
+    double* tfac;  // row-major copy (row i: (i, i-kl .. i+ubw) at [kl + c - i])
+    double* dinv;  // 1 / u_jj
     int* piv;
     int* status;
 };

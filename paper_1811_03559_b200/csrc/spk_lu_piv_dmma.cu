@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
     const unsigned full = 0xffffffffu;
     const int ald = A.akl + A.aku + 1;
     double* F = A.fac + P.fofs;
+    double* TF = A.tfac + P.tofs;
+    const int rowsT = P.rowsT;
     int* piv = A.piv + P.r0;
     const int nblk = (m + 7) / 8;
     const double* bbase = A.band + (P.rev ? (long long)(P.r0 + m - 1) * ald + A.aku : (long long)P.r0 * ald + A.aku);
@@ -114,10 +116,15 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         return i == c ? 1.0 : 0.0;
     };
 
-    // packed positions above row 0 that no step writes read as zero
+    // packed positions above row 0 (and row-major positions left of column 0)
+    // that no step writes read as zero
     for (int idx = threadIdx.x; idx < ubw * ubw; idx += blockDim.x) {
         const int c = idx / ubw, off = idx - c * ubw + 1;
         if (c < m && off > c) F[(long long)c * rows + d - off] = 0.0;
+    }
+    for (int idx = threadIdx.x; idx < kl * kl; idx += blockDim.x) {
+        const int r = idx / kl, off = idx - r * kl + 1;
+        if (r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
     }
 
     double acc[TRW][2];
@@ -321,7 +328,10 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int cc = 8 * (J + co) + 2 * q + e, off = cc - i;
-                if (cc < m && i < m && off <= ubw) F[(long long)cc * rows + d - off] = acc[0][e];
+                if (i < m && off <= ubw) {
+                    if (cc < m) F[(long long)cc * rows + d - off] = acc[0][e];
+                    TF[(long long)i * rowsT + kl + off] = cc < m ? acc[0][e] : 0.0;
+                }
             }
         }
         // U12 as B fragments: B[k][n] = U12[k][n] sits in lane k*4 + n/2, register n&1
@@ -382,9 +392,22 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
                     F[(long long)(j0 + c) * rows + d + off] = j0 + c + off < m ? S.lbuf[par][c][off] : 0.0;
             for (int e = lane; e < 64; e += 32) {
                 const int r = e >> 3, t = e & 7;
-                if (t >= r && t - r <= ubw && j0 + t < m) F[(long long)(j0 + t) * rows + d - (t - r)] = S.d11[par][e];
+                if (t >= r && t - r <= ubw && j0 + r < m) {
+                    const double v = j0 + t < m ? S.d11[par][e] : 0.0;
+                    if (j0 + t < m) F[(long long)(j0 + t) * rows + d - (t - r)] = v;
+                    TF[(long long)(j0 + r) * rowsT + kl + t - r] = v;
+                }
             }
-            if (lane < 8 && j0 + lane < m) piv[j0 + lane] = j0 + S.spiv[par][lane];
+            // row-major L: row j0+r takes columns j0+cc, cc < r, within kl (one run)
+            for (int r = 1 + lane; r < 8 + kl && j0 + r < m; r += 32) {
+                double* dst = TF + (long long)(j0 + r) * rowsT + kl - r;
+                const int c0 = max(0, r - kl), c1 = min(7, r - 1);
+                for (int cc = c0; cc <= c1; ++cc) dst[cc] = S.lbuf[par][cc][r - cc];
+            }
+            if (lane < 8 && j0 + lane < m) {
+                piv[j0 + lane] = j0 + S.spiv[par][lane];
+                A.dinv[P.r0 + j0 + lane] = 1.0 / S.d11[par][lane * 9];
+            }
         } else {
             update(J, co, tprev);
             if (co == 1) PIV_MARK(1);

@@ -42,18 +42,21 @@ int main(int argc, char** argv) {
         P.rows = rows;
         P.fofs = (long long)i * m * rows;
         P.bofs = -1;
-        P.tofs = -1;
+        P.tofs = (long long)i * m * (k + ubw + 1);
+        P.rowsT = k + ubw + 1;
         P.guard = -1;
         P.pivoting = 1;
         parts[i] = P;
         units[i] = i;
     }
-    double *dband, *dfac;
+    double *dband, *dfac, *dtfac, *ddinv;
     int *dpiv, *dstatus, *dunits;
     spk::PartDev* dparts;
     cudaMalloc(&dband, band.size() * 8);
     cudaMalloc(&dfac, (size_t)n * rows * 8);
     cudaMalloc(&dpiv, n * 4);
+    cudaMalloc(&dtfac, (size_t)n * (k + ubw + 1) * 8);
+    cudaMalloc(&ddinv, n * 8);
     cudaMalloc(&dstatus, 4);
     cudaMalloc(&dunits, nparts * 4);
     cudaMalloc(&dparts, nparts * sizeof(spk::PartDev));
@@ -61,7 +64,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(dunits, units.data(), nparts * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dparts, parts.data(), nparts * sizeof(spk::PartDev), cudaMemcpyHostToDevice);
     cudaMemset(dstatus, 0, 4);
-    spk::PivDmmaArgs A{dunits, dparts, dband, k, k, dfac, dpiv, dstatus};
+    spk::PivDmmaArgs A{dunits, dparts, dband, k, k, dfac, dtfac, ddinv, dpiv, dstatus};
     for (int rep = 0; rep < 3; ++rep) {
         unsigned long long z[8] = {0};
         cudaMemcpyToSymbol(spk::g_piv_prof, z, sizeof(z));
