@@ -140,10 +140,11 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
     // columns 8Jn ..) and the column block the panel warp of step Jn+1 takes
     // after its panel (block Jn+1+TCW, rows 8(Jn+2) ..).  Out-of-band slots
     // are stored as zeros, past-m slots as the identity; band values by cp.async.
-    auto stage = [&](int Jn) {
+    // (issued by the TCW-1 warps off the critical path: rank 0 .. TCW-2)
+    auto stage = [&](int Jn, int rank) {
         const int b = Jn & 1;
         constexpr int NR = 8 * 8 * TCW, NC = 8 * TRW * 8;
-        for (int idx = threadIdx.x; idx < NR + NC; idx += blockDim.x) {
+        for (int idx = rank * 32 + lane; idx < NR + NC; idx += 32 * (TCW - 1)) {
             int i, c;
             double* dst;
             if (idx < NR) {
@@ -285,6 +286,19 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         PIV_MARK(4);
     };
 
+    double u12[2];
+    auto write_u12 = [&](int J, int co) {
+        const int i = 8 * J + gi;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int cc = 8 * (J + co) + 2 * q + e, off = cc - i;
+            if (i < m && off <= ubw) {
+                if (cc < m) F[(long long)cc * rows + d - off] = u12[e];
+                TF[(long long)i * rowsT + kl + off] = cc < m ? u12[e] : 0.0;
+            }
+        }
+    };
+
     // update of step J on my tile column (column block J + co, co >= 1)
     auto update = [&](int J, int co, long long& tprev) {
         (void)tprev;
@@ -322,18 +336,10 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
             acc[0][0] = fma(-l, v0, acc[0][0]);
             acc[0][1] = fma(-l, v1, acc[0][1]);
         }
-        // U rows j0..j0+7 in my columns
-        {
-            const int i = j0 + gi;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int cc = 8 * (J + co) + 2 * q + e, off = cc - i;
-                if (i < m && off <= ubw) {
-                    if (cc < m) F[(long long)cc * rows + d - off] = acc[0][e];
-                    TF[(long long)i * rowsT + kl + off] = cc < m ? acc[0][e] : 0.0;
-                }
-            }
-        }
+        // U rows j0..j0+7 in my columns (the critical warp keeps them for later)
+        u12[0] = acc[0][0];
+        u12[1] = acc[0][1];
+        if (co != 1) write_u12(J, co);
         // U12 as B fragments: B[k][n] = U12[k][n] sits in lane k*4 + n/2, register n&1
         double bf[2];
 #pragma unroll
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
 
     // step 0: warp w holds column block w; warp 0 factors panel 0
     load_block(0, w);
-    stage(0);
+    if (w != 1) stage(0, w == 0 ? 0 : w - 1);
     long long tprev = 0;
 #ifdef SPK_PIV_PROFILE
     tprev = clock64();
@@ -382,11 +388,11 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
             if (threadIdx.x == 0) atomicMax(A.status, 2);
             return;
         }
-        if (J + 1 < nblk) stage(J + 1);
         if (co == 0) {
             // factor output of panel J (this warp factored it last step): L
-            // columns, U11 and the pivots
+            // columns, U11 and the pivots, and its U12 of step J-1
             const int par = J & 1, j0 = 8 * J;
+            if (J > 0) write_u12(J - 1, 1);
             for (int c = 0; c < 8 && j0 + c < m; ++c)
                 for (int off = 1 + lane; off <= kl; off += 32)
                     F[(long long)(j0 + c) * rows + d + off] = j0 + c + off < m ? S.lbuf[par][c][off] : 0.0;
@@ -408,8 +414,10 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
                 piv[j0 + lane] = j0 + S.spiv[par][lane];
                 A.dinv[P.r0 + j0 + lane] = 1.0 / S.d11[par][lane * 9];
             }
+            if (J + 1 < nblk) stage(J + 1, 0);
         } else {
             update(J, co, tprev);
+            if (co != 1 && J + 1 < nblk) stage(J + 1, co - 1);
             if (co == 1) PIV_MARK(1);
             if (co == 1 && J + 1 < nblk) {
                 panel(J + 1, tprev);
