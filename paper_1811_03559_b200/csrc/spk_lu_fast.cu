@@ -462,16 +462,29 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
             stage_elem(idx, b2, i, c, off);
             if (i - c > kl || c - i > ku) sm[S::ST + off] = 0.0;
         }
-    auto stage_load = [&](int Jr, bool rows) {
-        if (Jr >= 0 && Jr < nblk) {
-            const int lo = rows ? 64 * T : 0;
-            for (int idx = lo + threadIdx.x; idx < lo + 64 * T; idx += blockDim.x) {
-                int i, c, off;
-                stage_elem(idx, Jr, i, c, off);
-                if (i - c > kl || c - i > ku) continue;  // zero, never loaded
-                if (i < m && c < m) cp_async8(sm + S::ST + off, bbase + sg * ((long long)c * (ald - 1) + i));
-                else sm[S::ST + off] = i == c ? 1.0 : 0.0;
+    // issue: each warp instruction covers 4 rows x 8 columns of one tile, so
+    // the 32 smem destinations are 32 consecutive doubles (no bank conflicts)
+    // and the global sources are 8 sectors (4 consecutive rows per column)
+    // (warp `rank` of `nrank`: the diagonal warp of the step stays out)
+    auto stage_load = [&](int Jr, bool rows, int rank, int nrank) {
+        if (Jr < 0 || Jr >= nblk || rank < 0) return;
+        const int cc = lane & 7, r4 = lane >> 3;
+        for (int task = rank; task < 2 * T; task += nrank) {
+            const int tile = task >> 1, rr = ((task & 1) << 2) + r4;  // row within the tile
+            int i, c;
+            double* dst;
+            if (!rows) {  // entering column block: window rows 8(Jr+1) + 8 tile + rr, column cc
+                i = 8 * (Jr + 1) + 8 * tile + rr;
+                c = 8 * (Jr + T) + cc;
+                dst = sm + S::ST + (Jr & 1) * T * 64 + tile * 64 + rr * 8 + cc;
+            } else {      // entering row block: row rr, window column 8(Jr+1) + 8 tile + cc
+                i = 8 * (Jr + T) + rr;
+                c = 8 * (Jr + 1) + 8 * tile + cc;
+                dst = sm + S::ST + 2 * T * 64 + (Jr & 1) * T * 64 + tile * 64 + rr * 8 + cc;
             }
+            if (i - c > kl || c - i > ku) continue;  // zero, never loaded
+            if (i < m && c < m) cp_async8(dst, bbase + sg * ((long long)c * (ald - 1) + i));
+            else *dst = i == c ? 1.0 : 0.0;
         }
     };
 
@@ -560,17 +573,9 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
 
     double2* prow = reinterpret_cast<double2*>(sm + S::PROW) + lane;  // + parity * T * 32 + offset * 32
     double2* win = reinterpret_cast<double2*>(sm + S::WIN) + (size_t)w * NS * 32 + lane;
-    // transposed factor writes (row-major L rows, packed U columns): thread t
-    // owns one run of <= 8 entries; which of them lie in the band is fixed
+    // transposed factor writes (row-major L rows, packed U columns): runs of
+    // <= 8 entries, one per L row below / U column right of the panel
     const int tr_n = 15 + kl + ku;
-    unsigned tr_mask = 0;
-    if ((int)threadIdx.x < tr_n) {
-        const int t = threadIdx.x;
-        for (int qq = 0; qq < 8; ++qq) {
-            const bool in = t < 7 + kl ? (qq < t + 1 && t + 1 - qq <= kl) : (qq <= t - (7 + kl) && t - (7 + kl) - qq <= ku);
-            tr_mask |= (unsigned)in << qq;
-        }
-    }
     for (int attempt = 0; attempt < 2; ++attempt) {
         double acc[TR][2];  // my tile row, by column offset from the panel (offsets < TR)
         // offset c of my row as seen at step J: registers or window slot
@@ -628,7 +633,7 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                 prow[(T + c - 1) * 32] = make_double2(t0, t1);
             }
         }
-        stage_load(0, false);
+        stage_load(0, false, w, NW);
         cp_async_commit();
         __syncthreads();
 
@@ -638,8 +643,11 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
 #endif
         for (int J = 0; J < nblk; ++J) {
             const int par = J & 1, j0 = 8 * J;
-            stage_load(J + 1, false);
-            stage_load(J, true);
+            // the warp that factors the next diagonal block this step (ro == 1)
+            // does no staging and no output writes: they are off its chain
+            const int orank = ro == 1 ? -1 : ro - 2;
+            stage_load(J + 1, false, orank, NW - 1);
+            stage_load(J, true, orank, NW - 1);
             cp_async_commit();
             LU_MARK(0);
             double* sLc = sm + S::L + par * 64 * T;
@@ -784,7 +792,7 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                 const double* sD = sm + S::D + par * 64;
                 // L columns (packed column-major) and U rows (row-major copy): one
                 // contiguous run per warp
-                for (int sgm = w; sgm < 16; sgm += NW) {
+                for (int sgm = orank; sgm < 16 && orank >= 0; sgm += NW - 1) {
                     const int qq = sgm & 7, c = j0 + qq;
                     if (c >= m) continue;
                     if (sgm < 8) {
@@ -803,38 +811,19 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                         }
                     }
                 }
-                // L rows (row-major copy) and U columns (packed): one run of <= 8
-                // contiguous entries per thread
-                if ((int)threadIdx.x < tr_n) {
-                    const int t = threadIdx.x;
+                // L rows (row-major copy) and U columns (packed): runs of <= 8
+                // contiguous entries, 8 lanes per run (4 runs per warp store)
+                for (int e = orank * 32 + lane; e < tr_n * 8 && orank >= 0; e += 32 * (NW - 1)) {
+                    const int t = e >> 3, qq = e & 7;
                     const bool lrun = t < 7 + kl;
                     const int x = lrun ? t + 1 : t - (7 + kl);  // rr (L row) or cc (U column)
-                    if (j0 + x < m) {
-                        double v[8];
-                        if (x < 8) {
-#pragma unroll
-                            for (int qq = 0; qq < 8; ++qq) v[qq] = lrun ? sD[x * 8 + qq] : sD[qq * 8 + x];
-                        } else {
-                            const double* src = (lrun ? sLc : sUc) + (x >> 3) * 64 + (x & 7) * 4;
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const double2 p0 = *reinterpret_cast<const double2*>(src + 32 * h);
-                                const double2 p1 = *reinterpret_cast<const double2*>(src + 32 * h + 2);
-                                v[4 * h] = p0.x;
-                                v[4 * h + 1] = p0.y;
-                                v[4 * h + 2] = p1.x;
-                                v[4 * h + 3] = p1.y;
-                            }
-                            if (lrun)
-#pragma unroll
-                                for (int qq = 0; qq < 8; ++qq) v[qq] = -v[qq];
-                        }
-                        double* dst = lrun ? TF + (long long)(j0 + x) * rowsT + kl - x
-                                           : F + (long long)(j0 + x) * rows + d - x;
-#pragma unroll
-                        for (int qq = 0; qq < 8; ++qq)
-                            if (((tr_mask >> qq) & 1) && j0 + qq < m) dst[qq] = v[qq];
-                    }
+                    const bool in = lrun ? (qq < x && x - qq <= kl) : (qq <= x && x - qq <= ku);
+                    if (!in || j0 + x >= m || j0 + qq >= m) continue;
+                    double v;
+                    if (x < 8) v = lrun ? sD[x * 8 + qq] : sD[qq * 8 + x];
+                    else v = lrun ? -sLc[(x >> 3) * 64 + afrag(x & 7, qq)] : sUc[(x >> 3) * 64 + afrag(x & 7, qq)];
+                    double* dst = lrun ? TF + (long long)(j0 + x) * rowsT + kl - x : F + (long long)(j0 + x) * rows + d - x;
+                    dst[qq] = v;
                 }
                 if (threadIdx.x < 8 && j0 + threadIdx.x < m)
                     A.dinv[P.r0 + j0 + threadIdx.x] = sm[S::DINV + par * 8 + threadIdx.x];
