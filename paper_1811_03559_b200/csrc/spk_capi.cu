@@ -9,6 +9,7 @@
 // so a solve issues O(stages + reduced levels) launches independent of p.
 #include "../../include/spike_b200.h"
 #include "spk_launch.h"
+#include "spk_piv_blocked.cuh"
 #include "spk_sweep_fast.cuh"
 #include "spk_sweep_dmma.cuh"
 
@@ -436,6 +437,9 @@ struct spk_fact {
     double* d_tfac = nullptr;
     double* d_dinv = nullptr;
     long long tfac_size = 0;
+    double* d_lblk = nullptr;  // pivoted: blocked L records (spk_piv_blocked.cuh)
+    int lblk_trw = 0;
+    bool lblk_ok = false;      // written by the blocked pivoted LU of this factorization
     Program prog_factor, prog_fwd, prog_tr, prog_rfwd, prog_rtr;  // r*: reduced system only
     std::shared_ptr<struct Symbolic> sym;  // cached geometry + programs (shared by equal factorizations)
     std::vector<long long> factor_sweeps;
@@ -461,7 +465,8 @@ struct spk_fact {
         // outlive it); no device-wide synchronisation
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
-                        (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags, (void*)d_sblob_prev})
+                        (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags, (void*)d_sblob_prev,
+                        (void*)d_lblk})
             if (q) dfree(q, stream);
         if (upload_ev) cudaEventDestroy(upload_ev);
     }
@@ -1324,6 +1329,15 @@ struct Exec {
 
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
         if (nc <= 0) return true;
+        if (st.piv && st.mode == SW_FWD_L && f.lblk_ok) {
+            // pivoted forward sweep, 8 rows per step on the tensor cores from the
+            // LU's blocked records: <= 16 warps x 8 columns per CTA
+            const int groups = (nc + 127) / 128;
+            const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
+            const dim3 grid(st.njobs, (nc + cols - 1) / cols);
+            PivSweepArgs A{jobs, f.d_parts, f.d_lblk, B, ncols};
+            if (launch_sweep_piv_dmma(f.lblk_trw, cols / 8, grid, A, s)) return true;
+        }
         static const bool no_dmma = getenv("SPK_NO_DMMA_SWEEP") && atoi(getenv("SPK_NO_DMMA_SWEEP"));
         static const bool sweep_v1 = getenv("SPK_SWEEP_V1") && atoi(getenv("SPK_SWEEP_V1"));
         // producer/consumer DMMA sweep (spk_sweep_dmma2.cuh): <= 14 compute warps
@@ -1479,9 +1493,10 @@ struct Exec {
                         if (f.piv_on && !generic_only && !piv_old) {
                             // pivoted: blocked DMMA kernel (factor, pivots, row-major copy, 1/u_jj)
                             PivDmmaArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac,
-                                          f.d_tfac, f.d_dinv, f.d_piv, f.d_status};
+                                          f.d_tfac, f.d_dinv, f.d_piv, f.d_status, f.d_lblk};
                             if (launch_band_lu_piv_dmma(st.njobs, f.kl, f.ku, A, s)) {
                                 lu_fast_done = true;  // it writes the row-major copy and 1/u_jj too
+                                f.lblk_ok = f.d_lblk != nullptr;
                                 break;
                             }
                         }
@@ -1719,6 +1734,10 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     f.d_blob = dalloc<char>(std::max<size_t>(blob.size(), 1), s);
     f.d_tfac = dalloc<double>(f.tfac_size, s);
     f.d_dinv = dalloc<double>(f.n, s);
+    static const bool piv_sweep_old = getenv("SPK_PIV_SWEEP_OLD") && atoi(getenv("SPK_PIV_SWEEP_OLD"));
+    f.lblk_trw = (!f.reduced_only && f.piv_on && !piv_sweep_old) ? piv_trw(f.kl, f.ku) : 0;
+    if (f.lblk_trw)
+        f.d_lblk = dalloc<double>((f.bounds[p] / 8 + nparts + 2) * piv_rec_size(f.lblk_trw), s);
     tr.mark("allocations");
     f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
     ck(cudaMemsetAsync(f.d_flags, 0, sizeof(int) * std::max(f.npairs, 1), s), "memset");

@@ -88,8 +88,18 @@ struct PivDmmaArgs {
     double* dinv;  // 1 / u_jj
     int* piv;
     int* status;
+    double* lblk;  // blocked L records (spk_piv_blocked.cuh), or null
 };
 bool launch_band_lu_piv_dmma(int nunits, int kl, int ku, const PivDmmaArgs& A, cudaStream_t s);
+// blocked pivoted forward L sweep from the LU's records (spk_sweep_piv_dmma.cu)
+struct PivSweepArgs {
+    const SweepJob* jobs;
+    const PartDev* parts;
+    const double* lblk;
+    Bufs B;
+    int ncols;
+};
+bool launch_sweep_piv_dmma(int trw, int nwarps, dim3 grid, const PivSweepArgs& A, cudaStream_t s);
 struct PivLuArgs;
 bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);

@@ -38,6 +38,7 @@
 // Rows/columns past m continue as the identity (never selected as pivots).
 #include "spk_device.cuh"
 #include "spk_launch.h"
+#include "spk_piv_blocked.cuh"
 #include "spk_sweep_fast.cuh"  // cp_async8 / commit / wait
 
 #include <algorithm>
@@ -414,6 +415,31 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
                 piv[j0 + lane] = j0 + S.spiv[par][lane];
                 A.dinv[P.r0 + j0 + lane] = 1.0 / S.d11[par][lane * 9];
             }
+            if (A.lblk) {
+                // the panel's blocked L record (spk_piv_blocked.cuh)
+                using R = PivRec<TRW>;
+                double* rec = A.lblk + (P.r0 / 8 + u + J) * (long long)R::SIZE;
+                if (lane < 8) {  // column c = lane of L11^-1 by forward substitution
+                    const int c = lane;
+                    double y[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        double a = r == c ? 1.0 : 0.0;
+#pragma unroll
+                        for (int t = 0; t < r; ++t) a = fma(-S.d11[par][r * 8 + t], y[t], a);
+                        y[r] = r < c ? 0.0 : a;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) rec[pv_afrag(r, c)] = y[r];
+                }
+                for (int e = 64 + lane; e < 64 * TRW; e += 32) rec[e] = S.l21[par][e];
+                int* ri = reinterpret_cast<int*>(rec + R::SRC);
+                for (int e = lane; e < 8 * TRW; e += 32) ri[e] = S.src[par][e];
+                if (lane < R::NSLW) {
+                    ri[8 * TRW + lane] = S.mv_out[par][lane];
+                    ri[8 * TRW + R::NSLW + lane] = S.mv_in[par][lane];
+                }
+            }
             if (J + 1 < nblk) stage(J + 1, 0);
         } else {
             update(J, co, tprev);
@@ -449,11 +475,12 @@ static bool launch_piv_dmma(int nunits, const PivDmmaArgs& A, cudaStream_t s) {
 
 bool launch_band_lu_piv_dmma(int nunits, int kl, int ku, const PivDmmaArgs& A, cudaStream_t s) {
     // the reversed (UL) partition swaps kl and ku: tile rows for the larger
-    const int kr = std::max(kl, ku), kc = kl + ku;
-    if (kr <= 32 && kc <= 64) return launch_piv_dmma<5, 9>(nunits, A, s);
-    if (kr <= 64 && kc <= 128) return launch_piv_dmma<9, 17>(nunits, A, s);
-    if (kr <= 96 && kc <= 192) return launch_piv_dmma<13, 25>(nunits, A, s);
-    return false;
+    switch (piv_trw(kl, ku)) {
+        case 5: return launch_piv_dmma<5, 9>(nunits, A, s);
+        case 9: return launch_piv_dmma<9, 17>(nunits, A, s);
+        case 13: return launch_piv_dmma<13, 25>(nunits, A, s);
+        default: return false;
+    }
 }
 
 }  // namespace spk
