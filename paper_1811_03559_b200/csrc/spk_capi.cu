@@ -1514,6 +1514,20 @@ struct Exec {
                     }
                     {
                         static const bool no_small = getenv("SPK_LU_SMALL") && !atoi(getenv("SPK_LU_SMALL"));
+                        static const bool dense_old = getenv("SPK_DENSE_LU_OLD") && atoi(getenv("SPK_DENSE_LU_OLD"));
+                        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
+                        if (!st.partitions && !no_small && !dense_old && !generic_only) {
+                            // the pivoted 2k coupling units: blocked DMMA LU in place, then
+                            // the shared-memory kernel redoes any unit with an exactly zero
+                            // column (boosted non-pivoting fallback, kernels.cpp:67-77)
+                            PivDmmaArgs A{(const int*)jobs, f.d_parts, nullptr, 0, 0, f.d_fac, nullptr, nullptr,
+                                          f.d_piv, f.d_status, nullptr, f.d_flags, f.d_fell};
+                            if (launch_dense_lu_piv_dmma(st.njobs, st.max_r, A, s) &&
+                                launch_band_lu_small((const int*)jobs, st.njobs, st.max_r, f.d_parts, f.d_fac,
+                                                     f.d_piv, f.d_amax, f.boost_eps, f.d_boost, f.d_fell,
+                                                     f.d_status, f.d_flags, s, true))
+                                break;
+                        }
                         if (!no_small && launch_band_lu_small((const int*)jobs, st.njobs, st.max_r, f.d_parts,
                                                               f.d_fac, f.d_piv, f.d_amax, f.boost_eps, f.d_boost,
                                                               f.d_fell, f.d_status, f.d_flags, s))

@@ -200,11 +200,14 @@ __global__ void __launch_bounds__(kLuSmallThreads) k_band_lu_small(
     const int* __restrict__ units, const PartDev* __restrict__ parts, double* __restrict__ fac,
     int* __restrict__ piv_pool, const unsigned long long* __restrict__ amax_bits, double boost_eps,
     int* __restrict__ boost_cnt, int* __restrict__ fell_back, int* __restrict__ status,
-    const int* __restrict__ flags) {
+    const int* __restrict__ flags, int redo_only) {
     extern __shared__ double sa[];
     const int u = units[blockIdx.x];
     const PartDev P = parts[u];
     if (P.guard >= 0 && !guard_ok(flags, P.guard)) return;
+    // redo: the blocked pivoted kernel found an exactly zero column (marker 2);
+    // only the boosted non-pivoting fallback remains (the pivoted attempt is done)
+    if (redo_only && fell_back[u] != 2) return;
     double* F = fac + P.fofs;
     int* piv = piv_pool + P.r0;
     const int m = P.m, kl = P.kl, ubw = P.ubw, d = P.d, rows = P.rows;
@@ -217,7 +220,11 @@ __global__ void __launch_bounds__(kLuSmallThreads) k_band_lu_small(
     int nboost = 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = kLuSmallThreads / 32;
     auto in_band = [&](int i, int c) { return i - c <= kl && c - i <= ubw; };
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    if (redo_only) {
+        __syncthreads();
+        if (tid == 0) fell_back[u] = 1;
+    }
+    for (int attempt = redo_only ? 1 : 0; attempt < 2; ++attempt) {
         const double* src = attempt == 0 ? F : fac + P.bofs;
         for (int e = tid; e < m * m; e += kLuSmallThreads) {
             const int c = e / m, i = e - c * m;
@@ -332,13 +339,13 @@ __global__ void __launch_bounds__(kLuSmallThreads) k_band_lu_small(
 
 bool launch_band_lu_small(const int* d_units, int nunits, int max_m, const PartDev* d_parts, double* fac,
                           int* piv, const unsigned long long* amax, double boost_eps, int* boost_cnt,
-                          int* fell_back, int* status, const int* flags, cudaStream_t s) {
+                          int* fell_back, int* status, const int* flags, cudaStream_t s, bool redo_only) {
     if (nunits <= 0) return true;
     if (max_m > kLuSmallMaxM) return false;
     const size_t smem = (size_t)max_m * (max_m + 1) * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_band_lu_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_band_lu_small<<<nunits, kLuSmallThreads, smem, s>>>(d_units, d_parts, fac, piv, amax, boost_eps, boost_cnt,
-                                                          fell_back, status, flags);
+                                                          fell_back, status, flags, redo_only ? 1 : 0);
     count_launch();
     return true;
 }

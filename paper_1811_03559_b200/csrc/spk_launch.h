@@ -19,7 +19,8 @@ void launch_band_lu(const int* d_units, int nunits, const PartDev* d_parts, doub
 // false when a unit is larger (caller falls back to launch_band_lu)
 bool launch_band_lu_small(const int* d_units, int nunits, int max_m, const PartDev* d_parts, double* fac,
                           int* piv, const unsigned long long* amax, double boost_eps, int* boost_cnt,
-                          int* fell_back, int* status, const int* flags, cudaStream_t s);
+                          int* fell_back, int* status, const int* flags, cudaStream_t s,
+                          bool redo_only = false);
 // short units staged in shared memory (spk_kernels_generic.cu); false when
 // the shape is not covered (caller falls back to launch_sweep)
 bool launch_sweep_small(const SweepJob* d_jobs, int njobs, int max_nc, int chunks, int maxr,
@@ -89,8 +90,16 @@ struct PivDmmaArgs {
     int* piv;
     int* status;
     double* lblk;  // blocked L records (spk_piv_blocked.cuh), or null
+    // dense coupling units (launch_dense_lu_piv_dmma): factored in place from
+    // the band layout in `fac` (its backup on the fallback), job guards, and
+    // the per-unit redo marker (2) for an exactly singular unit
+    const int* flags;
+    int* redo;
 };
 bool launch_band_lu_piv_dmma(int nunits, int kl, int ku, const PivDmmaArgs& A, cudaStream_t s);
+// the pivoted 2k x 2k coupling units (m <= 128) on the same kernel; false when
+// not covered.  Units marked for redo need k_band_lu_small (its fallback).
+bool launch_dense_lu_piv_dmma(int nunits, int max_m, const PivDmmaArgs& A, cudaStream_t s);
 // blocked pivoted forward L sweep from the LU's records (spk_sweep_piv_dmma.cu)
 struct PivSweepArgs {
     const SweepJob* jobs;

@@ -89,24 +89,27 @@ struct PivDmmaSmem {
     int sing[2];
 };
 
-template <int TRW, int TCW>
+template <int TRW, int TCW, bool DENSE>
 __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A) {
     constexpr int NSL = (8 * TRW + 31) / 32;  // row slots per lane in the panel layout
     extern __shared__ __align__(16) unsigned char piv_smem_raw[];
     PivDmmaSmem<TRW, TCW>& S = *reinterpret_cast<PivDmmaSmem<TRW, TCW>*>(piv_smem_raw);
     const int u = A.units[blockIdx.x];
     const PartDev P = A.parts[u];
+    if (DENSE && P.guard >= 0 && !guard_ok(A.flags, P.guard)) return;
     const int m = P.m, kl = P.kl, ku = P.ku, ubw = P.ubw, d = P.d, rows = P.rows;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gi = lane >> 2, q = lane & 3;
     const unsigned full = 0xffffffffu;
-    const int ald = A.akl + A.aku + 1;
+    // dense coupling units read their band in place (fac, layout kernels.cpp:29-42)
+    const int ald = DENSE ? rows : A.akl + A.aku + 1;
     double* F = A.fac + P.fofs;
     double* TF = A.tfac + P.tofs;
     const int rowsT = P.rowsT;
     int* piv = A.piv + P.r0;
     const int nblk = (m + 7) / 8;
-    const double* bbase = A.band + (P.rev ? (long long)(P.r0 + m - 1) * ald + A.aku : (long long)P.r0 * ald + A.aku);
+    const double* bbase = DENSE ? A.fac + P.fofs + d
+                                : A.band + (P.rev ? (long long)(P.r0 + m - 1) * ald + A.aku : (long long)P.r0 * ald + A.aku);
     const long long sg = P.rev ? -1 : 1;
     // LU-space entry of the raw band; rows/columns past m continue as the identity
     auto val = [&](int i, int c) -> double {
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
     }
     for (int idx = threadIdx.x; idx < kl * kl; idx += blockDim.x) {
         const int r = idx / kl, off = idx - r * kl + 1;
-        if (r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
+        if (!DENSE && r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
     }
 
     double acc[TRW][2];
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
             const int cc = 8 * (J + co) + 2 * q + e, off = cc - i;
             if (i < m && off <= ubw) {
                 if (cc < m) F[(long long)cc * rows + d - off] = u12[e];
-                TF[(long long)i * rowsT + kl + off] = cc < m ? u12[e] : 0.0;
+                if (!DENSE) TF[(long long)i * rowsT + kl + off] = cc < m ? u12[e] : 0.0;
             }
         }
     };
@@ -386,7 +389,10 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         __syncthreads();
         if (co == 1) PIV_MARK(6);
         if (S.sing[J & 1]) {
-            if (threadIdx.x == 0) atomicMax(A.status, 2);
+            if (threadIdx.x == 0) {
+                if (DENSE && P.fallback) A.redo[u] = 2;  // k_band_lu_small redoes it (boosted fallback)
+                else atomicMax(A.status, 2);
+            }
             return;
         }
         if (co == 0) {
@@ -402,20 +408,20 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
                 if (t >= r && t - r <= ubw && j0 + r < m) {
                     const double v = j0 + t < m ? S.d11[par][e] : 0.0;
                     if (j0 + t < m) F[(long long)(j0 + t) * rows + d - (t - r)] = v;
-                    TF[(long long)(j0 + r) * rowsT + kl + t - r] = v;
+                    if (!DENSE) TF[(long long)(j0 + r) * rowsT + kl + t - r] = v;
                 }
             }
             // row-major L: row j0+r takes columns j0+cc, cc < r, within kl (one run)
-            for (int r = 1 + lane; r < 8 + kl && j0 + r < m; r += 32) {
+            for (int r = 1 + lane; !DENSE && r < 8 + kl && j0 + r < m; r += 32) {
                 double* dst = TF + (long long)(j0 + r) * rowsT + kl - r;
                 const int c0 = max(0, r - kl), c1 = min(7, r - 1);
                 for (int cc = c0; cc <= c1; ++cc) dst[cc] = S.lbuf[par][cc][r - cc];
             }
             if (lane < 8 && j0 + lane < m) {
                 piv[j0 + lane] = j0 + S.spiv[par][lane];
-                A.dinv[P.r0 + j0 + lane] = 1.0 / S.d11[par][lane * 9];
+                if (!DENSE) A.dinv[P.r0 + j0 + lane] = 1.0 / S.d11[par][lane * 9];
             }
-            if (A.lblk) {
+            if (!DENSE && A.lblk) {
                 // the panel's blocked L record (spk_piv_blocked.cuh)
                 using R = PivRec<TRW>;
                 double* rec = A.lblk + (P.r0 / 8 + u + J) * (long long)R::SIZE;
@@ -463,12 +469,12 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
     cp_async_wait<0>();
 }
 
-template <int TRW, int TCW>
+template <int TRW, int TCW, bool DENSE = false>
 static bool launch_piv_dmma(int nunits, const PivDmmaArgs& A, cudaStream_t s) {
     const int smem = (int)sizeof(PivDmmaSmem<TRW, TCW>);
     if (smem > 227 * 1024) return false;
-    cudaFuncSetAttribute(k_band_lu_piv_dmma<TRW, TCW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_band_lu_piv_dmma<TRW, TCW><<<nunits, 32 * TCW, smem, s>>>(A);
+    cudaFuncSetAttribute(k_band_lu_piv_dmma<TRW, TCW, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_band_lu_piv_dmma<TRW, TCW, DENSE><<<nunits, 32 * TCW, smem, s>>>(A);
     count_launch();
     return true;
 }
@@ -481,6 +487,17 @@ bool launch_band_lu_piv_dmma(int nunits, int kl, int ku, const PivDmmaArgs& A, c
         case 13: return launch_piv_dmma<13, 25>(nunits, A, s);
         default: return false;
     }
+}
+
+// Coupling units: a dense 2k x 2k matrix stored as a band with kl = ku = 2k-1
+// (kernels.cpp:67-77) is the window itself (8 TRW = 8 TCW >= 2k rows and
+// columns; everything past m is identity padding, so no entering blocks are
+// read), factored in place.
+bool launch_dense_lu_piv_dmma(int nunits, int max_m, const PivDmmaArgs& A, cudaStream_t s) {
+    if (nunits <= 0) return true;
+    if (max_m <= 64) return launch_piv_dmma<8, 8, true>(nunits, A, s);
+    if (max_m <= 128) return launch_piv_dmma<16, 16, true>(nunits, A, s);
+    return false;
 }
 
 }  // namespace spk
