@@ -1134,41 +1134,30 @@ void build_forward_program(spk_fact& f, ProgramBuilder& pb) {
         b.copy(imp);
         emit_unit_correction(f, b);
     }
-    // retrieval
-    b.memset_buf(B_S);
+    // retrieval (solve.cpp:180-223): x_i = A_i^-1 (f_i - C_i eta - B_i xi), solved
+    // again from F with corrected tip rows (X = F, X[tips] -= corner products,
+    // then the full L and U sweeps): no correction buffer, no memset, no
+    // X -= S pass; the D-stage result Y was only needed for its tips
+    b.memcpy_fx();
     std::vector<GemmJob> g;
     std::vector<SweepJob> r_fl, r_bu;
-    std::vector<CopyJob> r_sub_edge, r_sub_inner;
     const View tview = view(B_T, 0);
     for (int i = 0; i < p; ++i) {
         const PartDev& P = f.parts[i];
         const int m = P.m;
         const long long r0 = f.bounds[i];
-        const View sv = view(B_S, r0, 0, 0, m);
-        const View sr = view(B_S, r0, P.rev, 0, m);
-        const View xv = view(B_X, r0, P.rev, 0, m);
+        const View xp = view(B_X, r0, 0, 0, m);      // physical rows
+        const View xv = view(B_X, r0, P.rev, 0, m);  // LU space (reversed for the UL partition)
         const View bh = view(B_POOL, f.off_bhat + i * kk, 0, 0, 0, k);
         const View ch = view(B_POOL, f.off_chat + i * kk, 0, 0, 0, k);
-        if (!f.last(i)) g.push_back(gj(bh, 0, tview, 2 * (i + 1) * k, sv, m - k, k, k, GM_SET));
-        if (!f.first(i)) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, sv, 0, k, k, GM_SET));
-        if (f.first(i) || f.last(i)) {
-            r_fl.push_back(sj(sr, i, SW_FWD_L, P.trunc, 0));
-            r_sub_edge.push_back(cj(sr, xv, P.trunc, m, CP_SUB));
-            r_bu.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
-        } else {
-            r_fl.push_back(sj(sv, i, SW_FWD_L, 0, 0));
-            r_bu.push_back(sj(sv, i, SW_BWD_U, 0, m - 1));
-            r_sub_inner.push_back(cj(sv, xv, 0, m, CP_SUB));
-        }
+        if (!f.last(i)) g.push_back(gj(bh, 0, tview, 2 * (i + 1) * k, xp, m - k, k, k, GM_SUB));
+        if (!f.first(i)) g.push_back(gj(ch, 0, tview, (2 * i - 1) * k, xp, 0, k, k, GM_SUB));
+        r_fl.push_back(sj(xv, i, SW_FWD_L, 0, 0));
+        r_bu.push_back(sj(xv, i, SW_BWD_U, 0, m - 1));
     }
-    // edges subtract their truncated forward sweep first, so their full
-    // backward sweep (on X) shares one launch with the inner partitions'
-    // (on S) instead of running as a 2-job tail after it
     b.gemm(g);
     b.sweep(r_fl);
-    b.copy(r_sub_edge);
     b.sweep(r_bu);
-    b.copy(r_sub_inner);
 }
 
 // transpose solve program (solve.cpp:225-380)
@@ -2555,8 +2544,9 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
         dF = x->tF;
         dX = x->tX;
         lf = lx = n;
-    } else if (transpose) {
-        // the transpose program re-reads F after writing X: never alias
+    } else if (transpose || f.coupled()) {
+        // both programs re-read F after writing X (the transpose program's
+        // G tips, the forward retrieval's re-solve): never alias
         const char* f0 = (const char*)F;
         const char* f1 = (const char*)(F + ldf * (nrhs - 1) + n);
         const char* x0 = (const char*)X;
@@ -2578,7 +2568,7 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     B.ld[B_F] = lf;
     if (f.coupled()) {
         const long long H = 2LL * f.p * f.k, halo = f.open() ? f.k : 0;
-        x->S = dalloc<double>((size_t)n * nrhs, s);
+        if (transpose) x->S = dalloc<double>((size_t)n * nrhs, s);  // tau (the forward solve needs none)
         x->T = dalloc<double>((size_t)(H + 2 * halo) * nrhs, s);
         x->AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
         if (f.open()) {
