@@ -79,33 +79,51 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
         kbeg = blockIdx.z * ks;
         kend = min(jkk, kbeg + ks);
     }
-    auto stage = [=](int buf, int k0) {
-        // A tile: TM x TK, element (i, l) of opA(A)
-        for (int idx = tid; idx < TM * TK; idx += 128) {
-            int i, l;
-            if (transA) {  // A is kk x r: consecutive threads walk down a column of A
-                l = idx % TK;
-                i = idx / TK;
-            } else {
-                i = idx % TM;
-                l = idx / TM;
+    // Staging: each thread keeps its row pointer(s) and steps through the
+    // chunk with a constant stride (one add + one bounds test per element
+    // instead of a full view resolution).
+    auto rowp = [](const RV& v, int L) -> const double* {
+        return v.p + (v.rev ? (v.mrows - 1 - (L - v.off)) : (L - v.off));
+    };
+    // A, not transposed: thread -> row i = tid & 63, k offsets (tid >> 6) + 2 j
+    const int a_i = tid & (TM - 1), a_l = tid >> 6;
+    const bool a_rok = row0 + a_i < jr;
+    const double* a_row = transA ? nullptr : rowp(va, a_rok ? row0 + a_i : 0);
+    // A transposed (A is kk x r): thread -> k offset tid & 15, rows (tid >> 4) + 8 j
+    const int t_l = tid & (TK - 1), t_i = tid >> 4;
+    // B: thread -> k offset tid & 15, columns (tid >> 4) + 8 j
+    const int b_l = tid & (TK - 1), b_c = tid >> 4;
+    auto stage = [&](int buf, int k0) {
+        if (!transA) {
+            const double* src = a_row + (long long)(k0 + a_l) * va.ld;
+#pragma unroll
+            for (int j = 0; j < TK / 2; ++j) {
+                const int l = a_l + 2 * j;
+                double* dst = &sA[buf][a_i * SA + l];
+                if (a_rok && k0 + l < kend) cp_async8(dst, src + (long long)(2 * j) * va.ld);
+                else *dst = 0.0;
             }
-            double* dst = &sA[buf][i * SA + l];
-            const int gi = row0 + i, gl = k0 + l;
-            if (gi < jr && gl < kend) {
-                const double* src = transA ? va.at(gl, gi) : va.at(gi, gl);
-                cp_async8(dst, src);
-            } else {
-                *dst = 0.0;
+        } else {
+            const bool lok = k0 + t_l < kend;
+            const double* src = rowp(va, lok ? k0 + t_l : 0) + (long long)row0 * va.ld;
+#pragma unroll
+            for (int j = 0; j < TM / 8; ++j) {
+                const int i = t_i + 8 * j;
+                double* dst = &sA[buf][i * SA + t_l];
+                if (lok && row0 + i < jr) cp_async8(dst, src + (long long)i * va.ld);
+                else *dst = 0.0;
             }
         }
-        // B tile: TK x TN, stored [n][k]
-        for (int idx = tid; idx < TK * TN; idx += 128) {
-            const int l = idx % TK, c = idx / TK;
-            double* dst = &sB[buf][c * SB + l];
-            const int gl = k0 + l, gc = col0 + c;
-            if (gl < kend && gc < nc) cp_async8(dst, vb.at(brow0 + gl, gc));
-            else *dst = 0.0;
+        {
+            const bool lok = k0 + b_l < kend;
+            const double* src = rowp(vb, brow0 + (lok ? k0 + b_l : 0)) + (long long)col0 * vb.ld;
+#pragma unroll
+            for (int j = 0; j < TN / 8; ++j) {
+                const int c = b_c + 8 * j;
+                double* dst = &sB[buf][c * SB + b_l];
+                if (lok && col0 + c < nc) cp_async8(dst, src + (long long)c * vb.ld);
+                else *dst = 0.0;
+            }
         }
         cp_async_commit();
     };
