@@ -1651,11 +1651,13 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
             const int m = (int)(f.bounds[i + 1] - f.bounds[i]);
             const int rev = (f.coupled() && f.last(i)) ? 1 : 0;
             PartDev P = make_part(f.bounds[i], m, f.kl, f.ku, f.piv_on, rev, k);
+            // partition factors start on 64-byte boundaries: the LU's 8-entry
+            // runs (U columns, L rows) are then whole sectors for k = 0 mod 4
             P.fofs = fac_cursor;
-            fac_cursor += (long long)P.m * P.rows;
+            fac_cursor += ((long long)P.m * P.rows + 7) / 8 * 8;
             P.rowsT = P.kl + P.ubw + 1;
             P.tofs = f.tfac_size;
-            f.tfac_size += (long long)P.m * P.rowsT;
+            f.tfac_size += ((long long)P.m * P.rowsT + 7) / 8 * 8;
             f.parts.push_back(P);
         }
         if (f.coupled())
