@@ -387,6 +387,48 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     return 0
 
 
+def small_k_leg(spk, torch, dev, stream, steps=10, warmup=3):
+    """The BASELINE metric's "HBM GB/s small-k" half: C1 (n=1e5, kl=ku=16,
+    nrhs=1) factor + solve on the device, L2 flushed between steps; bytes are
+    SURVEY 8(d)'s algorithmic counts (factor: read A + write factors, solve: two
+    factor reads + F in, Y, X)."""
+    c = CONFIGS["c1"]
+    n, k, nrhs = c["n"], c["k"], c["nrhs"]
+    sptr = stream.cuda_stream
+    band = torch.empty((n, 2 * k + 1), dtype=torch.float64, device=dev)
+    F = torch.empty((nrhs, n), dtype=torch.float64, device=dev)
+    X = torch.empty_like(F)
+    spk.generate_band_device(SEED_A, n, k, k, c["dd"], band.data_ptr(), sptr)
+    spk.generate_rhs_device(SEED_A + 1, n, nrhs, F.data_ptr(), n, sptr)
+    plan = spk.gpu_plan(n, k, k, nrhs, False, 0)
+    opts = spk.FactorOptions(pivoting=False)
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float64, device=dev)
+
+    def step():
+        fact = spk.factorize_device(band.data_ptr(), n, k, k, plan, opts, sptr)
+        spk.solve_device(fact, F.data_ptr(), n, nrhs, X.data_ptr(), n, False, sptr)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    fbytes = 16.0 * n * (2 * k + 1)
+    sbytes = 2 * 8.0 * n * (2 * k + 1) + 32.0 * n * nrhs
+    gbs = (fbytes + sbytes) / (ms * 1e-3) / 1e9
+    peak = measured_peaks().get("hbm_gbs", HBM_PEAK_FALLBACK)
+    del band, F, X, flush
+    return {"workload": c["desc"], "ms_per_step": round(ms, 4), "hbm_gbs": round(gbs, 2),
+            "bytes_per_step": int(fbytes + sbytes), "peak_gbs": peak, "frac": round(gbs / peak, 5),
+            "partitions": plan.p, "note": "latency-bound: ~250 dependent launches per step at this size"}
+
+
 def impl_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -528,6 +570,11 @@ def impl_ours(args, cfg):
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "error": str(ex)[:200]}
 
+    small = None
+    if args.config == "c3" and not args.no_small_k:
+        torch.cuda.empty_cache()
+        small = small_k_leg(spk, torch, dev, stream)
+
     if rank == 0:
         line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": 1,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -540,6 +587,8 @@ def impl_ours(args, cfg):
                 "backward_error": berr,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "impl": "ours"}
+        if small is not None:
+            line["small_k"] = small
         print(json.dumps(line))
     return 0
 
@@ -554,6 +603,7 @@ def main():
     ap.add_argument("--p", type=int, default=0, help="force the partition count")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-small-k", action="store_true", help="skip the C1 small-k HBM leg of the default line")
     ap.add_argument("--slabs", action="store_true",
                     help="multi-GPU slab path even at N=1 (under torchrun; N>1 always uses it)")
     args = ap.parse_args()
