@@ -746,12 +746,17 @@ __global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) 
                     const double2 v0 = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
                     if (live) amax = fmax(amax, fmax(fabs(v0.x), fabs(v0.y)));
                 } else {
+                    // register tiles k-slice-major: a tile's two DMMAs are TR-1
+                    // instructions apart (back to back they stall on the DMMA latency)
 #pragma unroll
-                    for (int c = 1; c < T; ++c) {
-                        if (c < TR) {
-                            lu_dmma(acc[c < TR ? c : 0][0], acc[c < TR ? c : 0][1], la0, sUc[c * 64 + lane]);
-                            lu_dmma(acc[c < TR ? c : 0][0], acc[c < TR ? c : 0][1], la1, sUc[c * 64 + 32 + lane]);
-                        } else {
+                    for (int c = 1; c < TR; ++c)
+                        lu_dmma(acc[c][0], acc[c][1], la0, sUc[c * 64 + lane]);
+#pragma unroll
+                    for (int c = 1; c < TR; ++c)
+                        lu_dmma(acc[c][0], acc[c][1], la1, sUc[c * 64 + 32 + lane]);
+#pragma unroll
+                    for (int c = TR; c < T; ++c) {
+                        {
                             double t0, t1;
                             get(J, c, t0, t1);
                             lu_dmma(t0, t1, la0, sUc[c * 64 + lane]);

@@ -355,11 +355,11 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         }
         if (co == 1) PIV_MARK(7);
         const double* L21 = S.l21[par];
+        // k-slice-major: a tile's two DMMAs are TRW-1 instructions apart
 #pragma unroll
-        for (int t = 1; t < TRW; ++t) {
-            pv_dmma(acc[t][0], acc[t][1], L21[t * 64 + lane], bf[0]);
-            pv_dmma(acc[t][0], acc[t][1], L21[t * 64 + 32 + lane], bf[1]);
-        }
+        for (int t = 1; t < TRW; ++t) pv_dmma(acc[t][0], acc[t][1], L21[t * 64 + lane], bf[0]);
+#pragma unroll
+        for (int t = 1; t < TRW; ++t) pv_dmma(acc[t][0], acc[t][1], L21[t * 64 + 32 + lane], bf[1]);
         // the window moves down one tile row
 #pragma unroll
         for (int t = 0; t + 1 < TRW; ++t) {
