@@ -1335,6 +1335,28 @@ struct Exec {
         // the factor) and keeps >= 6 compute warps busy (with fewer, one warp's
         // dependency chain sets the pace and the synchronous kernel wins).
         static const bool sweep_v2 = getenv("SPK_SWEEP_V2") && atoi(getenv("SPK_SWEEP_V2"));
+        // narrow solves (<= 8 right-hand sides): the producer/consumer sweep
+        // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>)
+        static const bool pair_on = !(getenv("SPK_SWEEP_PAIR") && !atoi(getenv("SPK_SWEEP_PAIR")));
+        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= 8 && st.kwmax > 16 && st.kwmax <= 192) {
+            static const int ntws[] = {5, 9, 13, 17, 21, 25};
+            int ntw = 0;
+            for (int t : ntws)
+                if (8 * (t - 1) >= st.kwmax) {
+                    ntw = t;
+                    break;
+                }
+            FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
+            const dim3 grid(st.njobs, 1);
+            bool ok = false;
+            switch (st.mode) {
+                case SW_FWD_L: ok = launch_sweep_dmma2_fl(ntw, 2, grid, A, s, true); break;
+                case SW_BWD_U: ok = launch_sweep_dmma2_bu(ntw, 2, grid, A, s, true); break;
+                case SW_FWD_UT: ok = launch_sweep_dmma2_fut(ntw, 2, grid, A, s, true); break;
+                default: ok = launch_sweep_dmma2_blt(ntw, 2, grid, A, s, true); break;
+            }
+            if (ok) return true;
+        }
         const int groups2 = (nc + 111) / 112, groups1 = (nc + 127) / 128;
         const int cols2 = ((nc + groups2 - 1) / groups2 + 7) / 8 * 8;
         if (!no_dmma && !sweep_v1 && !st.piv && nc >= 8 && st.kwmax <= 192 &&

@@ -111,10 +111,14 @@ struct PivSweepArgs {
 bool launch_sweep_piv_dmma(int trw, int nwarps, dim3 grid, const PivSweepArgs& A, cudaStream_t s);
 struct PivLuArgs;
 bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s);
-bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma2_bu(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma2_fut(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma2_blt(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s);
+bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
+                           bool pair = false);
+bool launch_sweep_dmma2_bu(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
+                           bool pair = false);
+bool launch_sweep_dmma2_fut(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
+                           bool pair = false);
+bool launch_sweep_dmma2_blt(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
+                           bool pair = false);
 bool launch_sweep_dmma_fl(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
 bool launch_sweep_dmma_bu(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
 bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);

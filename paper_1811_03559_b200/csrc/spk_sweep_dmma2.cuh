@@ -69,13 +69,23 @@ struct Dmma2Geom {
     static constexpr int STAGE = 32 * SR + 32 + 4 * 64;        // 32 steps x SR rows + 32 x 1/u + 4 inverses
 };
 
-inline size_t dmma2_sweep_smem(int ntw) {
+// pair mode: + per pair two X buffers, two tile buffers and two mbarriers
+inline size_t dmma2_sweep_smem(int ntw, int ncw = 0, bool pair = false) {
     const int KWT = 8 * (ntw - 1);
     const int SR = ((8 + KWT + 15) / 16) * 16 + 4;
-    return (size_t)kDmma2Stages * (32 * SR + 32 + 4 * 64) * 8 + 2 * kDmma2Stages * 8 + 16;
+    return (size_t)kDmma2Stages * (32 * SR + 32 + 4 * 64) * 8 + 2 * kDmma2Stages * 8 + 16 +
+           (pair ? (size_t)(ncw / 2) * (4 * 64 * 8 + 16) : 0);
 }
 
-template <int NTW, int MODE>
+// PAIR (narrow solves, <= 8 right-hand sides): two compute warps share the 8
+// columns and split the window: warp A holds tiles 0 .. HA-1 and forms X, warp
+// B holds tiles HA .. NTW-1 and the incoming rows.  Per block A publishes -X
+// through shared memory and an mbarrier, and B publishes the tile leaving its
+// front, which A takes one block later.  A single warp issues a DMMA at most
+// every ~32 cycles (profiles/r01_dmma_occupancy.txt): with one column group
+// the per-block issue of one warp (2 NTW DMMAs) set the pace; split, each warp
+// issues about half.  (For wide solves the pairing measured slower.)
+template <int NTW, int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
     constexpr int SR = Dmma2Geom<NTW>::SR;
     constexpr int KWT = Dmma2Geom<NTW>::KWT;
@@ -95,7 +105,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
     const PartDev P = A.parts[J.part];
     const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
     const int ncw = (blockDim.x >> 5) - kDmma2Producers;  // compute warps
-    const int ncta = ncw * 8;
+    const int ncta = (PAIR ? ncw / 2 : ncw) * 8;
     const int colbase = blockIdx.y * ncta;
     if (colbase >= nc_total) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -134,6 +144,10 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
         mbar_init(full + threadIdx.x, kDmma2Producers * 32);  // producers arrive after forming the inverses
         mbar_init(empty + threadIdx.x, ncw);
     }
+    // pair handshakes (PAIR): per pair, X ready (A -> B) and front tile ready (B -> A)
+    unsigned long long* pbar = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<double*>(empty + NST) + (size_t)(ncw / 2) * 4 * 64);
+    if (PAIR && threadIdx.x < ncw) mbar_init(pbar + threadIdx.x, 32);
     __syncthreads();
 
     if (warp >= ncw) {
@@ -192,6 +206,156 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
     }
 
     // ---- compute warps
+    if constexpr (PAIR) {
+        constexpr int HA = (NTW + 1) / 2, HB = NTW - HA;
+        constexpr int LAP = 4;  // right-hand-side lookahead of warp B, blocks
+        const int g = lane >> 2, q = lane & 3;
+        const int pr_ = warp >> 1, role = warp & 1;
+        double* pbuf = reinterpret_cast<double*>(empty + NST) + (size_t)pr_ * 4 * 64;
+        double* xbuf = pbuf;         // [2][64]: -X as B fragments (A -> B)
+        double* tbuf = pbuf + 128;   // [2][64]: B's front tile after its update (B -> A)
+        unsigned long long* mbx = pbar + 2 * pr_;
+        unsigned long long* mbt = mbx + 1;
+        const View& v = J.v;
+        const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
+        double* const bbase = A.B.p[v.buf] + v.base;
+        auto phys = [&](int r) -> long long {
+            return v.rev ? (long long)(v.mrows - 1 - (r - v.off)) : (long long)(r - v.off);
+        };
+        const int c0 = J.c0 + colbase;
+        const int ncta_valid = min(ncta, nc_total - colbase);
+        const int lc0 = pr_ * 8 + 2 * q;
+        const bool cv0 = lc0 < ncta_valid, cv1 = lc0 + 1 < ncta_valid;
+        double* const cp0 = bbase + (long long)(c0 + (cv0 ? lc0 : 0)) * ld;
+        double* const cp1 = bbase + (long long)(c0 + (cv1 ? lc0 + 1 : 0)) * ld;
+        auto rhs = [&](int u, double& a, double& b) {
+            const bool ok = u < nsteps;
+            const long long pr = ok ? phys(rowof(u)) : 0;
+            a = (ok && cv0) ? cp0[pr] : 0.0;
+            b = (ok && cv1) ? cp1[pr] : 0.0;
+        };
+        const int nblocks = (nsteps + 7) / 8;
+        if (role == 0) {
+            // ---- warp A: window tiles 0 .. HA-1
+            double Wt[HA][2];
+#pragma unroll
+            for (int T = 0; T < HA; ++T) rhs(8 * T + g, Wt[T][0], Wt[T][1]);
+            for (int b = 0; b < nblocks; ++b) {
+                const int R = b >> 2, bb = b & 3, s = R % NST;
+                if (bb == 0) mbar_wait(full + s, (R / NST) & 1);
+                const double* Ab = s_st + s * STG + (size_t)(8 * bb) * SR;
+                const int u0 = 8 * b;
+                double p0 = 0.0, p1 = 0.0;
+                {
+                    const double* T = s_st + s * STG + 32 * SR + 32 + bb * 64;
+                    double pb[2];
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        const int src = 4 * (4 * s2 + q) + (g >> 1);
+                        const double v0 = __shfl_sync(0xffffffffu, Wt[0][0], src);
+                        const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
+                        pb[s2] = (g & 1) ? v1 : v0;
+                    }
+                    dmma2_acc(p0, p1, T[g * 8 + q], pb[0]);
+                    dmma2_acc(p0, p1, T[g * 8 + 4 + q], pb[1]);
+                }
+                double nb[2];
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const int src = 4 * (4 * s2 + q) + (g >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, p0, src);
+                    const double v1 = __shfl_sync(0xffffffffu, p1, src);
+                    nb[s2] = -((g & 1) ? v1 : v0);
+                }
+                *reinterpret_cast<double2*>(xbuf + (b & 1) * 64 + 2 * lane) = make_double2(nb[0], nb[1]);
+                // B has consumed X of block b-1 (and published its front tile)
+                // before X of block b is announced: one phase apart at most
+                if (b > 0) mbar_wait(mbt, (b - 1) & 1);
+                mbar_arrive(mbx);
+                if (b > 0) {  // my last tile is B's front tile of the previous block
+                    const double2 t = *reinterpret_cast<const double2*>(tbuf + ((b - 1) & 1) * 64 + 2 * lane);
+                    Wt[HA - 1][0] = t.x;
+                    Wt[HA - 1][1] = t.y;
+                }
+                {
+                    const int u = u0 + g;
+                    if (u < nsteps) {
+                        const long long pr = phys(rowof(u));
+                        if (cv0) cp0[pr] = p0;
+                        if (cv1) cp1[pr] = p1;
+                    }
+                }
+                dmma2_acc(Wt[1][0], Wt[1][1], Ab[q * SR + 8 + g], nb[0]);
+                dmma2_acc(Wt[1][0], Wt[1][1], Ab[(4 + q) * SR + 8 + g], nb[1]);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                    for (int i = 2; i < HA; ++i) dmma2_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * i + g], nb[s2]);
+                if (bb == 3 || b == nblocks - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + s);
+                }
+#pragma unroll
+                for (int i = 0; i < HA - 1; ++i) {
+                    Wt[i][0] = Wt[i + 1][0];
+                    Wt[i][1] = Wt[i + 1][1];
+                }
+            }
+        } else {
+            // ---- warp B: window tiles HA .. NTW-1 and the incoming rows
+            double Wt[HB][2];
+#pragma unroll
+            for (int T = 0; T < HB; ++T) rhs(8 * (HA + T) + g, Wt[T][0], Wt[T][1]);
+            double qv[LAP][2];
+#pragma unroll
+            for (int j = 0; j < LAP; ++j) rhs(8 * (NTW + j) + g, qv[j][0], qv[j][1]);
+            for (int b = 0; b < nblocks; ++b) {
+                const int R = b >> 2, bb = b & 3, s = R % NST;
+                if (bb == 0) mbar_wait(full + s, (R / NST) & 1);
+                const double* Ab = s_st + s * STG + (size_t)(8 * bb) * SR;
+                mbar_wait(mbx, b & 1);
+                const double2 x = *reinterpret_cast<const double2*>(xbuf + (b & 1) * 64 + 2 * lane);
+                const double nb[2] = {x.x, x.y};
+                // the front tile first: A takes it next block
+                dmma2_acc(Wt[0][0], Wt[0][1], Ab[q * SR + 8 * HA + g], nb[0]);
+                dmma2_acc(Wt[0][0], Wt[0][1], Ab[(4 + q) * SR + 8 * HA + g], nb[1]);
+                *reinterpret_cast<double2*>(tbuf + (b & 1) * 64 + 2 * lane) = make_double2(Wt[0][0], Wt[0][1]);
+                mbar_arrive(mbt);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                    for (int i = 1; i < HB; ++i)
+                        dmma2_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * (HA + i) + g], nb[s2]);
+                if (bb == 3 || b == nblocks - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + s);
+                }
+#pragma unroll
+                for (int i = 0; i < HB - 1; ++i) {
+                    Wt[i][0] = Wt[i + 1][0];
+                    Wt[i][1] = Wt[i + 1][1];
+                }
+                Wt[HB - 1][0] = qv[0][0];
+                Wt[HB - 1][1] = qv[0][1];
+#pragma unroll
+                for (int j = 0; j + 1 < LAP; ++j) {
+                    qv[j][0] = qv[j + 1][0];
+                    qv[j][1] = qv[j + 1][1];
+                }
+                rhs(8 * (b + 1 + NTW + LAP - 1) + g, qv[LAP - 1][0], qv[LAP - 1][1]);
+                {
+                    constexpr int PF = 8;
+                    const int u = 8 * (b + 1 + NTW + LAP - 1 + PF) + g;
+                    if (u < nsteps) {
+                        const long long pr = phys(rowof(u));
+                        if (cv0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp0 + pr));
+                        if (cv1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp1 + pr));
+                    }
+                }
+            }
+        }
+        return;
+    } else {
     const int g = lane >> 2, q = lane & 3;
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -294,6 +458,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
                 if (cv1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp1 + pr));
             }
         }
+    }
     }
 }
 

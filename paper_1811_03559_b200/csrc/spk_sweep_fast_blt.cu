@@ -68,20 +68,29 @@ bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const Fa
     return true;
 }
 
-bool launch_sweep_dmma2_blt(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s) {
+bool launch_sweep_dmma2_blt(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s, bool pair) {
     void (*fn)(FastSweepArgs) = nullptr;
     int slot = -1;
-    if (ntw == 3) { fn = k_sweep_dmma2<3, SW_BWD_LT>; slot = 0; }
-    if (ntw == 5) { fn = k_sweep_dmma2<5, SW_BWD_LT>; slot = 1; }
-    if (ntw == 9) { fn = k_sweep_dmma2<9, SW_BWD_LT>; slot = 2; }
-    if (ntw == 13) { fn = k_sweep_dmma2<13, SW_BWD_LT>; slot = 3; }
-    if (ntw == 17) { fn = k_sweep_dmma2<17, SW_BWD_LT>; slot = 4; }
-    if (ntw == 21) { fn = k_sweep_dmma2<21, SW_BWD_LT>; slot = 5; }
-    if (ntw == 25) { fn = k_sweep_dmma2<25, SW_BWD_LT>; slot = 6; }
+    if (!pair) {
+        if (ntw == 3) { fn = k_sweep_dmma2<3, SW_BWD_LT>; slot = 0; }
+        if (ntw == 5) { fn = k_sweep_dmma2<5, SW_BWD_LT>; slot = 1; }
+        if (ntw == 9) { fn = k_sweep_dmma2<9, SW_BWD_LT>; slot = 2; }
+        if (ntw == 13) { fn = k_sweep_dmma2<13, SW_BWD_LT>; slot = 3; }
+        if (ntw == 17) { fn = k_sweep_dmma2<17, SW_BWD_LT>; slot = 4; }
+        if (ntw == 21) { fn = k_sweep_dmma2<21, SW_BWD_LT>; slot = 5; }
+        if (ntw == 25) { fn = k_sweep_dmma2<25, SW_BWD_LT>; slot = 6; }
+    } else {
+        if (ntw == 5) { fn = k_sweep_dmma2<5, SW_BWD_LT, true>; slot = 7; }
+        if (ntw == 9) { fn = k_sweep_dmma2<9, SW_BWD_LT, true>; slot = 8; }
+        if (ntw == 13) { fn = k_sweep_dmma2<13, SW_BWD_LT, true>; slot = 9; }
+        if (ntw == 17) { fn = k_sweep_dmma2<17, SW_BWD_LT, true>; slot = 10; }
+        if (ntw == 21) { fn = k_sweep_dmma2<21, SW_BWD_LT, true>; slot = 11; }
+        if (ntw == 25) { fn = k_sweep_dmma2<25, SW_BWD_LT, true>; slot = 12; }
+    }
     if (!fn) return false;
-    const size_t smem = dmma2_sweep_smem(ntw);
+    const size_t smem = dmma2_sweep_smem(ntw, ncw, pair);
     if (smem > 227 * 1024) return false;
-    static bool attr_done[7] = {};
+    static bool attr_done[13] = {};
     if (!attr_done[slot]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done[slot] = true;
