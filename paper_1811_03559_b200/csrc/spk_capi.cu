@@ -1338,7 +1338,8 @@ struct Exec {
         // narrow solves (<= 8 right-hand sides): the producer/consumer sweep
         // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>)
         static const bool pair_on = !(getenv("SPK_SWEEP_PAIR") && !atoi(getenv("SPK_SWEEP_PAIR")));
-        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= 8 && st.kwmax > 16 && st.kwmax <= 192) {
+        static const int pair_maxnc = getenv("SPK_PAIR_MAXNC") ? atoi(getenv("SPK_PAIR_MAXNC")) : 8;
+        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= pair_maxnc && st.kwmax > 16 && st.kwmax <= 192) {
             static const int ntws[] = {5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
@@ -1347,13 +1348,14 @@ struct Exec {
                     break;
                 }
             FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
+            const int ncw = 2 * ((nc + 7) / 8);  // one warp pair per 8 columns
             const dim3 grid(st.njobs, 1);
             bool ok = false;
             switch (st.mode) {
-                case SW_FWD_L: ok = launch_sweep_dmma2_fl(ntw, 2, grid, A, s, true); break;
-                case SW_BWD_U: ok = launch_sweep_dmma2_bu(ntw, 2, grid, A, s, true); break;
-                case SW_FWD_UT: ok = launch_sweep_dmma2_fut(ntw, 2, grid, A, s, true); break;
-                default: ok = launch_sweep_dmma2_blt(ntw, 2, grid, A, s, true); break;
+                case SW_FWD_L: ok = launch_sweep_dmma2_fl(ntw, ncw, grid, A, s, true); break;
+                case SW_BWD_U: ok = launch_sweep_dmma2_bu(ntw, ncw, grid, A, s, true); break;
+                case SW_FWD_UT: ok = launch_sweep_dmma2_fut(ntw, ncw, grid, A, s, true); break;
+                default: ok = launch_sweep_dmma2_blt(ntw, ncw, grid, A, s, true); break;
             }
             if (ok) return true;
         }
