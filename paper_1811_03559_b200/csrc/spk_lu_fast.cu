@@ -407,7 +407,7 @@ __device__ __forceinline__ int bfrag(int k, int n) { return (k >> 2) * 32 + n * 
 // J), so the per-step rotation moves one tile in and one out.  T = 21 (k <=
 // 160) needs it: 20 warps leave 96 registers per thread.
 template <int T, int TR>
-__global__ void __launch_bounds__(32 * (T - 1), 1) k_band_lu_dmma(FastLuArgs A) {
+__global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(FastLuArgs A) {
     using S = LuDmmaSmem<T, TR>;
     constexpr int NS = T - TR;
     constexpr int NW = T - 1;
