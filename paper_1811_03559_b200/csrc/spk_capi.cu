@@ -1339,8 +1339,8 @@ struct Exec {
         // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>)
         static const bool pair_on = !(getenv("SPK_SWEEP_PAIR") && !atoi(getenv("SPK_SWEEP_PAIR")));
         static const int pair_maxnc = getenv("SPK_PAIR_MAXNC") ? atoi(getenv("SPK_PAIR_MAXNC")) : 8;
-        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= pair_maxnc && st.kwmax > 16 && st.kwmax <= 192) {
-            static const int ntws[] = {5, 9, 13, 17, 21, 25};
+        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= pair_maxnc && st.kwmax >= 8 && st.kwmax <= 192) {
+            static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
                 if (8 * (t - 1) >= st.kwmax) {

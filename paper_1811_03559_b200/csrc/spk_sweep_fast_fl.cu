@@ -104,6 +104,7 @@ bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, 
         if (ntw == 21) { fn = k_sweep_dmma2<21, SW_FWD_L>; slot = 5; }
         if (ntw == 25) { fn = k_sweep_dmma2<25, SW_FWD_L>; slot = 6; }
     } else {
+        if (ntw == 3) { fn = k_sweep_dmma2<3, SW_FWD_L, true>; slot = 13; }
         if (ntw == 5) { fn = k_sweep_dmma2<5, SW_FWD_L, true>; slot = 7; }
         if (ntw == 9) { fn = k_sweep_dmma2<9, SW_FWD_L, true>; slot = 8; }
         if (ntw == 13) { fn = k_sweep_dmma2<13, SW_FWD_L, true>; slot = 9; }
@@ -114,7 +115,7 @@ bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, 
     if (!fn) return false;
     const size_t smem = dmma2_sweep_smem(ntw, ncw, pair);
     if (smem > 227 * 1024) return false;
-    static bool attr_done[13] = {};
+    static bool attr_done[14] = {};
     if (!attr_done[slot]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done[slot] = true;
