@@ -98,7 +98,16 @@ spk_status guarded(F&& f) {
 }  // namespace
 
 namespace spk {
-void count_launch(int n) { g_launches += n; }
+// every launcher calls this right after its launch: a launch that failed
+// (configuration, resources) raises here instead of leaving its output unwritten
+void count_launch(int n) {
+    g_launches += n;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(SPK_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    }
+}
 }  // namespace spk
 
 #include <chrono>
@@ -1338,6 +1347,9 @@ struct Exec {
         // narrow solves (<= 8 right-hand sides): the producer/consumer sweep
         // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>)
         static const bool pair_on = !(getenv("SPK_SWEEP_PAIR") && !atoi(getenv("SPK_SWEEP_PAIR")));
+        // Measured: narrow solves (<= 8 columns) gain at every bandwidth; wider
+        // ones were slower paired (C2's 64/128-column factor sweeps, C5's
+        // 32-column solves, C3)
         static const int pair_maxnc = getenv("SPK_PAIR_MAXNC") ? atoi(getenv("SPK_PAIR_MAXNC")) : 8;
         if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= pair_maxnc && st.kwmax >= 8 && st.kwmax <= 192) {
             static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
@@ -1348,8 +1360,10 @@ struct Exec {
                     break;
                 }
             FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
-            const int ncw = 2 * ((nc + 7) / 8);  // one warp pair per 8 columns
-            const dim3 grid(st.njobs, 1);
+            const int groups = (nc + 55) / 56;  // <= 7 pairs per CTA (16 warps with the producers: launch bound 512)
+            const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
+            const int ncw = 2 * (cols / 8);  // one warp pair per 8 columns
+            const dim3 grid(st.njobs, (nc + cols - 1) / cols);
             bool ok = false;
             switch (st.mode) {
                 case SW_FWD_L: ok = launch_sweep_dmma2_fl(ntw, ncw, grid, A, s, true); break;
