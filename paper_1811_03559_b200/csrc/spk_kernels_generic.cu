@@ -927,7 +927,10 @@ void launch_sweep(const SweepJob* d_jobs, int njobs, int max_nc, const PartDev* 
 void launch_copy(const CopyJob* d_jobs, int njobs, long long max_elems, const Bufs& B, int ncols,
                  cudaStream_t s) {
     if (njobs <= 0 || max_elems <= 0) return;
-    dim3 g(grid_for(max_elems, 256, 2048), njobs);
+    // ~8k CTAs per launch at most: batched stages are often guarded off (the
+    // other coupling path) and every early-exiting CTA still costs a slot
+    const int cap = std::max(32, std::min(2048, 8192 / njobs));
+    dim3 g(grid_for(max_elems, 256, cap), njobs);
     k_copy<<<g, 256, 0, s>>>(d_jobs, B, ncols);
     count_launch();
 }
@@ -953,7 +956,9 @@ void launch_build_coupling(const CouplingJob* d_jobs, int njobs, long long max_e
                            const PartDev* d_parts, const double* pool, double* fac, int* piv,
                            unsigned long long* amax, const int* flags, cudaStream_t s) {
     if (njobs <= 0) return;
-    dim3 g(grid_for(max_elems, 256, 256), njobs);
+    // <= 32 blocks per pair: most launches are guarded off (Schur path) and a
+    // wide grid of early exits alone cost ~20 us per level
+    dim3 g(grid_for(max_elems, 256, 32), njobs);
     k_build_coupling<<<g, 256, 0, s>>>(d_jobs, d_parts, pool, fac, piv, amax, flags);
     count_launch();
 }
