@@ -1409,19 +1409,23 @@ struct Exec {
                     ntw = t;
                     break;
                 }
+            // 9..32 columns: warp pairs per 8 columns (the window split; a warp
+            // issues at most one DMMA per ~32 cycles)
+            static const int v1_pair_maxnc = getenv("SPK_V1_PAIR_MAXNC") ? atoi(getenv("SPK_V1_PAIR_MAXNC")) : 32;
+            const bool pair = ntw >= 9 && nc > 8 && nc <= v1_pair_maxnc;
             const int groups = (nc + 127) / 128;
             const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
-            const int nwd = cols / 8;
+            const int nwd = (pair ? 2 : 1) * (cols / 8);
             const dim3 grid(st.njobs, (nc + cols - 1) / cols);
-            const size_t smem = dmma_sweep_smem(ntw, nwd);
+            const size_t smem = dmma_sweep_smem(ntw, nwd, pair);
             FastSweepArgs A{jobs, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_piv, B, ncols};
             if (smem <= 227 * 1024) {
                 bool ok = false;
                 switch (st.mode) {
-                    case SW_FWD_L: ok = launch_sweep_dmma_fl(ntw, nwd, grid, smem, A, s); break;
-                    case SW_BWD_U: ok = launch_sweep_dmma_bu(ntw, nwd, grid, smem, A, s); break;
-                    case SW_FWD_UT: ok = launch_sweep_dmma_fut(ntw, nwd, grid, smem, A, s); break;
-                    default: ok = launch_sweep_dmma_blt(ntw, nwd, grid, smem, A, s); break;
+                    case SW_FWD_L: ok = launch_sweep_dmma_fl(ntw, nwd, grid, smem, A, s, pair); break;
+                    case SW_BWD_U: ok = launch_sweep_dmma_bu(ntw, nwd, grid, smem, A, s, pair); break;
+                    case SW_FWD_UT: ok = launch_sweep_dmma_fut(ntw, nwd, grid, smem, A, s, pair); break;
+                    default: ok = launch_sweep_dmma_blt(ntw, nwd, grid, smem, A, s, pair); break;
                 }
                 if (ok) return true;
             }

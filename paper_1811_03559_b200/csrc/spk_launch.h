@@ -119,10 +119,14 @@ bool launch_sweep_dmma2_fut(int ntw, int ncw, dim3 grid, const FastSweepArgs& A,
                            bool pair = false);
 bool launch_sweep_dmma2_blt(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
                            bool pair = false);
-bool launch_sweep_dmma_fl(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma_bu(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
-bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s);
+bool launch_sweep_dmma_fl(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s,
+                          bool pair = false);
+bool launch_sweep_dmma_bu(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s,
+                          bool pair = false);
+bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s,
+                          bool pair = false);
+bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s,
+                          bool pair = false);
 void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
                               double* tfac, double* dinv, cudaStream_t s);
 

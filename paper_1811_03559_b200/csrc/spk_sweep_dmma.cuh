@@ -38,14 +38,42 @@ struct DmmaGeom {
     static constexpr int SR = ((8 + KWT + 15) / 16) * 16 + 4;       // [step][row] stride, = 4 mod 16
 };
 
-inline size_t dmma_sweep_smem(int ntw, int nwarps) {
+// PAIR: nwarps counts both warps of each pair (ncta = 4 nwarps columns)
+inline size_t dmma_sweep_smem(int ntw, int nwarps, bool pair = false) {
     const int KWT = 8 * (ntw - 1);
     const int SR = ((8 + KWT + 15) / 16) * 16 + 4;
-    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * (nwarps * 8 + 1) * 8 + 4 * 64 * 8;
-    return 2 * per_stage + 64;
+    const int ncta = (pair ? nwarps / 2 : nwarps) * 8;
+    const size_t per_stage = (size_t)4 * 8 * SR * 8 + 32 * 8 + (size_t)32 * (ncta + 1) * 8 + 4 * 64 * 8;
+    return 2 * per_stage + 64 + (pair ? (size_t)(nwarps / 2) * (4 * 64 * 8 + 16) : 0);
 }
 
-template <int NTW, int MODE>
+__device__ __forceinline__ void sw_mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void sw_mbar_arrive(unsigned long long* bar) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void sw_mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// PAIR: two warps per 8 right-hand-side columns split the window (A: tiles
+// 0 .. HA-1 and X, B: tiles HA .. NTW-1 and the incoming rows), with the X
+// (A -> B) and front-tile (B -> A) handoffs of k_sweep_dmma2's pair mode;
+// each warp issues about half the DMMAs of a block (a warp issues at most one
+// per ~32 cycles, profiles/r01_dmma_occupancy.txt).
+template <int NTW, int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     constexpr int SR = DmmaGeom<NTW>::SR;
     constexpr int KWT = DmmaGeom<NTW>::KWT;
@@ -58,7 +86,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     const PartDev P = A.parts[J.part];
     const int nc_total = J.nc >= 0 ? J.nc : A.ncols;
     const int nwarps = blockDim.x >> 5;
-    const int ncta = nwarps * 8;
+    const int ncta = (PAIR ? nwarps / 2 : nwarps) * 8;
     const int sin_ld = ncta + 1;
     const int colbase = blockIdx.y * ncta;
     if (colbase >= nc_total) return;
@@ -99,7 +127,10 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     double* s_A = reinterpret_cast<double*>(smem_raw);      // [st][4 blocks][8 steps][SR rows]
     double* s_dg = s_A + 2 * 4 * 8 * SR;                     // [st][32]
     double* s_in = s_dg + 2 * 32;                            // [st][32 rows][ncta+1] (odd stride)
-    double* s_ti = s_in + 2 * 32 * (nwarps * 8 + 1);         // [st][4 blocks][8][8] inverse diagonal blocks
+    double* s_ti = s_in + 2 * 32 * (ncta + 1);               // [st][4 blocks][8][8] inverse diagonal blocks
+    double* s_pair = s_ti + 2 * 4 * 64;                       // PAIR: [pair][xbuf 2x64, tbuf 2x64]
+    unsigned long long* s_pbar = reinterpret_cast<unsigned long long*>(s_pair + (size_t)(nwarps / 2) * 4 * 64);
+    if (PAIR && threadIdx.x < nwarps) sw_mbar_init(s_pbar + threadIdx.x, 32);
 
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -111,7 +142,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
 
     const int c0 = J.c0 + colbase;
     const int ncta_valid = min(ncta, nc_total - colbase);
-    const int lc0 = warp * 8 + 2 * q;  // this lane's two columns (CTA-local)
+    const int lc0 = (PAIR ? warp >> 1 : warp) * 8 + 2 * q;  // this lane's two columns (CTA-local)
     const bool cv0 = lc0 < ncta_valid, cv1 = lc0 + 1 < ncta_valid;
     double* const cp0 = bbase + (long long)(c0 + (cv0 ? lc0 : 0)) * ld;
     double* const cp1 = bbase + (long long)(c0 + (cv1 ? lc0 + 1 : 0)) * ld;
@@ -149,16 +180,6 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
         cp_async_commit();
     };
 
-    // window: tile slot T <-> rows [8T, 8T+8) of the sweep, initially T = 0..NTW-1
-    double Wt[NTW][2];
-#pragma unroll
-    for (int T = 0; T < NTW; ++T) {
-        const int u = 8 * T + g;
-        const bool ok = u < nsteps;
-        const long long pr = ok ? phys(rowof(u)) : 0;
-        Wt[T][0] = (ok && cv0) ? cp0[pr] : 0.0;
-        Wt[T][1] = (ok && cv1) ? cp1[pr] : 0.0;
-    }
     load_round(0);
 
     // Per 8-row block the system is  P = M X  with M the 8x8 diagonal block of
@@ -192,66 +213,194 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
         __syncthreads();
     };
 
-    // The tile registers rotate by one slot per block, so Wt[0] is always the
-    // pivot tile and Wt[i] holds rows [8i, 8i+8) past it: one loop body.
-    const int nblocks = (nsteps + 7) / 8;
-    for (int b = 0; b < nblocks; ++b) {
-        const int st = (b >> 2) & 1, bb = b & 3;
-        if (bb == 0) {
-            cp_async_wait<0>();
-            __syncthreads();
-            prep_round(st, 8 * b);
-            load_round((b >> 2) + 1);
-        }
-        const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
-        const double* T = s_ti + (size_t)(st * 4 + bb) * 64;
-        // P (C layout: row g, cols 2q..2q+1) -> B fragments: B[k][n] = P[4s+k][n]
-        double pb[2];
+    if constexpr (PAIR) {
+        constexpr int HA = (NTW + 1) / 2, HB = NTW - HA;
+        const int pr_ = warp >> 1, role = warp & 1;
+        double* xbuf = s_pair + (size_t)pr_ * 4 * 64;  // [2][64]: -X as B fragments (A -> B)
+        double* tbuf = xbuf + 128;                      // [2][64]: B's front tile (B -> A)
+        unsigned long long* mbx = s_pbar + 2 * pr_;
+        unsigned long long* mbt = mbx + 1;
+        const int nblocks = (nsteps + 7) / 8;
+        if (role == 0) {
+            double Wt[HA][2];
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-            const int src = 4 * (4 * s2 + q) + (g >> 1);
-            const double v0 = __shfl_sync(0xffffffffu, Wt[0][0], src);
-            const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
-            pb[s2] = (g & 1) ? v1 : v0;
-        }
-        // X = Tinv P : the 8 finished rows (C layout)
-        double x0 = 0.0, x1 = 0.0;
-        dmma_acc(x0, x1, T[g * 8 + q], pb[0]);
-        dmma_acc(x0, x1, T[g * 8 + 4 + q], pb[1]);
-        // X -> B fragments (negated)
-        double nb[2];
+            for (int T = 0; T < HA; ++T) {
+                const int u = 8 * T + g;
+                const bool ok = u < nsteps;
+                const long long pr = ok ? phys(rowof(u)) : 0;
+                Wt[T][0] = (ok && cv0) ? cp0[pr] : 0.0;
+                Wt[T][1] = (ok && cv1) ? cp1[pr] : 0.0;
+            }
+            for (int b = 0; b < nblocks; ++b) {
+                const int st = (b >> 2) & 1, bb = b & 3;
+                if (bb == 0) {
+                    cp_async_wait<0>();
+                    __syncthreads();
+                    prep_round(st, 8 * b);
+                    load_round((b >> 2) + 1);
+                }
+                const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
+                const double* T = s_ti + (size_t)(st * 4 + bb) * 64;
+                double pb[2];
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-            const int src = 4 * (4 * s2 + q) + (g >> 1);
-            const double v0 = __shfl_sync(0xffffffffu, x0, src);
-            const double v1 = __shfl_sync(0xffffffffu, x1, src);
-            nb[s2] = -((g & 1) ? v1 : v0);
-        }
-        // rank-8 update: the next pivot tile first, then k-slice-major so the
-        // two DMMAs of a tile are NTW-2 instructions apart
-        dmma_acc(Wt[1][0], Wt[1][1], Ab[q * SR + 8 + g], nb[0]);
-        dmma_acc(Wt[1][0], Wt[1][1], Ab[(4 + q) * SR + 8 + g], nb[1]);
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const int src = 4 * (4 * s2 + q) + (g >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, Wt[0][0], src);
+                    const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
+                    pb[s2] = (g & 1) ? v1 : v0;
+                }
+                double x0 = 0.0, x1 = 0.0;
+                dmma_acc(x0, x1, T[g * 8 + q], pb[0]);
+                dmma_acc(x0, x1, T[g * 8 + 4 + q], pb[1]);
+                double nb[2];
 #pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2)
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const int src = 4 * (4 * s2 + q) + (g >> 1);
+                    const double v0 = __shfl_sync(0xffffffffu, x0, src);
+                    const double v1 = __shfl_sync(0xffffffffu, x1, src);
+                    nb[s2] = -((g & 1) ? v1 : v0);
+                }
+                *reinterpret_cast<double2*>(xbuf + (b & 1) * 64 + 2 * lane) = make_double2(nb[0], nb[1]);
+                if (b > 0) sw_mbar_wait(mbt, (b - 1) & 1);  // B took X of block b-1: one phase apart
+                sw_mbar_arrive(mbx);
+                if (b > 0) {  // my last tile is B's front tile of the previous block
+                    const double2 t = *reinterpret_cast<const double2*>(tbuf + ((b - 1) & 1) * 64 + 2 * lane);
+                    Wt[HA - 1][0] = t.x;
+                    Wt[HA - 1][1] = t.y;
+                }
+                dmma_acc(Wt[1][0], Wt[1][1], Ab[q * SR + 8 + g], nb[0]);
+                dmma_acc(Wt[1][0], Wt[1][1], Ab[(4 + q) * SR + 8 + g], nb[1]);
 #pragma unroll
-            for (int i = 2; i < NTW; ++i) dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * i + g], nb[s2]);
-        {
-            const int u = 8 * b + g;
-            if (u < nsteps) {
-                const long long pr = phys(rowof(u));
-                if (cv0) cp0[pr] = x0;
-                if (cv1) cp1[pr] = x1;
+                for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                    for (int i = 2; i < HA; ++i) dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * i + g], nb[s2]);
+                {
+                    const int u = 8 * b + g;
+                    if (u < nsteps) {
+                        const long long pr = phys(rowof(u));
+                        if (cv0) cp0[pr] = x0;
+                        if (cv1) cp1[pr] = x1;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < HA - 1; ++i) {
+                    Wt[i][0] = Wt[i + 1][0];
+                    Wt[i][1] = Wt[i + 1][1];
+                }
+            }
+        } else {
+            double Wt[HB][2];
+#pragma unroll
+            for (int T = 0; T < HB; ++T) {
+                const int u = 8 * (HA + T) + g;
+                const bool ok = u < nsteps;
+                const long long pr = ok ? phys(rowof(u)) : 0;
+                Wt[T][0] = (ok && cv0) ? cp0[pr] : 0.0;
+                Wt[T][1] = (ok && cv1) ? cp1[pr] : 0.0;
+            }
+            for (int b = 0; b < nblocks; ++b) {
+                const int st = (b >> 2) & 1, bb = b & 3;
+                if (bb == 0) {
+                    cp_async_wait<0>();
+                    __syncthreads();
+                    prep_round(st, 8 * b);
+                    load_round((b >> 2) + 1);
+                }
+                const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
+                sw_mbar_wait(mbx, b & 1);
+                const double2 x = *reinterpret_cast<const double2*>(xbuf + (b & 1) * 64 + 2 * lane);
+                const double nb[2] = {x.x, x.y};
+                dmma_acc(Wt[0][0], Wt[0][1], Ab[q * SR + 8 * HA + g], nb[0]);
+                dmma_acc(Wt[0][0], Wt[0][1], Ab[(4 + q) * SR + 8 * HA + g], nb[1]);
+                *reinterpret_cast<double2*>(tbuf + (b & 1) * 64 + 2 * lane) = make_double2(Wt[0][0], Wt[0][1]);
+                sw_mbar_arrive(mbt);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                    for (int i = 1; i < HB; ++i)
+                        dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * (HA + i) + g], nb[s2]);
+#pragma unroll
+                for (int i = 0; i < HB - 1; ++i) {
+                    Wt[i][0] = Wt[i + 1][0];
+                    Wt[i][1] = Wt[i + 1][1];
+                }
+                const double* in = s_in + (size_t)st * 32 * sin_ld + (8 * bb + g) * sin_ld + lc0;
+                Wt[HB - 1][0] = in[0];
+                Wt[HB - 1][1] = in[1];
             }
         }
-        // rotate; the freed slot takes rows 8(b+NTW)+g
+    } else {
+    // window: tile slot T <-> rows [8T, 8T+8) of the sweep, initially T = 0..NTW-1
+        double Wt[NTW][2];
 #pragma unroll
-        for (int i = 0; i < NTW - 1; ++i) {
-            Wt[i][0] = Wt[i + 1][0];
-            Wt[i][1] = Wt[i + 1][1];
+        for (int T = 0; T < NTW; ++T) {
+            const int u = 8 * T + g;
+            const bool ok = u < nsteps;
+            const long long pr = ok ? phys(rowof(u)) : 0;
+            Wt[T][0] = (ok && cv0) ? cp0[pr] : 0.0;
+            Wt[T][1] = (ok && cv1) ? cp1[pr] : 0.0;
         }
-        const double* in = s_in + (size_t)st * 32 * sin_ld + (8 * bb + g) * sin_ld + lc0;
-        Wt[NTW - 1][0] = in[0];
-        Wt[NTW - 1][1] = in[1];
+    // The tile registers rotate by one slot per block, so Wt[0] is always the
+        // pivot tile and Wt[i] holds rows [8i, 8i+8) past it: one loop body.
+        const int nblocks = (nsteps + 7) / 8;
+        for (int b = 0; b < nblocks; ++b) {
+            const int st = (b >> 2) & 1, bb = b & 3;
+            if (bb == 0) {
+                cp_async_wait<0>();
+                __syncthreads();
+                prep_round(st, 8 * b);
+                load_round((b >> 2) + 1);
+            }
+            const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
+            const double* T = s_ti + (size_t)(st * 4 + bb) * 64;
+            // P (C layout: row g, cols 2q..2q+1) -> B fragments: B[k][n] = P[4s+k][n]
+            double pb[2];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int src = 4 * (4 * s2 + q) + (g >> 1);
+                const double v0 = __shfl_sync(0xffffffffu, Wt[0][0], src);
+                const double v1 = __shfl_sync(0xffffffffu, Wt[0][1], src);
+                pb[s2] = (g & 1) ? v1 : v0;
+            }
+            // X = Tinv P : the 8 finished rows (C layout)
+            double x0 = 0.0, x1 = 0.0;
+            dmma_acc(x0, x1, T[g * 8 + q], pb[0]);
+            dmma_acc(x0, x1, T[g * 8 + 4 + q], pb[1]);
+            // X -> B fragments (negated)
+            double nb[2];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int src = 4 * (4 * s2 + q) + (g >> 1);
+                const double v0 = __shfl_sync(0xffffffffu, x0, src);
+                const double v1 = __shfl_sync(0xffffffffu, x1, src);
+                nb[s2] = -((g & 1) ? v1 : v0);
+            }
+            // rank-8 update: the next pivot tile first, then k-slice-major so the
+            // two DMMAs of a tile are NTW-2 instructions apart
+            dmma_acc(Wt[1][0], Wt[1][1], Ab[q * SR + 8 + g], nb[0]);
+            dmma_acc(Wt[1][0], Wt[1][1], Ab[(4 + q) * SR + 8 + g], nb[1]);
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int i = 2; i < NTW; ++i) dmma_acc(Wt[i][0], Wt[i][1], Ab[(4 * s2 + q) * SR + 8 * i + g], nb[s2]);
+            {
+                const int u = 8 * b + g;
+                if (u < nsteps) {
+                    const long long pr = phys(rowof(u));
+                    if (cv0) cp0[pr] = x0;
+                    if (cv1) cp1[pr] = x1;
+                }
+            }
+            // rotate; the freed slot takes rows 8(b+NTW)+g
+#pragma unroll
+            for (int i = 0; i < NTW - 1; ++i) {
+                Wt[i][0] = Wt[i + 1][0];
+                Wt[i][1] = Wt[i + 1][1];
+            }
+            const double* in = s_in + (size_t)st * 32 * sin_ld + (8 * bb + g) * sin_ld + lc0;
+            Wt[NTW - 1][0] = in[0];
+            Wt[NTW - 1][1] = in[1];
+        }
     }
     cp_async_wait<0>();
 }

@@ -47,18 +47,27 @@ bool launch_sweep_fast_fut(int tr, int nc, bool piv, int nwarps, dim3 grid, size
     return true;
 }
 
-bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s) {
+bool launch_sweep_dmma_fut(int ntw, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A, cudaStream_t s,
+                          bool pair) {
     void (*fn)(FastSweepArgs) = nullptr;
     int slot = -1;
-    if (ntw == 3) { fn = k_sweep_dmma<3, SW_FWD_UT>; slot = 0; }
-    if (ntw == 5) { fn = k_sweep_dmma<5, SW_FWD_UT>; slot = 1; }
-    if (ntw == 9) { fn = k_sweep_dmma<9, SW_FWD_UT>; slot = 2; }
-    if (ntw == 13) { fn = k_sweep_dmma<13, SW_FWD_UT>; slot = 3; }
-    if (ntw == 17) { fn = k_sweep_dmma<17, SW_FWD_UT>; slot = 4; }
-    if (ntw == 21) { fn = k_sweep_dmma<21, SW_FWD_UT>; slot = 5; }
-    if (ntw == 25) { fn = k_sweep_dmma<25, SW_FWD_UT>; slot = 6; }
+    if (!pair) {
+        if (ntw == 3) { fn = k_sweep_dmma<3, SW_FWD_UT>; slot = 0; }
+        if (ntw == 5) { fn = k_sweep_dmma<5, SW_FWD_UT>; slot = 1; }
+        if (ntw == 9) { fn = k_sweep_dmma<9, SW_FWD_UT>; slot = 2; }
+        if (ntw == 13) { fn = k_sweep_dmma<13, SW_FWD_UT>; slot = 3; }
+        if (ntw == 17) { fn = k_sweep_dmma<17, SW_FWD_UT>; slot = 4; }
+        if (ntw == 21) { fn = k_sweep_dmma<21, SW_FWD_UT>; slot = 5; }
+        if (ntw == 25) { fn = k_sweep_dmma<25, SW_FWD_UT>; slot = 6; }
+    } else {
+        if (ntw == 9) { fn = k_sweep_dmma<9, SW_FWD_UT, true>; slot = 7; }
+        if (ntw == 13) { fn = k_sweep_dmma<13, SW_FWD_UT, true>; slot = 8; }
+        if (ntw == 17) { fn = k_sweep_dmma<17, SW_FWD_UT, true>; slot = 9; }
+        if (ntw == 21) { fn = k_sweep_dmma<21, SW_FWD_UT, true>; slot = 10; }
+        if (ntw == 25) { fn = k_sweep_dmma<25, SW_FWD_UT, true>; slot = 11; }
+    }
     if (!fn) return false;
-    static bool attr_done[7] = {};
+    static bool attr_done[12] = {};
     if (!attr_done[slot]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done[slot] = true;
