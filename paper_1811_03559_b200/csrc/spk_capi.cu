@@ -1413,7 +1413,7 @@ struct Exec {
             // issues at most one DMMA per ~32 cycles)
             static const int v1_pair_maxnc = getenv("SPK_V1_PAIR_MAXNC") ? atoi(getenv("SPK_V1_PAIR_MAXNC")) : 32;
             const bool pair = ntw >= 9 && nc > 8 && nc <= v1_pair_maxnc;
-            const int groups = (nc + 127) / 128;
+            const int groups = pair ? (nc + 63) / 64 : (nc + 127) / 128;  // <= 16 warps per CTA
             const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
             const int nwd = (pair ? 2 : 1) * (cols / 8);
             const dim3 grid(st.njobs, (nc + cols - 1) / cols);
