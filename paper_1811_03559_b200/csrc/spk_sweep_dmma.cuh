@@ -47,27 +47,6 @@ inline size_t dmma_sweep_smem(int ntw, int nwarps, bool pair = false) {
     return 2 * per_stage + 64 + (pair ? (size_t)(nwarps / 2) * (4 * 64 * 8 + 16) : 0);
 }
 
-__device__ __forceinline__ void sw_mbar_init(unsigned long long* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
-}
-__device__ __forceinline__ void sw_mbar_arrive(unsigned long long* bar) {
-    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }\n" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void sw_mbar_wait(unsigned long long* bar, unsigned parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n"
-        " .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n"
-        "}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
 // PAIR: two warps per 8 right-hand-side columns split the window (A: tiles
 // 0 .. HA-1 and X, B: tiles HA .. NTW-1 and the incoming rows), with the X
 // (A -> B) and front-tile (B -> A) handoffs of k_sweep_dmma2's pair mode;
@@ -130,7 +109,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     double* s_ti = s_in + 2 * 32 * (ncta + 1);               // [st][4 blocks][8][8] inverse diagonal blocks
     double* s_pair = s_ti + 2 * 4 * 64;                       // PAIR: [pair][xbuf 2x64, tbuf 2x64]
     unsigned long long* s_pbar = reinterpret_cast<unsigned long long*>(s_pair + (size_t)(nwarps / 2) * 4 * 64);
-    if (PAIR && threadIdx.x < nwarps) sw_mbar_init(s_pbar + threadIdx.x, 32);
+    if (PAIR && threadIdx.x < nwarps) mbar_init(s_pbar + threadIdx.x, 32);
 
     const View& v = J.v;
     const long long ld = v.ld >= 0 ? v.ld : A.B.ld[v.buf];
@@ -261,8 +240,8 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
                     nb[s2] = -((g & 1) ? v1 : v0);
                 }
                 *reinterpret_cast<double2*>(xbuf + (b & 1) * 64 + 2 * lane) = make_double2(nb[0], nb[1]);
-                if (b > 0) sw_mbar_wait(mbt, (b - 1) & 1);  // B took X of block b-1: one phase apart
-                sw_mbar_arrive(mbx);
+                if (b > 0) mbar_wait(mbt, (b - 1) & 1);  // B took X of block b-1: one phase apart
+                mbar_arrive(mbx);
                 if (b > 0) {  // my last tile is B's front tile of the previous block
                     const double2 t = *reinterpret_cast<const double2*>(tbuf + ((b - 1) & 1) * 64 + 2 * lane);
                     Wt[HA - 1][0] = t.x;
@@ -307,13 +286,13 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
                     load_round((b >> 2) + 1);
                 }
                 const double* Ab = s_A + (size_t)((st * 4 + bb) * 8) * SR;
-                sw_mbar_wait(mbx, b & 1);
+                mbar_wait(mbx, b & 1);
                 const double2 x = *reinterpret_cast<const double2*>(xbuf + (b & 1) * 64 + 2 * lane);
                 const double nb[2] = {x.x, x.y};
                 dmma_acc(Wt[0][0], Wt[0][1], Ab[q * SR + 8 * HA + g], nb[0]);
                 dmma_acc(Wt[0][0], Wt[0][1], Ab[(4 + q) * SR + 8 * HA + g], nb[1]);
                 *reinterpret_cast<double2*>(tbuf + (b & 1) * 64 + 2 * lane) = make_double2(Wt[0][0], Wt[0][1]);
-                sw_mbar_arrive(mbt);
+                mbar_arrive(mbt);
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
