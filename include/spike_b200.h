@@ -302,6 +302,14 @@ void spk_arena_trim(void);
 /* Number of kernel launches issued by this library on the calling thread
  * since the last reset (instrumentation for bench.py's gpu_launches). */
 int64_t spk_launch_count(int32_t reset);
+/* Of those, launches of the generic correctness-baseline kernels (per-column
+ * sweeps, scalar GEMM, unblocked LU): stages no tuned kernel covers.  Zero on
+ * the BASELINE configurations; bench.py reports it. */
+int64_t spk_generic_launch_count(int32_t reset);
+/* Test hook: 1 routes every stage of factorizations created afterwards (and
+ * all solves) through the generic kernels, the correctness baseline the tuned
+ * kernels are compared against; 0 restores the tuned dispatch.  Process-wide. */
+void spk_set_generic_path(int32_t on);
 
 /* Optional per-kernel-class CUDA-event timing (calling thread): launches are
  * bracketed by events on their stream; spk_profile_read drains and returns

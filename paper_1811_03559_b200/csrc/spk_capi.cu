@@ -64,6 +64,12 @@ using namespace spk;
 namespace {
 thread_local std::string g_err;
 thread_local long long g_launches = 0;
+// launches of the generic correctness-baseline kernels (k_sweep, k_gemm,
+// k_band_lu): stages whose shape no tuned kernel covers, or every stage when
+// spk_set_generic_path(1) forces that path (tests)
+thread_local long long g_generic_launches = 0;
+std::atomic<int> g_generic{0};
+bool generic_path() { return g_generic.load(std::memory_order_relaxed) != 0; }
 
 struct SpkError {
     spk_status st;
@@ -107,6 +113,35 @@ void count_launch(int n) {
         (void)cudaGetLastError();
         fail(SPK_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
     }
+}
+
+// The dynamic shared-memory limit of a kernel is a per-device attribute: keep
+// the largest value set per (device, kernel) and only ever raise it, so
+// concurrent launchers never lower it under each other.
+void set_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    int& cur = done[{dev, fn}];
+    if (bytes <= cur) return;
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "cudaFuncSetAttribute");
+    cur = bytes;
+}
+
+int device_sms() {
+    static std::mutex mu;
+    static std::map<int, int> sms;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = sms.find(dev);
+    if (it != sms.end()) return it->second;
+    int v = 0;
+    ck(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    sms[dev] = v;
+    return v;
 }
 }  // namespace spk
 
@@ -455,11 +490,22 @@ struct spk_fact {
     int boost_count = 0, boost_warnings = 0;
     cudaStream_t stream = nullptr;
     // spk_factorize returns once the work is enqueued; the host-side finish
-    // (status, boost counts, coupling paths -> solve programs) runs at the
-    // first call that needs it (ensure_finished)
-    bool pending = false;
+    // (status, boost counts, coupling paths -> solve programs) runs once, at
+    // the first call that needs it (ensure_finished, under fin_mu).  Its
+    // outcome is sticky: every later consumer re-raises a failure.
+    std::mutex fin_mu;
+    std::atomic<bool> pending{false};
+    spk_status fin_status = SPK_OK;
+    std::string fin_msg;
     cudaEvent_t upload_ev = nullptr;  // host band upload done (orders later host-solve uploads after it)
+    // recorded on `stream` after the factor program and after every upload of
+    // solve jobs: solves on other streams wait on it (wait_ready)
+    cudaEvent_t ready_ev = nullptr;
     char* d_sblob_prev = nullptr;     // guarded solve jobs used while pending
+    // last use of the factorization by each solve stream other than `stream`:
+    // the destructor orders the release of the device memory after them
+    std::mutex use_mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
 
     // closed-edge predicates (reference kinds: the first partition has no W,
     // the last no V and is factored as UL)
@@ -471,13 +517,19 @@ struct spk_fact {
 
     ~spk_fact() {
         // stream-ordered release on the factorization's stream (which must
-        // outlive it); no device-wide synchronisation
+        // outlive it), after the last use by any other solve stream; no
+        // device-wide synchronisation
+        for (auto& u : uses) {
+            cudaStreamWaitEvent(stream, u.second, 0);
+            cudaEventDestroy(u.second);
+        }
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
                         (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags, (void*)d_sblob_prev,
                         (void*)d_lblk})
             if (q) dfree(q, stream);
         if (upload_ev) cudaEventDestroy(upload_ev);
+        if (ready_ev) cudaEventDestroy(ready_ev);
     }
 };
 
@@ -617,8 +669,7 @@ struct Builder {
         }
         s.max_nc = mx;
         // fast-path eligibility
-        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
-        bool fast = !generic_only && !f.reduced_only;
+        bool fast = !generic_path() && !f.reduced_only;
         int kwneed = 1, kwmax = 1;
         for (auto& j : jobs) {
             const PartDev& P = f.parts[j.part];
@@ -1336,22 +1387,13 @@ struct Exec {
             PivSweepArgs A{jobs, f.d_parts, f.d_lblk, B, ncols};
             if (launch_sweep_piv_dmma(f.lblk_trw, cols / 8, grid, A, s)) return true;
         }
-        static const bool no_dmma = getenv("SPK_NO_DMMA_SWEEP") && atoi(getenv("SPK_NO_DMMA_SWEEP"));
-        static const bool sweep_v1 = getenv("SPK_SWEEP_V1") && atoi(getenv("SPK_SWEEP_V1"));
-        // producer/consumer DMMA sweep (spk_sweep_dmma2.cuh): <= 14 compute warps
-        // (8 columns each) + 2 producer warps per CTA.  Taken when it needs no
-        // more column groups than the 16-warp kernel below (each group re-reads
-        // the factor) and keeps >= 6 compute warps busy (with fewer, one warp's
-        // dependency chain sets the pace and the synchronous kernel wins).
-        static const bool sweep_v2 = getenv("SPK_SWEEP_V2") && atoi(getenv("SPK_SWEEP_V2"));
         // narrow solves (<= 8 right-hand sides): the producer/consumer sweep
-        // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>)
-        static const bool pair_on = !(getenv("SPK_SWEEP_PAIR") && !atoi(getenv("SPK_SWEEP_PAIR")));
-        // Measured: narrow solves (<= 8 columns) gain at every bandwidth; wider
-        // ones were slower paired (C2's 64/128-column factor sweeps, C5's
-        // 32-column solves, C3)
-        static const int pair_maxnc = getenv("SPK_PAIR_MAXNC") ? atoi(getenv("SPK_PAIR_MAXNC")) : 8;
-        if (pair_on && !no_dmma && !sweep_v1 && !st.piv && nc <= pair_maxnc && st.kwmax >= 8 && st.kwmax <= 192) {
+        // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>).
+        // Measured: narrow solves gain at every bandwidth; wider ones were
+        // slower paired (C2's 64/128-column factor sweeps, C5's 32-column
+        // solves, C3)
+        constexpr int pair_maxnc = 8;
+        if (!st.piv && nc <= pair_maxnc && st.kwmax >= 8 && st.kwmax <= 192) {
             static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
@@ -1373,10 +1415,14 @@ struct Exec {
             }
             if (ok) return true;
         }
+        // producer/consumer DMMA sweep (spk_sweep_dmma2.cuh): <= 14 compute warps
+        // (8 columns each) + 2 producer warps per CTA.  Taken when it needs no
+        // more column groups than the 16-warp kernel below (each group re-reads
+        // the factor) and keeps >= 6 compute warps busy (with fewer, one warp's
+        // dependency chain sets the pace and the synchronous kernel wins).
         const int groups2 = (nc + 111) / 112, groups1 = (nc + 127) / 128;
         const int cols2 = ((nc + groups2 - 1) / groups2 + 7) / 8 * 8;
-        if (!no_dmma && !sweep_v1 && !st.piv && nc >= 8 && st.kwmax <= 192 &&
-            (sweep_v2 || (groups2 == groups1 && cols2 >= 48))) {
+        if (!st.piv && nc >= 8 && st.kwmax <= 192 && groups2 == groups1 && cols2 >= 48) {
             static const int ntws[] = {3, 5, 9, 13, 17, 21, 25};
             int ntw = 0;
             for (int t : ntws)
@@ -1396,7 +1442,7 @@ struct Exec {
             }
             if (ok) return true;
         }
-        if (!no_dmma && !st.piv && st.kwmax <= 192) {
+        if (!st.piv && st.kwmax <= 192) {
             // blocked tensor-core sweep: 8 columns per warp, <= 16 warps per CTA,
             // column groups balanced across CTAs.  Narrow solves (nc < 8) run
             // padded to one warp: the chain per 8-row block (~4 DMMA latencies)
@@ -1411,8 +1457,7 @@ struct Exec {
                 }
             // 9..32 columns: warp pairs per 8 columns (the window split; a warp
             // issues at most one DMMA per ~32 cycles)
-            static const int v1_pair_maxnc = getenv("SPK_V1_PAIR_MAXNC") ? atoi(getenv("SPK_V1_PAIR_MAXNC")) : 32;
-            const bool pair = ntw >= 9 && nc > 8 && nc <= v1_pair_maxnc;
+            const bool pair = ntw >= 9 && nc > 8 && nc <= 32;
             const int groups = pair ? (nc + 63) / 64 : (nc + 127) / 128;  // <= 16 warps per CTA
             const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
             const int nwd = (pair ? 2 : 1) * (cols / 8);
@@ -1470,11 +1515,11 @@ struct Exec {
                 case ST_SWEEP: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
                     if (st.fast && run_fast_sweep(st, (const SweepJob*)jobs, nc)) break;
-                    static const bool no_small = getenv("SPK_SWEEP_SMALL") && !atoi(getenv("SPK_SWEEP_SMALL"));
-                    if (st.small_ch > 0 && !no_small &&
+                    if (st.small_ch > 0 && !generic_path() &&
                         launch_sweep_small((const SweepJob*)jobs, st.njobs, nc, st.small_ch, st.small_rows, f.d_parts,
                                            f.d_fac, f.d_piv, B, ncols, s))
                         break;
+                    ++g_generic_launches;
                     launch_sweep((const SweepJob*)jobs, st.njobs, nc, f.d_parts, f.d_fac, f.d_piv, B,
                                  ncols, s);
                     break;
@@ -1493,8 +1538,8 @@ struct Exec {
                 }
                 case ST_GEMM: {
                     const int nc = st.max_nc < 0 ? ncols : st.max_nc;
-                    static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
-                    if (generic_only) {
+                    if (generic_path()) {
+                        ++g_generic_launches;
                         launch_gemm((const GemmJob*)jobs, st.njobs, st.max_r, nc, B, ncols, s);
                     } else {
                         const int ns = gemm_splitk_factor(st.njobs, st.max_r, nc, st.max_kk);
@@ -1510,7 +1555,7 @@ struct Exec {
                 }
                 case ST_LU: {
                     if (st.partitions) {
-                        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
+                        const bool generic_only = generic_path();
                         const int kmax = std::max(f.kl, f.ku);
                         if (!f.piv_on && !generic_only && kmax <= 160) {
                             FastLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac, f.d_tfac,
@@ -1520,8 +1565,7 @@ struct Exec {
                                 break;
                             }
                         }
-                        static const bool piv_old = getenv("SPK_LU_PIV_OLD") && atoi(getenv("SPK_LU_PIV_OLD"));
-                        if (f.piv_on && !generic_only && !piv_old) {
+                        if (f.piv_on && !generic_only) {
                             // pivoted: blocked DMMA kernel (factor, pivots, row-major copy, 1/u_jj)
                             PivDmmaArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac,
                                           f.d_tfac, f.d_dinv, f.d_piv, f.d_status, f.d_lblk};
@@ -1544,10 +1588,8 @@ struct Exec {
                                             f.d_amax, s);
                     }
                     {
-                        static const bool no_small = getenv("SPK_LU_SMALL") && !atoi(getenv("SPK_LU_SMALL"));
-                        static const bool dense_old = getenv("SPK_DENSE_LU_OLD") && atoi(getenv("SPK_DENSE_LU_OLD"));
-                        static const bool generic_only = getenv("SPK_GENERIC") && atoi(getenv("SPK_GENERIC"));
-                        if (!st.partitions && !no_small && !dense_old && !generic_only) {
+                        const bool generic_only = generic_path();
+                        if (!st.partitions && !generic_only) {
                             // the pivoted 2k coupling units: blocked DMMA LU in place, then
                             // the shared-memory kernel redoes any unit with an exactly zero
                             // column (boosted non-pivoting fallback, kernels.cpp:67-77)
@@ -1559,11 +1601,12 @@ struct Exec {
                                                      f.d_status, f.d_flags, s, true))
                                 break;
                         }
-                        if (!no_small && launch_band_lu_small((const int*)jobs, st.njobs, st.max_r, f.d_parts,
+                        if (!generic_only && launch_band_lu_small((const int*)jobs, st.njobs, st.max_r, f.d_parts,
                                                               f.d_fac, f.d_piv, f.d_amax, f.boost_eps, f.d_boost,
                                                               f.d_fell, f.d_status, f.d_flags, s))
                             break;
                     }
+                    ++g_generic_launches;
                     launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
                                    f.boost_eps, f.d_boost, f.d_fell, f.d_status, f.d_flags, s);
                     break;
@@ -1647,7 +1690,8 @@ std::string sym_key(const spk_fact& f) {
     std::string key;
     auto put = [&](long long v) { key.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
     for (long long v : {f.n, (long long)f.kl, (long long)f.ku, (long long)f.k, (long long)f.p, (long long)f.piv_on,
-                        (long long)f.open_l, (long long)f.open_r, (long long)f.reduced_only})
+                        (long long)f.open_l, (long long)f.open_r, (long long)f.reduced_only,
+                        (long long)generic_path()})
         put(v);
     for (long long b : f.bounds) put(b);
     return key;
@@ -1781,8 +1825,7 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     f.d_blob = dalloc<char>(std::max<size_t>(blob.size(), 1), s);
     f.d_tfac = dalloc<double>(f.tfac_size, s);
     f.d_dinv = dalloc<double>(f.n, s);
-    static const bool piv_sweep_old = getenv("SPK_PIV_SWEEP_OLD") && atoi(getenv("SPK_PIV_SWEEP_OLD"));
-    f.lblk_trw = (!f.reduced_only && f.piv_on && !piv_sweep_old) ? piv_trw(f.kl, f.ku) : 0;
+    f.lblk_trw = (!f.reduced_only && f.piv_on) ? piv_trw(f.kl, f.ku) : 0;
     if (f.lblk_trw)
         f.d_lblk = dalloc<double>((f.bounds[p] / 8 + nparts + 2) * piv_rec_size(f.lblk_trw), s);
     tr.mark("allocations");
@@ -1803,6 +1846,34 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
 
 void build_solve_programs(spk_fact& f, cudaStream_t s);
 
+// the factorization's device state (factors, pool, flags, solve jobs) is
+// complete on f.stream up to here
+void mark_ready(spk_fact& f, cudaStream_t s) {
+    if (!f.ready_ev) ck(cudaEventCreateWithFlags(&f.ready_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(f.ready_ev, s), "event");
+}
+
+// order work on s after the factorization (a no-op on its own stream)
+void wait_ready(const spk_fact& f, cudaStream_t s) {
+    if (f.ready_ev && s != f.stream) ck(cudaStreamWaitEvent(s, f.ready_ev, 0), "wait");
+}
+
+// record the last use of f by stream s (see ~spk_fact)
+void note_use(const spk_fact& fc, cudaStream_t s) {
+    if (s == fc.stream) return;
+    spk_fact& f = const_cast<spk_fact&>(fc);
+    std::lock_guard<std::mutex> lk(f.use_mu);
+    for (auto& u : f.uses)
+        if (u.first == s) {
+            ck(cudaEventRecord(u.second, s), "event");
+            return;
+        }
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(e, s), "event");
+    f.uses.emplace_back(s, e);
+}
+
 void finish_factor(spk_fact& f, cudaStream_t s) {
     Tracer tr("finish");
     int status = 0;
@@ -1811,6 +1882,10 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     ck(cudaMemcpyAsync(&status, f.d_status, sizeof(int), cudaMemcpyDeviceToHost, s), "download");
     ck(cudaMemcpyAsync(boost.data(), f.d_boost, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
     ck(cudaMemcpyAsync(fell.data(), f.d_fell, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
+    // coupling paths, known once the factor program ran
+    std::vector<int> flags(std::max(f.npairs, 1), 0);
+    if (f.npairs > 0)
+        ck(cudaMemcpyAsync(flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost, s), "flags");
     ck(cudaStreamSynchronize(s), "factorize");
     tr.mark("stream synced");
     ck(cudaGetLastError(), "factorize kernels");
@@ -1824,10 +1899,9 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     if (!f.reduced_only && f.coupled())
         for (int i = 0; i < f.p; ++i) f.factor_sweeps[i] = (!f.first(i) && !f.last(i)) ? 3 : 0;
     // coupling paths are known now: compile the solve programs without guards
-    f.flags.assign(std::max(f.npairs, 1), 0);
-    if (f.npairs > 0)
-        ck(cudaMemcpy(f.flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost), "flags");
+    f.flags = std::move(flags);
     build_solve_programs(f, s);
+    mark_ready(f, s);
 }
 
 // Solve programs for f.flags (the per-pair coupling paths), or -- flags empty,
@@ -1895,10 +1969,24 @@ void build_solve_programs(spk_fact& f, cudaStream_t s) {
 // the deferred host-side finish of a factorization (stream-ordered
 // spk_factorize): synchronises its stream, reports an exactly singular pivot
 void ensure_finished(const spk_fact* fc) {
-    if (!fc || !fc->pending) return;
+    if (!fc) fail(SPK_EINVAL, "null factorization handle");
     spk_fact& f = const_cast<spk_fact&>(*fc);
-    f.pending = false;
-    finish_factor(f, f.stream);
+    if (f.pending.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lk(f.fin_mu);
+        if (f.pending.load(std::memory_order_relaxed)) {
+            try {
+                finish_factor(f, f.stream);
+            } catch (const SpkError& e) {
+                f.fin_status = e.st;
+                f.fin_msg = e.msg;
+            } catch (const std::bad_alloc&) {
+                f.fin_status = SPK_ENOMEM;
+                f.fin_msg = "host allocation failed";
+            }
+            f.pending.store(false, std::memory_order_release);
+        }
+    }
+    if (f.fin_status != SPK_OK) fail(f.fin_status, f.fin_msg);
 }
 
 Bufs make_bufs(const spk_fact* f = nullptr) {
@@ -1954,6 +2042,14 @@ int64_t spk_launch_count(int32_t reset) {
     if (reset) g_launches = 0;
     return v;
 }
+
+int64_t spk_generic_launch_count(int32_t reset) {
+    const long long v = g_generic_launches;
+    if (reset) g_generic_launches = 0;
+    return v;
+}
+
+void spk_set_generic_path(int32_t on) { g_generic.store(on ? 1 : 0); }
 
 void spk_compute_ratios(double K, int32_t nrhs, int32_t k, double* r12, double* r13) {
     // partition.cpp:47-54
@@ -2071,7 +2167,11 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
             // their sweeps are latency-bound at <= 8 warps per partition (C5:
             // 238 -> 216 ms per step); wide ones fill an SM per partition (C3:
             // p = 296 would cost 9 ms).
-            const int sms = 148;
+            // SMs of the current device (148 on B200; the planner is host-only
+            // and may run without a GPU, where it plans for a B200)
+            int ndev = 0, sms = 148;
+            if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) sms = device_sms();
+            (void)cudaGetLastError();
             if (k >= 96) pp = nrhs <= 64 ? 2 * sms : sms;
             else if (k >= 32) pp = 2 * sms;
             // narrow bands: up to 8 partitions per SM, but no shorter than
@@ -2220,8 +2320,8 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
                                  const spk_plan* plan, const spk_factor_options* opts, int open_l, int open_r,
                                  void* stream, spk_fact** out) {
     return guarded([&] {
-        *out = nullptr;
         if (!out) fail(SPK_EINVAL, "factorize: null output");
+        *out = nullptr;
         if (n < 1 || kl < 0 || ku < 0 || kl >= n || ku >= n) fail(SPK_EINVAL, "BandedMatrix: bad shape");
         validate_plan(n, plan);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -2287,11 +2387,12 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         ex.n = n;
         ex.band = dband;
         ex.run(f->prog_factor, f->d_blob);
+        mark_ready(*f, s);
         tr.mark("enqueued");
         if (fs) dfree(fs, s);
         if (auxf) dfree(auxf, s);
         if (tmp) dfree(tmp, s);
-        f->pending = true;  // finished lazily (ensure_finished)
+        f->pending.store(true);  // finished lazily (ensure_finished)
         *out = f.release();
     });
 }
@@ -2333,7 +2434,7 @@ spk_status spk_fact_unit_tips(const spk_fact* f, double* d_tips, void* stream) {
     });
 }
 
-int32_t spk_fact_open(const spk_fact* f) { return f->open_l | (f->open_r << 1); }
+int32_t spk_fact_open(const spk_fact* f) { return f ? (f->open_l | (f->open_r << 1)) : 0; }
 
 void spk_fact_destroy(spk_fact* f) { delete f; }
 
@@ -2361,7 +2462,9 @@ spk_status spk_fact_info(const spk_fact* f, int64_t* n, int32_t* kl, int32_t* ku
 }
 
 spk_status spk_fact_bounds(const spk_fact* f, int64_t* bounds) {
-    return guarded([&] { std::copy(f->bounds.begin(), f->bounds.end(), bounds); });
+    return guarded([&] {
+        if (!f || !bounds) fail(SPK_EINVAL, "fact_bounds: null argument");
+        std::copy(f->bounds.begin(), f->bounds.end(), bounds); });
 }
 
 spk_status spk_fact_factor_sweeps(const spk_fact* f, int64_t* sweeps) {
@@ -2406,7 +2509,7 @@ int64_t spk_fact_dump(const spk_fact* f, int32_t which, double* out) {
 }
 
 int32_t spk_fact_units(const spk_fact* f, int32_t l) {
-    if (l < 0 || l >= (int)f->levels.size()) return 0;
+    if (!f || l < 0 || l >= (int)f->levels.size()) return 0;
     return f->levels[l].units;
 }
 
@@ -2570,6 +2673,7 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
                                        int32_t nrhs, double* X, int64_t ldx, int32_t mem, cudaStream_t s) {
     spk_fact& f = const_cast<spk_fact&>(*fc);
     const long long n = f.n;
+    wait_ready(f, s);
     auto x = std::make_unique<spk_xsolve>();
     x->f = &f;
     x->transpose = transpose;
@@ -2661,10 +2765,16 @@ CopyStreams& copy_streams() {
 void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf, int32_t nrhs,
                           double* X, int64_t ldx, cudaStream_t s) {
     const long long n = fc->n;
+    // no host wait for a pending factorization: its guarded solve programs
+    // are used, and fin_mu keeps a concurrent finish from swapping them while
+    // this call enqueues
+    spk_fact& fm = const_cast<spk_fact&>(*fc);
+    std::lock_guard<std::mutex> lk(fm.fin_mu);
+    if (!fm.pending.load() && fm.fin_status != SPK_OK) fail(fm.fin_status, fm.fin_msg);
     CopyStreams& cs = copy_streams();
     // three column chunks: enough to hide the solve behind PCIe in both
     // directions while each chunk still fills the sweep kernels
-    static const int want = getenv("SPK_HOST_CHUNKS") ? std::max(1, atoi(getenv("SPK_HOST_CHUNKS"))) : 3;
+    constexpr int want = 3;
     const int chunk = std::max(16, ((nrhs + want - 1) / want + 7) / 8 * 8);
     const int nch = (nrhs + chunk - 1) / chunk;
     // F's staging buffer belongs to the upload stream, so the uploads start
@@ -2702,6 +2812,7 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
     // stream-ordered completion: s (and whoever synchronises it) is ordered
     // after the downloads; the host is not blocked
     ck(cudaStreamWaitEvent(s, ev[3 * nch - 1], 0), "wait");
+    note_use(*fc, s);
     dfree(dX, s);
     ck(cudaGetLastError(), "solve kernels");
     for (auto& e : ev) cudaEventDestroy(e);
@@ -2724,6 +2835,8 @@ extern "C" {
 spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int64_t ldf, int32_t nrhs,
                      double* X, int64_t ldx, int32_t mem, void* stream, spk_solve_stats* stats) {
     return guarded([&] {
+        if (!fc) fail(SPK_EINVAL, "solve: null factorization handle");
+        if (nrhs > 0 && (!F || !X)) fail(SPK_EINVAL, "solve: null F or X");
         const spk_fact& f = *fc;
         const long long n = f.n;
         if (nrhs < 0) fail(SPK_EINVAL, "solve: negative nrhs");
@@ -2740,6 +2853,7 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
         ensure_finished(fc);
         auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, mem, s);
         x->run_phase();
+        note_use(f, s);
         if (mem == SPK_MEM_HOST)
             ck(cudaMemcpy2DAsync(X, sizeof(double) * ldx, x->tX, sizeof(double) * n, sizeof(double) * n, nrhs,
                                  cudaMemcpyDeviceToHost, s),
@@ -2751,14 +2865,15 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
 }
 
 int32_t spk_xsolve_exchanges(const spk_fact* f, int32_t transpose) {
-    return f->open() && f->coupled() ? (transpose ? 2 : 1) : 0;
+    return f && f->open() && f->coupled() ? (transpose ? 2 : 1) : 0;
 }
 
 spk_status spk_xsolve_begin(const spk_fact* f, int32_t transpose, const double* d_F, int64_t ldf, int32_t nrhs,
                             double* d_X, int64_t ldx, void* stream, double* d_export, spk_xsolve** out) {
     return guarded([&] {
-        ensure_finished(f);
+        if (!out) fail(SPK_EINVAL, "xsolve: null output");
         *out = nullptr;
+        ensure_finished(f);
         if (nrhs < 1) fail(SPK_EINVAL, "xsolve: nrhs must be positive");
         if (ldf < f->n || ldx < f->n) fail(SPK_EINVAL, "xsolve: F.rows must equal n");
         if (!f->open() || !f->coupled()) fail(SPK_EINVAL, "xsolve: not a slab factorization");
@@ -2768,12 +2883,14 @@ spk_status spk_xsolve_begin(const spk_fact* f, int32_t transpose, const double* 
         const long long rows = x->export_rows(0);
         ck(cudaMemcpyAsync(d_export, x->XCH, sizeof(double) * rows * nrhs, cudaMemcpyDeviceToDevice, s), "export");
         ck(cudaGetLastError(), "xsolve");
+        note_use(*f, s);
         *out = x.release();
     });
 }
 
 spk_status spk_xsolve_step(spk_xsolve* x, const double* d_import, double* d_export) {
     return guarded([&] {
+        if (!x) fail(SPK_EINVAL, "xsolve: null handle");
         if (x->phase >= x->nphases) fail(SPK_EINVAL, "xsolve: solve already complete");
         const long long k = x->f->k;
         ck(cudaMemcpyAsync(x->XIN, d_import, sizeof(double) * 2 * k * x->nrhs, cudaMemcpyDeviceToDevice, x->s),
@@ -2785,6 +2902,7 @@ spk_status spk_xsolve_step(spk_xsolve* x, const double* d_import, double* d_expo
                                cudaMemcpyDeviceToDevice, x->s),
                "export");
         ck(cudaGetLastError(), "xsolve");
+        note_use(*x->f, x->s);
     });
 }
 
@@ -2793,8 +2911,10 @@ void spk_xsolve_end(spk_xsolve* x) { delete x; }
 spk_status spk_reduced_create(const double* vt, const double* vb, const double* wt, const double* wb, int32_t p,
                               int32_t k, double boost_eps, spk_reduced** out) {
     return guarded([&] {
+        if (!out) fail(SPK_EINVAL, "reduce_factorize: null output");
         *out = nullptr;
         if (p < 1 || k < 0) fail(SPK_EINVAL, "reduce_factorize: bad shape");
+        if (p > 1 && k > 0 && (!vt || !vb || !wt || !wb)) fail(SPK_EINVAL, "reduce_factorize: null tips");
         auto r = std::make_unique<spk_reduced>();
         r->f = std::make_unique<spk_fact>();
         spk_fact& f = *r->f;
@@ -2850,6 +2970,7 @@ static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t trans
     return guarded([&] {
         if (couplings) *couplings += (f.p > 1 && f.k > 0) ? f.p - 1 : 0;
         if (ncols == 0 || f.p < 2 || f.k == 0) return;
+        wait_ready(f, s);
         const long long rows = 2LL * f.p * f.k;
         double* T = device ? z : dalloc<double>((size_t)rows * ncols, s);
         double* AUX = dalloc<double>((size_t)f.aux_rows * ncols, s);
@@ -2863,6 +2984,7 @@ static spk_status reduced_solve_on(spk_fact& f, bool own_programs, int32_t trans
         Exec ex{f, s, B, ncols};
         ex.run(own_programs ? (transpose ? f.prog_tr : f.prog_fwd) : (transpose ? f.prog_rtr : f.prog_rfwd), f.d_sblob);
         dfree(AUX, s);
+        note_use(f, s);
         if (device) {
             ck(cudaGetLastError(), "reduced_solve");
             return;
@@ -2951,6 +3073,7 @@ void device_solve(const spk_fact* fc, int transpose, const double* F, long long 
     ensure_finished(fc);
     auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, SPK_MEM_DEVICE, s);
     x->run_phase();
+    note_use(*fc, s);
 }
 
 }  // namespace
@@ -3078,6 +3201,7 @@ spk_status spk_refine(const spk_fact* fc, const double* band, const double* F, i
                       int64_t ldx, int32_t transpose, int32_t max_iters, double tol, int32_t mem, void* stream,
                       spk_refine_result* res) {
     return guarded([&] {
+        if (!fc) fail(SPK_EINVAL, "null factorization handle");
         const spk_fact& f = *fc;
         const long long n = f.n;
         if (ldf < n || ldx < n) fail(SPK_EINVAL, "iterative_refine: F.rows must equal n");
@@ -3098,6 +3222,7 @@ spk_status spk_refine(const spk_fact* fc, const double* band, const double* F, i
 
 spk_status spk_condest_1norm(const spk_fact* fc, const double* band, int32_t mem, void* stream, double* cond) {
     return guarded([&] {
+        if (!fc) fail(SPK_EINVAL, "null factorization handle");
         const spk_fact& f = *fc;
         const long long n = f.n;
         if (f.open()) fail(SPK_EINVAL, "condition_estimate: slab factorization");
@@ -3224,11 +3349,7 @@ Staging& staging(size_t want) {
     return st;
 }
 
-size_t spkb_chunk_bytes() {
-    static const size_t c = getenv("SPK_SPKB_CHUNK") ? std::max<size_t>(8, strtoull(getenv("SPK_SPKB_CHUNK"), 0, 10))
-                                                     : (size_t)64 << 20;
-    return c;
-}
+size_t spkb_chunk_bytes() { return (size_t)64 << 20; }
 
 }  // namespace
 

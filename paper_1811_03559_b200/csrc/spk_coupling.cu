@@ -329,7 +329,7 @@ void launch_dense_lu(const CouplingJob* d_jobs, int njobs, int n, const PartDev*
                      int* flags, cudaStream_t s) {
     if (njobs <= 0) return;
     const size_t smem = (size_t)n * (n + 1) * 8;
-    cudaFuncSetAttribute(k_dense_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_attr((const void*)k_dense_lu, (int)smem);
     k_dense_lu<<<njobs, 512, smem, s>>>(d_jobs, d_parts, fac, piv, flags);
     count_launch();
 }

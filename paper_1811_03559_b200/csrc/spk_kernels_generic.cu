@@ -343,7 +343,7 @@ bool launch_band_lu_small(const int* d_units, int nunits, int max_m, const PartD
     if (nunits <= 0) return true;
     if (max_m > kLuSmallMaxM) return false;
     const size_t smem = (size_t)max_m * (max_m + 1) * sizeof(double);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_band_lu_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) set_smem_attr((const void*)k_band_lu_small, (int)smem);
     k_band_lu_small<<<nunits, kLuSmallThreads, smem, s>>>(d_units, d_parts, fac, piv, amax, boost_eps, boost_cnt,
                                                           fell_back, status, flags, redo_only ? 1 : 0);
     count_launch();
@@ -652,7 +652,7 @@ bool launch_sweep_small(const SweepJob* d_jobs, int njobs, int max_nc, int chunk
 #define SPK_SMALL(CH)                                                                                    \
     {                                                                                                   \
         if (smem > 48 * 1024)                                                                           \
-            cudaFuncSetAttribute(k_sweep_small<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            set_smem_attr((const void*)k_sweep_small<CH>, (int)smem); \
         k_sweep_small<CH><<<g, 32 * kSmallWpb, smem, s>>>(d_jobs, d_parts, fac, piv, B, ncols, maxr);   \
         count_launch();                                                                                 \
         return true;                                                                                    \

@@ -8,6 +8,11 @@
 namespace spk {
 
 void count_launch(int n = 1);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel,
+// size), thread-safe; a failure raises SPK_ECUDA (spk_capi.cu)
+void set_smem_attr(const void* fn, int bytes);
+// multiprocessors of the current device (cached per device)
+int device_sms();
 
 void launch_fill_factors(const double* band, long long n, int akl, int aku, const PartDev* d_parts,
                          int nparts, long long max_elems, double* fac, int* piv, unsigned long long* amax,

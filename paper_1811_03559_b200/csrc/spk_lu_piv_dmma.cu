@@ -473,7 +473,7 @@ template <int TRW, int TCW, bool DENSE = false>
 static bool launch_piv_dmma(int nunits, const PivDmmaArgs& A, cudaStream_t s) {
     const int smem = (int)sizeof(PivDmmaSmem<TRW, TCW>);
     if (smem > 227 * 1024) return false;
-    cudaFuncSetAttribute(k_band_lu_piv_dmma<TRW, TCW, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem_attr((const void*)k_band_lu_piv_dmma<TRW, TCW, DENSE>, (int)smem);
     k_band_lu_piv_dmma<TRW, TCW, DENSE><<<nunits, 32 * TCW, smem, s>>>(A);
     count_launch();
     return true;

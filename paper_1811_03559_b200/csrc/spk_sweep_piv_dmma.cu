@@ -197,7 +197,7 @@ template <int TRW>
 static bool launch_piv_sweep(int nwarps, dim3 grid, const PivSweepArgs& A, cudaStream_t s) {
     const size_t smem = piv_sweep_smem<TRW>(nwarps);
     if (smem > 227 * 1024) return false;
-    cudaFuncSetAttribute(k_sweep_piv_dmma<TRW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_attr((const void*)k_sweep_piv_dmma<TRW>, (int)smem);
     k_sweep_piv_dmma<TRW><<<grid, 32 * nwarps, smem, s>>>(A);
     count_launch();
     return true;

@@ -103,6 +103,10 @@ def lib():
         L.spk_last_error.restype = C.c_char_p
         L.spk_version.restype = C.c_char_p
         L.spk_launch_count.restype = C.c_int64
+        L.spk_generic_launch_count.restype = C.c_int64
+        L.spk_generic_launch_count.argtypes = [C.c_int32]
+        L.spk_set_generic_path.argtypes = [C.c_int32]
+        L.spk_set_generic_path.restype = None
         L.spk_launch_count.argtypes = [C.c_int32]
         L.spk_compute_ratios.argtypes = [C.c_double, C.c_int32, C.c_int32, _dp, _dp]
         L.spk_compute_ratios.restype = None
@@ -209,6 +213,24 @@ def _check(rc):
 
 def launch_count(reset=False) -> int:
     return int(lib().spk_launch_count(1 if reset else 0))
+
+
+def generic_launch_count(reset=False) -> int:
+    """Launches of the generic correctness-baseline kernels (0 on tuned shapes)."""
+    return int(lib().spk_generic_launch_count(1 if reset else 0))
+
+
+class generic_path:
+    """Context manager: factorizations created inside run every stage on the
+    generic kernels (the correctness baseline of the tuned ones)."""
+
+    def __enter__(self):
+        lib().spk_set_generic_path(1)
+        return self
+
+    def __exit__(self, *exc):
+        lib().spk_set_generic_path(0)
+        return False
 
 
 def default_boost_eps() -> float:

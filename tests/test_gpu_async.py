@@ -117,3 +117,141 @@ def test_singular_reported_by_fact_sync(spk):
         assert L.spk_fact_sync(h) != 0
     finally:
         L.spk_fact_destroy(h)
+
+
+def _raw_factorize(spk, band_ptr, mem, n, k, plan, piv, stream):
+    L = spk.lib()
+    st, keep = spk.spike._plan_struct(plan)
+    o = spk.spike._Opts(int(piv), spk.FactorOptions().boost_eps)
+    h = C.c_void_p()
+    spk.spike._check(L.spk_factorize(C.c_void_p(band_ptr), mem, n, k, k, C.byref(st), C.byref(o),
+                                     C.c_void_p(stream), C.byref(h)))
+    return h
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_solve_on_other_stream_orders_after_factorization(oracle, spk, transpose):
+    """Factorize on stream A and solve device-resident on stream B right away
+    (no host sync in between): the solve must wait for A's factor program and
+    the upload of its solve jobs.  Destroying the factorization right after
+    (a still-pending solve on B) must not let A's next allocations reuse the
+    memory B is reading."""
+    L = spk.lib()
+    n, k, nrhs, p = 400000, 64, 8, 148
+    band = oracle.generate_band(777, n, k, k, 1.2)
+    F = np.asfortranarray(oracle.generate_rhs(778, n, nrhs))
+    plan = spk.gpu_plan(n, k, k, nrhs, False, p)
+    want = (spk.transpose_solve if transpose else spk.solve)(
+        spk.factorize(spk.BandedMatrix(n, k, k, band), plan), F)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    dband = torch.from_numpy(np.ascontiguousarray(band)).cuda()
+    dF = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()  # column-major n x nrhs
+    dX = torch.full_like(dF, float("nan"))
+    torch.cuda.synchronize()
+    for rep in range(3):
+        dX.fill_(float("nan"))
+        torch.cuda.synchronize()
+        h = _raw_factorize(spk, dband.data_ptr(), 1, n, k, plan, False, sa.cuda_stream)
+        spk.spike._check(L.spk_solve(h, int(transpose), C.c_void_p(dF.data_ptr()), n, nrhs,
+                                     C.c_void_p(dX.data_ptr()), n, 1, C.c_void_p(sb.cuda_stream), None))
+        L.spk_fact_destroy(h)
+        # A reuses the released blocks at once: a second factorization of another matrix
+        other = torch.from_numpy(np.ascontiguousarray(oracle.generate_band(779, n, k, k, 1.2))).cuda()
+        h2 = _raw_factorize(spk, other.data_ptr(), 1, n, k, plan, False, sa.cuda_stream)
+        sb.synchronize()
+        sa.synchronize()
+        L.spk_fact_destroy(h2)
+        got = dX.cpu().numpy().T
+        assert rel_componentwise(got, want) <= 1e-13, rep
+
+
+def test_concurrent_first_solves_on_pending_factorization(oracle, spk):
+    """Two threads make the first solves on a freshly enqueued (pending) raw
+    C-ABI handle: the host-side finish runs once, both get the synchronous
+    path's result bit for bit."""
+    import threading
+    L = spk.lib()
+    n, k, nrhs = 60000, 16, 4
+    band = oracle.generate_band(811, n, k, k, 1.5)
+    F = np.asfortranarray(oracle.generate_rhs(812, n, nrhs))
+    plan = spk.gpu_plan(n, k, k, nrhs, False, 64)
+    fact = spk.factorize(spk.BandedMatrix(n, k, k, band), plan)
+    want = {False: spk.solve(fact, F), True: spk.transpose_solve(fact, F)}
+    for rep in range(4):
+        h = _raw_factorize(spk, np.ascontiguousarray(band).ctypes.data, 0, n, k, plan, False, 0)
+        out, errs = {}, []
+
+        def work(tr):
+            try:
+                x = np.zeros((n, nrhs), order="F")
+                s = torch.cuda.Stream()
+                spk.spike._check(L.spk_solve(h, int(tr), C.c_void_p(F.ctypes.data), n, nrhs,
+                                             C.c_void_p(x.ctypes.data), n, 0, C.c_void_p(s.cuda_stream), None))
+                s.synchronize()
+                out[tr] = x
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        ts = [threading.Thread(target=work, args=(tr,)) for tr in (False, True)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        L.spk_fact_destroy(h)
+        assert not errs, errs
+        for tr in (False, True):
+            assert np.array_equal(out[tr], want[tr]), (rep, tr)
+
+
+def test_singular_status_is_sticky(spk):
+    """After the deferred finish reports SPK_ESINGULAR, every later consumer
+    of the handle (solves, getters) reports it too."""
+    n, k = 4000, 3
+    a = spk.BandedMatrix(n, k, k)
+    for i in range(n):
+        a.set(i, i, 2.0)
+    for i in range(1234 - k, 1234 + k + 1):
+        a.set(i, 1234, 0.0)
+    plan = spk.gpu_plan(n, k, k, 1, True, 4)
+    L = spk.lib()
+    band = np.ascontiguousarray(a.data)
+    h = _raw_factorize(spk, band.ctypes.data, 0, n, k, plan, True, 0)
+    try:
+        F = np.ones((n, 1), order="F")
+        X = np.zeros((n, 1), order="F")
+        assert L.spk_fact_sync(h) == 2
+        assert L.spk_fact_sync(h) == 2
+        assert L.spk_solve(h, 0, C.c_void_p(F.ctypes.data), n, 1, C.c_void_p(X.ctypes.data), n, 0, None,
+                           None) == 2
+        assert b"singular" in L.spk_last_error()
+    finally:
+        L.spk_fact_destroy(h)
+
+
+def test_null_handles_are_rejected(spk):
+    L = spk.lib()
+    assert L.spk_solve(None, 0, None, 10, 1, None, 10, 0, None, None) == 1
+    assert L.spk_factorize(None, 0, 10, 1, 1, None, None, None, None) == 1
+    assert L.spk_fact_sync(None) == 1
+
+
+@pytest.mark.parametrize("piv", [False, True])
+def test_generic_path_matches_tuned_kernels(oracle, spk, piv):
+    """The generic kernels (spk_set_generic_path) are the correctness baseline
+    of the tuned ones: same answers to rounding on one input; the tuned run
+    launches no generic kernel on this shape."""
+    n, k, nrhs = 30000, 24, 6
+    band = oracle.generate_band(901, n, k, k, 1.4)
+    F = oracle.generate_rhs(902, n, nrhs)
+    plan = spk.gpu_plan(n, k, k, nrhs, piv, 20)
+    a = spk.BandedMatrix(n, k, k, band)
+    spk.generic_launch_count(reset=True)
+    fact = spk.factorize(a, plan, spk.FactorOptions(pivoting=piv))
+    tuned = [spk.solve(fact, F), spk.transpose_solve(fact, F)]
+    assert spk.generic_launch_count(reset=True) == 0
+    with spk.generic_path():
+        gfact = spk.factorize(a, plan, spk.FactorOptions(pivoting=piv))
+        gen = [spk.solve(gfact, F), spk.transpose_solve(gfact, F)]
+    assert spk.generic_launch_count(reset=True) > 0
+    for t, g in zip(tuned, gen):
+        assert rel_componentwise(t, g) <= 1e-11
