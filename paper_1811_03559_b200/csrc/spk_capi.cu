@@ -674,7 +674,8 @@ struct Builder {
         for (auto& j : jobs) {
             const PartDev& P = f.parts[j.part];
             if (j.part >= f.p) fast = false;
-            if (j.mode == SW_BWD_LT && P.pivoting) fast = false;
+            // pivoted transposed L sweeps need the blocked L records
+            if (j.mode == SW_BWD_LT && P.pivoting && !piv_trw(f.kl, f.ku)) fast = false;
             if (j.mode != jobs[0].mode) fast = false;
             const int kw = (j.mode == SW_FWD_L || j.mode == SW_BWD_LT) ? P.kl : P.ubw;
             kwmax = std::max(kwmax, kw);
@@ -703,7 +704,7 @@ struct Builder {
         s.mode = jobs[0].mode;
         s.kwmax = kwmax;
         s.tr = tr;
-        s.piv = f.piv_on && jobs[0].mode == SW_FWD_L;
+        s.piv = f.piv_on && (jobs[0].mode == SW_FWD_L || jobs[0].mode == SW_BWD_LT);
         prog.push_back(s);
     }
     void transpose_factors() { prog.push_back(Stage{ST_TRANSPOSE}); }
@@ -1378,15 +1379,20 @@ struct Exec {
 
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
         if (nc <= 0) return true;
-        if (st.piv && st.mode == SW_FWD_L && f.lblk_ok) {
-            // pivoted forward sweep, 8 rows per step on the tensor cores from the
-            // LU's blocked records: <= 16 warps x 8 columns per CTA
+        if (st.piv && f.lblk_ok) {
+            // pivoted forward / transposed L sweeps, 8 rows per step on the
+            // tensor cores from the LU's blocked records: <= 16 warps x 8
+            // columns per CTA
             const int groups = (nc + 127) / 128;
             const int cols = ((nc + groups - 1) / groups + 7) / 8 * 8;
             const dim3 grid(st.njobs, (nc + cols - 1) / cols);
-            PivSweepArgs A{jobs, f.d_parts, f.d_lblk, B, ncols};
-            if (launch_sweep_piv_dmma(f.lblk_trw, cols / 8, grid, A, s)) return true;
+            PivSweepArgs A{jobs, f.d_parts, f.d_lblk, B, ncols, f.d_fac, f.d_piv};
+            if (st.mode == SW_FWD_L ? launch_sweep_piv_dmma(f.lblk_trw, cols / 8, grid, A, s)
+                                    : launch_sweep_piv_dmma_t(f.lblk_trw, cols / 8, grid, A, s))
+                return true;
         }
+        // pivoted transposed sweeps have no register-window kernel
+        if (st.piv && st.mode == SW_BWD_LT) return false;
         // narrow solves (<= 8 right-hand sides): the producer/consumer sweep
         // with the window split over a pair of warps (k_sweep_dmma2<..., PAIR>).
         // Measured: narrow solves gain at every bandwidth; wider ones were

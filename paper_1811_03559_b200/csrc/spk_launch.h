@@ -112,8 +112,14 @@ struct PivSweepArgs {
     const double* lblk;
     Bufs B;
     int ncols;
+    // the transposed sweep's unaligned first panel runs the reference's
+    // per-row steps from the packed gbtf2 factor and pivots
+    const double* fac;
+    const int* piv;
 };
 bool launch_sweep_piv_dmma(int trw, int nwarps, dim3 grid, const PivSweepArgs& A, cudaStream_t s);
+// pivoted transposed L sweep (B := P^T L^-T B) from the same records
+bool launch_sweep_piv_dmma_t(int trw, int nwarps, dim3 grid, const PivSweepArgs& A, cudaStream_t s);
 struct PivLuArgs;
 bool launch_band_lu_piv(const int* d_units, int nunits, int kl, int ku, const PivLuArgs& A, cudaStream_t s);
 bool launch_sweep_dmma2_fl(int ntw, int ncw, dim3 grid, const FastSweepArgs& A, cudaStream_t s,
