@@ -303,8 +303,9 @@ void spk_arena_trim(void);
  * since the last reset (instrumentation for bench.py's gpu_launches). */
 int64_t spk_launch_count(int32_t reset);
 /* Of those, launches of the generic correctness-baseline kernels (per-column
- * sweeps, scalar GEMM, unblocked LU): stages no tuned kernel covers.  Zero on
- * the BASELINE configurations; bench.py reports it. */
+ * sweeps, unblocked LU) on SPIKE-partition stages no tuned kernel covers (all
+ * generic kernels under spk_set_generic_path).  Zero on the BASELINE
+ * configurations; bench.py reports it. */
 int64_t spk_generic_launch_count(int32_t reset);
 /* Test hook: 1 routes every stage of factorizations created afterwards (and
  * all solves) through the generic kernels, the correctness baseline the tuned

@@ -249,6 +249,8 @@ class Reference:
         L.ref_time_path.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
                                     C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _ip]
         L.ref_hw_threads.restype = C.c_int
+        L.ref_iterative_refine.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int, C.c_double, C.c_int, _ip,
+                                           _dp]
         L.ref_write_spkb.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
         L.ref_read_spkb.argtypes = [C.c_char_p, _ip, _ip, _ip, _dp]
 
@@ -380,6 +382,17 @@ class RefFact(OracleFact):
         out = np.zeros((self.k, self.k))
         self.o.L.ref_fact_tip(self.h, self.TIPS.index(which), i, _d(out))
         return out.T
+
+    def iterative_refine(self, F, x0, max_iters, tol, transpose=False):
+        """solve.cpp:404-432 -> (x, iterations, converged, stagnated, residual)"""
+        F = np.asfortranarray(F, dtype=np.float64)
+        X = np.asfortranarray(x0, dtype=np.float64).copy(order="F")
+        info = (C.c_int * 3)()
+        res = C.c_double()
+        if self.o.L.ref_iterative_refine(self.h, _d(F), F.shape[1], _d(X), max_iters, tol, int(transpose), info,
+                                         C.byref(res)):
+            raise RuntimeError(self.o.err())
+        return X, info[0], bool(info[1]), bool(info[2]), res.value
 
     def solve(self, F, transpose=False):
         F = np.asfortranarray(F, dtype=np.float64)

@@ -238,6 +238,24 @@ int ref_time_path(const double* band, int n, int kl, int ku, const double* F, in
     });
 }
 
+// iterative_refine (solve.cpp:404-432) on a reference factorization: X holds
+// x0 on entry and the refined x on return; info = {iterations, converged,
+// stagnated}
+int ref_iterative_refine(void* h, const double* F, int nrhs, double* X, int max_iters, double tol,
+                         int transpose, int* info, double* residual) {
+    return guarded([&] {
+        auto* hh = static_cast<RefHandle*>(h);
+        const auto& f = hh->fact;
+        RefineResult r = iterative_refine(f, hh->a, block_from(F, f.n, nrhs), block_from(X, f.n, nrhs),
+                                          max_iters, tol, transpose != 0);
+        if (!r.x.data.empty()) std::memcpy(X, r.x.data.data(), sizeof(double) * r.x.data.size());
+        info[0] = r.iterations;
+        info[1] = r.converged ? 1 : 0;
+        info[2] = r.stagnated ? 1 : 0;
+        *residual = r.residual;
+    });
+}
+
 // band_io.cpp: the reference's own .spkb writer / reader (golden fixtures)
 int ref_write_spkb(const double* band, int n, int kl, int ku, const char* path) {
     return guarded([&] { write_matrix(band_from(band, n, kl, ku), path, MatrixFormat::Spkb); });

@@ -64,9 +64,11 @@ using namespace spk;
 namespace {
 thread_local std::string g_err;
 thread_local long long g_launches = 0;
-// launches of the generic correctness-baseline kernels (k_sweep, k_gemm,
-// k_band_lu): stages whose shape no tuned kernel covers, or every stage when
-// spk_set_generic_path(1) forces that path (tests)
+// launches of the generic correctness-baseline kernels (k_sweep, k_band_lu)
+// on SPIKE-partition stages whose shape no tuned kernel covers, or of every
+// generic kernel when spk_set_generic_path(1) forces that path (tests).  The
+// coupling units' generic pivoted LU is not counted: it is the designated
+// path of pairs with |W| > 1 (guarded off on the device otherwise)
 thread_local long long g_generic_launches = 0;
 std::atomic<int> g_generic{0};
 bool generic_path() { return g_generic.load(std::memory_order_relaxed) != 0; }
@@ -262,7 +264,7 @@ struct Stage {
     int mode = 0, kwmax = 0, tr = 0, piv = 0;
     // sweeps on short units: shared-memory staged kernel (k_sweep_small)
     int small_ch = 0, small_rows = 0;
-    bool partitions = false;  // ST_LU over SPIKE partitions (fill from the input band)
+    bool partitions = false;  // ST_LU / ST_SWEEP over SPIKE partitions (LU: fill from the input band)
 };
 
 struct ProgramBuilder {
@@ -701,6 +703,7 @@ struct Builder {
             s.small_ch = std::max(1, (sbw + 31) / 32);
         }
         s.fast = fast;
+        s.partitions = jobs[0].part < f.p && !f.reduced_only;
         s.mode = jobs[0].mode;
         s.kwmax = kwmax;
         s.tr = tr;
@@ -1525,7 +1528,7 @@ struct Exec {
                         launch_sweep_small((const SweepJob*)jobs, st.njobs, nc, st.small_ch, st.small_rows, f.d_parts,
                                            f.d_fac, f.d_piv, B, ncols, s))
                         break;
-                    ++g_generic_launches;
+                    if (st.partitions) ++g_generic_launches;
                     launch_sweep((const SweepJob*)jobs, st.njobs, nc, f.d_parts, f.d_fac, f.d_piv, B,
                                  ncols, s);
                     break;
@@ -1612,7 +1615,7 @@ struct Exec {
                                                               f.d_fell, f.d_status, f.d_flags, s))
                             break;
                     }
-                    ++g_generic_launches;
+                    if (st.partitions) ++g_generic_launches;
                     launch_band_lu((const int*)jobs, st.njobs, f.d_parts, f.d_fac, f.d_piv, f.d_amax,
                                    f.boost_eps, f.d_boost, f.d_fell, f.d_status, f.d_flags, s);
                     break;

@@ -82,12 +82,31 @@ struct PivDmmaSmem {
     double l21[2][TRW * 64];  // -L21 per tile row (tile 0 unused), A-fragment order
     double srow[2][8 * RLD];  // staged entering row tile of step J (rows 8(J+TRW).., window columns)
     double scol[2][8 * TRW * 8];  // staged entering column block for the panel warp of step J+1
-    double xs[TCW][8 * TRW * 8];  // per-warp row exchange scratch, by window position
+    double xs[TCW][16 * 8];       // per-warp row exchange scratch, by slot (piv_xslot)
     int src[2][8 * TRW];          // original position of the row at each final position
     unsigned mv_out[2][(8 * TRW + 31) / 32];  // rows leaving their position (by original position)
     unsigned mv_in[2][(8 * TRW + 31) / 32];   // positions receiving another row
     int sing[2];
 };
+
+// Scratch slot of window position pos for a panel's row exchange: tile 0 in
+// slots 0..7, the (at most 8) pivot rows outside tile 0 packed after it in
+// position order.  Outside tile 0 the rows leaving their position (mv_out)
+// are exactly the positions receiving one (a pivot row goes to tile 0 and
+// takes a tile-0 row), so one mask serves both directions.
+template <int NW>
+__device__ __forceinline__ int piv_xslot(const unsigned* mv_out, int pos) {
+    if (pos < 8) return pos;
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const unsigned mk = w == 0 ? (mv_out[0] & ~0xffu) : mv_out[w];
+        const int lo = 32 * w;
+        if (pos >= lo + 32) c += __popc(mk);
+        else if (pos > lo) c += __popc(mk & ((1u << (pos - lo)) - 1u));
+    }
+    return 8 + c;
+}
 
 template <int TRW, int TCW, bool DENSE>
 __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A) {
@@ -313,18 +332,22 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         // the pivot rows, so nothing else is touched)
         {
             double* xs = S.xs[w];
+            constexpr int NW = (8 * TRW + 31) / 32;
+            const unsigned* mvo = S.mv_out[par];
 #pragma unroll
             for (int t = 0; t < TRW; ++t) {
                 const unsigned mo = S.mv_out[par][(8 * t) >> 5];
                 if (t == 0 || ((mo >> (((8 * t) & 31) + gi)) & 1u))
-                    *reinterpret_cast<double2*>(&xs[(8 * t + gi) * 8 + 2 * q]) = make_double2(acc[t][0], acc[t][1]);
+                    *reinterpret_cast<double2*>(&xs[piv_xslot<NW>(mvo, 8 * t + gi) * 8 + 2 * q]) =
+                        make_double2(acc[t][0], acc[t][1]);
             }
             __syncwarp();
 #pragma unroll
             for (int t = 0; t < TRW; ++t) {
                 const unsigned mi = S.mv_in[par][(8 * t) >> 5];
                 if (t == 0 || ((mi >> (((8 * t) & 31) + gi)) & 1u)) {
-                    const double2 v = *reinterpret_cast<const double2*>(&xs[S.src[par][8 * t + gi] * 8 + 2 * q]);
+                    const int sl = piv_xslot<NW>(mvo, S.src[par][8 * t + gi]);
+                    const double2 v = *reinterpret_cast<const double2*>(&xs[sl * 8 + 2 * q]);
                     acc[t][0] = v.x;
                     acc[t][1] = v.y;
                 }

@@ -69,6 +69,36 @@ def main():
         out[pre + "relres"] = np.array([ref.relative_residual(band, n, kl, ku, x, F, False),
                                         ref.relative_residual(band, n, kl, ku, xt, F, True)])
         print(name, "p", fact.p, "levels", fact.levels, "relres", out[pre + "relres"])
+    # diagonal boosting (kernels.cpp:104-109): exact zeros on the first pivot
+    # of every partition (the UL partition's first pivot is its last row), so
+    # the boost count is known (one per partition) and the boosted
+    # factorization is pinned: its solution and the reference's
+    # iterative_refine (solve.cpp:404-432) from x0 = 0 on it
+    n, k, nrhs, t = 4000, 8, 2, 4
+    band = o.generate_band(SEED + 77, n, k, k, 1.5)
+    F = o.generate_rhs(SEED + 78, n, nrhs)
+    r12, r13 = ref.compute_ratios(1.0, nrhs, k)
+    plan = ref.make_plan(n, k, k, t, r12, r13)
+    b = plan["bounds"]
+    for r in [0] + b[1:-2] + [n - 1]:
+        band[r, k] = 0.0  # A(r, r): packed row ku of column r
+    fact = ref.factorize_t(band, n, k, k, t, r12, r13, False)
+    x, _, _ = fact.solve(F, False)
+    xt, _, _ = fact.solve(F, True)
+    xr, its, conv, stag, res = fact.iterative_refine(F, np.zeros((n, nrhs)), 10, 1e-14, False)
+    xrt, itst, convt, stagt, rest = fact.iterative_refine(F, np.zeros((n, nrhs)), 10, 1e-14, True)
+    pre = "boost/"
+    out[pre + "shape"] = np.array([n, k, k, nrhs, t, 0], dtype=np.int64)
+    out[pre + "band"] = band
+    out[pre + "F"] = F
+    out[pre + "bounds"] = np.array(b, dtype=np.int64)
+    out[pre + "boost_count"] = np.array([fact.boost_count], dtype=np.int64)
+    out[pre + "x"] = x
+    out[pre + "xt"] = xt
+    out[pre + "x_refined"] = xr
+    out[pre + "xt_refined"] = xrt
+    out[pre + "refine"] = np.array([[its, conv, stag, res], [itst, convt, stagt, rest]])
+    print("boost", "p", fact.p, "boosts", fact.boost_count, "refine", out[pre + "refine"])
     # reduced-system brute force vectors (test_acceptance.cpp:109-151 shape)
     rng = np.random.default_rng(4242)
     for p in (2, 4, 8):

@@ -377,45 +377,7 @@ def test_gpu_matches_reference_golden(oracle, spk, name):
             assert rel_componentwise(getattr(fact, w)[i], ref[i]) <= (1e-9 if piv else 1e-12), (w, i)
 
 
-BASELINE = {  # name: n, k, nrhs, dd, pivoting, transpose
-    "C1": (100_000, 16, 1, 2.0, False, False),
-    "C2": (1_000_000, 64, 1, 1.1, False, False),
-    "C3": (1_000_000, 160, 160, 1.5, False, True),
-    "C4": (1_000_000, 64, 4, -1.0, True, False),
-}
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("cfg", sorted(BASELINE))
-def test_baseline_config_backward_error(spk, cfg):
-    """Full BASELINE sizes on the device (inputs generated in HBM): normwise
-    backward error max_c ||A x_c - f_c||_inf / (||A||_inf ||x_c||_inf) <= 1e-12
-    (SURVEY.md 8(d)(i)), forward and transpose."""
-    import torch
-    n, k, nrhs, dd, piv, tr = BASELINE[cfg]
-    dev = torch.device("cuda", 0)
-    s = torch.cuda.current_stream().cuda_stream
-    band = torch.empty((n, 2 * k + 1), dtype=torch.float64, device=dev)
-    F = torch.empty((nrhs, n), dtype=torch.float64, device=dev)
-    X = torch.empty_like(F)
-    R = torch.empty_like(F)
-    spk.generate_band_device(20181108, n, k, k, dd, band.data_ptr(), s)
-    spk.generate_rhs_device(20181109, n, nrhs, F.data_ptr(), n, s)
-    plan = spk.gpu_plan(n, k, k, nrhs, piv)
-    fact = spk.factorize_device(band.data_ptr(), n, k, k, plan, spk.FactorOptions(pivoting=piv), s)
-    # ||A||_inf: row sums of |A| (band row i spans columns i-k..i+k)
-    absb = band.abs()
-    rows = torch.zeros(n, dtype=torch.float64, device=dev)
-    for q in range(2 * k + 1):  # packed row q of column j holds A(j + q - k, j)
-        i = torch.arange(n, device=dev) + q - k
-        ok = (i >= 0) & (i < n)
-        rows.index_add_(0, i[ok], absb[ok, q])
-    for t in ([False, True] if tr else [False]):
-        spk.solve_device(fact, F.data_ptr(), n, nrhs, X.data_ptr(), n, t, s)
-        spk.lib().spk_band_matmul(band.data_ptr(), n, k, k, X.data_ptr(), n, nrhs, int(t), R.data_ptr(), n, 1, s)
-        anorm = (absb.sum(dim=1).max() if t else rows.max()).item()
-        berr = ((R - F).abs().amax(dim=1) / (anorm * X.abs().amax(dim=1))).max().item()
-        assert berr <= 1e-12, (cfg, t, berr)
+# Full BASELINE sizes against the compiled reference: tests/test_gpu_scale_parity.py
 
 
 # Blocked pivoted DMMA LU + pivoted DMMA forward sweep (spk_lu_piv_dmma.cu,

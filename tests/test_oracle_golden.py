@@ -12,6 +12,7 @@ from conftest import rel_componentwise
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.npz")
 SEED = 20181108
+BOOST_TOL = 1e-8
 
 
 @pytest.fixture(scope="module")
@@ -93,3 +94,25 @@ def test_reference_oracle_cross_check_when_available(oracle, reference):
     of = oracle.factorize(band, n, k, k, rf.bounds(), False)
     for tr in (False, True):
         assert rel_componentwise(rf.solve(F, tr)[0], of.solve(F, tr)[0]) <= 1e-12
+
+
+def test_oracle_boosted_factorization_matches_reference(oracle, gold):
+    """Diagonal boosting (kernels.cpp:104-109): exact zero first pivots in every
+    partition.  The restatement boosts the same pivots (count) and its boosted
+    solution equals the reference's to rounding."""
+    n, kl, ku, nrhs, t, piv = [int(x) for x in gold["boost/shape"]]
+    band = gold["boost/band"]
+    F = gold["boost/F"]
+    bounds = [int(b) for b in gold["boost/bounds"]]
+    fact = oracle.factorize(band, n, kl, ku, bounds, False)
+    assert fact.boost_count == int(gold["boost/boost_count"][0]) == len(bounds) - 1
+    x, _, _ = fact.solve(F, False)
+    xt, _, _ = fact.solve(F, True)
+    # a boosted pivot is sqrt(eps) max|A_i|: rounding differences between two
+    # correct implementations grow by up to 1/sqrt(eps) through it
+    assert rel_componentwise(x, gold["boost/x"]) <= BOOST_TOL
+    assert rel_componentwise(xt, gold["boost/xt"]) <= BOOST_TOL
+    # the reference's refinement converged to the true solution
+    xo = oracle.oracle_solve(band, n, kl, ku, F, False, True)
+    assert rel_componentwise(gold["boost/x_refined"], xo) <= 1e-12
+    assert gold["boost/refine"][0][1] == 1 and gold["boost/refine"][1][1] == 1
