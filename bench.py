@@ -10,10 +10,10 @@ higher is better, with time per step beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl ours|reference]
 
-N > 1 (torchrun, one process per GPU, NCCL): weak scaling -- ONE global
-system of N*n rows, each GPU factoring and solving its slab with the
-slab-level reduced system exchanged by all-gathers
-(paper_1811_03559_b200/distributed.py).
+N > 1 (torchrun, one process per GPU, NCCL): strong scaling -- the
+configuration's fixed system sharded into N slabs (--weak: N*n rows), each
+GPU factoring and solving its slab with the slab-level reduced system
+exchanged by all-gathers (paper_1811_03559_b200/distributed.py).
 
 Inputs are seeded synthetic data (include/spike_b200_gen.h), generated in HBM
 for the device-resident `value`, and in pinned host memory for `e2e`, which
@@ -31,6 +31,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -129,6 +131,45 @@ def _ref_libs():
     return Oracle(), ref
 
 
+def host_cpu():
+    """lscpu model, physical cores and logical CPUs of this host."""
+    info = {"model": None, "physical_cores": None, "logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                a, b = line.split(":", 1)
+                kv[a.strip()] = b.strip()
+        info["model"] = kv.get("Model name")
+        cps, sockets = kv.get("Core(s) per socket"), kv.get("Socket(s)")
+        if cps and sockets and cps.isdigit() and sockets.isdigit():
+            info["physical_cores"] = int(cps) * int(sockets)
+    except Exception:
+        pass
+    return info
+
+
+def reference_full(cfg, t, steps, want_x=False):
+    """The reference CPU path (make_plan(t) -> factorize -> solve
+    [-> transpose_solve], spike_cli.cpp:119-169) on the FULL configuration,
+    `steps` times; returns the per-step seconds, p and (optionally) X / X^T of
+    the last step."""
+    o, ref = _ref_libs()
+    k, nrhs, n = cfg["k"], cfg["nrhs"], cfg["n"]
+    band = o.generate_band(SEED_A, n, k, k, cfg["dd"])
+    F = o.generate_rhs(SEED_A + 1, n, nrhs)
+    times, parts, p, X, XT = [], [], None, None, None
+    for i in range(steps):
+        r = ref.time_path(band, n, k, k, F, t, 1.0, cfg["piv"], cfg["transpose"], want_x=want_x and i == steps - 1)
+        times.append(r["factor"] + r["solve"] + r["tsolve"])
+        parts.append([r["factor"], r["solve"], r["tsolve"]])
+        p = r["p"]
+        if r["X"] is not None:
+            X, XT = r["X"], r["XT"]
+    return times, parts, p, X, XT
+
+
 def reference_step_sample(cfg, target_s=8.0, t=None, calib=None):
     """Pick a row count so one reference factor+solve(s) step takes ~target_s."""
     o, ref = _ref_libs()
@@ -167,25 +208,36 @@ def impl_reference(args, cfg):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libspike_ref.so not built (reference sources absent at build time)"}))
         return 0
-    budget = 150.0
-    target = max(1.0, min(10.0, budget / max(1, args.steps + args.warmup)))
-    n_s, t = reference_step_sample(cfg, target_s=target)
-    times, p = run_reference_steps(cfg, n_s, t, args.warmup + args.steps)
-    timed = times[args.warmup:]
-    sample_cfg = dict(cfg, n=n_s)
-    fl, useful = alg_flops(sample_cfg)
+    hc = host_cpu()
+    t = hc["physical_cores"] or os.cpu_count()
+    # the full configuration (same n, k, nrhs, dd as our arm); C5 alone is
+    # sampled when the whole run would exceed ~15 min on the host cores
+    n_s = cfg["n"]
+    if cfg["n"] > 4_000_000:
+        n_est, _ = reference_step_sample(cfg, target_s=8.0, t=t)
+        per_step = 8.0 * cfg["n"] / max(n_est, 1)
+        if per_step * (args.steps + args.warmup) > 900.0:
+            n_s = int(cfg["n"] * 900.0 / (per_step * (args.steps + args.warmup)))
+    run_cfg = dict(cfg, n=n_s)
+    times, parts, p, _, _ = reference_full(run_cfg, t, args.warmup + args.steps)
+    timed = sorted(times[args.warmup:])
+    fl, useful = alg_flops(run_cfg)
     ms = 1e3 * sum(timed) / len(timed)
     value = fl / (ms * 1e-3) / 1e9
-    sample = f"n={n_s} of {cfg['n']} rows, same k/nrhs/dd; make_plan(t={t}) -> p={p}; factorize+solve" + \
-             ("+transpose_solve" if cfg["transpose"] else "")
+    sample = (f"full system n={n_s}" if n_s == cfg["n"] else f"n={n_s} of {cfg['n']} rows (same k/nrhs/dd)") + \
+        f"; reference make_plan(t={t}) -> p={p}; factorize+solve" + \
+        ("+transpose_solve" if cfg["transpose"] else "") + f"; median step {timed[len(timed) // 2]:.3f} s"
     line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h)",
-            "config": {"workload": cfg["desc"], "sample_rows": n_s, "threads": t},
+            "config": {"workload": cfg["desc"], "n": n_s, "kl": cfg["k"], "ku": cfg["k"], "nrhs": cfg["nrhs"],
+                       "threads": t, "partitions": p, "host_cpu": hc,
+                       "phase_seconds_median": [sorted(x[i] for x in parts[args.warmup:])[len(timed) // 2]
+                                                for i in range(3)]},
             "impl": "reference",
             "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": t, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": hc["model"]},
             "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -258,8 +310,11 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     lib = spk.lib()
-    n_loc, k, nrhs = cfg["n"], cfg["k"], cfg["nrhs"]
-    n_glob = world * n_loc
+    k, nrhs = cfg["k"], cfg["nrhs"]
+    # strong scaling (default): the configuration's fixed system sharded over
+    # the GPUs, as BASELINE C5 specifies; --weak: n rows per GPU
+    n_glob = world * cfg["n"] if args.weak else cfg["n"]
+    n_loc = n_glob // world
     rows = D.slab_rows(n_glob, world)
     r0, r1 = rows[rank], rows[rank + 1]
     n = r1 - r0
@@ -371,10 +426,12 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     if rank == 0:
         line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+                "dtype": "f64",
                 "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h; each GPU "
                         "generates its slab + halo columns in HBM)",
-                "config": {"workload": cfg["desc"] + f"; weak scaling: one global system of {world} x n rows",
+                "config": {"workload": cfg["desc"] + (f"; weak scaling: one global system of {world} x n rows"
+                                                      if args.weak else f"; strong scaling over {world} GPUs"),
                            "n": n_glob, "n_per_gpu": n_loc, "kl": k, "ku": k, "nrhs": nrhs,
                            "partitions_per_gpu": plan.p, "parallelism": f"slabs{world} (NCCL tip all-gathers)",
                            "l2": "inputs larger than L2"},
@@ -481,10 +538,15 @@ def impl_ours(args, cfg):
         berr = max(berr, spk.backward_error_device(band.data_ptr(), n, k, k, XT.data_ptr(), n, F.data_ptr(), n,
                                                    nrhs, True, sptr))
     del fact
+    # host copies of the device solutions: compared with the reference's
+    # (cpu_baseline leg) and with the e2e leg's host-buffer results
+    hXdev = X.cpu()
+    hXTdev = XT.cpu() if cfg["transpose"] else None
     torch.cuda.empty_cache()  # the library's own arena allocates next
 
     torch.cuda.synchronize()
     spk.lib().spk_launch_count(1)
+    spk.lib().spk_generic_launch_count(1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -495,6 +557,7 @@ def impl_ours(args, cfg):
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     launches = int(spk.lib().spk_launch_count(1))
+    generic = int(spk.lib().spk_generic_launch_count(1))
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     fl, useful = alg_flops(cfg)
     value = fl / (ms * 1e-3) / 1e9
@@ -548,25 +611,47 @@ def impl_ours(args, cfg):
         torch.cuda.synchronize()
         ems = (time.perf_counter() - t0) * 1e3 / e_steps
         nsol = 2 if cfg["transpose"] else 1
+        same = bool(torch.equal(hX, hXdev)) and (not cfg["transpose"] or bool(torch.equal(hXT, hXTdev)))
         e2e = {"value": round(fl / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                "ms_per_step": round(ems, 3),
                "h2d_bytes_per_step": int(hband.numel() * 8 + nsol * hF.numel() * 8),
-               "d2h_bytes_per_step": int(nsol * hX.numel() * 8)}
+               "d2h_bytes_per_step": int(nsol * hX.numel() * 8),
+               "x_bit_identical_to_device_run": same}
 
     # CPU baseline: the compiled reference on the box's host cores (rank 0, N=1)
+    # the full system (C5: a row sample, its host RAM and ~1 min per step), median
+    # of 3 steps on all physical cores (spike_cli.cpp:80-91), plus a t=1 figure
+    # on a bounded row sample; the reference's X / X^T of the full run are
+    # compared with the GPU's
     cpu = None
     if not args.no_cpu:
         try:
             from oracle.oracle import Reference
             if Reference.load() is not None:
-                n_s, t = reference_step_sample(cfg, target_s=12.0)
-                times, p = run_reference_steps(cfg, n_s, t, 1)
+                hc = host_cpu()
+                t = hc["physical_cores"] or os.cpu_count()
+                n_s = n if n <= 4_000_000 else 1_000_000
+                times, parts, p, Xr, XTr = reference_full(dict(cfg, n=n_s), t, 3, want_x=(n_s == n))
+                med = sorted(times)[1]
                 fls, _ = alg_flops(dict(cfg, n=n_s))
-                cpu = {"value": round(fls / times[0] / 1e9, 3), "unit": "GFLOP/s", "cores": t,
-                       "kind": "reference",
-                       "sample": f"n={n_s} of {n} rows (same k/nrhs/dd), reference make_plan(t={t}) -> p={p}, "
-                                 f"one factorize+solve" + ("+transpose_solve" if cfg["transpose"] else "") +
-                                 f" step in {times[0]:.2f} s"}
+                n1, t1 = reference_step_sample(cfg, target_s=4.0, t=1)
+                fl1, _ = alg_flops(dict(cfg, n=n1))
+                t1s, _ = run_reference_steps(cfg, n1, 1, 1)
+                cpu = {"value": round(fls / med / 1e9, 3), "unit": "GFLOP/s", "cores": t, "kind": "reference",
+                       "cpu_model": hc["model"], "logical_cpus": hc["logical_cpus"],
+                       "sample": (f"full system n={n}" if n_s == n else f"n={n_s} of {n} rows (same k/nrhs/dd)") +
+                                 f", reference make_plan(t={t}) -> p={p}, median of 3 factorize+solve" +
+                                 ("+transpose_solve" if cfg["transpose"] else "") +
+                                 f" steps: {med:.3f} s (all: " + ", ".join(f"{x:.3f}" for x in times) + ")",
+                       "phase_seconds_median": [sorted(x[i] for x in parts)[1] for i in range(3)],
+                       "t1": {"value": round(fl1 / t1s[0] / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
+                              "sample": f"n={n1} rows, make_plan(t=1), one step in {t1s[0]:.2f} s"}}
+                if Xr is not None:
+                    xr = torch.from_numpy(np.ascontiguousarray(Xr.T))
+                    cpu["dx_vs_gpu"] = (hXdev - xr).abs().max().item() / xr.abs().max().item()
+                    if cfg["transpose"] and XTr is not None:
+                        xtr = torch.from_numpy(np.ascontiguousarray(XTr.T))
+                        cpu["dx_vs_gpu_transpose"] = (hXTdev - xtr).abs().max().item() / xtr.abs().max().item()
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "error": str(ex)[:200]}
 
@@ -578,7 +663,7 @@ def impl_ours(args, cfg):
     if rank == 0:
         line = {"metric": args.metric, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": 1,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded counter-based generator, include/spike_b200_gen.h; generated in HBM)",
                 "config": {"workload": cfg["desc"], "n": n, "kl": k, "ku": k, "nrhs": nrhs,
                            "partitions": plan.p, "parallelism": "1gpu",
@@ -586,6 +671,7 @@ def impl_ours(args, cfg):
                 "useful_gflops": round(useful / (ms * 1e-3) / 1e9, 3),
                 "backward_error": berr,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "generic_kernel_launches": generic,
                 "clocks": clk.summary(), "impl": "ours"}
         if small is not None:
             line["small_k"] = small
@@ -604,6 +690,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-small-k", action="store_true", help="skip the C1 small-k HBM leg of the default line")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: n rows per GPU (one global system of N*n rows) instead of the fixed system")
     ap.add_argument("--slabs", action="store_true",
                     help="multi-GPU slab path even at N=1 (under torchrun; N>1 always uses it)")
     args = ap.parse_args()
