@@ -98,6 +98,9 @@ void reverse_rows_inplace(MatView v);
 DenseBlock reversed_rows(ConstMatView v);
 void gemm_minus(MatView c, ConstMatView a, ConstMatView b);
 void gemm_minus_t(MatView c, ConstMatView a, ConstMatView b);
+// spike2x2.hpp:12: the rows x cols block of A at (row0, col0); zero where the
+// band does not reach (the corner blocks B-hat / C-hat)
+DenseBlock band_corner(const BandedMatrix& a, int row0, int col0, int rows, int cols);
 
 // ---------------------------------------------------------------- planning
 enum class PartitionKind { FirstLast, InnerSingle, InnerDual };
@@ -225,6 +228,8 @@ double relative_residual(const BandedMatrix& a, const DenseBlock& x, const Dense
 double frobenius_norm(const DenseBlock& b);
 double norm1(const BandedMatrix& a);
 double max_abs(const BandedMatrix& a);
+// A^T as a band (kl and ku swap), band_ops.hpp
+BandedMatrix band_transpose(const BandedMatrix& a);
 // Hager's kappa_1 estimate (oracle.hpp condition_estimate_1norm) computed with
 // the factorization's GPU solves instead of a serial banded GE
 double condition_estimate_1norm(const SpikeFactorization& fact, const BandedMatrix& a);

@@ -266,6 +266,9 @@ spk_status spk_reduced_solve(const spk_reduced *r, int32_t transpose, double *z 
 spk_status spk_reduced_solve_device(const spk_reduced *r, int32_t transpose, double *d_z,
                                     int32_t ncols, void *stream);
 int32_t spk_reduced_levels(const spk_reduced *r);
+/* The hierarchy's factorization object, for the spk_fact_level_spike /
+ * spk_fact_coupling / spk_fact_units getters (owned by r). */
+const spk_fact *spk_reduced_fact(const spk_reduced *r);
 /* The reduced-system solve of a factorization on its own (2pk tip block). */
 spk_status spk_fact_reduced_solve(const spk_fact *f, int32_t transpose, double *z, int32_t ncols,
                                   int64_t *couplings);

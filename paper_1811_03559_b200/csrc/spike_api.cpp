@@ -42,12 +42,6 @@ DenseBlock fetch_tip(spk_fact* f, int which, int i, int k) {
     return b;
 }
 
-std::vector<int> level_units(int p) {
-    std::vector<int> u;
-    for (int x = p; x > 1; x = (x + 1) / 2) u.push_back(x);
-    return u;
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ storage
@@ -85,6 +79,19 @@ MatView DenseBlock::view() { return {data.data(), rows, cols, rows}; }
 ConstMatView DenseBlock::view() const { return {data.data(), rows, cols, rows}; }
 MatView DenseBlock::block(int row0, int nrows) { return view().block(row0, nrows); }
 ConstMatView DenseBlock::block(int row0, int nrows) const { return view().block(row0, nrows); }
+
+// band_corner (spike2x2.hpp:12, spike2x2.cpp:17-26): the rows x cols block of
+// A at (row0, col0), zero where the band (or the matrix) does not reach; the
+// B-hat / C-hat corners the device computes in k_corners
+DenseBlock band_corner(const BandedMatrix& a, int row0, int col0, int rows, int cols) {
+    DenseBlock out(rows, cols);
+    for (int j = 0; j < cols; ++j)
+        for (int i = 0; i < rows; ++i) {
+            const int gi = row0 + i, gj = col0 + j;
+            if (a.in_band(gi, gj)) out.at(i, j) = a.at(gi, gj);
+        }
+    return out;
+}
 
 DenseBlock copy_of(ConstMatView v) {
     DenseBlock out(v.rows, v.cols);
@@ -192,6 +199,8 @@ PartitionPlan gpu_plan(int n, int kl, int ku, int nrhs, bool pivoting, int p_hin
 }
 
 // ------------------------------------------------------------------ factors
+static void mirror_levels(ReducedLevels& rl, const spk_fact* h, int nlev, int k);
+
 SpikeFactorization factorize(const BandedMatrix& a, const PartitionPlan& plan, FactorOptions opts) {
     if (plan.n() != a.n()) throw std::invalid_argument("factorize: plan does not match matrix");
     for (int i = 0; i < plan.p; ++i)
@@ -224,6 +233,13 @@ SpikeFactorization factorize(const BandedMatrix& a, const PartitionPlan& plan, F
     rl.k = f.k;
     rl.boost_warnings = warn;
     rl.device = f.handle;
+    mirror_levels(rl, h, nlev, f.k);
+    return f;
+}
+
+// Host mirrors of the reduced hierarchy (ReducedLevels, factorize.hpp:26-49):
+// per level the units' V / W spike columns and the factored 2k coupling blocks
+static void mirror_levels(ReducedLevels& rl, const spk_fact* h, int nlev, int k) {
     for (int l = 0; l < nlev; ++l) {
         const int units = spk_fact_units(h, l);
         rl.v.emplace_back();
@@ -232,12 +248,12 @@ SpikeFactorization factorize(const BandedMatrix& a, const PartitionPlan& plan, F
             for (int which = 0; which < 2; ++which) {
                 int32_t hh = 0;
                 check(spk_fact_level_spike(h, l, which, u, &hh, nullptr));
-                DenseBlock b(hh, f.k);
+                DenseBlock b(hh, k);
                 check(spk_fact_level_spike(h, l, which, u, &hh, b.data.data()));
                 (which == 0 ? rl.v : rl.w).back().push_back(std::move(b));
             }
         rl.pairs.emplace_back();
-        const int nn = 2 * f.k;
+        const int nn = 2 * k;
         for (int a2 = 0; a2 < units / 2; ++a2) {
             std::vector<double> lu(static_cast<std::size_t>(nn) * nn);
             std::vector<int> piv(nn);
@@ -246,7 +262,6 @@ SpikeFactorization factorize(const BandedMatrix& a, const PartitionPlan& plan, F
             rl.pairs.back().emplace_back(nn, std::move(lu), std::move(piv), fb == 0);
         }
     }
-    return f;
 }
 
 ReducedLevels reduce_factorize(const std::vector<DenseBlock>& vt, const std::vector<DenseBlock>& vb,
@@ -270,8 +285,7 @@ ReducedLevels reduce_factorize(const std::vector<DenseBlock>& vt, const std::vec
     rl.standalone = true;
     rl.device = std::shared_ptr<void>(r, [](void* q) { spk_reduced_destroy(static_cast<spk_reduced*>(q)); });
     rl.boost_warnings = spk_reduced_boost_warnings(r);
-    if (k > 0)
-        for (int units : level_units(p)) rl.pairs.emplace_back(units / 2);
+    if (k > 0) mirror_levels(rl, spk_reduced_fact(r), spk_reduced_levels(r), k);
     return rl;
 }
 
@@ -366,6 +380,14 @@ double max_abs(const BandedMatrix& a) {
     double best = 0.0;
     for (double v : a.data()) best = std::max(best, std::fabs(v));
     return best;
+}
+
+// A^T as a band: packed column j of A^T holds row j of A (kl and ku swap)
+BandedMatrix band_transpose(const BandedMatrix& a) {
+    BandedMatrix t(a.n(), a.ku(), a.kl());
+    for (int i = 0; i < a.n(); ++i)
+        for (int j = std::max(0, i - a.kl()); j <= std::min(a.n() - 1, i + a.ku()); ++j) t.set(j, i, a.at(i, j));
+    return t;
 }
 
 // solve.cpp:404-432, the loop on the device (spk_refine): residual on the

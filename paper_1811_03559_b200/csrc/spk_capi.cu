@@ -3025,6 +3025,7 @@ int32_t spk_reduced_levels(const spk_reduced* r) {
     return r->f->levels.empty() ? 0 : (int)r->f->levels.size() - 1;
 }
 int32_t spk_reduced_boost_warnings(const spk_reduced* r) { return r->f->boost_warnings; }
+const spk_fact* spk_reduced_fact(const spk_reduced* r) { return r ? r->f.get() : nullptr; }
 void spk_reduced_destroy(spk_reduced* r) { delete r; }
 
 spk_status spk_band_matmul(const double* band, int64_t n, int32_t kl, int32_t ku, const double* X, int64_t ldx,
