@@ -144,6 +144,11 @@ spk_status spk_factorize_slab(const double *band, int32_t band_mem, int64_t n, i
                               int32_t ku, const spk_plan *plan, const spk_factor_options *opts,
                               int32_t open_left, int32_t open_right, void *stream,
                               spk_fact **out);
+/* Which engine factored f: 0 the general stage programs, 1 the small-k
+ * engine (spk_smallk.cu: kl, ku <= 16, non-pivoting), 2 the small-k engine
+ * whose reduced hierarchy fell back to the general programs (a pair needed the
+ * pivoted 2k coupling); -1 on error.  Waits for the factorization. */
+int32_t spk_fact_engine(const spk_fact *f);
 /* bit 0: open left edge, bit 1: open right edge */
 int32_t spk_fact_open(const spk_fact *f);
 /* The slab unit's tips [vt; vb; wt; wb] (4 blocks of k*k column-major, device):

@@ -487,6 +487,16 @@ struct spk_fact {
     int lblk_trw = 0;
     bool lblk_ok = false;      // written by the blocked pivoted LU of this factorization
     Program prog_factor, prog_fwd, prog_tr, prog_rfwd, prog_rtr;  // r*: reduced system only
+    // the general reduced-hierarchy stages (factorize.cpp:46-120); prog_factor
+    // holds the partition stages before them
+    Program prog_levels;
+    // small-k engine (spk_smallk.cu): tables in the factor blob, a fallback
+    // flag and grid-barrier words per factorization
+    bool sk = false;
+    bool sk_schur_all = false;  // finished, every pair on the Schur path: k_sk_solve applies
+    size_t sk_units = 0, sk_pairs = 0, sk_items = 0, sk_levels = 0;  // blob offsets
+    int sk_nlevels = 0, sk_mmax = 0;
+    unsigned* d_skmisc = nullptr;  // [0] fallback, [2..3] barrier
     std::shared_ptr<struct Symbolic> sym;  // cached geometry + programs (shared by equal factorizations)
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
@@ -528,7 +538,7 @@ struct spk_fact {
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
                         (void*)d_tfac, (void*)d_dinv, (void*)d_sblob, (void*)d_flags, (void*)d_sblob_prev,
-                        (void*)d_lblk})
+                        (void*)d_lblk, (void*)d_skmisc})
             if (q) dfree(q, stream);
         if (upload_ev) cudaEventDestroy(upload_ev);
         if (ready_ev) cudaEventDestroy(ready_ev);
@@ -946,6 +956,7 @@ void emit_pair_solves(Builder& b, const std::vector<PairZ>& zs, int redbuf, long
 // factor program (factorize.cpp:133-257 + reduce_factorize :46-120)
 void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
     Builder b{f, pb, f.prog_factor};
+    Builder bl{f, pb, f.prog_levels};
     const int p = f.p, k = f.k;
     const long long n = f.n, kk = (long long)k * k;
     if (!f.reduced_only) {
@@ -1054,14 +1065,14 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
             }
         }
         if (schur_ok) {
-            b.cjobs(ST_WCHECK, cplS);
-            b.cjobs(ST_SCHUR_INIT, cplS);
-            b.gemm(sgemm);
+            bl.cjobs(ST_WCHECK, cplS);
+            bl.cjobs(ST_SCHUR_INIT, cplS);
+            bl.gemm(sgemm);
             for (int a = 0; a < np; ++a) cplS[a].aux = lv.sinv[a];
-            b.cjobs(ST_SCHUR_INV, cplS);  // S^-1 into the pool (S stays in the factor pool)
+            bl.cjobs(ST_SCHUR_INV, cplS);  // S^-1 into the pool (S stays in the factor pool)
         }
-        b.cpl(cplG);
-        b.lu(lus);
+        bl.cpl(cplG);
+        bl.lu(lus);
         const Level& nx = f.levels[l + 1];
         std::vector<CopyJob> init;
         std::vector<PairZ> zs;
@@ -1098,8 +1109,8 @@ void build_factor_program(spk_fact& f, ProgramBuilder& pb) {
                 init.push_back(cj(src, dst, 0, h, CP_COPY, 0, k));
             }
         }
-        b.copy(init);
-        emit_pair_solves(b, zs, B_AUX, -1, k, false, k);
+        bl.copy(init);
+        emit_pair_solves(bl, zs, B_AUX, -1, k, false, k);
     }
     f.auxf_rows = std::max<long long>(red_cursor, 1);
 }
@@ -1680,7 +1691,10 @@ struct Symbolic {
     long long off_bhat = 0, off_chat = 0, pool_size = 0, fac_size = 0, piv_size = 0, tfac_size = 0;
     long long aux_rows = 0, auxf_rows = 0;
     int tau_w = 0, npairs = 0;
-    Program prog_factor;
+    Program prog_factor, prog_levels;
+    bool sk = false;
+    size_t sk_units = 0, sk_pairs = 0, sk_items = 0, sk_levels = 0;
+    int sk_nlevels = 0, sk_mmax = 0;
     std::vector<char> blob;
     std::map<std::vector<int>, SolveProgs> solves;
 };
@@ -1707,6 +1721,62 @@ std::string sym_key(const spk_fact& f) {
 }
 
 void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob);
+
+// The small-k engine takes non-pivoting closed systems with kl, ku <= 16, at
+// least two partitions, every partition at least 2k rows and short enough
+// for its shared-memory staging (spk_smallk.cu).
+constexpr int kSkMaxRows = 384;
+bool sk_eligible(const spk_fact& f) {
+    if (f.piv_on || f.open() || f.reduced_only || generic_path()) return false;
+    if (f.kl > 16 || f.ku > 16 || f.k < 1 || f.p < 2) return false;
+    for (int i = 0; i < f.p; ++i) {
+        const long long m = f.bounds[i + 1] - f.bounds[i];
+        if (m < 2LL * f.k || m > kSkMaxRows) return false;
+    }
+    return true;
+}
+
+// Level tables of the small-k engine (SkUnit / SkPair / SkItem / SkLevel, in
+// the factor blob): units of every level with their pool offsets, pairs with
+// their S^-1 slot, and per level the work items (pair, 32-row chunk of the
+// merged unit; carried odd units).
+void build_sk_tables(spk_fact& f, ProgramBuilder& pb) {
+    std::vector<SkUnit> units;
+    std::vector<SkPair> pairs;
+    std::vector<SkItem> items;
+    std::vector<SkLevel> lvls;
+    std::vector<int> ubase;
+    for (const Level& lv : f.levels) {
+        ubase.push_back((int)units.size());
+        for (int u = 0; u < lv.units; ++u) units.push_back(SkUnit{lv.voff[u], lv.woff[u], lv.uh[u], lv.uoff[u]});
+    }
+    const int L = (int)f.levels.size() - 1;
+    for (int l = 0; l < L; ++l) {
+        const Level& lv = f.levels[l];
+        const int np = lv.units / 2, pbase = (int)pairs.size();
+        SkLevel d{(int)items.size(), 0};
+        for (int a = 0; a < np; ++a) {
+            pairs.push_back(SkPair{lv.sinv[a], lv.gidx[a], ubase[l] + 2 * a, ubase[l + 1] + a, 0});
+            const int H = lv.uh[2 * a] + lv.uh[2 * a + 1];
+            for (int r = 0; r < H; r += kSkChunk) items.push_back(SkItem{pbase + a, r, -1, 0});
+        }
+        if (lv.units % 2 == 1) {
+            const int u = lv.units - 1;
+            for (int r = 0; r < lv.uh[u]; r += kSkChunk)
+                items.push_back(SkItem{-(ubase[l] + u) - 1, r, ubase[l + 1] + np, 0});
+        }
+        d.nitems = (int)items.size() - d.item0;
+        lvls.push_back(d);
+    }
+    f.sk_units = pb.push(units);
+    f.sk_pairs = pb.push(pairs);
+    f.sk_items = pb.push(items);
+    f.sk_levels = pb.push(lvls);
+    f.sk_nlevels = L;
+    int mmax = 0;
+    for (int i = 0; i < f.p; ++i) mmax = std::max(mmax, f.parts[i].m);
+    f.sk_mmax = mmax;
+}
 
 // Symbolic part: geometry, pool layout, programs (cached), device allocations.
 void setup_fact(spk_fact& f, cudaStream_t s) {
@@ -1735,6 +1805,14 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
         f.tau_w = y.tau_w;
         f.npairs = y.npairs;
         f.prog_factor = y.prog_factor;
+        f.prog_levels = y.prog_levels;
+        f.sk = y.sk;
+        f.sk_units = y.sk_units;
+        f.sk_pairs = y.sk_pairs;
+        f.sk_items = y.sk_items;
+        f.sk_levels = y.sk_levels;
+        f.sk_nlevels = y.sk_nlevels;
+        f.sk_mmax = y.sk_mmax;
         tr.mark("symbolic (cached)");
         alloc_fact(f, s, y.blob);
         return;
@@ -1791,6 +1869,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     tr.mark("geometry");
     ProgramBuilder pb;
     build_factor_program(f, pb);
+    if (f.sk) build_sk_tables(f, pb);
     tr.mark("factor program");
     auto y = std::make_shared<Symbolic>();
     y->parts = f.parts;
@@ -1806,6 +1885,14 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     y->tau_w = f.tau_w;
     y->npairs = f.npairs;
     y->prog_factor = f.prog_factor;
+    y->prog_levels = f.prog_levels;
+    y->sk = f.sk;
+    y->sk_units = f.sk_units;
+    y->sk_pairs = f.sk_pairs;
+    y->sk_items = f.sk_items;
+    y->sk_levels = f.sk_levels;
+    y->sk_nlevels = f.sk_nlevels;
+    y->sk_mmax = f.sk_mmax;
     y->blob = std::move(pb.blob);
     {
         SymCache& c = sym_cache();
@@ -1840,6 +1927,10 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     tr.mark("allocations");
     f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
     ck(cudaMemsetAsync(f.d_flags, 0, sizeof(int) * std::max(f.npairs, 1), s), "memset");
+    if (f.sk) {
+        f.d_skmisc = dalloc<unsigned>(4, s);
+        ck(cudaMemsetAsync(f.d_skmisc, 0, sizeof(unsigned) * 4, s), "memset");
+    }
     ck(cudaMemcpyAsync(f.d_parts, f.parts.data(), sizeof(PartDev) * nparts, cudaMemcpyHostToDevice, s), "upload");
     ck(cudaMemcpyAsync(f.d_bounds, f.bounds.data(), sizeof(long long) * (p + 1), cudaMemcpyHostToDevice, s),
        "upload");
@@ -1854,6 +1945,30 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
 }
 
 void build_solve_programs(spk_fact& f, cudaStream_t s);
+Bufs make_bufs(const spk_fact* f);
+
+// The small-k engine's factorization: partitions (LU, factor layouts,
+// corners, level-0 tips) and the whole reduced hierarchy, two launches.
+// false when its kernels do not cover the shape (the caller runs the general
+// programs).
+bool run_sk_factor(spk_fact& f, const double* dband, cudaStream_t s) {
+    const char* blob = f.d_blob;
+    SkPartsArgs P{dband, f.n, f.kl, f.ku, f.k, f.p, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_boost, f.d_pool,
+                  f.off_bhat, f.off_chat, reinterpret_cast<const SkUnit*>(blob + f.sk_units), f.boost_eps, f.sk_mmax};
+    {
+        ProfScope ps(ST_LU, s, 8.0 * f.n * f.k * f.k, 16.0 * f.n * (f.kl + f.ku + 1));
+        if (!launch_sk_parts(P, s)) return false;
+    }
+    SkLevelsArgs L{f.d_pool, reinterpret_cast<const SkUnit*>(blob + f.sk_units),
+                   reinterpret_cast<const SkPair*>(blob + f.sk_pairs), reinterpret_cast<const SkItem*>(blob + f.sk_items),
+                   reinterpret_cast<const SkLevel*>(blob + f.sk_levels), f.sk_nlevels, f.k, f.d_flags,
+                   reinterpret_cast<int*>(f.d_skmisc), f.d_skmisc + 2};
+    {
+        ProfScope ps(ST_CPL, s, 0.0, 0.0);
+        launch_sk_levels(L, s);
+    }
+    return true;
+}
 
 // the factorization's device state (factors, pool, flags, solve jobs) is
 // complete on f.stream up to here
@@ -1895,7 +2010,29 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     std::vector<int> flags(std::max(f.npairs, 1), 0);
     if (f.npairs > 0)
         ck(cudaMemcpyAsync(flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost, s), "flags");
+    unsigned skfb = 0;
+    if (f.sk) ck(cudaMemcpyAsync(&skfb, f.d_skmisc, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "download");
     ck(cudaStreamSynchronize(s), "factorize");
+    if (skfb) {
+        // a pair needs the pivoted 2k coupling: the general hierarchy program
+        // from the (untouched) level-0 tips
+        tr.mark("small-k fallback");
+        double* auxf = dalloc<double>((size_t)f.auxf_rows * f.k, s);
+        Bufs B = make_bufs(&f);
+        B.p[B_POOL] = f.d_pool;
+        B.p[B_AUX] = auxf;
+        B.ld[B_AUX] = f.auxf_rows;
+        Exec ex{f, s, B, f.k};
+        ex.n = f.n;
+        ex.run(f.prog_levels, f.d_blob);
+        dfree(auxf, s);
+        ck(cudaMemcpyAsync(&status, f.d_status, sizeof(int), cudaMemcpyDeviceToHost, s), "download");
+        ck(cudaMemcpyAsync(fell.data(), f.d_fell, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
+        if (f.npairs > 0)
+            ck(cudaMemcpyAsync(flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost, s), "flags");
+        ck(cudaStreamSynchronize(s), "factorize");
+    }
+    f.sk_schur_all = f.sk && !skfb;
     tr.mark("stream synced");
     ck(cudaGetLastError(), "factorize kernels");
     if (status == 2) fail(SPK_ESINGULAR, "lu_factor: exactly singular column in pivoting mode");
@@ -2186,8 +2323,11 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
             // narrow bands: up to 8 partitions per SM, but no shorter than
             // ~2k rows (more reduced-system levels cost more than the shorter
             // column chain saves: C1 n=1e5 p=1184 3.6 ms, p=148 2.0 ms)
+            // narrow non-pivoting bands take the small-k engine (spk_smallk.cu):
+            // partitions of ~192 rows (register-window LU per warp), staged
+            // in shared memory
+            else if (!pivoting && kl <= 16 && ku <= 16) pp = (int)std::max<long long>(2, (n + 191) / 192);
             else pp = (int)std::min<long long>(8 * sms, std::max<long long>(sms, n / 2048));
-            (void)pivoting;
         }
         pp = (int)std::max<long long>(1, std::min<long long>(pp, n / std::max<long long>(min_part, 1)));
         if (pp > cap) fail(SPK_EINVAL, "gpu_plan: capacity too small");
@@ -2348,6 +2488,7 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         f->kinds.assign(plan->p, SPK_INNER_SINGLE);
         if (plan->kinds) f->kinds.assign(plan->kinds, plan->kinds + plan->p);
         f->stream = s;
+        f->sk = sk_eligible(*f);
         Tracer tr("factorize");
         setup_fact(*f, s);
         // until the factorization is finished (ensure_finished) solves run
@@ -2371,9 +2512,15 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         }
         dband += ld * hl;  // column 0 of the slab
         const int p = f->p;
-        long long max_elems = 0;
-        for (int i = 0; i < p; ++i) max_elems = std::max(max_elems, (long long)f->parts[i].m * f->parts[i].rows);
-        (void)max_elems;
+        if (f->sk && run_sk_factor(*f, dband, s)) {
+            mark_ready(*f, s);
+            tr.mark("enqueued (small-k engine)");
+            if (tmp) dfree(tmp, s);
+            f->pending.store(true);
+            *out = f.release();
+            return;
+        }
+        f->sk = false;
         {
             ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);
             launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->open_l, f->open_r, f->d_pool + f->off_bhat,
@@ -2396,6 +2543,7 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         ex.n = n;
         ex.band = dband;
         ex.run(f->prog_factor, f->d_blob);
+        ex.run(f->prog_levels, f->d_blob);
         mark_ready(*f, s);
         tr.mark("enqueued");
         if (fs) dfree(fs, s);
@@ -2441,6 +2589,12 @@ spk_status spk_fact_unit_tips(const spk_fact* f, double* d_tips, void* stream) {
                "unit tips");
         }
     });
+}
+
+int32_t spk_fact_engine(const spk_fact* f) {
+    if (!f) return -1;
+    if (guarded([&] { ensure_finished(f); }) != SPK_OK) return -1;
+    return f->sk ? (f->sk_schur_all ? 1 : 2) : 0;
 }
 
 int32_t spk_fact_open(const spk_fact* f) { return f ? (f->open_l | (f->open_r << 1)) : 0; }
@@ -2654,16 +2808,34 @@ struct spk_xsolve {
     cudaStream_t s = nullptr;
     double *S = nullptr, *T = nullptr, *AUX = nullptr, *tF = nullptr, *tX = nullptr;
     double *XCH = nullptr, *XIN = nullptr;
+    // small-k engine (k_sk_solve): second tip buffer, grid-barrier words
+    bool sk = false;
+    double* T2 = nullptr;
+    unsigned* bar = nullptr;
     Bufs B;
 
     ~spk_xsolve() {
-        for (double* q : {S, T, AUX, tF, tX, XCH, XIN})
+        for (double* q : {S, T, AUX, tF, tX, XCH, XIN, T2})
             if (q) dfree(q, s);
+        if (bar) dfree(bar, s);
     }
     const Program& prog() const { return transpose ? f->prog_tr : f->prog_fwd; }
     // rows of the export block after phase q (column-major, ld = rows)
     int export_rows(int q) const { return (transpose && q == 1) ? 4 * f->k : 2 * f->k; }
     void run_phase() {
+        if (sk) {
+            const char* blob = f->d_blob;
+            SkSolveArgs A{f->d_parts, f->p, f->k, nrhs, f->d_fac, f->d_pool, f->off_bhat, f->off_chat,
+                          reinterpret_cast<const SkUnit*>(blob + f->sk_units),
+                          reinterpret_cast<const SkPair*>(blob + f->sk_pairs),
+                          reinterpret_cast<const SkItem*>(blob + f->sk_items),
+                          reinterpret_cast<const SkLevel*>(blob + f->sk_levels), f->sk_nlevels, B.p[B_F], B.ld[B_F],
+                          B.p[B_X], B.ld[B_X], T, T2, bar, f->sk_mmax};
+            ProfScope ps(ST_SWEEP, s, 8.0 * f->n * f->k * nrhs, 16.0 * f->n * (f->kl + f->ku + 1));
+            launch_sk_solve(A, s);
+            ++phase;
+            return;
+        }
         Exec ex{*f, s, B, nrhs};
         ex.n = f->n;
         if (phase + 1 < nphases) {
@@ -2748,6 +2920,17 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     }
     B.p[B_POOL] = f.d_pool;
     B.ld[B_POOL] = 1;
+    // forward solves with few right-hand sides of a small-k factorization
+    // whose pairs all took the Schur path: one cooperative kernel
+    if (f.sk_schur_all && !transpose && nrhs >= 1 && nrhs <= kSkMaxRhs && !f.open() && f.coupled()) {
+        x->sk = true;
+        const long long H = 2LL * f.p * f.k;
+        x->T2 = dalloc<double>((size_t)H * nrhs, s);
+        x->bar = static_cast<unsigned*>(arena().alloc(2 * sizeof(unsigned), s));
+        ck(cudaMemsetAsync(x->bar, 0, 2 * sizeof(unsigned), s), "memset");
+        B.ld[B_T] = H;
+        B.p[B_T] = x->T;
+    }
     return x;
 }
 
@@ -2778,6 +2961,7 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
     // are used, and fin_mu keeps a concurrent finish from swapping them while
     // this call enqueues
     spk_fact& fm = const_cast<spk_fact&>(*fc);
+    if (fm.sk) ensure_finished(fc);  // a small-k fallback replaces the hierarchy at the finish
     std::lock_guard<std::mutex> lk(fm.fin_mu);
     if (!fm.pending.load() && fm.fin_status != SPK_OK) fail(fm.fin_status, fm.fin_msg);
     CopyStreams& cs = copy_streams();
@@ -2967,6 +3151,7 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
             B.ld[B_AUX] = f.auxf_rows;
             Exec ex{f, s, B, k};
             ex.run(f.prog_factor, f.d_blob);
+            ex.run(f.prog_levels, f.d_blob);
             dfree(auxf, s);
         }
         finish_factor(f, s);

@@ -141,6 +141,85 @@ bool launch_sweep_dmma_blt(int ntw, int nwarps, dim3 grid, size_t smem, const Fa
 void launch_transpose_factors(const PartDev* d_parts, int nparts, long long max_elems, const double* fac,
                               double* tfac, double* dinv, cudaStream_t s);
 
+// ---------------------------------------------------------------------------
+// small-k engine (spk_smallk.cu): non-pivoting bands with kl, ku <= 31.  One
+// warp per partition for the partition work (register-window LU, spike tips),
+// one cooperative persistent kernel for the reduced hierarchy and one for the
+// forward solve, levels separated by a grid barrier.
+struct SkUnit {
+    long long voff, woff;  // pool offsets of the unit's V / W spike (h x k, ld h), -1: none
+    int uh, uoff;          // height (rows of the reduced system), first reduced row
+};
+struct SkPair {
+    long long sinv;  // pool offset of S^-1 (k x k, ld k)
+    int gidx;        // flag index (1 = Schur path)
+    int left;        // global index of the left unit (right = left + 1)
+    int next;        // global index of the merged unit on the next level
+    int pad;
+};
+struct SkItem {
+    int pair;  // >= 0: pair (global index); < 0: carried unit -(pair + 1) (global unit index)
+    int row0;  // first row of this item's chunk of the merged unit
+    int next;  // carried unit: its global index on the next level
+    int pad;
+};
+struct SkLevel {
+    int item0, nitems;
+};
+constexpr int kSkChunk = 256;  // merged-unit rows per work item
+struct SkPartsArgs {
+    const double* band;
+    long long n;
+    int akl, aku, k, p;
+    const PartDev* parts;
+    double* fac;
+    double* tfac;
+    double* dinv;
+    int* boost;
+    double* pool;
+    long long off_bhat, off_chat;
+    const SkUnit* units;  // level 0: one per partition
+    double boost_eps;
+    int mmax;  // longest partition
+};
+struct SkLevelsArgs {
+    double* pool;
+    const SkUnit* units;
+    const SkPair* pairs;
+    const SkItem* items;
+    const SkLevel* levels;
+    int nlevels, k;
+    int* flags;
+    int* fallback;   // set when a pair needs the generic (pivoted 2k) coupling
+    unsigned* bar;   // grid barrier: {count, generation}, zeroed
+};
+struct SkSolveArgs {
+    const PartDev* parts;
+    int p, k, nrhs;
+    const double* fac;
+    const double* pool;
+    long long off_bhat, off_chat;
+    const SkUnit* units;
+    const SkPair* pairs;
+    const SkItem* items;
+    const SkLevel* levels;
+    int nlevels;
+    const double* F;
+    long long ldf;
+    double* X;
+    long long ldx;
+    double* T0;
+    double* T1;  // reduced right-hand sides, ping-pong per level (2pk x nrhs, ld 2pk)
+    unsigned* bar;
+    int mmax;
+};
+// false when the shape is not covered (kl or ku > 31)
+bool launch_sk_parts(const SkPartsArgs& A, cudaStream_t s);
+void launch_sk_levels(const SkLevelsArgs& A, cudaStream_t s);
+// forward solve, nrhs <= kSkMaxRhs
+constexpr int kSkMaxRhs = 8;
+void launch_sk_solve(const SkSolveArgs& A, cudaStream_t s);
+
 void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd, long long col0,
                           long long ncols, double* band, cudaStream_t s);
 void launch_generate_rhs(unsigned long long seed, long long row0, long long nrows, int ncols, double* F,

@@ -188,6 +188,8 @@ def lib():
         L.spk_factorize_slab.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                          C.POINTER(_Plan), C.POINTER(_Opts), C.c_int32, C.c_int32,
                                          C.c_void_p, C.POINTER(C.c_void_p)]
+        L.spk_fact_engine.argtypes = [C.c_void_p]
+        L.spk_fact_engine.restype = C.c_int32
         L.spk_fact_open.argtypes = [C.c_void_p]
         L.spk_fact_open.restype = C.c_int32
         L.spk_fact_unit_tips.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -213,6 +215,11 @@ def _check(rc):
 
 def launch_count(reset=False) -> int:
     return int(lib().spk_launch_count(1 if reset else 0))
+
+
+def fact_engine(fact) -> int:
+    """0: general stage programs, 1: small-k engine, 2: small-k with the general hierarchy fallback."""
+    return int(lib().spk_fact_engine(fact._h))
 
 
 def generic_launch_count(reset=False) -> int:
