@@ -149,6 +149,10 @@ spk_status spk_factorize_slab(const double *band, int32_t band_mem, int64_t n, i
  * whose reduced hierarchy fell back to the general programs (a pair needed the
  * pivoted 2k coupling); -1 on error.  Waits for the factorization. */
 int32_t spk_fact_engine(const spk_fact *f);
+/* Debug hook: a device buffer of 2 x 65536 u64 the small-k engine's
+ * cooperative kernels stamp with %globaltimer per (level phase, CTA, mark)
+ * (factor hierarchy at [0, 65536), forward solve after it); null disables. */
+void spk_debug_set_trace(void *d_buf);
 /* bit 0: open left edge, bit 1: open right edge */
 int32_t spk_fact_open(const spk_fact *f);
 /* The slab unit's tips [vt; vb; wt; wb] (4 blocks of k*k column-major, device):

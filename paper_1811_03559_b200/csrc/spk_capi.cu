@@ -132,6 +132,8 @@ void set_smem_attr(const void* fn, int bytes) {
     cur = bytes;
 }
 
+unsigned long long* g_sk_trace = nullptr;
+
 int device_sms() {
     static std::mutex mu;
     static std::map<int, int> sms;
@@ -495,8 +497,13 @@ struct spk_fact {
     bool sk = false;
     bool sk_schur_all = false;  // finished, every pair on the Schur path: k_sk_solve applies
     size_t sk_units = 0, sk_pairs = 0, sk_items = 0, sk_levels = 0;  // blob offsets
-    int sk_nlevels = 0, sk_mmax = 0;
-    unsigned* d_skmisc = nullptr;  // [0] fallback, [2..3] barrier
+    int sk_nlevels = 0, sk_mmax = 0, sk_rmax = 0;
+    unsigned* d_skmisc = nullptr;  // small-k: [0] status, [2, 2+nparts) fell, then 4 barrier words
+    bool tables_shared = false;    // d_parts / d_bounds / d_blob belong to the symbolic
+    // the small-k engine writes the packed factor only; the row-major copy the
+    // general programs' transposed sweeps read is made at their first use
+    std::atomic<bool> tfac_ready{true};
+    std::mutex tfac_mu;
     std::shared_ptr<struct Symbolic> sym;  // cached geometry + programs (shared by equal factorizations)
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
@@ -534,6 +541,15 @@ struct spk_fact {
         for (auto& u : uses) {
             cudaStreamWaitEvent(stream, u.second, 0);
             cudaEventDestroy(u.second);
+        }
+        if (tables_shared) {
+            d_parts = nullptr;
+            d_bounds = nullptr;
+            d_blob = nullptr;
+        }
+        if (d_skmisc) {  // status / fell live inside it
+            d_status = nullptr;
+            d_fell = nullptr;
         }
         for (void* q : {(void*)d_parts, (void*)d_fac, (void*)d_piv, (void*)d_pool, (void*)d_bounds,
                         (void*)d_amax, (void*)d_boost, (void*)d_fell, (void*)d_status, (void*)d_blob,
@@ -1694,9 +1710,19 @@ struct Symbolic {
     Program prog_factor, prog_levels;
     bool sk = false;
     size_t sk_units = 0, sk_pairs = 0, sk_items = 0, sk_levels = 0;
-    int sk_nlevels = 0, sk_mmax = 0;
+    int sk_nlevels = 0, sk_mmax = 0, sk_rmax = 0;
     std::vector<char> blob;
     std::map<std::vector<int>, SolveProgs> solves;
+    // device copies of parts / bounds / blob for the small-k engine (one
+    // upload per shape and device instead of one per factorization); kept
+    // for the process lifetime of the cache entry
+    struct DevTables {
+        PartDev* parts = nullptr;
+        long long* bounds = nullptr;
+        char* blob = nullptr;
+    };
+    std::mutex dev_mu;
+    std::map<int, DevTables> dev;
 };
 
 namespace {
@@ -1754,9 +1780,16 @@ void build_sk_tables(spk_fact& f, ProgramBuilder& pb) {
     for (int l = 0; l < L; ++l) {
         const Level& lv = f.levels[l];
         const int np = lv.units / 2, pbase = (int)pairs.size();
-        SkLevel d{(int)items.size(), 0};
+        SkLevel d{(int)items.size(), 0, pbase, np, -1, -1};
+        if (lv.units % 2 == 1) {
+            d.carry = ubase[l] + lv.units - 1;
+            d.carry_next = ubase[l + 1] + np;
+        }
         for (int a = 0; a < np; ++a) {
-            pairs.push_back(SkPair{lv.sinv[a], lv.gidx[a], ubase[l] + 2 * a, ubase[l + 1] + a, 0});
+            const Level& nx = f.levels[l + 1];
+            pairs.push_back(SkPair{lv.sinv[a], lv.voff[2 * a], lv.woff[2 * a], lv.voff[2 * a + 1], lv.woff[2 * a + 1],
+                                   nx.voff[a], nx.woff[a], lv.uh[2 * a], lv.uh[2 * a + 1], lv.uoff[2 * a], lv.gidx[a],
+                                   ubase[l] + 2 * a, ubase[l + 1] + a});
             const int H = lv.uh[2 * a] + lv.uh[2 * a + 1];
             for (int r = 0; r < H; r += kSkChunk) items.push_back(SkItem{pbase + a, r, -1, 0});
         }
@@ -1773,9 +1806,13 @@ void build_sk_tables(spk_fact& f, ProgramBuilder& pb) {
     f.sk_items = pb.push(items);
     f.sk_levels = pb.push(lvls);
     f.sk_nlevels = L;
-    int mmax = 0;
-    for (int i = 0; i < f.p; ++i) mmax = std::max(mmax, f.parts[i].m);
+    int mmax = 0, rmax = 0;
+    for (int i = 0; i < f.p; ++i) {
+        mmax = std::max(mmax, f.parts[i].m);
+        rmax = std::max(rmax, f.parts[i].rows);
+    }
     f.sk_mmax = mmax;
+    f.sk_rmax = rmax;
 }
 
 // Symbolic part: geometry, pool layout, programs (cached), device allocations.
@@ -1813,6 +1850,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
         f.sk_levels = y.sk_levels;
         f.sk_nlevels = y.sk_nlevels;
         f.sk_mmax = y.sk_mmax;
+        f.sk_rmax = y.sk_rmax;
         tr.mark("symbolic (cached)");
         alloc_fact(f, s, y.blob);
         return;
@@ -1893,6 +1931,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
     y->sk_levels = f.sk_levels;
     y->sk_nlevels = f.sk_nlevels;
     y->sk_mmax = f.sk_mmax;
+    y->sk_rmax = f.sk_rmax;
     y->blob = std::move(pb.blob);
     {
         SymCache& c = sym_cache();
@@ -1905,10 +1944,53 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
 }
 
 // device allocations (stream ordered) and uploads of the symbolic state
+// The symbolic's device tables for the current device, uploaded once.
+Symbolic::DevTables sym_device_tables(Symbolic& y, const spk_fact& f) {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "device");
+    std::lock_guard<std::mutex> lk(y.dev_mu);
+    auto it = y.dev.find(dev);
+    if (it != y.dev.end()) return it->second;
+    Symbolic::DevTables t;
+    ck(cudaMalloc(&t.parts, sizeof(PartDev) * std::max<size_t>(y.parts.size(), 1)), "alloc");
+    ck(cudaMalloc(&t.bounds, sizeof(long long) * (f.p + 1)), "alloc");
+    ck(cudaMalloc(&t.blob, std::max<size_t>(y.blob.size(), 1)), "alloc");
+    ck(cudaMemcpy(t.parts, y.parts.data(), sizeof(PartDev) * y.parts.size(), cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemcpy(t.bounds, f.bounds.data(), sizeof(long long) * (f.p + 1), cudaMemcpyHostToDevice), "upload");
+    if (!y.blob.empty()) ck(cudaMemcpy(t.blob, y.blob.data(), y.blob.size(), cudaMemcpyHostToDevice), "upload");
+    y.dev[dev] = t;
+    return t;
+}
+
 void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     Tracer tr("alloc");
     const int p = f.p;
     const int nparts = (int)f.parts.size();
+    if (f.sk && f.sym) {
+        // small-k engine: the symbolic's device tables, the factor, the pool
+        // (every entry any consumer reads is written by the engine's kernels:
+        // no memset) and one small zeroed block (status, fell, barrier words)
+        const Symbolic::DevTables t = sym_device_tables(*f.sym, f);
+        f.d_parts = t.parts;
+        f.d_bounds = t.bounds;
+        f.d_blob = t.blob;
+        f.tables_shared = true;
+        f.d_fac = dalloc<double>(f.fac_size, s);
+        f.d_pool = dalloc<double>(f.pool_size, s);
+        f.d_tfac = dalloc<double>(f.tfac_size, s);
+        f.d_dinv = dalloc<double>(f.n, s);
+        f.d_piv = dalloc<int>(1, s);
+        f.d_amax = dalloc<unsigned long long>(1, s);
+        f.d_boost = dalloc<int>(nparts, s);
+        f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
+        const size_t misc = 2 + nparts + 4;  // status, pad, fell[nparts], barrier words
+        f.d_skmisc = dalloc<unsigned>(misc, s);
+        ck(cudaMemsetAsync(f.d_skmisc, 0, sizeof(unsigned) * misc, s), "memset");
+        f.d_status = reinterpret_cast<int*>(f.d_skmisc);
+        f.d_fell = reinterpret_cast<int*>(f.d_skmisc) + 2;
+        tr.mark("small-k allocations");
+        return;
+    }
     f.d_parts = dalloc<PartDev>(nparts, s);
     f.d_fac = dalloc<double>(f.fac_size, s);
     f.d_piv = dalloc<int>(f.piv_size, s);
@@ -1953,7 +2035,7 @@ Bufs make_bufs(const spk_fact* f);
 // programs).
 bool run_sk_factor(spk_fact& f, const double* dband, cudaStream_t s) {
     const char* blob = f.d_blob;
-    SkPartsArgs P{dband, f.n, f.kl, f.ku, f.k, f.p, f.d_parts, f.d_fac, f.d_tfac, f.d_dinv, f.d_boost, f.d_pool,
+    SkPartsArgs P{dband, f.n, f.kl, f.ku, f.k, f.p, f.d_parts, f.d_fac, f.d_dinv, f.d_boost, f.d_pool,
                   f.off_bhat, f.off_chat, reinterpret_cast<const SkUnit*>(blob + f.sk_units), f.boost_eps, f.sk_mmax};
     {
         ProfScope ps(ST_LU, s, 8.0 * f.n * f.k * f.k, 16.0 * f.n * (f.kl + f.ku + 1));
@@ -1962,7 +2044,7 @@ bool run_sk_factor(spk_fact& f, const double* dband, cudaStream_t s) {
     SkLevelsArgs L{f.d_pool, reinterpret_cast<const SkUnit*>(blob + f.sk_units),
                    reinterpret_cast<const SkPair*>(blob + f.sk_pairs), reinterpret_cast<const SkItem*>(blob + f.sk_items),
                    reinterpret_cast<const SkLevel*>(blob + f.sk_levels), f.sk_nlevels, f.k, f.d_flags,
-                   reinterpret_cast<int*>(f.d_skmisc), f.d_skmisc + 2};
+                   f.boost_eps, f.d_skmisc + 2 + f.parts.size(), g_sk_trace};
     {
         ProfScope ps(ST_CPL, s, 0.0, 0.0);
         launch_sk_levels(L, s);
@@ -1975,6 +2057,27 @@ bool run_sk_factor(spk_fact& f, const double* dband, cudaStream_t s) {
 void mark_ready(spk_fact& f, cudaStream_t s) {
     if (!f.ready_ev) ck(cudaEventCreateWithFlags(&f.ready_ev, cudaEventDisableTiming), "event");
     ck(cudaEventRecord(f.ready_ev, s), "event");
+}
+
+// forward solves with few right-hand sides of a small-k factorization run
+// the engine's own cooperative kernel (k_sk_solve)
+bool sk_kernel_solve(const spk_fact& f, int transpose, int nrhs) {
+    return f.sk_schur_all && !transpose && nrhs >= 1 && nrhs <= kSkMaxRhs && !f.open() && f.coupled() &&
+           sk_solve_smem(f.sk_mmax, f.sk_rmax, nrhs) <= 227u * 1024;
+}
+
+// the row-major factor copy of a small-k factorization, once, ordered on
+// the factorization's stream (later solves on other streams wait on ready_ev)
+void ensure_tfac(const spk_fact* fc) {
+    spk_fact& f = const_cast<spk_fact&>(*fc);
+    if (f.tfac_ready.load()) return;
+    std::lock_guard<std::mutex> lk(f.tfac_mu);
+    if (f.tfac_ready.load()) return;
+    long long mx = 0;
+    for (int i = 0; i < f.p; ++i) mx = std::max(mx, (long long)f.parts[i].m * f.parts[i].rowsT);
+    launch_transpose_factors(f.d_parts, f.p, mx, f.d_fac, f.d_tfac, f.d_dinv, f.stream);
+    mark_ready(f, f.stream);
+    f.tfac_ready.store(true);
 }
 
 // order work on s after the factorization (a no-op on its own stream)
@@ -2010,29 +2113,7 @@ void finish_factor(spk_fact& f, cudaStream_t s) {
     std::vector<int> flags(std::max(f.npairs, 1), 0);
     if (f.npairs > 0)
         ck(cudaMemcpyAsync(flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost, s), "flags");
-    unsigned skfb = 0;
-    if (f.sk) ck(cudaMemcpyAsync(&skfb, f.d_skmisc, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "download");
     ck(cudaStreamSynchronize(s), "factorize");
-    if (skfb) {
-        // a pair needs the pivoted 2k coupling: the general hierarchy program
-        // from the (untouched) level-0 tips
-        tr.mark("small-k fallback");
-        double* auxf = dalloc<double>((size_t)f.auxf_rows * f.k, s);
-        Bufs B = make_bufs(&f);
-        B.p[B_POOL] = f.d_pool;
-        B.p[B_AUX] = auxf;
-        B.ld[B_AUX] = f.auxf_rows;
-        Exec ex{f, s, B, f.k};
-        ex.n = f.n;
-        ex.run(f.prog_levels, f.d_blob);
-        dfree(auxf, s);
-        ck(cudaMemcpyAsync(&status, f.d_status, sizeof(int), cudaMemcpyDeviceToHost, s), "download");
-        ck(cudaMemcpyAsync(fell.data(), f.d_fell, sizeof(int) * nparts, cudaMemcpyDeviceToHost, s), "download");
-        if (f.npairs > 0)
-            ck(cudaMemcpyAsync(flags.data(), f.d_flags, sizeof(int) * f.npairs, cudaMemcpyDeviceToHost, s), "flags");
-        ck(cudaStreamSynchronize(s), "factorize");
-    }
-    f.sk_schur_all = f.sk && !skfb;
     tr.mark("stream synced");
     ck(cudaGetLastError(), "factorize kernels");
     if (status == 2) fail(SPK_ESINGULAR, "lu_factor: exactly singular column in pivoting mode");
@@ -2323,10 +2404,11 @@ spk_status spk_gpu_plan(int64_t n, int32_t kl, int32_t ku, int32_t nrhs, int32_t
             // narrow bands: up to 8 partitions per SM, but no shorter than
             // ~2k rows (more reduced-system levels cost more than the shorter
             // column chain saves: C1 n=1e5 p=1184 3.6 ms, p=148 2.0 ms)
-            // narrow non-pivoting bands take the small-k engine (spk_smallk.cu):
-            // partitions of ~192 rows (register-window LU per warp), staged
-            // in shared memory
-            else if (!pivoting && kl <= 16 && ku <= 16) pp = (int)std::max<long long>(2, (n + 191) / 192);
+            // narrow non-pivoting bands take the small-k engine (spk_smallk*.cu):
+            // partitions of ~96 rows (a half-warp per partition, the block
+            // staged in shared memory; the solve keeps a warp's partition
+            // factor resident between its D-stage and retrieval)
+            else if (!pivoting && kl <= 16 && ku <= 16) pp = (int)std::max<long long>(2, (n + 95) / 96);
             else pp = (int)std::min<long long>(8 * sms, std::max<long long>(sms, n / 2048));
         }
         pp = (int)std::max<long long>(1, std::min<long long>(pp, n / std::max<long long>(min_part, 1)));
@@ -2494,7 +2576,7 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         // until the factorization is finished (ensure_finished) solves run
         // device-guarded programs; built and uploaded here, ahead of the work
         f->flags.clear();
-        build_solve_programs(*f, s);
+        if (!f->sk) build_solve_programs(*f, s);  // small-k: built at the finish, when a general program needs them
         tr.mark("setup (symbolic)");
         // band on device; a slab's band starts k halo columns early when its
         // left edge is open and carries k more when its right edge is
@@ -2512,7 +2594,10 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         }
         dband += ld * hl;  // column 0 of the slab
         const int p = f->p;
-        if (f->sk && run_sk_factor(*f, dband, s)) {
+        if (f->sk) {
+            if (!run_sk_factor(*f, dband, s)) fail(SPK_ECUDA, "factorize: small-k engine launch");
+            f->tfac_ready.store(false);
+            f->sk_schur_all = true;
             mark_ready(*f, s);
             tr.mark("enqueued (small-k engine)");
             if (tmp) dfree(tmp, s);
@@ -2520,7 +2605,6 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
             *out = f.release();
             return;
         }
-        f->sk = false;
         {
             ProfScope ps(PC_CORNERS, s, 0.0, 16.0 * p * f->k * f->k);
             launch_corners(dband, n, kl, ku, f->d_bounds, p, f->k, f->open_l, f->open_r, f->d_pool + f->off_bhat,
@@ -2590,6 +2674,8 @@ spk_status spk_fact_unit_tips(const spk_fact* f, double* d_tips, void* stream) {
         }
     });
 }
+
+void spk_debug_set_trace(void* d_buf) { spk::g_sk_trace = static_cast<unsigned long long*>(d_buf); }
 
 int32_t spk_fact_engine(const spk_fact* f) {
     if (!f) return -1;
@@ -2665,6 +2751,10 @@ int64_t spk_fact_dump(const spk_fact* f, int32_t which, double* out) {
     const double* src = which == 0 ? f->d_fac : which == 1 ? f->d_tfac : f->d_dinv;
     try {
         ensure_finished(f);
+        if (which == 1) {
+            ensure_tfac(f);
+            cudaStreamSynchronize(f->stream);
+        }
     } catch (...) {
     }
     if (out) cudaMemcpy(out, src, sizeof(double) * sz, cudaMemcpyDeviceToHost);
@@ -2742,7 +2832,25 @@ spk_status spk_fact_coupling(const spk_fact* f, int32_t l, int32_t a, double* lu
             ck(cudaMalloc(&d_s, sizeof(double) * fsz), "coupling");
             ck(cudaMalloc(&d_i, sizeof(int) * (S.m + 1)), "coupling");
             ck(cudaMalloc(&d_meta, sizeof(PartDev) + sizeof(CouplingJob)), "coupling");
-            ck(cudaMemcpy(d_s, f->d_fac + S.fofs, sizeof(double) * fsz, cudaMemcpyDeviceToDevice), "coupling");
+            if (f->sk_schur_all) {
+                // the small-k engine keeps only S^-1: S = I - Wt Vb from the level's spikes
+                const int hL = lv.uh[2 * a], hR = lv.uh[2 * a + 1];
+                std::vector<double> vl((size_t)hL * k), wr((size_t)hR * k), band(fsz, 0.0);
+                ck(cudaMemcpy(vl.data(), f->d_pool + lv.voff[2 * a], sizeof(double) * vl.size(),
+                              cudaMemcpyDeviceToHost), "coupling");
+                ck(cudaMemcpy(wr.data(), f->d_pool + lv.woff[2 * a + 1], sizeof(double) * wr.size(),
+                              cudaMemcpyDeviceToHost), "coupling");
+                for (int j = 0; j < k; ++j)
+                    for (int i = 0; i < k; ++i) {
+                        double v = i == j ? 1.0 : 0.0;
+                        for (int t = 0; t < k; ++t) v -= wr[(size_t)t * hR + i] * vl[(size_t)j * hL + hL - k + t];
+                        const int q = S.d + i - j;
+                        if (q >= 0 && q < S.rows) band[(size_t)j * S.rows + q] = v;
+                    }
+                ck(cudaMemcpy(d_s, band.data(), sizeof(double) * fsz, cudaMemcpyHostToDevice), "coupling");
+            } else {
+                ck(cudaMemcpy(d_s, f->d_fac + S.fofs, sizeof(double) * fsz, cudaMemcpyDeviceToDevice), "coupling");
+            }
             S.fofs = 0;
             S.r0 = 0;
             CouplingJob J{};
@@ -2808,14 +2916,13 @@ struct spk_xsolve {
     cudaStream_t s = nullptr;
     double *S = nullptr, *T = nullptr, *AUX = nullptr, *tF = nullptr, *tX = nullptr;
     double *XCH = nullptr, *XIN = nullptr;
-    // small-k engine (k_sk_solve): second tip buffer, grid-barrier words
+    // small-k engine (k_sk_solve): grid-barrier words
     bool sk = false;
-    double* T2 = nullptr;
     unsigned* bar = nullptr;
     Bufs B;
 
     ~spk_xsolve() {
-        for (double* q : {S, T, AUX, tF, tX, XCH, XIN, T2})
+        for (double* q : {S, T, AUX, tF, tX, XCH, XIN})
             if (q) dfree(q, s);
         if (bar) dfree(bar, s);
     }
@@ -2825,12 +2932,13 @@ struct spk_xsolve {
     void run_phase() {
         if (sk) {
             const char* blob = f->d_blob;
-            SkSolveArgs A{f->d_parts, f->p, f->k, nrhs, f->d_fac, f->d_pool, f->off_bhat, f->off_chat,
+            SkSolveArgs A{f->d_parts, f->p, f->k, nrhs, f->d_fac, f->fac_size, f->d_pool, f->off_bhat, f->off_chat,
                           reinterpret_cast<const SkUnit*>(blob + f->sk_units),
                           reinterpret_cast<const SkPair*>(blob + f->sk_pairs),
                           reinterpret_cast<const SkItem*>(blob + f->sk_items),
                           reinterpret_cast<const SkLevel*>(blob + f->sk_levels), f->sk_nlevels, B.p[B_F], B.ld[B_F],
-                          B.p[B_X], B.ld[B_X], T, T2, bar, f->sk_mmax};
+                          B.p[B_X], B.ld[B_X], T, bar, f->sk_mmax, f->sk_rmax,
+                          g_sk_trace ? g_sk_trace + 4096 * 16 : nullptr};
             ProfScope ps(ST_SWEEP, s, 8.0 * f->n * f->k * nrhs, 16.0 * f->n * (f->kl + f->ku + 1));
             launch_sk_solve(A, s);
             ++phase;
@@ -2854,6 +2962,8 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
                                        int32_t nrhs, double* X, int64_t ldx, int32_t mem, cudaStream_t s) {
     spk_fact& f = const_cast<spk_fact&>(*fc);
     const long long n = f.n;
+    const bool sk_kernel = sk_kernel_solve(f, transpose, nrhs);
+    if (!sk_kernel) ensure_tfac(fc);
     wait_ready(f, s);
     auto x = std::make_unique<spk_xsolve>();
     x->f = &f;
@@ -2899,7 +3009,7 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
         const long long H = 2LL * f.p * f.k, halo = f.open() ? f.k : 0;
         if (transpose) x->S = dalloc<double>((size_t)n * nrhs, s);  // tau (the forward solve needs none)
         x->T = dalloc<double>((size_t)(H + 2 * halo) * nrhs, s);
-        x->AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
+        if (!sk_kernel) x->AUX = dalloc<double>((size_t)f.aux_rows * nrhs, s);
         if (f.open()) {
             // dead tips of closed edges are read (times zero) by transposed
             // pair solves: keep them finite
@@ -2922,10 +3032,9 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     B.ld[B_POOL] = 1;
     // forward solves with few right-hand sides of a small-k factorization
     // whose pairs all took the Schur path: one cooperative kernel
-    if (f.sk_schur_all && !transpose && nrhs >= 1 && nrhs <= kSkMaxRhs && !f.open() && f.coupled()) {
+    if (sk_kernel) {
         x->sk = true;
         const long long H = 2LL * f.p * f.k;
-        x->T2 = dalloc<double>((size_t)H * nrhs, s);
         x->bar = static_cast<unsigned*>(arena().alloc(2 * sizeof(unsigned), s));
         ck(cudaMemsetAsync(x->bar, 0, 2 * sizeof(unsigned), s), "memset");
         B.ld[B_T] = H;
@@ -2961,7 +3070,10 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
     // are used, and fin_mu keeps a concurrent finish from swapping them while
     // this call enqueues
     spk_fact& fm = const_cast<spk_fact&>(*fc);
-    if (fm.sk) ensure_finished(fc);  // a small-k fallback replaces the hierarchy at the finish
+    if (fm.sk) {
+        ensure_finished(fc);  // a small-k fallback replaces the hierarchy at the finish
+        ensure_tfac(fc);
+    }
     std::lock_guard<std::mutex> lk(fm.fin_mu);
     if (!fm.pending.load() && fm.fin_status != SPK_OK) fail(fm.fin_status, fm.fin_msg);
     CopyStreams& cs = copy_streams();
@@ -3043,7 +3155,9 @@ spk_status spk_solve(const spk_fact* fc, int32_t transpose, const double* F, int
             solve_host_pipelined(fc, transpose, F, ldf, nrhs, X, ldx, s);
             return;
         }
-        ensure_finished(fc);
+        // the small-k engine's own solve kernel reads only device state: no
+        // host finish (and no host wait) before it
+        if (!sk_kernel_solve(f, transpose, nrhs)) ensure_finished(fc);
         auto x = open_solve(fc, transpose, F, ldf, nrhs, X, ldx, mem, s);
         x->run_phase();
         note_use(f, s);

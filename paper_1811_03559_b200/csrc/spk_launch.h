@@ -151,11 +151,14 @@ struct SkUnit {
     int uh, uoff;          // height (rows of the reduced system), first reduced row
 };
 struct SkPair {
-    long long sinv;  // pool offset of S^-1 (k x k, ld k)
-    int gidx;        // flag index (1 = Schur path)
-    int left;        // global index of the left unit (right = left + 1)
-    int next;        // global index of the merged unit on the next level
-    int pad;
+    long long sinv;            // pool offset of S^-1 (k x k, ld k)
+    long long vl, wl, vr, wr;  // pool offsets of the children's spikes (left / right unit), -1: none
+    long long nv, nw;          // the merged unit's spikes, -1: none
+    int hL, hR;                // children heights
+    int zb;                    // first reduced row of the merged unit
+    int gidx;                  // flag index (1 = Schur path)
+    int left;                  // global index of the left unit (right = left + 1)
+    int next;                  // global index of the merged unit on the next level
 };
 struct SkItem {
     int pair;  // >= 0: pair (global index); < 0: carried unit -(pair + 1) (global unit index)
@@ -164,16 +167,17 @@ struct SkItem {
     int pad;
 };
 struct SkLevel {
-    int item0, nitems;
+    int item0, nitems;     // row items (pairs' merged units, the carried unit)
+    int pair0, npairs;     // pairs of the level (global indices)
+    int carry, carry_next; // carried odd unit (global index on this / the next level), -1: none
 };
-constexpr int kSkChunk = 256;  // merged-unit rows per work item
+constexpr int kSkChunk = 512;  // merged-unit rows per work item
 struct SkPartsArgs {
     const double* band;
     long long n;
     int akl, aku, k, p;
     const PartDev* parts;
-    double* fac;
-    double* tfac;
+    double* fac;   // packed LU (the row-major copy follows lazily, ensure_tfac)
     double* dinv;
     int* boost;
     double* pool;
@@ -190,13 +194,15 @@ struct SkLevelsArgs {
     const SkLevel* levels;
     int nlevels, k;
     int* flags;
-    int* fallback;   // set when a pair needs the generic (pivoted 2k) coupling
-    unsigned* bar;   // grid barrier: {count, generation}, zeroed
+    double boost_eps;  // an exactly singular Schur complement: its zero pivots boosted
+    unsigned* bar;     // grid barrier: {count, generation}, zeroed
+    unsigned long long* trace;  // debug: globaltimer per (phase, CTA, mark), or null
 };
 struct SkSolveArgs {
     const PartDev* parts;
     int p, k, nrhs;
     const double* fac;
+    long long fac_size;  // doubles in the factor pool (bulk copies stay inside it)
     const double* pool;
     long long off_bhat, off_chat;
     const SkUnit* units;
@@ -208,16 +214,20 @@ struct SkSolveArgs {
     long long ldf;
     double* X;
     long long ldx;
-    double* T0;
-    double* T1;  // reduced right-hand sides, ping-pong per level (2pk x nrhs, ld 2pk)
+    double* T;  // reduced right-hand sides (2pk x nrhs, ld 2pk), updated in place
     unsigned* bar;
-    int mmax;
+    int mmax, rmax;  // longest partition, largest packed column height
+    unsigned long long* trace;  // debug: globaltimer per (phase, CTA, mark), or null
 };
+// debug hook (spk_debug_set_trace): device buffer the small-k kernels stamp
+extern unsigned long long* g_sk_trace;
 // false when the shape is not covered (kl or ku > 31)
 bool launch_sk_parts(const SkPartsArgs& A, cudaStream_t s);
 void launch_sk_levels(const SkLevelsArgs& A, cudaStream_t s);
-// forward solve, nrhs <= kSkMaxRhs
+// forward solve, nrhs <= kSkMaxRhs; its dynamic shared memory (the caller
+// checks it fits)
 constexpr int kSkMaxRhs = 8;
+size_t sk_solve_smem(int mmax, int rmax, int nrhs);
 void launch_sk_solve(const SkSolveArgs& A, cudaStream_t s);
 
 void launch_generate_band(unsigned long long seed, long long n, int kl, int ku, double dd, long long col0,

@@ -3,7 +3,7 @@
 // one per forward solve instead of the general engine's stage programs
 // (~250 dependent launches at BASELINE C1).
 //
-//   k_sk_parts   one warp per partition: the partition's band columns (plus k
+//   k_sk_parts   (spk_smallk_parts.cu) one warp per partition: the partition's band columns (plus k
 //                halo columns each side for the corners) land in shared
 //                memory with ONE bulk async copy (cp.async.bulk, TMA 1-D,
 //                mbarrier completion); register-window LU with diagonal
@@ -43,494 +43,362 @@
 
 namespace spk {
 
+// ===========================================================================
+// reduced hierarchy (reduce_factorize, factorize.cpp:46-120), one cooperative
+// kernel, one grid barrier per level.
+//
+// Pair a of level l: left unit (hL rows; V = vl, W = wl), right unit (hR rows;
+// V = vr, W = wr).  Coupling [[I, Vb], [Wt, I]] with Vb = vl[hL-k : hL],
+// Wt = wr[0 : k]; while max|W| <= 1 partial pivoting on it takes the identity
+// pivots (kernels.cpp:94), so it factors through the Schur complement
+// S = I - Wt Vb.  The merged unit's spikes are the pair solves of [0; vr] and
+// [wl; 0] (factorize.cpp:19-32):
+//   z2 = S^-1 (y2 - Wt y1), z1 = y1 - Vb z2,
+//   rows [0, hL-k) -= vl[0:hL-k] z2 (left rows), rows [hL+k, H) -= wr[k:hR] z1.
+// Phase ph runs two tasks:
+//   A (level ph, one warp per pair): the pair's k x k algebra only -- S,
+//     S^-1 (Gauss-Jordan in registers, a row of [S | I] per lane pair; no row
+//     search when S is column diagonally dominant, where partial pivoting
+//     takes the diagonal anyway), z1, z2, and the merged unit's TIP rows (top
+//     k, bottom k) straight from the children's tips, so the next level's
+//     task A needs nothing else;
+//   B (level ph-1, a CTA per row item): the merged units' other rows.
 namespace {
+constexpr int kLvWarps = 4;
+constexpr int kLvThreads = 32 * kLvWarps;
+constexpr int kLd = 18;          // 16 x 16 blocks, row-major, ld 18 (16-byte rows, spread banks)
+constexpr int kBlk = 16 * kLd;
+enum { B_WT, B_VB, B_Y2, B_Y1, B_VLT, B_WLT, B_VRB, B_WRB, B_S, B_UW, B_SI, B_Z2V, B_Z2W, B_Z1V, B_Z1W, NBLK };
+constexpr int kWarpSmem = NBLK * kBlk;  // doubles per warp
 
-constexpr int kSkWarpsMax = 4;
-
-// shared memory per warp (doubles) of k_sk_parts
-__host__ __device__ inline long long sk_parts_warp_smem(int mmax, int k, int ld) {
-    const long long slab = (long long)(mmax + 2 * k) * ld + 4;  // + alignment slack
-    const long long xs = (long long)mmax * 32;                   // forward spike rows, <= 32 columns
-    return (slab + xs + 2 * 32 + 8 + 1) / 2 * 2;                 // + U-row buffers, mbarrier
+// lane (r = lane & 15, h = lane >> 4) owns row r, columns 8h .. 8h+7 of a block
+// acc = A[r, :] B[:, 8h .. 8h+7]
+__device__ __forceinline__ void wgemm(const double* Am, const double* Bm, double acc[8], int lane) {
+    const int r = lane & 15, h = lane >> 4;
+    double a[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double2 v = *reinterpret_cast<const double2*>(Am + r * kLd + 2 * q);
+        a[2 * q] = v.x;
+        a[2 * q + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        const double* b = Bm + t * kLd + 8 * h;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 v = *reinterpret_cast<const double2*>(b + 2 * q);
+            acc[2 * q] = fma(a[t], v.x, acc[2 * q]);
+            acc[2 * q + 1] = fma(a[t], v.y, acc[2 * q + 1]);
+        }
+    }
+}
+// C = (Cin or 0) - A B   (C may alias Cin, not A or B)
+__device__ __forceinline__ void wgemm_sub(const double* Am, const double* Bm, const double* Cin, double* C, int lane) {
+    double acc[8];
+    wgemm(Am, Bm, acc, lane);
+    const int e = (lane & 15) * kLd + 8 * (lane >> 4);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) C[e + c] = (Cin ? Cin[e + c] : 0.0) - acc[c];
 }
 
-}  // namespace
-
-// ===========================================================================
-// partitions: LU + factor layouts + corners + level-0 spike tips
-//
-// Windows of KS = 17 register slots (kl, ku <= 16): the LU holds columns
-// j .. j+16 of each window row (column c in slot c mod KS), the spike sweeps
-// rows j .. j+16 of each column (row r in slot (r - start) mod KS); the step
-// loops are unrolled KS times so every slot index is a constant.  LU-space
-// element (li, lj) of the staged band is base[off0 + lj * cj + li * ci]
-// (the reversed last partition runs the other way), so addresses step by
-// constants.
-constexpr int kSkSlots = 17;
-
-template <int CPL>
-__global__ void __launch_bounds__(32 * kSkWarpsMax) k_sk_parts(SkPartsArgs A) {
-    constexpr int KS = kSkSlots;
-    extern __shared__ __align__(16) double sk_smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    const int i = blockIdx.x * nw + warp;
-    if (i >= A.p) return;
-    const int ld = A.akl + A.aku + 1, k = A.k;
-    const long long wsm = sk_parts_warp_smem(A.mmax, k, ld);
-    double* const wbase = sk_smem + (long long)warp * wsm;
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wbase + wsm - 2);
-    double* const ubuf = wbase + wsm - 2 - 64;  // [2][32]
-    double* const Xs = ubuf - (long long)A.mmax * 32;
-    const PartDev P = A.parts[i];
-    const int m = P.m, rev = P.rev;
-    const long long r0 = P.r0;
-    const long long c0 = r0 - k > 0 ? r0 - k : 0;
-    const long long c1 = r0 + m + k < A.n ? r0 + m + k : A.n;
-
-    // ---- stage the band columns [c0, c1) (contiguous) with one bulk copy
-    const long long e0 = c0 * ld, e1 = c1 * ld, etot = A.n * ld;
-    const long long a0 = e0 & ~1LL;
-    long long a1 = (e1 + 1) & ~1LL;
-    if (a1 > etot) a1 -= 2;  // never read past the band
-    double* const slab_raw = wbase;
-    double* const slab = slab_raw + (e0 - a0);
-    if (lane == 0) {
-        mbar_init1(mbar);
-        const unsigned bytes = (unsigned)((a1 - a0) * 8);
-        mbar_expect_tx(mbar, bytes);
-        bulk_g2s(slab_raw, A.band + a0, bytes, mbar);
-    }
-    __syncwarp();
-    mbar_wait0(mbar);
-    for (long long e = a1 + lane; e < e1; e += 32) slab_raw[e - a0] = A.band[e];  // tail element
-    __syncwarp();
-
-    double* const base = slab + (int)(r0 - c0) * ld + A.aku;
-    const int kl = P.kl, ku = P.ku;  // LU space (swapped for rev)
-    const int ci = rev ? -1 : 1, cj = rev ? -(ld - 1) : ld - 1, off0 = rev ? (m - 1) * ld : 0;
-    auto sid = [&](int li, int lj) -> int { return off0 + lj * cj + li * ci; };
-    auto inband = [&](int li, int lj) -> bool {
-        return li >= 0 && lj >= 0 && li < m && lj < m && li - lj <= kl && lj - li <= ku;
-    };
-
-    // boost threshold over the partition block (kernels.cpp:80-85): column pj,
-    // packed rows q on the lanes
-    double amax = 0.0;
-    for (int pj = 0; pj < m; ++pj)
-        for (int q = lane; q < ld; q += 32) {
-            const int pi = pj + q - A.aku;
-            if (pi >= 0 && pi < m) amax = fmax(amax, fabs(base[pj * ld + q - A.aku]));
-        }
-    amax = warp_max(amax);
-    const double scale = amax == 0.0 ? 1.0 : amax;
-    const double zero_thresh = DBL_EPSILON * scale, boost_mag = A.boost_eps * scale;
-
-    // ---- register-window LU: lane (row mod 32) holds its row's columns
-    //      j .. j+KS-1 (column c in slot c mod KS)
-    double W[KS];
-#pragma unroll
-    for (int c = 0; c < KS; ++c) W[c] = (lane <= kl && inband(lane, c)) ? base[sid(lane, c)] : 0.0;
-    int boosts = 0;
-    for (int j0 = 0; j0 < m; j0 += KS) {
-#pragma unroll
-        for (int t = 0; t < KS; ++t) {
-            const int j = j0 + t;
-            if (j >= m) break;
-            const int o = (lane - j) & 31;
-            double* ub = ubuf + (j & 1) * 32;
-            const int sjj = sid(j, j);
-            if (o == 0) {
-                double u = W[t];
-                if (fabs(u) < zero_thresh) {
-                    u = u == 0.0 ? boost_mag : copysign(boost_mag, u);
-                    ++boosts;
-                }
-                W[t] = u;
-                const double inv = 1.0 / u;
-                ub[0] = inv;
-#pragma unroll
-                for (int c = 1; c < KS; ++c) ub[c] = W[(t + c) % KS];
-                const int ce = min(ku, m - 1 - j);
-                base[sjj] = u;
-#pragma unroll
-                for (int c = 1; c < KS; ++c)
-                    if (c <= ce) base[sjj + c * cj] = W[(t + c) % KS];
-                A.dinv[r0 + j] = inv;
-            }
-            __syncwarp();
-            if (o >= 1 && o <= kl) {
-                const double l = W[t] * ub[0];
-                if (j + o < m) base[sjj + o * ci] = l;
-#pragma unroll
-                for (int c = 1; c < KS; ++c) W[(t + c) % KS] = fma(-l, ub[c], W[(t + c) % KS]);
-                // entering column j + KS: in band iff KS - o <= ku
-                const int cn = j + KS;
-                W[t] = (KS - o <= ku && cn < m && j + o < m) ? base[sjj + o * ci + KS * cj] : 0.0;
-            } else if (o == ((kl + 1) & 31)) {  // entering row j + kl + 1: columns j+1 .. j+KS
-                const int r = j + kl + 1;
-                const int sb = sid(r, j + 1);
-#pragma unroll
-                for (int c = 0; c < KS; ++c)
-                    W[(t + 1 + c) % KS] = (c <= kl + ku && r < m && j + 1 + c < m) ? base[sb + c * cj] : 0.0;
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) boosts += __shfl_xor_sync(0xffffffffu, boosts, o);
-    if (lane == 0) A.boost[i] = boosts;
-    __syncwarp();
-
-    // ---- factor layouts: packed LU at fofs (column lj, packed rows on the
-    //      lanes), row-major copy at tofs (row li)
+__device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm, int lane) {
+    const unsigned full = 0xffffffffu;
+    const int k = A.k;
+    const int hL = pr.hL, hR = pr.hR, H = hL + hR;
+    const bool hv = pr.nv >= 0, hw = pr.nw >= 0;
+    auto B = [&](int i) { return sm + i * kBlk; };
+    // the eight k x k tips straight into shared memory (cp.async), zero padding
     {
-        double* F = A.fac + P.fofs;
-        const int rows = P.rows, d = P.d;
-        for (int lj = 0; lj < m; ++lj)
-            for (int q = lane; q < rows; q += 32) {
-                const int li = lj + q - d;
-                F[(long long)lj * rows + q] = inband(li, lj) ? base[sid(li, lj)] : 0.0;
+        const double* vl = A.pool + pr.vl;
+        const double* wr = A.pool + pr.wr;
+        const double* wl = A.pool + (hw ? pr.wl : 0);
+        const double* vr = A.pool + (hv ? pr.vr : 0);
+        for (int e = lane; e < 256; e += 32) {
+            const int r = e >> 4, c = e & 15, o = r * kLd + c;
+            if (r < k && c < k) {
+                sk_cp8(B(B_WT) + o, wr + (long long)c * hR + r);
+                sk_cp8(B(B_VB) + o, vl + (long long)c * hL + hL - k + r);
+                sk_cp8(B(B_VLT) + o, vl + (long long)c * hL + r);
+                sk_cp8(B(B_WRB) + o, wr + (long long)c * hR + hR - k + r);
+                if (hv) {
+                    sk_cp8(B(B_Y2) + o, vr + (long long)c * hR + r);
+                    sk_cp8(B(B_VRB) + o, vr + (long long)c * hR + hR - k + r);
+                } else {
+                    B(B_Y2)[o] = 0.0;
+                    B(B_VRB)[o] = 0.0;
+                }
+                if (hw) {
+                    sk_cp8(B(B_Y1) + o, wl + (long long)c * hL + hL - k + r);
+                    sk_cp8(B(B_WLT) + o, wl + (long long)c * hL + r);
+                } else {
+                    B(B_Y1)[o] = 0.0;
+                    B(B_WLT)[o] = 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int b = B_WT; b <= B_WRB; ++b) B(b)[o] = 0.0;
             }
-        double* TF = A.tfac + P.tofs;
-        const int rt = P.rowsT;
-        for (int li = 0; li < m; ++li)
-            for (int q = lane; q < rt; q += 32) {
-                const int lj = li - kl + q;
-                TF[(long long)li * rt + q] = inband(li, lj) ? base[sid(li, lj)] : 0.0;
-            }
+        }
+        sk_cp_wait_all();
+        __syncwarp();
     }
-    if (A.p < 2 || k == 0) return;
-
-    // ---- corners (physical; k_corners, spike2x2.cpp:17-26)
-    const bool first = i == 0, last = i == A.p - 1;
-    const long long kk = (long long)k * k;
-    auto bhat = [&](int rr, int c) -> double {  // A(r0+m-k+rr, r0+m+c)
-        const int q = A.aku - k + rr - c;
-        const long long pc = r0 + m + c;
-        return (pc < c1 && q >= 0 && q < ld) ? slab[(pc - c0) * ld + q] : 0.0;
-    };
-    auto chat = [&](int rr, int c) -> double {  // A(r0+rr, r0-k+c)
-        const int q = A.aku + rr + k - c;
-        const long long pc = r0 - k + c;
-        return (pc >= c0 && q >= 0 && q < ld) ? slab[(pc - c0) * ld + q] : 0.0;
-    };
+    // S = I - Wt Vb (padding: identity), UW = -Wt Y1
+    {
+        double acc[8];
+        wgemm(B(B_WT), B(B_VB), acc, lane);
+        const int r = lane & 15, c0 = 8 * (lane >> 4);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) B(B_S)[r * kLd + c0 + c] = (r == c0 + c ? 1.0 : 0.0) - acc[c];
+        wgemm_sub(B(B_WT), B(B_Y1), nullptr, B(B_UW), lane);
+    }
+    __syncwarp();
+    // column diagonal dominance of S (then partial pivoting takes the diagonal)
+    bool dom = true;
+    if (lane < 16) {
+        double o = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o += i == lane ? 0.0 : fabs(B(B_S)[i * kLd + lane]);
+        dom = fabs(B(B_S)[lane * kLd + lane]) > o;
+    }
+    dom = __all_sync(full, dom);
+    // Gauss-Jordan on [S | I] in registers: lane (r, h) holds row r, columns
+    // 16h .. 16h+15 of the augmented matrix
+    const int r = lane & 15, h = lane >> 4;
+    double a[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) a[c] = h == 0 ? B(B_S)[r * kLd + c] : (r == c ? 1.0 : 0.0);
+    unsigned used = 0u;
+    int jr = r;  // S^-1 row held by this lane's I-part: the step whose pivot row is r
+    double boost = 0.0;  // an exactly singular S: zero pivots boosted (kernels.cpp:104-109 rule)
+    if (!dom) {
+        double mx = 0.0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) mx = fmax(mx, h == 0 ? fabs(a[c]) : 0.0);
+        boost = A.boost_eps * fmax(warp_max(mx), 1.0);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const double colv = __shfl_sync(full, a[j], r);  // aug[r][j] (S part, lane (r, 0))
+        int p = j;
+        if (!dom) {
+            double v = (lane < 16 && !((used >> lane) & 1u)) ? fabs(colv) : -1.0;
+            int idx = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(full, v, o);
+                const int oi = __shfl_xor_sync(full, idx, o);
+                if (ov > v || (ov == v && oi < idx)) {
+                    v = ov;
+                    idx = oi;
+                }
+            }
+            // all candidates zero: the first unused row, its pivot boosted
+            p = v > 0.0 ? idx : __ffs(~used & 0xffffu) - 1;
+        }
+        used |= 1u << p;
+        if (r == p) jr = j;
+        double piv = __shfl_sync(full, a[j], p);  // aug[p][j]
+        if (piv == 0.0) piv = boost;
+        const double inv = 1.0 / piv;
+        const double g = colv * inv;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const double pv = __shfl_sync(full, a[c], p + 16 * h);
+            a[c] = r == p ? pv * inv : fma(-g, pv, a[c]);
+        }
+    }
+    if (h == 1) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) B(B_SI)[jr * kLd + c] = a[c];
+    }
+    __syncwarp();
     for (int e = lane; e < k * k; e += 32) {
         const int c = e / k, rr = e - c * k;
-        if (!last) A.pool[A.off_bhat + i * kk + e] = bhat(rr, c);
-        if (!first) A.pool[A.off_chat + i * kk + e] = chat(rr, c);
+        A.pool[pr.sinv + e] = B(B_SI)[rr * kLd + c];
     }
-
-    // ---- spike tips.  Columns: inner partitions V (0..k-1) and W (k..2k-1);
-    //      first: V; last (reversed): its W through the reversed LU in the V slot
-    const int nc = (!first && !last) ? 2 * k : k;
-    const int js = (!first && !last) ? 0 : m - k;  // forward start (trunc_start)
-    const SkUnit U0 = A.units[i];
-    auto rhs = [&](int r, int col) -> double {
-        if (r >= m || col >= nc) return 0.0;
-        if (col < k) {
-            if (r < m - k) return 0.0;
-            return last ? chat(m - 1 - r, col) : bhat(r - (m - k), col);
-        }
-        return r < k ? chat(r, col - k) : 0.0;
-    };
-    // forward L (unit lower), push form, rows js .. m-1; row j in slot (j-js) mod KS
-    double X[CPL][KS];
+    if (lane == 0) A.flags[pr.gidx] = 1;
+    // z2v = S^-1 y2, z2w = S^-1 (-Wt y1)
+    wgemm_sub(B(B_SI), B(B_Y2), nullptr, B(B_Z2V), lane);  // = -S^-1 y2
+    wgemm_sub(B(B_SI), B(B_UW), nullptr, B(B_Z2W), lane);  // = S^-1 Wt y1
+    __syncwarp();
+    // (signs: Z2V, Z2W hold -z2v, -z2w)  z1v = -Vb z2v, z1w = y1 - Vb z2w;
+    // top tips vt' = -vl_top z2v, wt' = wl_top - vl_top z2w
+    {
+        double p1[8], p2[8], p3[8], p4[8];
+        wgemm(B(B_VB), B(B_Z2V), p1, lane);
+        wgemm(B(B_VB), B(B_Z2W), p2, lane);
+        wgemm(B(B_VLT), B(B_Z2V), p3, lane);
+        wgemm(B(B_VLT), B(B_Z2W), p4, lane);
+        const int e = (lane & 15) * kLd + 8 * (lane >> 4);
+        __syncwarp();
 #pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int s = 0; s < KS; ++s) X[q][s] = rhs(js + s, lane + 32 * q);
-    for (int j0 = js; j0 < m; j0 += KS) {
-#pragma unroll
-        for (int t = 0; t < KS; ++t) {
-            const int j = j0 + t;
-            if (j >= m) break;
-            // L column j (broadcast reads, issued together; rows past the band
-            // or the partition contribute zero)
-            const int sjj = sid(j, j);
-            double lv[KS];
-#pragma unroll
-            for (int o = 1; o < KS; ++o) lv[o] = (o <= kl && j + o < m) ? base[sjj + o * ci] : 0.0;
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) Xs[(long long)j * 32 * CPL + lane + 32 * q] = X[q][t];
-#pragma unroll
-            for (int o = 1; o < KS; ++o)
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) X[q][(t + o) % KS] = fma(-lv[o], X[q][t], X[q][(t + o) % KS]);
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) X[q][t] = rhs(j + KS, lane + 32 * q);
+        for (int c = 0; c < 8; ++c) {
+            B(B_Z1V)[e + c] = p1[c];
+            B(B_Z1W)[e + c] = B(B_Y1)[e + c] + p2[c];
+            B(B_VLT)[e + c] = p3[c];
+            B(B_WLT)[e + c] += p4[c];
+            B(B_Z2V)[e + c] = -B(B_Z2V)[e + c];
+            B(B_Z2W)[e + c] = -B(B_Z2W)[e + c];
         }
     }
     __syncwarp();
-    // backward U, rows m-1 down to je (inner: 0; first / last: the bottom tip)
-    const int je = (!first && !last) ? 0 : m - k;
-    auto emit = [&](int j, int col, double v) {
-        if (col >= nc) return;
-        if (last) {  // reversed W: LU row j in [m-k, m) is physical row m-1-j of wt
-            A.pool[U0.woff + (long long)col * 2 * k + (m - 1 - j)] = v;
-            return;
+    // bottom tips: vb' = vr_bot - wr_bot z1v, wb' = -wr_bot z1w
+    {
+        double p1[8], p2[8];
+        wgemm(B(B_WRB), B(B_Z1V), p1, lane);
+        wgemm(B(B_WRB), B(B_Z1W), p2, lane);
+        const int e = (lane & 15) * kLd + 8 * (lane >> 4);
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            B(B_VRB)[e + c] -= p1[c];
+            B(B_WRB)[e + c] = -p2[c];
         }
-        if (j >= k && j < m - k) return;
-        const int rr = j >= m - k ? k + j - (m - k) : j;  // bottom tip rows k.., top rows 0..
-        if (col < k) A.pool[U0.voff + (long long)col * 2 * k + rr] = v;
-        else A.pool[U0.woff + (long long)(col - k) * 2 * k + rr] = v;
+    }
+    __syncwarp();
+    auto out = [&](int blk, long long off, int r0) {
+        double* dst = A.pool + off;
+        for (int e = lane; e < k * k; e += 32) {
+            const int c = e / k, rr = e - c * k;
+            dst[(long long)c * H + r0 + rr] = B(blk)[rr * kLd + c];
+        }
     };
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int s = 0; s < KS; ++s) {
-            const int r = m - 1 - s;
-            X[q][s] = r >= js ? Xs[(long long)r * 32 * CPL + lane + 32 * q] : 0.0;
-        }
-    for (int j0 = 0; m - 1 - j0 >= je; j0 += KS) {
-#pragma unroll
-        for (int t = 0; t < KS; ++t) {
-            const int j = m - 1 - (j0 + t);
-            if (j < je) break;
-            const int sjj = sid(j, j);
-            double uv[KS];
-#pragma unroll
-            for (int o = 1; o < KS; ++o) uv[o] = (o <= ku && j - o >= je) ? base[sjj - o * ci] : 0.0;
-            const double dv = 1.0 / base[sjj];
-            double xj[CPL];
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) {
-                xj[q] = X[q][t] * dv;
-                emit(j, lane + 32 * q, xj[q]);
-            }
-#pragma unroll
-            for (int o = 1; o < KS; ++o)
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) X[q][(t + o) % KS] = fma(-uv[o], xj[q], X[q][(t + o) % KS]);
-            const int rn = j - KS;
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) X[q][t] = rn >= js ? Xs[(long long)rn * 32 * CPL + lane + 32 * q] : 0.0;
-        }
+    if (hv) {
+        out(B_VLT, pr.nv, 0);
+        out(B_Z1V, pr.nv, hL - k);
+        out(B_Z2V, pr.nv, hL);
+        out(B_VRB, pr.nv, H - k);
+    }
+    if (hw) {
+        out(B_WLT, pr.nw, 0);
+        out(B_Z1W, pr.nw, hL - k);
+        out(B_Z2W, pr.nw, hL);
+        out(B_WRB, pr.nw, H - k);
     }
 }
 
-template <int CPL>
-static bool launch_parts_t(const SkPartsArgs& A, cudaStream_t s) {
-    const int ld = A.akl + A.aku + 1;
-    const size_t wsm = sizeof(double) * sk_parts_warp_smem(A.mmax, A.k, ld);
-    int nw = (int)std::min<size_t>(kSkWarpsMax, (227u * 1024) / wsm);
-    if (nw < 1) return false;
-    const size_t smem = wsm * nw;
-    set_smem_attr((const void*)k_sk_parts<CPL>, (int)smem);
-    k_sk_parts<CPL><<<(A.p + nw - 1) / nw, 32 * nw, smem, s>>>(A);
-    count_launch();
-    return true;
+// carried odd unit: its tip rows move up now (the rest in task B)
+__device__ void sk_carry_tips(const SkLevelsArgs& A, int u, int nu_i, int lane) {
+    const int k = A.k;
+    const SkUnit u0 = A.units[u], u1 = A.units[nu_i];
+    const int h = u0.uh;
+    for (int e = lane; e < 2 * k * k; e += 32) {
+        const int c = e / (2 * k), q = e - c * 2 * k;
+        const int rr = q < k ? q : h - 2 * k + q;
+        if (u0.voff >= 0) A.pool[u1.voff + (long long)c * h + rr] = A.pool[u0.voff + (long long)c * h + rr];
+        if (u0.woff >= 0) A.pool[u1.woff + (long long)c * h + rr] = A.pool[u0.woff + (long long)c * h + rr];
+    }
 }
 
-bool launch_sk_parts(const SkPartsArgs& A, cudaStream_t s) {
-    if (A.akl > 16 || A.aku > 16 || (reinterpret_cast<uintptr_t>(A.band) & 15)) return false;
-    return launch_parts_t<1>(A, s);
+// task B: rows [k, hL-k) and [hL+k, H-k) of a merged unit, one per thread
+__device__ void sk_rows_task(const SkLevelsArgs& A, const SkItem& I, double* zs) {
+    const int k = A.k, tid = threadIdx.x;
+    if (I.pair < 0) {  // carried unit: the non-tip rows
+        const SkUnit u0 = A.units[-(I.pair + 1)], u1 = A.units[I.next];
+        const int h = u0.uh;
+        for (int rr = I.row0 + tid; rr < h - k && rr < I.row0 + kSkChunk; rr += blockDim.x) {
+            if (rr < k) continue;
+            for (int c = 0; c < k; ++c) {
+                if (u0.voff >= 0) A.pool[u1.voff + (long long)c * h + rr] = A.pool[u0.voff + (long long)c * h + rr];
+                if (u0.woff >= 0) A.pool[u1.woff + (long long)c * h + rr] = A.pool[u0.woff + (long long)c * h + rr];
+            }
+        }
+        return;
+    }
+    const SkPair pr = A.pairs[I.pair];
+    const int hL = pr.hL, hR = pr.hR, H = hL + hR;
+    const bool hv = pr.nv >= 0, hw = pr.nw >= 0;
+    // z blocks from the merged unit's middle rows: zs[0] z2v, [1] z2w, [2] z1v, [3] z1w (row-major ld 16)
+    __syncthreads();
+    for (int e = tid; e < 4 * 256; e += blockDim.x) {
+        const int w = e >> 8, q = e & 255, rr = q >> 4, c = q & 15;
+        double v = 0.0;
+        if (rr < k && c < k) {
+            const int row = (w < 2 ? hL : hL - k) + rr;
+            const bool isv = (w & 1) == 0;
+            if (isv && hv) v = A.pool[pr.nv + (long long)c * H + row];
+            if (!isv && hw) v = A.pool[pr.nw + (long long)c * H + row];
+        }
+        zs[e] = v;
+    }
+    __syncthreads();
+    for (int rr = I.row0 + tid; rr < H && rr < I.row0 + kSkChunk; rr += blockDim.x) {
+        const bool left = rr >= k && rr < hL - k;
+        const bool right = rr >= hL + k && rr < H - k;
+        if (!left && !right) continue;
+        const double* M = A.pool + (left ? pr.vl : pr.wr);
+        const int hm = left ? hL : hR, ro = left ? rr : rr - hL;
+        double mrow[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) mrow[q] = q < k ? M[(long long)q * hm + ro] : 0.0;
+        // merged V: left rows -vl z2v, right rows vr - wr z1v; merged W: left
+        // rows wl - vl z2w, right rows -wr z1w
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool isv = pass == 0;
+            if (isv ? !hv : !hw) continue;
+            const long long bo = (isv && !left) ? pr.vr : (!isv && left) ? pr.wl : -1;
+            double acc[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = (c < k && bo >= 0) ? A.pool[bo + (long long)c * hm + ro] : 0.0;
+            const double* z = zs + ((left ? 0 : 2) + (isv ? 0 : 1)) * 256;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                if (q >= k) break;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) acc[c] = fma(-mrow[q], z[q * 16 + c], acc[c]);
+            }
+            double* dst = A.pool + (isv ? pr.nv : pr.nw);
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < k) dst[(long long)c * H + rr] = acc[c];
+        }
+    }
 }
-
-// ===========================================================================
-// reduced hierarchy: per level, items (pair, chunk of kSkLvRows rows of the
-// merged unit), one CTA per item
-//
-// Pair (left unit hL rows: V = vl, W = wl; right unit hR rows: V = vr, W = wr),
-// coupling [[I, Vb], [Wt, I]] with Vb = vl[hL-k : hL], Wt = wr[0 : k]; Schur
-// complement S = I - Wt Vb.  The merged unit's spikes are the pair solves
-// (factorize.cpp:19-32) of [0; vr] and [wl; 0]:
-//   z2 = S^-1 (y2 - Wt y1), z1 = y1 - Vb z2,
-//   rows [0, hL-k) -= vl[0:hL-k] z2, rows [hL+k, H) -= wr[k:hR] z1.
-// The k x k work (S, S^-1 by Gauss-Jordan with partial pivoting, the z
-// blocks) runs one element per thread; the rows one row per thread.
-namespace {
-constexpr int kSkLvThreads = 256;
-constexpr int kSkLvRows = 256;  // rows per work item (one per thread)
 }  // namespace
 
-__global__ void __launch_bounds__(kSkLvThreads) k_sk_levels(SkLevelsArgs A) {
-    // k <= 16: k x k blocks row-major with ld 16
-    __shared__ double Wt[256], Vb[256], Si[256], y2v[256], y1w[256], uw[256], z2v[256], z1v[256], z2w[256],
-        z1w[256], colj[16];
-    __shared__ double aug[16][33], rowp[32];
-    __shared__ int s_pr, s_bad, s_perm[16];
-    const int tid = threadIdx.x;
-    const int k = A.k;
-    const int er = tid & 15, ec = tid >> 4;  // element (row, column) of a k x k block
-    const bool el = er < k && ec < k;
+__global__ void __launch_bounds__(kLvThreads, 1) k_sk_levels(SkLevelsArgs A) {
+    extern __shared__ __align__(16) double lv_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* const wsm = lv_smem + warp * kWarpSmem;
+    const int nwarps = gridDim.x * kLvWarps;
     unsigned target = 0;
-    for (int l = 0; l < A.nlevels; ++l) {
-        const SkLevel L = A.levels[l];
-        for (int it = blockIdx.x; it < L.nitems; it += gridDim.x) {
-            const SkItem I = A.items[L.item0 + it];
-            if (I.pair < 0) {  // carried odd unit: spikes move up unchanged
-                const SkUnit u = A.units[-(I.pair + 1)], nu = A.units[I.next];
-                const int r = I.row0 + tid;
-                if (r < u.uh)
-                    for (int c = 0; c < k; ++c) {
-                        if (u.voff >= 0) A.pool[nu.voff + (long long)c * nu.uh + r] = A.pool[u.voff + (long long)c * u.uh + r];
-                        if (u.woff >= 0) A.pool[nu.woff + (long long)c * nu.uh + r] = A.pool[u.woff + (long long)c * u.uh + r];
-                    }
-                continue;
+    for (int ph = 0; ph <= A.nlevels; ++ph) {
+        sk_stamp(A.trace, ph, 0);
+        if (ph < A.nlevels) {
+            const SkLevel L = A.levels[ph];
+            const int ntask = L.npairs + (L.carry >= 0 ? 1 : 0);
+            for (int a = blockIdx.x * kLvWarps + warp; a < ntask; a += nwarps) {
+                if (a < L.npairs) sk_pair_task(A, A.pairs[L.pair0 + a], wsm, lane);
+                else sk_carry_tips(A, L.carry, L.carry_next, lane);
+                __syncwarp();
             }
-            const SkPair pr = A.pairs[I.pair];
-            const SkUnit uL = A.units[pr.left], uR = A.units[pr.left + 1], nu = A.units[pr.next];
-            const int hL = uL.uh, hR = uR.uh, H = hL + hR;
-            const bool hv = nu.voff >= 0, hw = nu.woff >= 0;
-            const double* vl = A.pool + uL.voff;
-            const double* wl = hw ? A.pool + uL.woff : nullptr;
-            const double* vr = hv ? A.pool + uR.voff : nullptr;
-            const double* wr = A.pool + uR.woff;
-            if (tid == 0) s_bad = 0;
-            __syncthreads();
-            if (el) {
-                const double w = wr[(long long)ec * hR + er];
-                if (fabs(w) > 1.0) s_bad = 1;
-                Wt[er * 16 + ec] = w;
-                Vb[er * 16 + ec] = vl[(long long)ec * hL + hL - k + er];
-                y2v[er * 16 + ec] = hv ? vr[(long long)ec * hR + er] : 0.0;
-                y1w[er * 16 + ec] = hw ? wl[(long long)ec * hL + hL - k + er] : 0.0;
-            }
-            __syncthreads();
-            if (s_bad) {  // |W| > 1: the pivoted 2k coupling (general programs)
-                if (tid == 0) {
-                    A.flags[pr.gidx] = 0;
-                    atomicExch(A.fallback, 1);
-                }
-                __syncthreads();
-                continue;
-            }
-            // S = I - Wt Vb into aug[:, 0:k], I into aug[:, k:2k]; uw = -Wt y1w
-            if (el) {
-                double sv = er == ec ? 1.0 : 0.0, u = 0.0;
-                for (int t = 0; t < k; ++t) {
-                    sv = fma(-Wt[er * 16 + t], Vb[t * 16 + ec], sv);
-                    u = fma(-Wt[er * 16 + t], y1w[t * 16 + ec], u);
-                }
-                aug[er][ec] = sv;
-                aug[er][k + ec] = er == ec ? 1.0 : 0.0;
-                uw[er * 16 + ec] = u;
-            }
-            __syncthreads();
-            // Gauss-Jordan, partial pivoting: first maximum among unused rows
-            unsigned used = 0u;
-            int perm = 0;  // thread j: pivot row of step j
-            bool sing = false;
-            for (int j = 0; j < k; ++j) {
-                if (tid < 32) {
-                    double best = (tid < k && !((used >> tid) & 1u)) ? fabs(aug[tid][j]) : -1.0;
-                    int idx = tid;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-                        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-                        if (ov > best || (ov == best && oi < idx)) {
-                            best = ov;
-                            idx = oi;
-                        }
-                    }
-                    if (tid == 0) s_pr = best > 0.0 ? idx : -1;
-                }
-                __syncthreads();
-                const int prw = s_pr;
-                if (prw < 0) {
-                    sing = true;
-                    break;
-                }
-                used |= 1u << prw;
-                if (tid == j) perm = prw;
-                if (tid < k) colj[tid] = aug[tid][j];
-                if (tid < 2 * k) rowp[tid] = aug[prw][tid] / aug[prw][j];
-                __syncthreads();
-                for (int e = tid; e < k * 2 * k; e += kSkLvThreads) {
-                    const int r = e / (2 * k), c = e - r * 2 * k;
-                    const double pc = rowp[c];
-                    aug[r][c] = r == prw ? pc : fma(-colj[r], pc, aug[r][c]);
-                }
-                __syncthreads();
-            }
-            if (sing) {
-                if (tid == 0) {
-                    A.flags[pr.gidx] = 0;
-                    atomicExch(A.fallback, 1);
-                }
-                __syncthreads();
-                continue;
-            }
-            // S^-1 row j = aug[perm(j)][k:2k]
-            if (tid < k) s_perm[tid] = perm;
-            __syncthreads();
-            if (el) Si[er * 16 + ec] = aug[s_perm[er]][k + ec];
-            __syncthreads();
-            if (I.row0 == 0) {
-                if (el) A.pool[pr.sinv + (long long)ec * k + er] = Si[er * 16 + ec];
-                if (tid == 0) A.flags[pr.gidx] = 1;
-            }
-            // z2 = S^-1 [vr top | uw]; z1 = [0 | y1w] - Vb z2
-            if (el) {
-                double a = 0.0, b = 0.0;
-                for (int t = 0; t < k; ++t) {
-                    a = fma(Si[er * 16 + t], y2v[t * 16 + ec], a);
-                    b = fma(Si[er * 16 + t], uw[t * 16 + ec], b);
-                }
-                z2v[er * 16 + ec] = a;
-                z2w[er * 16 + ec] = b;
-            }
-            __syncthreads();
-            if (el) {
-                double a = 0.0, b = y1w[er * 16 + ec];
-                for (int t = 0; t < k; ++t) {
-                    a = fma(-Vb[er * 16 + t], z2v[t * 16 + ec], a);
-                    b = fma(-Vb[er * 16 + t], z2w[t * 16 + ec], b);
-                }
-                z1v[er * 16 + ec] = a;
-                z1w[er * 16 + ec] = b;
-            }
-            __syncthreads();
-            // rows of the merged unit: one per thread
-            const int r = I.row0 + tid;
-            if (r < H && r < I.row0 + kSkLvRows) {
-                double* nv = hv ? A.pool + nu.voff : nullptr;
-                double* nwp = hw ? A.pool + nu.woff : nullptr;
-                if (r < hL - k || r >= hL + k) {
-                    const bool left = r < hL - k;
-                    const int rr = left ? r : r - hL;
-                    const double* M = left ? vl : wr;
-                    const int hm = left ? hL : hR;
-                    const double* zv = left ? z2v : z1v;
-                    const double* zw = left ? z2w : z1w;
-                    double mrow[16];
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) mrow[t] = t < k ? M[(long long)t * hm + rr] : 0.0;
-                    for (int c = 0; c < k; ++c) {
-                        double a = left ? 0.0 : (hv ? vr[(long long)c * hR + rr] : 0.0);
-                        double b = left ? (hw ? wl[(long long)c * hL + rr] : 0.0) : 0.0;
-#pragma unroll
-                        for (int t = 0; t < 16; ++t)
-                            if (t < k) {
-                                a = fma(-mrow[t], zv[t * 16 + c], a);
-                                b = fma(-mrow[t], zw[t * 16 + c], b);
-                            }
-                        if (hv) nv[(long long)c * H + r] = a;
-                        if (hw) nwp[(long long)c * H + r] = b;
-                    }
-                } else {
-                    const bool top = r < hL;  // z1 rows [hL-k, hL), z2 rows [hL, hL+k)
-                    const int rr = top ? r - (hL - k) : r - hL;
-                    for (int c = 0; c < k; ++c) {
-                        if (hv) nv[(long long)c * H + r] = (top ? z1v : z2v)[rr * 16 + c];
-                        if (hw) nwp[(long long)c * H + r] = (top ? z1w : z2w)[rr * 16 + c];
-                    }
-                }
-            }
-            __syncthreads();
         }
-        if (l + 1 < A.nlevels) grid_barrier(A.bar, target);
+        __syncthreads();
+        sk_stamp(A.trace, ph, 1);
+        if (ph >= 1) {
+            const SkLevel L = A.levels[ph - 1];
+            for (int it = gridDim.x - 1 - blockIdx.x; it < L.nitems; it += gridDim.x)
+                sk_rows_task(A, A.items[L.item0 + it], lv_smem);
+        }
+        sk_stamp(A.trace, ph, 2);
+        if (ph < A.nlevels) grid_barrier(A.bar, target);
+        sk_stamp(A.trace, ph, 3);
     }
 }
 
 void launch_sk_levels(const SkLevelsArgs& A, cudaStream_t s) {
     if (A.nlevels <= 0) return;
-    const int grid = sk_coop_grid((const void*)k_sk_levels, kSkLvThreads, 0);
+    const int smem = (int)(sizeof(double) * kWarpSmem * kLvWarps);
+    set_smem_attr((const void*)k_sk_levels, smem);
     SkLevelsArgs a = A;
     void* args[] = {&a};
-    (void)cudaLaunchCooperativeKernel((const void*)k_sk_levels, grid, kSkLvThreads, args, 0, s);
+    (void)cudaLaunchCooperativeKernel((const void*)k_sk_levels, device_sms(), kLvThreads, args, smem, s);
     count_launch();  // reports a failed launch
 }
+
 
 }  // namespace spk

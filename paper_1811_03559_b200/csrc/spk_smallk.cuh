@@ -25,7 +25,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(bar, 1u);
-        while (ld_acquire_u32(bar) < target) __nanosleep(64);
+        while (ld_acquire_u32(bar) < target) __nanosleep(1000);
     }
     __syncthreads();
 }
@@ -58,6 +58,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
             (unsigned)__cvta_generic_to_shared(dst)),
         "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
         : "memory");
+}
+
+// cp.async (LDGSTS) 8-byte copy global -> shared, no register round trip;
+// sk_cp_wait_all waits for all of the thread's copies
+__device__ __forceinline__ void sk_cp8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void sk_cp_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void sk_stamp(unsigned long long* trace, int ph, int mark) {
+    if (trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace[((long long)ph * gridDim.x + blockIdx.x) * 4 + mark] = t;
+    }
 }
 
 __device__ __forceinline__ double warp_max(double v) {

@@ -1,6 +1,23 @@
-// spk_smallk_solve.cu — the small-k engine's forward solve (k_sk_solve), see
-// spk_smallk.cu for the engine: D-stage per partition, the reduced solve
-// level by level, retrieval per partition, one cooperative kernel.
+// spk_smallk_solve.cu — the small-k engine's forward solve (k_sk_solve) for
+// nrhs <= 8: one cooperative kernel (solve.cpp:81-223).
+//
+//   D-stage   a warp per partition: the packed factor block lands in shared
+//             memory with one TMA bulk copy (cp.async.bulk, mbarrier
+//             completion), the right-hand sides with cp.async; forward L and
+//             backward U sweeps with lanes = window rows (a step is one
+//             shuffle of the pivot row's x and one FMA per column on the rows
+//             it updates, the factor entries are shared-memory reads); the
+//             tips of Y = D^-1 F go to T.
+//   reduced   (reduced_solve, solve.cpp:33-43) level by level, one grid
+//             barrier per level.  Phase ph: task A (level ph, a warp per pair)
+//             forms z2 = S^-1 (y2 - Wt y1), z1 = y1 - Vb z2 and the merged
+//             unit's boundary rows (top k: y - vl_top z2, bottom k:
+//             y - wr_bot z1) straight from k x k blocks, so the next level
+//             needs nothing else; task B (level ph-1, a CTA per row item)
+//             updates the merged units' other rows.  T is updated in place:
+//             the two tasks of a phase touch disjoint rows.
+//   retrieval a warp per partition, the factor still in shared memory:
+//             X_i = A_i^-1 (F_i - B^_i x_top(i+1) - C^_i x_bot(i-1)).
 #include "spk_device.cuh"
 #include "spk_launch.h"
 #include "spk_smallk.cuh"
@@ -11,136 +28,271 @@
 
 namespace spk {
 
-// ===========================================================================
-// forward solve: D-stage, reduced levels, retrieval (one cooperative kernel)
 namespace {
-constexpr int kSkSvWarps = 4;
+constexpr int kSvWarps = 8;
+constexpr int kSvThreads = 32 * kSvWarps;
 
-// Forward L then backward U over one partition's rows (LU space) for nr <= 8
-// columns.  Lanes hold the window rows (forward: row r in lane r mod 32,
-// backward: row r in lane (m-1-r) mod 32), so a step is one shuffle of the
-// pivot row's x and one FMA per column on the rows it updates; the factor
-// entries of the next kSkPf steps (each lane's own row: L column j / U column
-// j, contiguous in the packed factor) and the rows entering the window are
-// prefetched into register rings, so no step waits on memory.  x enters from
-// load(r, c); the forward results go to the warp's Xs (m x 8); the backward
-// value of row j (j >= bwd_lo) goes to store(j, c, v).
-constexpr int kSkPf = 8;
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "SKWP_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra SKWP_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
 
-template <int NR, class Load, class Store>
-__device__ void sk_fwd_bwd(const PartDev& P, const double* fac, double* Xs, int lane, int bwd_lo, Load load,
-                           Store store) {
+// per-warp shared memory (doubles): factor block (+2 alignment slack), 1/u,
+// right-hand-side rows, mbarrier
+__host__ __device__ inline long long sv_warp_smem(int mmax, int rmax, int nr) {
+    return ((long long)mmax * rmax + 2 + mmax + (long long)mmax * nr + 2 + 1) / 2 * 2;
+}
+
+struct SvWarp {
+    double* Fs;   // packed factor of the staged partition (column j at j * rows)
+    double* dv;   // 1 / u_jj
+    double* Ys;   // right-hand-side rows (LU space), then the forward results
+    unsigned long long* bar;
+    unsigned phase;
+};
+
+// Stage partition P: the factor block by one bulk copy (16-byte aligned
+// window, the odd tail element by a plain load), 1/u_jj from its diagonal.
+__device__ void sv_stage_factor(const SkSolveArgs& A, const PartDev& P, SvWarp& w, double*& Fs, int lane) {
+    const long long e0 = P.fofs, e1 = P.fofs + (long long)P.m * P.rows;
+    const long long a0 = e0 & ~1LL;
+    long long a1 = (e1 + 1) & ~1LL;
+    if (a1 > A.fac_size) a1 -= 2;
+    Fs = w.Fs + (e0 - a0);
+    if (lane == 0) {
+        const unsigned bytes = (unsigned)((a1 - a0) * 8);
+        mbar_expect_tx(w.bar, bytes);
+        bulk_g2s(w.Fs, A.fac + a0, bytes, w.bar);
+    }
+    for (long long e = a1 + lane; e < e1; e += 32) w.Fs[e - a0] = A.fac[e];
+    mbar_wait_parity(w.bar, w.phase);
+    w.phase ^= 1u;
+    __syncwarp();
+    for (int j = lane; j < P.m; j += 32) w.dv[j] = 1.0 / Fs[(long long)j * P.rows + P.d];
+    __syncwarp();
+}
+
+// Forward L then backward U over the partition (LU space) for NR columns of
+// Ys (row-major, NR per row).  Forward: row r in lane r mod 32; backward: row
+// r in lane (m-1-r) mod 32.  The forward results overwrite Ys; backward values
+// of rows j >= bwd_lo go to store(j, c, v).
+template <int NR, class Store>
+__device__ __forceinline__ void sv_sweeps(const PartDev& P, const double* Fs, const double* dv, double* Ys, int lane,
+                                          int bwd_lo, Store store) {
     const unsigned full = 0xffffffffu;
     const int m = P.m, kl = P.kl, ku = P.ku, rows = P.rows, d = P.d;
-    const double* F = fac + P.fofs;
     double x[NR];
-    double rf[kSkPf];       // factor entry of step j + s for this lane's row
-    double rx[kSkPf][NR];   // the row entering at step j + s (only on its lane)
-    // ---- forward, rows 0 .. m-1
 #pragma unroll
-    for (int c = 0; c < NR; ++c) x[c] = lane < m ? load(lane, c) : 0.0;
-    auto fpref = [&](int j, int s) {
+    for (int c = 0; c < NR; ++c) x[c] = lane < m ? Ys[lane * NR + c] : 0.0;
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) {
         const int o = (lane - j) & 31;
-        rf[s] = (j < m && o >= 1 && o <= kl && j + o < m) ? F[(long long)j * rows + d + o] : 0.0;
-        if (o == 0 && j + 32 < m)
+        const double l = (o >= 1 && o <= kl) ? Fs[(long long)j * rows + d + o] : 0.0;
+        double xj[NR];
 #pragma unroll
-            for (int c = 0; c < NR; ++c) rx[s][c] = load(j + 32, c);
-    };
+        for (int c = 0; c < NR; ++c) xj[c] = __shfl_sync(full, x[c], j & 31);
+        if (o == 0) {
 #pragma unroll
-    for (int s = 0; s < kSkPf; ++s) fpref(s, s);
-    for (int j0 = 0; j0 < m; j0 += kSkPf) {
-#pragma unroll
-        for (int s = 0; s < kSkPf; ++s) {
-            const int j = j0 + s;
-            if (j >= m) break;
-            const int o = (lane - j) & 31;
-            double xj[NR];
-#pragma unroll
-            for (int c = 0; c < NR; ++c) xj[c] = __shfl_sync(full, x[c], j & 31);
-            if (o == 0) {
-#pragma unroll
-                for (int c = 0; c < NR; ++c) {
-                    Xs[j * 8 + c] = xj[c];
-                    x[c] = j + 32 < m ? rx[s][c] : 0.0;
-                }
-            } else if (o <= kl) {
-#pragma unroll
-                for (int c = 0; c < NR; ++c) x[c] = fma(-rf[s], xj[c], x[c]);
+            for (int c = 0; c < NR; ++c) {
+                Ys[j * NR + c] = xj[c];
+                x[c] = j + 32 < m ? Ys[(j + 32) * NR + c] : 0.0;
             }
-            fpref(j + kSkPf, s);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NR; ++c) x[c] = fma(-l, xj[c], x[c]);
         }
     }
     __syncwarp();
-    // ---- backward, rows m-1 .. bwd_lo
-    double rd[kSkPf];  // 1 / u_jj of step j
 #pragma unroll
-    for (int c = 0; c < NR; ++c) x[c] = m - 1 - lane >= 0 ? Xs[(m - 1 - lane) * 8 + c] : 0.0;
-    auto bpref = [&](int j, int s) {  // step j = row j (descending)
+    for (int c = 0; c < NR; ++c) x[c] = m - 1 - lane >= 0 ? Ys[(m - 1 - lane) * NR + c] : 0.0;
+#pragma unroll 4
+    for (int j = m - 1; j >= bwd_lo; --j) {
         const int o = (lane - (m - 1 - j)) & 31;
-        rf[s] = (j >= 0 && o >= 1 && o <= ku && j - o >= 0) ? F[(long long)j * rows + d - o] : 0.0;
-        rd[s] = j >= 0 ? 1.0 / F[(long long)j * rows + d] : 0.0;
-        if (o == 0 && j - 32 >= 0)
+        const double u = (o >= 1 && o <= ku) ? Fs[(long long)j * rows + d - o] : 0.0;
+        const double r = dv[j];
+        double xj[NR];
 #pragma unroll
-            for (int c = 0; c < NR; ++c) rx[s][c] = Xs[(j - 32) * 8 + c];
-    };
+        for (int c = 0; c < NR; ++c) xj[c] = __shfl_sync(full, x[c], (m - 1 - j) & 31) * r;
+        if (o == 0) {
 #pragma unroll
-    for (int s = 0; s < kSkPf; ++s) bpref(m - 1 - s, s);
-    for (int j0 = 0; m - 1 - j0 >= bwd_lo; j0 += kSkPf) {
-#pragma unroll
-        for (int s = 0; s < kSkPf; ++s) {
-            const int j = m - 1 - (j0 + s);
-            if (j < bwd_lo) break;
-            const int o = (lane - (m - 1 - j)) & 31;
-            double xj[NR];
-#pragma unroll
-            for (int c = 0; c < NR; ++c) xj[c] = __shfl_sync(full, x[c], (m - 1 - j) & 31) * rd[s];
-            if (o == 0) {
-#pragma unroll
-                for (int c = 0; c < NR; ++c) {
-                    store(j, c, xj[c]);
-                    x[c] = j - 32 >= 0 ? rx[s][c] : 0.0;
-                }
-            } else if (o <= ku) {
-#pragma unroll
-                for (int c = 0; c < NR; ++c) x[c] = fma(-rf[s], xj[c], x[c]);
+            for (int c = 0; c < NR; ++c) {
+                store(j, c, xj[c]);
+                x[c] = j - 32 >= 0 ? Ys[(j - 32) * NR + c] : 0.0;
             }
-            bpref(j - kSkPf, s);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NR; ++c) x[c] = fma(-u, xj[c], x[c]);
         }
     }
     __syncwarp();
 }
+
+// task A of the reduced solve: one warp per pair, lanes 0..15 = rows
+template <int NR>
+__device__ void sv_pair_task(const SkSolveArgs& A, const SkPair& pr, int lane) {
+    const unsigned full = 0xffffffffu;
+    const int k = A.k, nr = A.nrhs;
+    const long long H = 2LL * A.p * k;
+    const SkUnit uL = A.units[pr.left], uR = A.units[pr.left + 1];
+    const int hL = uL.uh, hR = uR.uh, Hu = hL + hR;
+    const long long zb = uL.uoff;
+    const double* vl = A.pool + uL.voff;
+    const double* wr = A.pool + uR.woff;
+    const double* si = A.pool + pr.sinv;
+    const int r = lane & 15;
+    const bool rv = lane < 16 && r < k;
+    // every load first: rows of Wt, Vb, S^-1, vl_top, wr_bot; the four tips
+    double Wt[16], Vb[16], Si[16], Vt[16], Wb[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        const bool ok = rv && t < k;
+        Wt[t] = ok ? wr[(long long)t * hR + r] : 0.0;
+        Vb[t] = ok ? vl[(long long)t * hL + hL - k + r] : 0.0;
+        Si[t] = ok ? si[(long long)t * k + r] : 0.0;
+        Vt[t] = ok ? vl[(long long)t * hL + r] : 0.0;
+        Wb[t] = ok ? wr[(long long)t * hR + hR - k + r] : 0.0;
+    }
+    double y1[NR], y2[NR], yt[NR], yb[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+        const bool ok = rv && c < nr;
+        const double* Tc = A.T + (long long)c * H + zb;
+        y1[c] = ok ? Tc[hL - k + r] : 0.0;
+        y2[c] = ok ? Tc[hL + r] : 0.0;
+        yt[c] = ok ? Tc[r] : 0.0;
+        yb[c] = ok ? Tc[Hu - k + r] : 0.0;
+    }
+    // row r of M times the vector v (v[t] on lane t)
+    auto mv = [&](const double* M, const double* v, double* out) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) out[c] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+#pragma unroll
+            for (int c = 0; c < NR; ++c) out[c] = fma(M[t], __shfl_sync(full, v[c], t), out[c]);
+        }
+    };
+    double a[NR], z2[NR], z1[NR];
+    mv(Wt, y1, a);
+#pragma unroll
+    for (int c = 0; c < NR; ++c) a[c] = y2[c] - a[c];
+    mv(Si, a, z2);
+    mv(Vb, z2, a);
+#pragma unroll
+    for (int c = 0; c < NR; ++c) z1[c] = y1[c] - a[c];
+    double b[NR];
+    mv(Vt, z2, a);
+    mv(Wb, z1, b);
+    if (rv) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+            if (c >= nr) break;
+            double* Tc = A.T + (long long)c * H + zb;
+            Tc[hL - k + r] = z1[c];
+            Tc[hL + r] = z2[c];
+            Tc[r] = yt[c] - a[c];
+            Tc[Hu - k + r] = yb[c] - b[c];
+        }
+    }
+}
+
+// task B: rows [k, hL-k) -= vl z2, rows [hL+k, H-k) -= wr z1 of a merged unit
+template <int NR>
+__device__ void sv_rows_task(const SkSolveArgs& A, const SkItem& I, double* zs) {
+    if (I.pair < 0) return;  // carried unit: its rows stay
+    const int k = A.k, nr = A.nrhs, tid = threadIdx.x;
+    const long long H = 2LL * A.p * k;
+    const SkPair pr = A.pairs[I.pair];
+    const SkUnit uL = A.units[pr.left], uR = A.units[pr.left + 1];
+    const int hL = uL.uh, hR = uR.uh, Hu = hL + hR;
+    const long long zb = uL.uoff;
+    __syncthreads();
+    for (int e = tid; e < 2 * 16 * NR; e += blockDim.x) {  // zs[0]: z2 (16 x NR), zs[1]: z1
+        const int w = e / (16 * NR), q = e - w * 16 * NR, t = q / NR, c = q - t * NR;
+        zs[e] = (t < k && c < nr) ? A.T[(long long)c * H + zb + (w == 0 ? hL : hL - k) + t] : 0.0;
+    }
+    __syncthreads();
+    for (int rr = I.row0 + tid; rr < Hu && rr < I.row0 + kSkChunk; rr += blockDim.x) {
+        const bool left = rr >= k && rr < hL - k;
+        const bool right = rr >= hL + k && rr < Hu - k;
+        if (!left && !right) continue;
+        const double* M = left ? A.pool + uL.voff : A.pool + uR.woff;
+        const int hm = left ? hL : hR, ro = left ? rr : rr - hL;
+        const double* z = zs + (left ? 0 : 16 * NR);
+        double mrow[16], v[NR];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) mrow[t] = t < k ? M[(long long)t * hm + ro] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) v[c] = c < nr ? A.T[(long long)c * H + zb + rr] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+#pragma unroll
+            for (int c = 0; c < NR; ++c) v[c] = fma(-mrow[t], z[t * NR + c], v[c]);
+#pragma unroll
+        for (int c = 0; c < NR; ++c)
+            if (c < nr) A.T[(long long)c * H + zb + rr] = v[c];
+    }
+}
 }  // namespace
 
 template <int NR>
-__global__ void __launch_bounds__(32 * kSkSvWarps) k_sk_solve(SkSolveArgs A) {
+__global__ void __launch_bounds__(kSvThreads, 1) k_sk_solve(SkSolveArgs A) {
     extern __shared__ __align__(16) double sv_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kSkSvWarps + warp, nwarps = gridDim.x * kSkSvWarps;
-    const int k = A.k, p = A.p;
+    const int gw = blockIdx.x * kSvWarps + warp, nwarps = gridDim.x * kSvWarps;
+    const int k = A.k, p = A.p, nr = A.nrhs;
     const long long H = 2LL * p * k, kk = (long long)k * k;
-    const int nr = A.nrhs;  // columns < nr exist (NR rounds nrhs up)
-    double* Xs = sv_smem + (long long)warp * A.mmax * 8;
+    const long long wsm = sv_warp_smem(A.mmax, A.rmax, NR);
+    double* const wb = sv_smem + warp * wsm;
+    SvWarp w{wb, wb + (long long)A.mmax * A.rmax + 2, wb + (long long)A.mmax * A.rmax + 2 + A.mmax,
+             reinterpret_cast<unsigned long long*>(wb + wsm - 2), 0u};
+    if (lane == 0) mbar_init1(w.bar);
+    __syncwarp();
+    double* Fs = nullptr;
+    int staged = -1;
 
-    // ---- D-stage: tips of Y = D^-1 F into T0
+    // the right-hand-side rows of partition i (LU space) into Ys, with cp.async
+    auto stage_rhs = [&](const PartDev& P) {
+        const int m = P.m;
+        for (int e = lane; e < m * NR; e += 32) {
+            const int r = e / NR, c = e - r * NR;
+            const long long pr = P.rev ? (long long)(m - 1 - r) : (long long)r;
+            if (c < nr) sk_cp8(w.Ys + e, A.F + (long long)c * A.ldf + P.r0 + pr);
+            else w.Ys[e] = 0.0;
+        }
+        sk_cp_wait_all();
+        __syncwarp();
+    };
+
+    // ---- D-stage: tips of Y = D^-1 F into T
     for (int i = gw; i < p; i += nwarps) {
         const PartDev P = A.parts[i];
         const int m = P.m;
         const bool first = i == 0, last = i == p - 1;
-        auto phys = [&](int r) -> long long { return P.rev ? (long long)(m - 1 - r) : (long long)r; };
-        auto load = [&](int r, int c) -> double { return c < nr ? A.F[(long long)c * A.ldf + P.r0 + phys(r)] : 0.0; };
-        double* T = A.T0;
+        sv_stage_factor(A, P, w, Fs, lane);
+        staged = i;
+        stage_rhs(P);
+        double* T = A.T;
         if (first) {
             for (int e = lane; e < k * nr; e += 32) T[(long long)(e / k) * H + (e % k)] = 0.0;  // dead top tip
-            sk_fwd_bwd<NR>(P, A.fac, Xs, lane, m - k, load, [&](int j, int c, double v) {
+            sv_sweeps<NR>(P, Fs, w.dv, w.Ys, lane, m - k, [&](int j, int c, double v) {
                 if (c < nr) T[(long long)c * H + k + (j - (m - k))] = v;
             });
         } else if (last) {
             for (int e = lane; e < k * nr; e += 32) T[(long long)(e / k) * H + (2LL * i + 1) * k + (e % k)] = 0.0;
-            sk_fwd_bwd<NR>(P, A.fac, Xs, lane, m - k, load, [&](int j, int c, double v) {
+            sv_sweeps<NR>(P, Fs, w.dv, w.Ys, lane, m - k, [&](int j, int c, double v) {
                 if (c < nr) T[(long long)c * H + 2LL * i * k + (m - 1 - j)] = v;
             });
         } else {
-            sk_fwd_bwd<NR>(P, A.fac, Xs, lane, 0, load, [&](int j, int c, double v) {
+            sv_sweeps<NR>(P, Fs, w.dv, w.Ys, lane, 0, [&](int j, int c, double v) {
                 if (c >= nr) return;
                 if (j < k) T[(long long)c * H + 2LL * i * k + j] = v;
                 else if (j >= m - k) T[(long long)c * H + (2LL * i + 1) * k + (j - (m - k))] = v;
@@ -148,130 +300,78 @@ __global__ void __launch_bounds__(32 * kSkSvWarps) k_sk_solve(SkSolveArgs A) {
         }
     }
     unsigned target = 0;
+    sk_stamp(A.trace, 0, 1);  // D-stage done (this CTA)
     grid_barrier(A.bar, target);
 
-    // ---- reduced solve (solve.cpp:33-43): level by level, ping-pong T; one
-    //      CTA per item (pair, kSkChunk rows of the merged unit)
-    double* Tin = A.T0;
-    double* Tout = A.T1;
-    __shared__ double sWt[256], sVb[256], sSi[256], su[16 * 8], sz2[16 * 8], sz1[16 * 8];
-    const int tid = threadIdx.x;
-    for (int l = 0; l < A.nlevels; ++l) {
-        const SkLevel L = A.levels[l];
-        for (int it = blockIdx.x; it < L.nitems; it += gridDim.x) {
-            const SkItem I = A.items[L.item0 + it];
-            if (I.pair < 0) {
-                const SkUnit u = A.units[-(I.pair + 1)];
-                for (int r = I.row0 + tid; r < u.uh && r < I.row0 + kSkChunk; r += blockDim.x)
-#pragma unroll
-                    for (int c = 0; c < NR; ++c)
-                        if (c < nr) Tout[(long long)c * H + u.uoff + r] = Tin[(long long)c * H + u.uoff + r];
-                continue;
-            }
-            const SkPair pr = A.pairs[I.pair];
-            const SkUnit uL = A.units[pr.left], uR = A.units[pr.left + 1];
-            const int hL = uL.uh, hR = uR.uh, Hu = hL + hR;
-            const long long zb = uL.uoff;
-            const double* vl = A.pool + uL.voff;
-            const double* wr = A.pool + uR.woff;
-            for (int e = tid; e < k * k; e += blockDim.x) {
-                const int c = e / k, r = e - c * k;
-                sWt[r * 16 + c] = wr[(long long)c * hR + r];
-                sVb[r * 16 + c] = vl[(long long)c * hL + hL - k + r];
-                sSi[r * 16 + c] = A.pool[pr.sinv + e];
-            }
-            __syncthreads();
-            // z2 = S^-1 (y2 - Wt y1), z1 = y1 - Vb z2: one element per thread
-            const int er = tid % 16, ec = tid / 16;
-            const bool el = er < k && ec < nr;
-            if (el) {
-                double v = Tin[(long long)ec * H + zb + hL + er];
-                for (int t = 0; t < k; ++t) v = fma(-sWt[er * 16 + t], Tin[(long long)ec * H + zb + hL - k + t], v);
-                su[er * 8 + ec] = v;
-            }
-            __syncthreads();
-            if (el) {
-                double v = 0.0;
-                for (int t = 0; t < k; ++t) v = fma(sSi[er * 16 + t], su[t * 8 + ec], v);
-                sz2[er * 8 + ec] = v;
-            }
-            __syncthreads();
-            if (el) {
-                double v = Tin[(long long)ec * H + zb + hL - k + er];
-                for (int t = 0; t < k; ++t) v = fma(-sVb[er * 16 + t], sz2[t * 8 + ec], v);
-                sz1[er * 8 + ec] = v;
-            }
-            __syncthreads();
-            for (int r = I.row0 + tid; r < Hu && r < I.row0 + kSkChunk; r += blockDim.x) {
-                if (r < hL - k || r >= hL + k) {
-                    const bool left = r < hL - k;
-                    const double* M = left ? vl : wr;
-                    const int hm = left ? hL : hR, rr = left ? r : r - hL;
-                    const double* z = left ? sz2 : sz1;
-                    double v[NR];
-#pragma unroll
-                    for (int c = 0; c < NR; ++c) v[c] = c < nr ? Tin[(long long)c * H + zb + r] : 0.0;
-                    for (int t = 0; t < k; ++t) {
-                        const double mt = M[(long long)t * hm + rr];
-#pragma unroll
-                        for (int c = 0; c < NR; ++c) v[c] = fma(-mt, z[t * 8 + c], v[c]);
-                    }
-#pragma unroll
-                    for (int c = 0; c < NR; ++c)
-                        if (c < nr) Tout[(long long)c * H + zb + r] = v[c];
-                } else {
-                    const bool top = r < hL;
-                    const int rr = top ? r - (hL - k) : r - hL;
-#pragma unroll
-                    for (int c = 0; c < NR; ++c)
-                        if (c < nr) Tout[(long long)c * H + zb + r] = (top ? sz1 : sz2)[rr * 8 + c];
-                }
-            }
-            __syncthreads();
+    // ---- reduced solve, level by level (task A: level ph, task B: level ph-1)
+    double* zs = sv_smem + kSvWarps * wsm;
+    for (int ph = 0; ph <= A.nlevels; ++ph) {
+        sk_stamp(A.trace, ph, 0);
+        if (ph < A.nlevels) {
+            const SkLevel L = A.levels[ph];
+            for (int a = gw; a < L.npairs; a += nwarps) sv_pair_task<NR>(A, A.pairs[L.pair0 + a], lane);
         }
+        if (ph >= 1) {
+            const SkLevel L = A.levels[ph - 1];
+            for (int it = gridDim.x - 1 - blockIdx.x; it < L.nitems; it += gridDim.x)
+                sv_rows_task<NR>(A, A.items[L.item0 + it], zs);
+        }
+        sk_stamp(A.trace, ph, 2);
         grid_barrier(A.bar, target);
-        double* tmp = Tin;
-        Tin = Tout;
-        Tout = tmp;
+        sk_stamp(A.trace, ph, 3);
     }
 
-    // ---- retrieval (solve.cpp:180-223): X_i = A_i^-1 (F_i - B_i xi - C_i eta)
+    // ---- retrieval (solve.cpp:180-223): X_i = A_i^-1 (F_i - B^_i xi - C^_i eta)
     for (int i = gw; i < p; i += nwarps) {
         const PartDev P = A.parts[i];
         const int m = P.m;
         const bool first = i == 0, last = i == p - 1;
+        if (staged != i) {
+            sv_stage_factor(A, P, w, Fs, lane);
+            staged = i;
+        }
+        stage_rhs(P);
+        // boundary rows: physical rows [m-k, m) -= B^ x_top(i+1), [0, k) -= C^ x_bot(i-1)
         const double* bh = A.pool + A.off_bhat + i * kk;
         const double* ch = A.pool + A.off_chat + i * kk;
-        auto phys = [&](int r) -> int { return P.rev ? m - 1 - r : r; };
-        auto load = [&](int r, int c) -> double {
-            const int pr = phys(r);
-            if (c >= nr) return 0.0;
-            double v = A.F[(long long)c * A.ldf + P.r0 + pr];
-            if (!last && pr >= m - k) {  // - bhat_i x_top(i+1)
-                const int rr = pr - (m - k);
-                for (int t = 0; t < k; ++t) v = fma(-bh[(long long)t * k + rr], Tin[(long long)c * H + 2LL * (i + 1) * k + t], v);
+        for (int e = lane; e < 2 * k * NR; e += 32) {
+            const int side = e / (k * NR), q = e - side * k * NR, rr = q / NR, c = q - rr * NR;
+            const bool on = c < nr && (side == 0 ? !last : !first);
+            const double* M = side == 0 ? bh : ch;
+            const double* Tv = A.T + (long long)c * H + (side == 0 ? 2LL * (i + 1) * k : (2LL * i - 1) * k);
+            double mv[16], tv[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                mv[t] = (on && t < k) ? M[(long long)t * k + rr] : 0.0;
+                tv[t] = (on && t < k) ? Tv[t] : 0.0;
             }
-            if (!first && pr < k) {  // - chat_i x_bot(i-1)
-                for (int t = 0; t < k; ++t) v = fma(-ch[(long long)t * k + pr], Tin[(long long)c * H + (2LL * i - 1) * k + t], v);
-            }
-            return v;
-        };
-        sk_fwd_bwd<NR>(P, A.fac, Xs, lane, 0, load,
-                       [&](int j, int c, double v) {
-                           if (c < nr) A.X[(long long)c * A.ldx + P.r0 + phys(j)] = v;
-                       });
+            double v = 0.0;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v = fma(mv[t], tv[t], v);
+            const int pr = side == 0 ? m - k + rr : rr;
+            const int lr = P.rev ? m - 1 - pr : pr;
+            if (c < nr) w.Ys[lr * NR + c] -= v;
+        }
+        __syncwarp();
+        sv_sweeps<NR>(P, Fs, w.dv, w.Ys, lane, 0, [&](int j, int c, double v) {
+            if (c < nr) A.X[(long long)c * A.ldx + P.r0 + (P.rev ? m - 1 - j : j)] = v;
+        });
     }
 }
 
 template <int NR>
 static void launch_solve_t(const SkSolveArgs& A, cudaStream_t s) {
-    const size_t smem = sizeof(double) * kSkSvWarps * (size_t)A.mmax * 8;
+    const size_t smem = sizeof(double) * (kSvWarps * (size_t)sv_warp_smem(A.mmax, A.rmax, NR) + 2 * 16 * NR);
     set_smem_attr((const void*)k_sk_solve<NR>, (int)smem);
-    const int grid = sk_coop_grid((const void*)k_sk_solve<NR>, 32 * kSkSvWarps, smem);
     SkSolveArgs a = A;
     void* args[] = {&a};
-    (void)cudaLaunchCooperativeKernel((const void*)k_sk_solve<NR>, grid, 32 * kSkSvWarps, args, smem, s);
+    (void)cudaLaunchCooperativeKernel((const void*)k_sk_solve<NR>, device_sms(), kSvThreads, args, smem, s);
     count_launch();  // reports a failed launch
+}
+
+size_t sk_solve_smem(int mmax, int rmax, int nrhs) {
+    const int nr = nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <= 4 ? 4 : 8;
+    return sizeof(double) * (kSvWarps * (size_t)sv_warp_smem(mmax, rmax, nr) + 2 * 16 * nr);
 }
 
 void launch_sk_solve(const SkSolveArgs& A, cudaStream_t s) {
