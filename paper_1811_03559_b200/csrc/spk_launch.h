@@ -171,7 +171,7 @@ struct SkLevel {
     int pair0, npairs;     // pairs of the level (global indices)
     int carry, carry_next; // carried odd unit (global index on this / the next level), -1: none
 };
-constexpr int kSkChunk = 512;  // merged-unit rows per work item
+constexpr int kSkChunk = 128;  // merged-unit rows per work item
 struct SkPartsArgs {
     const double* band;
     long long n;

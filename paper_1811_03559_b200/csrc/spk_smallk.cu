@@ -104,6 +104,17 @@ __device__ __forceinline__ void wgemm_sub(const double* Am, const double* Bm, co
     for (int c = 0; c < 8; ++c) C[e + c] = (Cin ? Cin[e + c] : 0.0) - acc[c];
 }
 
+__device__ __forceinline__ double rcp_nr(double x) {
+    // reciprocal: MUFU seed and two Newton steps (no IEEE-division slow path;
+    // pivots here are normal numbers)
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm, int lane) {
     const unsigned full = 0xffffffffu;
     const int k = A.k;
@@ -117,7 +128,7 @@ __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm
         const double* wl = A.pool + (hw ? pr.wl : 0);
         const double* vr = A.pool + (hv ? pr.vr : 0);
         for (int e = lane; e < 256; e += 32) {
-            const int r = e >> 4, c = e & 15, o = r * kLd + c;
+            const int r = e & 15, c = e >> 4, o = r * kLd + c;  // column-major walk: coalesced reads
             if (r < k && c < k) {
                 sk_cp8(B(B_WT) + o, wr + (long long)c * hR + r);
                 sk_cp8(B(B_VB) + o, vl + (long long)c * hL + hL - k + r);
@@ -202,7 +213,7 @@ __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm
         if (r == p) jr = j;
         double piv = __shfl_sync(full, a[j], p);  // aug[p][j]
         if (piv == 0.0) piv = boost;
-        const double inv = 1.0 / piv;
+        const double inv = rcp_nr(piv);
         const double g = colv * inv;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -313,16 +324,25 @@ __device__ void sk_rows_task(const SkLevelsArgs& A, const SkItem& I, double* zs)
     const bool hv = pr.nv >= 0, hw = pr.nw >= 0;
     // z blocks from the merged unit's middle rows: zs[0] z2v, [1] z2w, [2] z1v, [3] z1w (row-major ld 16)
     __syncthreads();
-    for (int e = tid; e < 4 * 256; e += blockDim.x) {
-        const int w = e >> 8, q = e & 255, rr = q >> 4, c = q & 15;
-        double v = 0.0;
-        if (rr < k && c < k) {
+    {
+        // every load of the thread in one batch (one memory round trip)
+        constexpr int kPer = 4 * 256 / kLvThreads;
+        double v[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int e = tid + i * kLvThreads;
+            const int w = e >> 8, q = e & 255, rr = q & 15, c = q >> 4;
             const int row = (w < 2 ? hL : hL - k) + rr;
             const bool isv = (w & 1) == 0;
-            if (isv && hv) v = A.pool[pr.nv + (long long)c * H + row];
-            if (!isv && hw) v = A.pool[pr.nw + (long long)c * H + row];
+            const long long off = isv ? pr.nv : pr.nw;
+            v[i] = (rr < k && c < k && off >= 0) ? A.pool[off + (long long)c * H + row] : 0.0;
         }
-        zs[e] = v;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int e = tid + i * kLvThreads;
+            const int w = e >> 8, q = e & 255;
+            zs[w * 256 + (q & 15) * 16 + (q >> 4)] = v[i];
+        }
     }
     __syncthreads();
     for (int rr = I.row0 + tid; rr < H && rr < I.row0 + kSkChunk; rr += blockDim.x) {
@@ -331,19 +351,23 @@ __device__ void sk_rows_task(const SkLevelsArgs& A, const SkItem& I, double* zs)
         if (!left && !right) continue;
         const double* M = A.pool + (left ? pr.vl : pr.wr);
         const int hm = left ? hL : hR, ro = left ? rr : rr - hL;
-        double mrow[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) mrow[q] = q < k ? M[(long long)q * hm + ro] : 0.0;
         // merged V: left rows -vl z2v, right rows vr - wr z1v; merged W: left
-        // rows wl - vl z2w, right rows -wr z1w
+        // rows wl - vl z2w, right rows -wr z1w.  All loads first.
+        const long long bo = left ? (hw ? pr.wl : -1) : (hv ? pr.vr : -1);
+        double mrow[16], base[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            mrow[q] = q < k ? M[(long long)q * hm + ro] : 0.0;
+            base[q] = (q < k && bo >= 0) ? A.pool[bo + (long long)q * hm + ro] : 0.0;
+        }
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
             const bool isv = pass == 0;
             if (isv ? !hv : !hw) continue;
-            const long long bo = (isv && !left) ? pr.vr : (!isv && left) ? pr.wl : -1;
+            const bool hasb = isv ? !left : left;  // the pass that adds the base spike
             double acc[16];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) acc[c] = (c < k && bo >= 0) ? A.pool[bo + (long long)c * hm + ro] : 0.0;
+            for (int c = 0; c < 16; ++c) acc[c] = hasb ? base[c] : 0.0;
             const double* z = zs + ((left ? 0 : 2) + (isv ? 0 : 1)) * 256;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {

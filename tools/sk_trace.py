@@ -50,8 +50,3 @@ for name, base in (("factor levels", 0), ("solve", 65536)):
         end = (r[ok, 3].max() - t0) / 1e3 if (r[ok, 3] > 0).any() else float("nan")
         print(f"  phase {ph:2d}: start {st:7.2f} us  taskA max {ta:6.2f}  taskB max {tb:6.2f}  barrier out {end:7.2f}")
 
-d = t[60000:60000 + 16 * 16].reshape(16, 16)
-print("task A stamps (CTA 0 group 0), us from its start:")
-for ph in range(16):
-    if d[ph, 0] > 0:
-        print("  phase", ph, " ".join(f"{(x - d[ph, 0]) / 1e3:6.2f}" for x in d[ph, :7]))
