@@ -303,9 +303,10 @@ def profile_roofline(spk, cfg, steps, ms):
 
 
 def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
-    """N > 1: one global system of N*n rows (weak scaling: n rows per GPU),
-    each GPU factoring its slab (paper_1811_03559_b200/distributed.py); the
-    only collectives are the tip all-gathers of the slab-level reduced system."""
+    """N > 1 (or --slabs): the configuration's system sharded into N slabs
+    (strong scaling; --weak: N*n rows), each GPU factoring its slab through the
+    C++ data plane (csrc/spk_dist.cu); the only collectives are the library's
+    NCCL all-gathers of the slab-level reduced system's tip blocks."""
     from paper_1811_03559_b200 import distributed as D
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
@@ -329,12 +330,16 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
     spk.spike._check(lib.spk_generate_rhs_rows(SEED_A + 1, r0, n, nrhs, F.data_ptr(), n, sptr))
     plan = spk.gpu_plan(n, k, k, nrhs, cfg["piv"], args.p)
     opts = spk.FactorOptions(pivoting=cfg["piv"])
+    # the C++ data plane (csrc/spk_dist.cu): the library's own NCCL
+    # communicator (unique id broadcast over the process group); it issues the
+    # tip all-gathers itself on this stream
+    plane = D.NcclPlane()
 
     def run_step(band_t, F_t, X_t, XT_t):
-        df = D.factorize_distributed(band_t.data_ptr(), n, k, k, plan, opts)
-        D.solve_distributed(df, F_t.data_ptr(), n, nrhs, X_t.data_ptr(), n, False)
+        df = plane.factorize(band_t.data_ptr(), n, k, k, plan, opts, sptr)
+        plane.solve(df, F_t.data_ptr(), n, nrhs, X_t.data_ptr(), n, False, sptr)
         if cfg["transpose"]:
-            D.solve_distributed(df, F_t.data_ptr(), n, nrhs, XT_t.data_ptr(), n, True)
+            plane.solve(df, F_t.data_ptr(), n, nrhs, XT_t.data_ptr(), n, True, sptr)
 
     def step():
         run_step(band, F, X, XT)
@@ -433,7 +438,8 @@ def impl_ours_slabs(args, cfg, spk, torch, dist, rank, world, dev):
                 "config": {"workload": cfg["desc"] + (f"; weak scaling: one global system of {world} x n rows"
                                                       if args.weak else f"; strong scaling over {world} GPUs"),
                            "n": n_glob, "n_per_gpu": n_loc, "kl": k, "ku": k, "nrhs": nrhs,
-                           "partitions_per_gpu": plan.p, "parallelism": f"slabs{world} (NCCL tip all-gathers)",
+                           "partitions_per_gpu": plan.p,
+                           "parallelism": f"slabs{world} (NCCL tip all-gathers issued by the C++ data plane)",
                            "l2": "inputs larger than L2"},
                 "useful_gflops": round(useful / (ms * 1e-3) / 1e9, 3),
                 "backward_error": berr,

@@ -269,6 +269,12 @@ spk_status spk_spkb_store(const char *path, const double *band, int64_t n, int32
 spk_status spk_reduced_create(const double *vt, const double *vb, const double *wt,
                               const double *wb, int32_t p, int32_t k, double boost_eps,
                               spk_reduced **out);
+/* The same from device tips: d_tips holds p units of [vt; vb; wt; wb] (4 k x k
+ * column-major blocks each, the layout spk_fact_unit_tips writes, e.g. an
+ * all-gather of the slabs' unit tips); assembled and factored on `stream`,
+ * no host copy of the tips. */
+spk_status spk_reduced_create_device(const double *d_tips, int32_t p, int32_t k, double boost_eps,
+                                     void *stream, spk_reduced **out);
 spk_status spk_reduced_solve(const spk_reduced *r, int32_t transpose, double *z /* host 2pk x ncols */,
                              int32_t ncols, int64_t *couplings);
 /* Same on a device block (2pk x ncols, ld 2pk), ordered on stream. */
@@ -331,6 +337,48 @@ void spk_profile_enable(int32_t on);
 int32_t spk_profile_classes(void);
 const char *spk_profile_read(int32_t cls, double *ms, double *flops, double *bytes, int64_t *launches);
 void spk_profile_reset(void);
+
+/* ---- multi-GPU data plane (spk_dist.cu): one slab of rows per GPU, the
+ * reduced-system tip blocks exchanged by NCCL all-gathers; the slab-level
+ * reduced system (reduce_factorize, factorize.cpp:46-120, p = number of
+ * GPUs) assembled on every GPU from the gathered tips.  No reference
+ * counterpart: the reference is single-node (parallel_util.hpp:13-45).
+ * NCCL is loaded at run time (libnccl.so.2; SPK_NCCL_LIB overrides); its
+ * absence or a collective failure is SPK_ENCCL. */
+typedef struct spk_comm spk_comm;
+typedef struct spk_dist spk_dist;
+#define SPK_COMM_ID_BYTES 128
+/* rank 0 creates the id and shares it (any side channel), then every rank
+ * initialises; or wrap an existing ncclComm_t (not owned) */
+spk_status spk_comm_unique_id(uint8_t *id /* SPK_COMM_ID_BYTES */);
+spk_status spk_comm_init(const uint8_t *id, int32_t nranks, int32_t rank, spk_comm **out);
+spk_status spk_comm_wrap(void *nccl_comm, int32_t nranks, int32_t rank, spk_comm **out);
+void spk_comm_destroy(spk_comm *c);
+/* Collective: this rank's slab (d_band: packed columns with k halo columns per
+ * open edge, as spk_factorize_slab; edges open toward rank-1 / rank+1) is
+ * factored, the unit tips all-gathered, the slab-level system factored. */
+spk_status spk_dist_factorize(const double *d_band, int64_t n_local, int32_t kl, int32_t ku,
+                              const spk_plan *plan, const spk_factor_options *opts, spk_comm *comm,
+                              void *stream, spk_dist **out);
+/* Collective: this rank's rows of X := A^-1 F (transpose: A^-T F), device
+ * buffers; one (forward) or two (transpose) all-gathers of tip blocks. */
+spk_status spk_dist_solve(const spk_dist *d, int32_t transpose, const double *d_F, int64_t ldf,
+                          int32_t nrhs, double *d_X, int64_t ldx, void *stream);
+const spk_fact *spk_dist_slab(const spk_dist *d);
+void spk_dist_destroy(spk_dist *d);
+const char *spk_dist_last_error(void);
+/* The exchange arithmetic between the all-gathers (distributed.py's
+ * formulas), exported for virtual-rank tests: gathered blocks of G ranks ->
+ * the slab-level right-hand side / this rank's import. */
+enum {
+    SPK_XCH_FWD_TOP_RHS = 0, /* (G, nrhs, 2k) -> z (2Gk x nrhs)                        */
+    SPK_XCH_FWD_IMPORT = 1,  /* z -> [x_top(rank+1); x_bot(rank-1)] (2k x nrhs)        */
+    SPK_XCH_TR_IMPORT1 = 2,  /* (G, nrhs, 2, k) -> [bhat^T tau_b(rank-1); chat^T tau_t(rank+1)] */
+    SPK_XCH_TR_TOP_RHS = 3,  /* (G, nrhs, 4, k) -> t - C^T t_int (2Gk x nrhs)          */
+    SPK_XCH_TR_IMPORT2 = 4   /* z -> this rank's [z_top; z_bot] (2k x nrhs)            */
+};
+spk_status spk_dist_exchange(int32_t op, const double *d_src, double *d_dst, int32_t G, int32_t rank,
+                             int32_t k, int32_t nrhs, void *stream);
 
 #ifdef __cplusplus
 }

@@ -52,7 +52,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if errs:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     if force or cmds or _needs(LIB, objs):
-        link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
+        link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-ldl"]
         subprocess.run(link, check=True)
     return LIB
 

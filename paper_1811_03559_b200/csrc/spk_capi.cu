@@ -3215,13 +3215,17 @@ spk_status spk_xsolve_step(spk_xsolve* x, const double* d_import, double* d_expo
 
 void spk_xsolve_end(spk_xsolve* x) { delete x; }
 
-spk_status spk_reduced_create(const double* vt, const double* vb, const double* wt, const double* wb, int32_t p,
-                              int32_t k, double boost_eps, spk_reduced** out) {
+// The slab-level (or any) reduced system from its units' tips.  load(l0,
+// pool) writes each unit's [vt; vb] / [wt; wb] (2k x k, column-major) at
+// l0.voff / l0.woff; everything else runs on stream s.
+}  // extern "C"
+template <class Load>
+static spk_status reduced_create_impl(int32_t p, int32_t k, double boost_eps, cudaStream_t s, spk_reduced** out,
+                                      Load load) {
     return guarded([&] {
         if (!out) fail(SPK_EINVAL, "reduce_factorize: null output");
         *out = nullptr;
         if (p < 1 || k < 0) fail(SPK_EINVAL, "reduce_factorize: bad shape");
-        if (p > 1 && k > 0 && (!vt || !vb || !wt || !wb)) fail(SPK_EINVAL, "reduce_factorize: null tips");
         auto r = std::make_unique<spk_reduced>();
         r->f = std::make_unique<spk_fact>();
         spk_fact& f = *r->f;
@@ -3232,32 +3236,10 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
         f.p = p;
         f.boost_eps = boost_eps > 0 ? boost_eps : std::sqrt(DBL_EPSILON);
         f.bounds.assign(p + 1, 0);
-        cudaStream_t s = nullptr;
+        f.stream = s;
         setup_fact(f, s);
         if (p > 1 && k > 0) {
-            const long long kk = (long long)k * k;
-            const Level& l0 = f.levels[0];
-            std::vector<double> col(2 * kk);
-            for (int i = 0; i < p; ++i) {
-                if (l0.voff[i] >= 0) {
-                    for (int c = 0; c < k; ++c)
-                        for (int q = 0; q < k; ++q) {
-                            col[(size_t)c * 2 * k + q] = vt[i * kk + (size_t)c * k + q];
-                            col[(size_t)c * 2 * k + k + q] = vb[i * kk + (size_t)c * k + q];
-                        }
-                    ck(cudaMemcpy(f.d_pool + l0.voff[i], col.data(), sizeof(double) * 2 * kk, cudaMemcpyHostToDevice),
-                       "tips");
-                }
-                if (l0.woff[i] >= 0) {
-                    for (int c = 0; c < k; ++c)
-                        for (int q = 0; q < k; ++q) {
-                            col[(size_t)c * 2 * k + q] = wt[i * kk + (size_t)c * k + q];
-                            col[(size_t)c * 2 * k + k + q] = wb[i * kk + (size_t)c * k + q];
-                        }
-                    ck(cudaMemcpy(f.d_pool + l0.woff[i], col.data(), sizeof(double) * 2 * kk, cudaMemcpyHostToDevice),
-                       "tips");
-                }
-            }
+            load(f.levels[0], f.d_pool);
             double* auxf = dalloc<double>((size_t)f.auxf_rows * k, s);
             Bufs B = make_bufs(&f);
             B.p[B_POOL] = f.d_pool;
@@ -3270,6 +3252,58 @@ spk_status spk_reduced_create(const double* vt, const double* vb, const double* 
         }
         finish_factor(f, s);
         *out = r.release();
+    });
+}
+extern "C" {
+
+spk_status spk_reduced_create(const double* vt, const double* vb, const double* wt, const double* wb, int32_t p,
+                              int32_t k, double boost_eps, spk_reduced** out) {
+    if (p > 1 && k > 0 && (!vt || !vb || !wt || !wb)) {
+        if (out) *out = nullptr;
+        return guarded([] { fail(SPK_EINVAL, "reduce_factorize: null tips"); });
+    }
+    const long long kk = (long long)k * k;
+    return reduced_create_impl(p, k, boost_eps, nullptr, out, [&](const Level& l0, double* pool) {
+        std::vector<double> col(2 * kk);
+        auto put = [&](long long off, const double* top, const double* bot) {
+            for (int c = 0; c < k; ++c)
+                for (int q = 0; q < k; ++q) {
+                    col[(size_t)c * 2 * k + q] = top[(size_t)c * k + q];
+                    col[(size_t)c * 2 * k + k + q] = bot[(size_t)c * k + q];
+                }
+            ck(cudaMemcpy(pool + off, col.data(), sizeof(double) * 2 * kk, cudaMemcpyHostToDevice), "tips");
+        };
+        for (int i = 0; i < p; ++i) {
+            if (l0.voff[i] >= 0) put(l0.voff[i], vt + i * kk, vb + i * kk);
+            if (l0.woff[i] >= 0) put(l0.woff[i], wt + i * kk, wb + i * kk);
+        }
+    });
+}
+
+spk_status spk_reduced_create_device(const double* d_tips, int32_t p, int32_t k, double boost_eps, void* stream,
+                                     spk_reduced** out) {
+    if (p > 1 && k > 0 && !d_tips) {
+        if (out) *out = nullptr;
+        return guarded([] { fail(SPK_EINVAL, "reduce_factorize: null tips"); });
+    }
+    const long long kk = (long long)k * k;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return reduced_create_impl(p, k, boost_eps, s, out, [&](const Level& l0, double* pool) {
+        // unit i's tips [vt; vb; wt; wb] at d_tips + 4 i k^2: columns of vt and vb
+        // interleave into the 2k x k unit spike (two strided copies each)
+        auto put = [&](long long off, const double* top, const double* bot) {
+            ck(cudaMemcpy2DAsync(pool + off, sizeof(double) * 2 * k, top, sizeof(double) * k, sizeof(double) * k, k,
+                                 cudaMemcpyDeviceToDevice, s),
+               "tips");
+            ck(cudaMemcpy2DAsync(pool + off + k, sizeof(double) * 2 * k, bot, sizeof(double) * k, sizeof(double) * k,
+                                 k, cudaMemcpyDeviceToDevice, s),
+               "tips");
+        };
+        for (int i = 0; i < p; ++i) {
+            const double* t = d_tips + 4 * i * kk;
+            if (l0.voff[i] >= 0) put(l0.voff[i], t, t + kk);
+            if (l0.woff[i] >= 0) put(l0.woff[i], t + 2 * kk, t + 3 * kk);
+        }
     });
 }
 

@@ -1,5 +1,13 @@
 """Multi-GPU SPIKE: one slab of rows per GPU, two-level reduced system.
 
+The production data plane is C++ (paper_1811_03559_b200/csrc/spk_dist.cu:
+spk_comm_* / spk_dist_factorize / spk_dist_solve, NCCL all-gathers issued by
+the library on the caller's stream); :class:`NcclPlane` below wires it to a
+torch.distributed process group (the NCCL unique id travels over the group).
+The generator protocol in this module is the same algorithm written over
+torch tensors: the CPU (gloo) tests and the one-GPU virtual-rank tests run it,
+and the GPU tests check the C++ exchange arithmetic against it.
+
 SURVEY.md section 8(e).  The reference has no multi-GPU path (it is a
 single-node fork-join library, ``proj/include/spike/parallel_util.hpp:13-45``);
 this module extends its algorithm along the line the paper's recursive
@@ -244,11 +252,11 @@ class CudaSlab:
         return tips
 
     def top_create(self, gathered: torch.Tensor, boost_eps: float) -> _Top:
-        vt, vb, wt, wb = gather_tips_host(gathered, self.k)
+        # the gathered (G, 4k^2) tips stay in HBM: assembled and factored on the device
+        g = gathered.contiguous()
         h = C.c_void_p()
-        dp = _spk._dp
-        _check(lib().spk_reduced_create(vt.ctypes.data_as(dp), vb.ctypes.data_as(dp), wt.ctypes.data_as(dp),
-                                        wb.ctypes.data_as(dp), self.world, self.k, boost_eps, C.byref(h)))
+        _check(lib().spk_reduced_create_device(C.c_void_p(g.data_ptr()), self.world, self.k, boost_eps,
+                                               C.c_void_p(self.stream), C.byref(h)))
         return _Top(h.value, self.world, self.k)
 
     def top_solve(self, top: _Top, transpose: bool, z: torch.Tensor) -> None:
@@ -309,3 +317,92 @@ def solve_distributed(df: DistributedFactorization, f_ptr: int, ldf: int, nrhs: 
         return
     df.slab.bind(f_ptr, ldf, nrhs, x_ptr, ldx)
     collective(solve_steps(df.slab, df.top, transpose), group)
+
+
+# ----------------------------------------------------------------------------
+# the C++ data plane (spk_dist.cu)
+def exchange_device(op: int, src: torch.Tensor, G: int, rank: int, k: int, nrhs: int, stream: int = 0) -> torch.Tensor:
+    """spk_dist_exchange: the library's exchange arithmetic (ops SPK_XCH_*),
+    returned as a flat device tensor."""
+    n_out = 2 * G * k * nrhs if op in (XCH_FWD_TOP_RHS, XCH_TR_TOP_RHS) else 2 * k * nrhs
+    dst = torch.empty(n_out, dtype=torch.float64, device=src.device)
+    _spk._dcheck(lib().spk_dist_exchange(op, C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), G, rank, k,
+                                         nrhs, C.c_void_p(stream)))
+    return dst
+
+
+XCH_FWD_TOP_RHS, XCH_FWD_IMPORT, XCH_TR_IMPORT1, XCH_TR_TOP_RHS, XCH_TR_IMPORT2 = range(5)
+
+
+class NcclPlane:
+    """One rank of the C++ multi-GPU data plane: an NCCL communicator owned by
+    the library (its unique id broadcast over the torch.distributed group),
+    slab factorizations and solves whose tip exchanges the library issues
+    itself on the caller's stream."""
+
+    ID_BYTES = 128
+
+    def __init__(self, group=None, rank: Optional[int] = None, world: Optional[int] = None):
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        uid = torch.zeros(self.ID_BYTES, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (C.c_uint8 * self.ID_BYTES)()
+            _spk._dcheck(lib().spk_comm_unique_id(buf))
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if self.world > 1:
+            dev_uid = uid.to("cuda") if dist.get_backend(group) == "nccl" else uid
+            dist.broadcast(dev_uid, 0, group=group)
+            uid = dev_uid.cpu()
+        raw = (C.c_uint8 * self.ID_BYTES)(*uid.tolist())
+        h = C.c_void_p()
+        _spk._dcheck(lib().spk_comm_init(raw, self.world, self.rank, C.byref(h)))
+        self.h = h.value
+
+    @classmethod
+    def single(cls):
+        """A one-rank plane (no process group): the data plane's G = 1 case."""
+        self = cls.__new__(cls)
+        self.rank, self.world = 0, 1
+        buf = (C.c_uint8 * cls.ID_BYTES)()
+        _spk._dcheck(lib().spk_comm_unique_id(buf))
+        h = C.c_void_p()
+        _spk._dcheck(lib().spk_comm_init(buf, 1, 0, C.byref(h)))
+        self.h = h.value
+        return self
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().spk_comm_destroy(C.c_void_p(self.h))
+        except Exception:
+            pass
+
+    def factorize(self, band_ptr: int, n_local: int, kl: int, ku: int, plan: PartitionPlan,
+                  opts: Optional[FactorOptions] = None, stream: int = 0) -> "DistFact":
+        opts = opts or FactorOptions()
+        st, keep = _plan_struct(plan)
+        o = _Opts(int(bool(opts.pivoting)), float(opts.boost_eps))
+        h = C.c_void_p()
+        _spk._dcheck(lib().spk_dist_factorize(C.c_void_p(band_ptr), n_local, kl, ku, C.byref(st), C.byref(o),
+                                              C.c_void_p(self.h), C.c_void_p(stream), C.byref(h)))
+        return DistFact(h.value, self)
+
+    def solve(self, df: "DistFact", f_ptr: int, ldf: int, nrhs: int, x_ptr: int, ldx: int,
+              transpose: bool = False, stream: int = 0) -> None:
+        _spk._dcheck(lib().spk_dist_solve(C.c_void_p(df.h), int(transpose), C.c_void_p(f_ptr), ldf, nrhs,
+                                          C.c_void_p(x_ptr), ldx, C.c_void_p(stream)))
+
+
+class DistFact:
+    def __init__(self, h, plane):
+        self.h, self.plane = h, plane
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().spk_dist_destroy(C.c_void_p(self.h))
+        except Exception:
+            pass

@@ -201,6 +201,25 @@ def lib():
         L.spk_xsolve_end.argtypes = [C.c_void_p]
         L.spk_xsolve_end.restype = None
         L.spk_reduced_solve_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
+        L.spk_reduced_create_device.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_void_p,
+                                                C.POINTER(C.c_void_p)]
+        # multi-GPU data plane (spk_dist.cu)
+        L.spk_comm_unique_id.argtypes = [C.c_void_p]
+        L.spk_comm_init.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        L.spk_comm_wrap.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        L.spk_comm_destroy.argtypes = [C.c_void_p]
+        L.spk_comm_destroy.restype = None
+        L.spk_dist_factorize.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_Plan),
+                                         C.POINTER(_Opts), C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.spk_dist_solve.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                     C.c_int64, C.c_void_p]
+        L.spk_dist_slab.argtypes = [C.c_void_p]
+        L.spk_dist_slab.restype = C.c_void_p
+        L.spk_dist_destroy.argtypes = [C.c_void_p]
+        L.spk_dist_destroy.restype = None
+        L.spk_dist_last_error.restype = C.c_char_p
+        L.spk_dist_exchange.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_void_p]
         L.spk_arena_cached.restype = C.c_int64
         L.spk_arena_trim.restype = None
         _lib = L
@@ -211,6 +230,12 @@ def _check(rc):
     if rc != 0:
         msg = lib().spk_last_error().decode()
         raise _STATUS.get(rc, SpikeError)(msg)
+
+
+def _dcheck(rc):
+    """Status of a multi-GPU data-plane call (spk_dist.cu keeps its own message)."""
+    if rc != 0:
+        raise _STATUS.get(rc, SpikeError)(lib().spk_dist_last_error().decode())
 
 
 def launch_count(reset=False) -> int:
