@@ -227,6 +227,29 @@ __global__ void __launch_bounds__(32 * NW, 1) k_schur_inverse(const CouplingJob*
             s_inv[buf] = 1.0 / bv;
         }
     };
+    // Column diagonal dominance (with a margin): partial pivoting then takes
+    // the diagonal at every step, so the owner of column j+1 publishes it --
+    // pivot j+1, no search -- right after the multipliers of step j are known,
+    // before its bulk update: the search and the update leave the chain.
+    bool dom_ok = true;
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+        const int c = w + NW * cb;
+        double off = 0.0, dg = 0.0;
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) {
+            const int r = lane + 32 * ra;
+            if (r == c) dg = fabs(a[ra][cb]);
+            else off += fabs(a[ra][cb]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            dg += __shfl_xor_sync(0xffffffffu, dg, o);
+        }
+        if (c < n && !(dg > 1.0001 * off)) dom_ok = false;
+    }
+    const bool dom = __syncthreads_and(dom_ok) != 0;
     if (w == 0) publish(0);
     for (int j = 0; j < n; ++j) {
         __syncthreads();
@@ -253,6 +276,23 @@ __global__ void __launch_bounds__(32 * NW, 1) k_schur_inverse(const CouplingJob*
         double f[RA];
 #pragma unroll
         for (int ra = 0; ra < RA; ++ra) f[ra] = s_col[buf][lane + 32 * ra];
+        if (dom && j + 1 < n && w == (j + 1) % NW) {
+            const int jb1 = (j + 1) / NW, nb = buf ^ 1;
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb)
+                if (cb == jb1) {
+                    const double u = s_row[w][cb];
+#pragma unroll
+                    for (int ra = 0; ra < RA; ++ra) {
+                        const double v = (ra == ia && lane == il) ? u : fma(-f[ra], u, a[ra][cb]);
+                        s_col[nb][lane + 32 * ra] = v;
+                        if (lane + 32 * ra == j + 1) {
+                            s_ip[nb] = j + 1;
+                            s_inv[nb] = 1.0 / v;
+                        }
+                    }
+                }
+        }
         // rank-1 elimination on every element (pivot row and column j are
         // rewritten below)
 #pragma unroll
@@ -275,7 +315,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_schur_inverse(const CouplingJob*
 #pragma unroll
                 for (int cb = 0; cb < CB; ++cb) a[ra][cb] = (w + NW * cb == j) ? inv : s_row[w][cb];
             }
-        if (j + 1 < n && w == (j + 1) % NW) publish(j + 1);
+        if (!dom && j + 1 < n && w == (j + 1) % NW) publish(j + 1);
     }
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += blockDim.x) s_q[s_perm[j]] = j;

@@ -392,9 +392,12 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_sk_levels(SkLevelsArgs A) {
     unsigned target = 0;
     for (int ph = 0; ph <= A.nlevels; ++ph) {
         sk_stamp(A.trace, ph, 0);
+        // task A on the first CTAs (a warp per pair), task B first on the CTAs
+        // that have no pair: the phase costs max(A, B), not A + B
+        const int ntask = ph < A.nlevels ? A.levels[ph].npairs + (A.levels[ph].carry >= 0 ? 1 : 0) : 0;
+        const int ctasA = min((int)gridDim.x, (ntask + kLvWarps - 1) / kLvWarps);
         if (ph < A.nlevels) {
             const SkLevel L = A.levels[ph];
-            const int ntask = L.npairs + (L.carry >= 0 ? 1 : 0);
             for (int a = blockIdx.x * kLvWarps + warp; a < ntask; a += nwarps) {
                 if (a < L.npairs) sk_pair_task(A, A.pairs[L.pair0 + a], wsm, lane);
                 else sk_carry_tips(A, L.carry, L.carry_next, lane);
@@ -405,8 +408,11 @@ __global__ void __launch_bounds__(kLvThreads, 1) k_sk_levels(SkLevelsArgs A) {
         sk_stamp(A.trace, ph, 1);
         if (ph >= 1) {
             const SkLevel L = A.levels[ph - 1];
-            for (int it = gridDim.x - 1 - blockIdx.x; it < L.nitems; it += gridDim.x)
-                sk_rows_task(A, A.items[L.item0 + it], lv_smem);
+            const int nb = (int)gridDim.x - ctasA;  // CTAs without a pair
+            const int b0 = nb > 0 ? (int)blockIdx.x - ctasA : (int)blockIdx.x;
+            if (b0 >= 0)
+                for (int it = b0; it < L.nitems; it += (nb > 0 ? nb : (int)gridDim.x))
+                    sk_rows_task(A, A.items[L.item0 + it], lv_smem);
         }
         sk_stamp(A.trace, ph, 2);
         if (ph < A.nlevels) grid_barrier(A.bar, target);

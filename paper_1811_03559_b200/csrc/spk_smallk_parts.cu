@@ -40,6 +40,9 @@ namespace {
 
 constexpr int kPitch = 34;  // staged row: 33 band positions + 1/u_ii
 constexpr int KS = 17;      // register window slots
+constexpr int kPad = 17;    // zero rows before and after a CTA's staged blocks: the sweeps read
+                            // window rows past a partition's ends without tests (neighbours'
+                            // rows or padding; only rows that are never used are touched)
 
 __device__ __forceinline__ double half_max(double v) {
 #pragma unroll
@@ -55,6 +58,7 @@ __device__ __forceinline__ int half_sum(int v) {
 }  // namespace
 
 size_t sk_parts_smem_per_part(int mmax) { return sizeof(double) * (size_t)mmax * kPitch; }
+size_t sk_parts_smem_pad() { return sizeof(double) * (size_t)2 * kPad * kPitch; }
 
 template <int NW>
 __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
@@ -63,7 +67,15 @@ __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
     const int warp = threadIdx.x >> 5;
     const int i = (blockIdx.x * NW + warp) * 2 + half;  // partition of this half-warp
     const bool live = i < A.p;
-    double* const S = sk_slab + (size_t)(warp * 2 + half) * A.mmax * kPitch;
+    double* const S = sk_slab + kPad * kPitch + (size_t)(warp * 2 + half) * A.mmax * kPitch;
+    {  // zero the CTA's pad rows (front and back)
+        double* pf = sk_slab;
+        double* pb = sk_slab + kPad * kPitch + (size_t)2 * NW * A.mmax * kPitch;
+        for (int e = threadIdx.x; e < kPad * kPitch; e += blockDim.x) {
+            pf[e] = 0.0;
+            pb[e] = 0.0;
+        }
+    }
 
     PartDev P{};
     if (live) P = A.parts[i];
@@ -143,23 +155,40 @@ __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
                     ++boosts;
                 }
                 R[t] = u;
-                double* row = S + j * kPitch + 16;
+                double* row = S + j * kPitch + 16;  // 16-byte aligned (pitch 34, offset 16)
 #pragma unroll
-                for (int c = 0; c < KS; ++c) row[c] = R[(t + c) % KS];
-                row[17] = 1.0 / u;
+                for (int c = 0; c < 16; c += 2)
+                    *reinterpret_cast<double2*>(row + c) = make_double2(R[(t + c) % KS], R[(t + c + 1) % KS]);
+                *reinterpret_cast<double2*>(row + 16) = make_double2(R[(t + 16) % KS], 1.0 / u);
                 // row j+16, columns j .. j+16 (untouched so far)
-                const bool nx = j + 16 < m;
                 const double* nrow = S + (j + 16) * kPitch;
+                if (j + 16 < m) {
 #pragma unroll
-                for (int c = 0; c < KS; ++c) R[(t + c) % KS] = nx ? nrow[c] : 0.0;
+                    for (int c = 0; c < 16; c += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(nrow + c);
+                        R[(t + c) % KS] = v.x;
+                        R[(t + c + 1) % KS] = v.y;
+                    }
+                    R[(t + 16) % KS] = nrow[16];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KS; ++c) R[c] = 0.0;
+                }
             }
             __syncwarp();
             if (act) {
                 const double* urow = S + j * kPitch + 16;
                 double uj[KS];
+                uj[1] = urow[1];
 #pragma unroll
-                for (int c = 1; c < KS; ++c) uj[c] = urow[c];
-                const double inv = urow[17];
+                for (int c = 2; c < 16; c += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(urow + c);
+                    uj[c] = v.x;
+                    uj[c + 1] = v.y;
+                }
+                const double2 tail = *reinterpret_cast<const double2*>(urow + 16);
+                uj[16] = tail.x;
+                const double inv = tail.y;
                 const int r = j + 1 + ((hl - j - 1) & 15);
                 const bool rv = r < m;
                 const double l = R[t] * inv;
@@ -204,59 +233,67 @@ __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
             }
     }
 
-    // ---- forward sweeps, lanes = spike columns (c = hl < k).  "V" registers:
-    //      the bottom-loaded spike (B^; the last partition: C^ reversed);
-    //      "W" registers: inner partitions' W (C^ at the top)
+    // ---- spike sweeps, lanes = spike columns (c = hl < k)
     const bool inner = !first && !last;
     const int c = hl;
     const bool cv = c < k;
     const int mk = m - k;
-    // register columns indexed at run time: a select over the 16 slots
-    auto pick = [&](const double* col, int rr) -> double {
-        double v = 0.0;
+    // V (first, inner: B^ in rows >= m-k; the last, reversed: C^ reversed):
+    // truncated forward sweep over the last k rows, row j in slot m-1-j
+    // (distance from the bottom) -- the backward sweep's own slot order.  It
+    // reads the L columns before the W sweep overwrites them.
+    double V[KS];
+    {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v = q == rr ? col[q] : v;
-        return v;
-    };
-    auto vrhs = [&](int r) -> double {  // r in [m-k, m)
-        return last ? pick(ch, m - 1 - r) : pick(bh, r - mk);
-    };
-    double V[KS], W[KS];
+        for (int u = 0; u < 16; ++u) {  // row m-1-u: B^ row k-1-u, or C^ row u (reversed)
+            const int rr = last ? u : k - 1 - u;
+            double v = 0.0;
+            if (cv && u < k) {
+                const int bb = last ? aku + k + rr - c : aku - k + rr - c;
+                const long long col = last ? r0 - k + c : r0 + m + c;
+                const bool ok = last ? (col >= 0) : (col < A.n);
+                if (ok && bb >= 0 && bb < ld) v = A.band[col * ld + bb];
+            }
+            V[u] = v;
+        }
+        V[16] = 0.0;
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-        V[s] = (cv && s < m && s >= mk) ? vrhs(s) : 0.0;
-        W[s] = (cv && inner && s < k) ? ch[s] : 0.0;
+        for (int u = 15; u >= 0; --u) {
+            if (u >= k) continue;
+            const int j = m - 1 - u;
+            const double x = V[u];
+#pragma unroll
+            for (int o = 1; o < 16; ++o)
+                if (u - o >= 0) V[u - o] = fma(-S[(j + o) * kPitch + 16 - o], x, V[u - o]);
+        }
     }
-    for (int j0 = 0; j0 < m; j0 += KS) {
+    // W (inner partitions: C^ in rows < k): full forward L sweep, row r in
+    // slot r mod 17; row j's result is stored over its dead L entries
+    // (positions 0..15 of staged row j) for the backward sweep
+    if (inner) {
+        double W[KS];
 #pragma unroll
-        for (int t = 0; t < KS; ++t) {
-            const int j = j0 + t;
-            if (j >= m) break;
-            double lv[KS];
+        for (int s2 = 0; s2 < KS; ++s2) W[s2] = (cv && s2 < k) ? ch[s2] : 0.0;
+        for (int j0 = 0; j0 < m; j0 += KS) {
 #pragma unroll
-            for (int o = 1; o < KS; ++o) lv[o] = j + o < m ? S[(j + o) * kPitch + 16 - o] : 0.0;
-            if (inner) {
+            for (int t = 0; t < KS; ++t) {
+                const int j = j0 + t;
+                if (j >= m) break;
+                double lv[KS];  // L(j+o, j); rows past m read a neighbour's rows or padding
+#pragma unroll
+                for (int o = 1; o < KS; ++o) lv[o] = S[(j + o) * kPitch + 16 - o];
                 const double x = W[t];
 #pragma unroll
                 for (int o = 1; o < KS; ++o) W[(t + o) % KS] = fma(-lv[o], x, W[(t + o) % KS]);
-            }
-            if (j >= mk) {
-                const double x = V[t];
-#pragma unroll
-                for (int o = 1; o < KS; ++o) V[(t + o) % KS] = fma(-lv[o], x, V[(t + o) % KS]);
-            }
-            __syncwarp();  // the L column of row j is read: its slots take W(j, :)
-            if (inner) S[j * kPitch + c] = W[t];
-            if (j + KS < m) {
-                const int r = j + KS;  // entering row
-                W[t] = 0.0;            // C^ rows are < k <= 16
-                V[t] = (cv && r >= mk) ? vrhs(r) : 0.0;
+                __syncwarp();  // the L column of row j is read: its slots take W(j, :)
+                S[j * kPitch + c] = x;
+                W[t] = 0.0;  // entering row j + 17: C^ rows are < k <= 16
             }
         }
+        __syncwarp();
     }
-    __syncwarp();
-
-    // ---- backward U sweep (rows m-1 .. je), tips out
+    // backward U sweep, rows m-1 .. je (inner: all rows, tips at both ends;
+    // first / last: the bottom k), row j in slot (m-1-j) mod 17
     const int je = inner ? 0 : mk;
     const SkUnit U0 = A.units[i];
     const long long twok = 2LL * k;
@@ -266,16 +303,19 @@ __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
     if (cv && last) {  // dead bottom rows of the last partition's W unit
         for (int r = 0; r < k; ++r) A.pool[U0.woff + c * twok + k + r] = 0.0;
     }
-    const int jb0 = ((m - 1) / KS) * KS;
-    for (int jb = jb0; jb >= 0; jb -= KS) {
+    double W[KS];
 #pragma unroll
-        for (int t = KS - 1; t >= 0; --t) {
-            const int j = jb + t;
-            if (j >= m) continue;
-            if (j < je) break;
-            double uv[KS];
+    for (int s2 = 0; s2 < KS; ++s2) W[s2] = inner ? S[(m - 1 - s2) * kPitch + c] : 0.0;  // (padding above row 0)
+    const int ns = m - je;  // backward steps
+    for (int s0 = 0; s0 < ns; s0 += KS) {
 #pragma unroll
-            for (int o = 1; o < KS; ++o) uv[o] = j - o >= 0 ? S[(j - o) * kPitch + 16 + o] : 0.0;
+        for (int t = 0; t < KS; ++t) {
+            const int sd = s0 + t;
+            if (sd >= ns) break;
+            const int j = m - 1 - sd;
+            double uv[KS];  // U(j-o, j); rows above 0 read a neighbour's rows or padding
+#pragma unroll
+            for (int o = 1; o < KS; ++o) uv[o] = S[(j - o) * kPitch + 16 + o];
             const double dv = S[j * kPitch + 33];
             const double xv = V[t] * dv;
             const double xw = W[t] * dv;
@@ -292,18 +332,17 @@ __global__ void __launch_bounds__(32 * NW) k_sk_parts(SkPartsArgs A) {
                     A.pool[U0.voff + c * twok + k + (j - mk)] = xv;
                 }
             }
-            // row j - o sits in slot (j - o) mod 17
+            // row j - o sits in slot (sd + o) mod 17
 #pragma unroll
-            for (int o = 1; o < KS; ++o) V[(t + KS - o) % KS] = fma(-uv[o], xv, V[(t + KS - o) % KS]);
+            for (int o = 1; o < KS; ++o) V[(t + o) % KS] = fma(-uv[o], xv, V[(t + o) % KS]);
             if (inner) {
 #pragma unroll
-                for (int o = 1; o < KS; ++o) W[(t + KS - o) % KS] = fma(-uv[o], xw, W[(t + KS - o) % KS]);
+                for (int o = 1; o < KS; ++o) W[(t + o) % KS] = fma(-uv[o], xw, W[(t + o) % KS]);
             }
-            // entering row j - 17 (its slot is row j's): W from its stored
-            // forward result; V is zero above m - k
-            const int r = j - KS;
+            // entering row j - 17 (its slot is row j's): V is zero above m - k;
+            // W from its stored forward result (padding above row 0)
             V[t] = 0.0;
-            W[t] = (inner && r >= 0) ? S[r * kPitch + c] : 0.0;
+            W[t] = inner ? S[(j - KS) * kPitch + c] : 0.0;
         }
     }
 }
@@ -319,12 +358,12 @@ static bool launch_parts_t(const SkPartsArgs& A, size_t smem, cudaStream_t s) {
 
 bool launch_sk_parts(const SkPartsArgs& A, cudaStream_t s) {
     if (A.akl > 16 || A.aku > 16) return false;
-    const size_t per = sk_parts_smem_per_part(A.mmax);
+    const size_t per = sk_parts_smem_per_part(A.mmax), pad = sk_parts_smem_pad();
     // as many warps per CTA as fit in 227 KB (one CTA per SM)
-    const int nw = (int)std::min<size_t>(4, (227u * 1024) / (2 * per));
-    if (nw >= 4) return launch_parts_t<4>(A, 8 * per, s);
-    if (nw >= 2) return launch_parts_t<2>(A, 4 * per, s);
-    if (nw >= 1) return launch_parts_t<1>(A, 2 * per, s);
+    const size_t cap = 227u * 1024;
+    if (8 * per + pad <= cap) return launch_parts_t<4>(A, 8 * per + pad, s);
+    if (4 * per + pad <= cap) return launch_parts_t<2>(A, 4 * per + pad, s);
+    if (2 * per + pad <= cap) return launch_parts_t<1>(A, 2 * per + pad, s);
     return false;
 }
 

@@ -311,10 +311,15 @@ __global__ void __launch_bounds__(kSvThreads, 1) k_sk_solve(SkSolveArgs A) {
             const SkLevel L = A.levels[ph];
             for (int a = gw; a < L.npairs; a += nwarps) sv_pair_task<NR>(A, A.pairs[L.pair0 + a], lane);
         }
-        if (ph >= 1) {
+        if (ph >= 1) {  // first on the CTAs without a pair of task A
+            const int npA = ph < A.nlevels ? A.levels[ph].npairs : 0;
+            const int ctasA = min((int)gridDim.x, (npA + kSvWarps - 1) / kSvWarps);
             const SkLevel L = A.levels[ph - 1];
-            for (int it = gridDim.x - 1 - blockIdx.x; it < L.nitems; it += gridDim.x)
-                sv_rows_task<NR>(A, A.items[L.item0 + it], zs);
+            const int nb = (int)gridDim.x - ctasA;
+            const int b0 = nb > 0 ? (int)blockIdx.x - ctasA : (int)blockIdx.x;
+            if (b0 >= 0)
+                for (int it = b0; it < L.nitems; it += (nb > 0 ? nb : (int)gridDim.x))
+                    sv_rows_task<NR>(A, A.items[L.item0 + it], zs);
         }
         sk_stamp(A.trace, ph, 2);
         grid_barrier(A.bar, target);
