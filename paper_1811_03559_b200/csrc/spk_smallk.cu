@@ -66,42 +66,60 @@ namespace spk {
 namespace {
 constexpr int kLvWarps = 4;
 constexpr int kLvThreads = 32 * kLvWarps;
-constexpr int kLd = 18;          // 16 x 16 blocks, row-major, ld 18 (16-byte rows, spread banks)
+constexpr int kLd = 20;          // 16 x 16 blocks, row-major, ld 20 (16-byte rows; a fragment's 8 rows hit all banks)
 constexpr int kBlk = 16 * kLd;
 enum { B_WT, B_VB, B_Y2, B_Y1, B_VLT, B_WLT, B_VRB, B_WRB, B_S, B_UW, B_SI, B_Z2V, B_Z2W, B_Z1V, B_Z1W, NBLK };
 constexpr int kWarpSmem = NBLK * kBlk;  // doubles per warp
 
-// lane (r = lane & 15, h = lane >> 4) owns row r, columns 8h .. 8h+7 of a block
-// acc = A[r, :] B[:, 8h .. 8h+7]
-__device__ __forceinline__ void wgemm(const double* Am, const double* Bm, double acc[8], int lane) {
-    const int r = lane & 15, h = lane >> 4;
-    double a[16];
+// 16 x 16 products on the FP64 tensor cores (mma.sync m8n8k4): 4 output
+// tiles, 4 k-steps; operand fragments are single 8-byte shared loads (row
+// pitch kLd = 20 spreads the 8 rows of a fragment over all banks).  Tile
+// t = 2 ti + tj holds rows 8ti + (lane>>2), columns 8tj + 2(lane&3) + {0,1}.
+__device__ __forceinline__ void sk_dmma(double d[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void dgemm16(const double* Am, const double* Bm, double d[4][2], int lane) {
+    const int g = lane >> 2, q = lane & 3;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const double2 v = *reinterpret_cast<const double2*>(Am + r * kLd + 2 * q);
-        a[2 * q] = v.x;
-        a[2 * q + 1] = v.y;
-    }
+    for (int t = 0; t < 4; ++t) d[t][0] = d[t][1] = 0.0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-        const double* b = Bm + t * kLd + 8 * h;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double2 v = *reinterpret_cast<const double2*>(b + 2 * q);
-            acc[2 * q] = fma(a[t], v.x, acc[2 * q]);
-            acc[2 * q + 1] = fma(a[t], v.y, acc[2 * q + 1]);
-        }
+    for (int kk = 0; kk < 4; ++kk) {
+        const double a0 = Am[g * kLd + 4 * kk + q], a1 = Am[(8 + g) * kLd + 4 * kk + q];
+        const double b0 = Bm[(4 * kk + q) * kLd + g], b1 = Bm[(4 * kk + q) * kLd + 8 + g];
+        sk_dmma(d[0], a0, b0);
+        sk_dmma(d[1], a0, b1);
+        sk_dmma(d[2], a1, b0);
+        sk_dmma(d[3], a1, b1);
     }
 }
-// C = (Cin or 0) - A B   (C may alias Cin, not A or B)
-__device__ __forceinline__ void wgemm_sub(const double* Am, const double* Bm, const double* Cin, double* C, int lane) {
-    double acc[8];
-    wgemm(Am, Bm, acc, lane);
-    const int e = (lane & 15) * kLd + 8 * (lane >> 4);
+// element e (0, 1) of tile t: block offset
+__device__ __forceinline__ int toff(int t, int lane) {
+    return (8 * (t >> 1) + (lane >> 2)) * kLd + 8 * (t & 1) + 2 * (lane & 3);
+}
+// C = sa * d + (base ? base : 0) into shared memory (C may alias base)
+__device__ __forceinline__ void tiles_put(double* C, const double d[4][2], double sa, const double* base, int lane) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) C[e + c] = (Cin ? Cin[e + c] : 0.0) - acc[c];
+    for (int t = 0; t < 4; ++t) {
+        const int o = toff(t, lane);
+        double2 v = make_double2(sa * d[t][0], sa * d[t][1]);
+        if (base) {
+            const double2 b = *reinterpret_cast<const double2*>(base + o);
+            v.x += b.x;
+            v.y += b.y;
+        }
+        *reinterpret_cast<double2*>(C + o) = v;
+    }
+}
+// a k x k block held in shared memory to rows [r0, r0 + k) of a spike
+// (column-major, ld h) in global memory
+__device__ __forceinline__ void blk_store(double* dst, long long h, int r0, const double* Bm, int k, int lane) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int e = lane + 32 * i, c = e >> 4, r = e & 15;  // rows fastest: coalesced
+        if (r < k && c < k) dst[(long long)c * h + r0 + r] = Bm[r * kLd + c];
+    }
 }
 
 __device__ __forceinline__ double rcp_nr(double x) {
@@ -158,12 +176,17 @@ __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm
     }
     // S = I - Wt Vb (padding: identity), UW = -Wt Y1
     {
-        double acc[8];
-        wgemm(B(B_WT), B(B_VB), acc, lane);
-        const int r = lane & 15, c0 = 8 * (lane >> 4);
+        double d[4][2], e[4][2];
+        dgemm16(B(B_WT), B(B_VB), d, lane);
+        dgemm16(B(B_WT), B(B_Y1), e, lane);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) B(B_S)[r * kLd + c0 + c] = (r == c0 + c ? 1.0 : 0.0) - acc[c];
-        wgemm_sub(B(B_WT), B(B_Y1), nullptr, B(B_UW), lane);
+        for (int t = 0; t < 4; ++t) {  // identity on the diagonal tiles
+            const int r = 8 * (t >> 1) + (lane >> 2), c0 = 8 * (t & 1) + 2 * (lane & 3);
+            d[t][0] = (r == c0 ? 1.0 : 0.0) - d[t][0];
+            d[t][1] = (r == c0 + 1 ? 1.0 : 0.0) - d[t][1];
+        }
+        tiles_put(B(B_S), d, 1.0, nullptr, lane);
+        tiles_put(B(B_UW), e, -1.0, nullptr, lane);
     }
     __syncwarp();
     // column diagonal dominance of S (then partial pivoting takes the diagonal)
@@ -180,7 +203,11 @@ __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm
     const int r = lane & 15, h = lane >> 4;
     double a[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) a[c] = h == 0 ? B(B_S)[r * kLd + c] : (r == c ? 1.0 : 0.0);
+    for (int c = 0; c < 16; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(B(B_S) + r * kLd + c);
+        a[c] = h == 0 ? v.x : (r == c ? 1.0 : 0.0);
+        a[c + 1] = h == 0 ? v.y : (r == c + 1 ? 1.0 : 0.0);
+    }
     unsigned used = 0u;
     int jr = r;  // S^-1 row held by this lane's I-part: the step whose pivot row is r
     double boost = 0.0;  // an exactly singular S: zero pivots boosted (kernels.cpp:104-109 rule)
@@ -221,73 +248,66 @@ __device__ void sk_pair_task(const SkLevelsArgs& A, const SkPair& pr, double* sm
             a[c] = r == p ? pv * inv : fma(-g, pv, a[c]);
         }
     }
+    // S^-1 row jr = this lane's I part (h = 1): shared memory and the pool
     if (h == 1) {
+        double* d = B(B_SI) + jr * kLd;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) B(B_SI)[jr * kLd + c] = a[c];
-    }
-    __syncwarp();
-    for (int e = lane; e < k * k; e += 32) {
-        const int c = e / k, rr = e - c * k;
-        A.pool[pr.sinv + e] = B(B_SI)[rr * kLd + c];
+        for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(d + c) = make_double2(a[c], a[c + 1]);
+        if (jr < k) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < k) A.pool[pr.sinv + (long long)c * k + jr] = a[c];
+        }
     }
     if (lane == 0) A.flags[pr.gidx] = 1;
-    // z2v = S^-1 y2, z2w = S^-1 (-Wt y1)
-    wgemm_sub(B(B_SI), B(B_Y2), nullptr, B(B_Z2V), lane);  // = -S^-1 y2
-    wgemm_sub(B(B_SI), B(B_UW), nullptr, B(B_Z2W), lane);  // = S^-1 Wt y1
     __syncwarp();
-    // (signs: Z2V, Z2W hold -z2v, -z2w)  z1v = -Vb z2v, z1w = y1 - Vb z2w;
-    // top tips vt' = -vl_top z2v, wt' = wl_top - vl_top z2w
+    // z2v = S^-1 y2, z2w = S^-1 (-Wt y1): rows [hL, hL+k) of the merged unit
     {
-        double p1[8], p2[8], p3[8], p4[8];
-        wgemm(B(B_VB), B(B_Z2V), p1, lane);
-        wgemm(B(B_VB), B(B_Z2W), p2, lane);
-        wgemm(B(B_VLT), B(B_Z2V), p3, lane);
-        wgemm(B(B_VLT), B(B_Z2W), p4, lane);
-        const int e = (lane & 15) * kLd + 8 * (lane >> 4);
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            B(B_Z1V)[e + c] = p1[c];
-            B(B_Z1W)[e + c] = B(B_Y1)[e + c] + p2[c];
-            B(B_VLT)[e + c] = p3[c];
-            B(B_WLT)[e + c] += p4[c];
-            B(B_Z2V)[e + c] = -B(B_Z2V)[e + c];
-            B(B_Z2W)[e + c] = -B(B_Z2W)[e + c];
-        }
+        double d[4][2], e[4][2];
+        dgemm16(B(B_SI), B(B_Y2), d, lane);
+        dgemm16(B(B_SI), B(B_UW), e, lane);
+        tiles_put(B(B_Z2V), d, 1.0, nullptr, lane);
+        tiles_put(B(B_Z2W), e, 1.0, nullptr, lane);
     }
     __syncwarp();
-    // bottom tips: vb' = vr_bot - wr_bot z1v, wb' = -wr_bot z1w
+    // z1v = -Vb z2v, z1w = y1 - Vb z2w: rows [hL-k, hL); top tips
+    // vt' = -vl_top z2v, wt' = wl_top - vl_top z2w: rows [0, k)
     {
-        double p1[8], p2[8];
-        wgemm(B(B_WRB), B(B_Z1V), p1, lane);
-        wgemm(B(B_WRB), B(B_Z1W), p2, lane);
-        const int e = (lane & 15) * kLd + 8 * (lane >> 4);
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            B(B_VRB)[e + c] -= p1[c];
-            B(B_WRB)[e + c] = -p2[c];
-        }
+        double d[4][2], e[4][2], f[4][2], g4[4][2];
+        dgemm16(B(B_VB), B(B_Z2V), d, lane);
+        dgemm16(B(B_VB), B(B_Z2W), e, lane);
+        dgemm16(B(B_VLT), B(B_Z2V), f, lane);
+        dgemm16(B(B_VLT), B(B_Z2W), g4, lane);
+        __syncwarp();  // VLT / WLT are rewritten in place
+        tiles_put(B(B_Z1V), d, -1.0, nullptr, lane);
+        tiles_put(B(B_Z1W), e, -1.0, B(B_Y1), lane);
+        tiles_put(B(B_VLT), f, -1.0, nullptr, lane);
+        tiles_put(B(B_WLT), g4, -1.0, B(B_WLT), lane);
     }
     __syncwarp();
-    auto out = [&](int blk, long long off, int r0) {
-        double* dst = A.pool + off;
-        for (int e = lane; e < k * k; e += 32) {
-            const int c = e / k, rr = e - c * k;
-            dst[(long long)c * H + r0 + rr] = B(blk)[rr * kLd + c];
-        }
-    };
+    // bottom tips: vb' = vr_bot - wr_bot z1v, wb' = -wr_bot z1w: rows [H-k, H)
+    {
+        double d[4][2], e[4][2];
+        dgemm16(B(B_WRB), B(B_Z1V), d, lane);
+        dgemm16(B(B_WRB), B(B_Z1W), e, lane);
+        __syncwarp();  // WRB is rewritten in place
+        tiles_put(B(B_VRB), d, -1.0, B(B_VRB), lane);
+        tiles_put(B(B_WRB), e, -1.0, nullptr, lane);
+    }
+    __syncwarp();
     if (hv) {
-        out(B_VLT, pr.nv, 0);
-        out(B_Z1V, pr.nv, hL - k);
-        out(B_Z2V, pr.nv, hL);
-        out(B_VRB, pr.nv, H - k);
+        double* nv = A.pool + pr.nv;
+        blk_store(nv, H, 0, B(B_VLT), k, lane);
+        blk_store(nv, H, hL - k, B(B_Z1V), k, lane);
+        blk_store(nv, H, hL, B(B_Z2V), k, lane);
+        blk_store(nv, H, H - k, B(B_VRB), k, lane);
     }
     if (hw) {
-        out(B_WLT, pr.nw, 0);
-        out(B_Z1W, pr.nw, hL - k);
-        out(B_Z2W, pr.nw, hL);
-        out(B_WRB, pr.nw, H - k);
+        double* nw = A.pool + pr.nw;
+        blk_store(nw, H, 0, B(B_WLT), k, lane);
+        blk_store(nw, H, hL - k, B(B_Z1W), k, lane);
+        blk_store(nw, H, hL, B(B_Z2W), k, lane);
+        blk_store(nw, H, H - k, B(B_WRB), k, lane);
     }
 }
 
@@ -341,10 +361,51 @@ __device__ void sk_rows_task(const SkLevelsArgs& A, const SkItem& I, double* zs)
         for (int i = 0; i < kPer; ++i) {
             const int e = tid + i * kLvThreads;
             const int w = e >> 8, q = e & 255;
-            zs[w * 256 + (q & 15) * 16 + (q >> 4)] = v[i];
+            zs[w * kBlk + (q & 15) * kLd + (q >> 4)] = v[i];
         }
     }
     __syncthreads();
+    if (k == 16) {
+        // the FP64 tensor cores: 8-row tiles of the item, a warp per tile;
+        // D = base - M z as mma.sync with A = -M (fragments straight from the
+        // spike's columns), C = the base spike's rows, B = z from shared memory
+        const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+        for (int t = warp; t < kSkChunk / 8; t += kLvWarps) {
+            const int R0 = I.row0 + 8 * t;
+            if (R0 >= H) break;
+            const bool left = R0 >= k && R0 + 8 <= hL - k;
+            const bool right = R0 >= hL + k && R0 + 8 <= H - k;
+            if (!left && !right) continue;
+            const double* M = A.pool + (left ? pr.vl : pr.wr);
+            const int hm = left ? hL : hR, ro = (left ? R0 : R0 - hL) + g;
+            double am[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) am[kk] = -M[(long long)(4 * kk + q) * hm + ro];
+#pragma unroll
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool isv = pass == 0;
+                if (isv ? !hv : !hw) continue;
+                const long long bo = isv ? (left ? -1 : pr.vr) : (left ? pr.wl : -1);
+                const double* z = zs + ((left ? 0 : 2) + (isv ? 0 : 1)) * kBlk;
+                double d[2][2];
+#pragma unroll
+                for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        d[tj][e] = bo >= 0 ? A.pool[bo + (long long)(8 * tj + 2 * q + e) * hm + ro] : 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj) sk_dmma(d[tj], am[kk], z[(4 * kk + q) * kLd + 8 * tj + g]);
+                double* dst = A.pool + (isv ? pr.nv : pr.nw);
+#pragma unroll
+                for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) dst[(long long)(8 * tj + 2 * q + e) * H + R0 + g] = d[tj][e];
+            }
+        }
+        return;
+    }
     for (int rr = I.row0 + tid; rr < H && rr < I.row0 + kSkChunk; rr += blockDim.x) {
         const bool left = rr >= k && rr < hL - k;
         const bool right = rr >= hL + k && rr < H - k;
@@ -368,12 +429,12 @@ __device__ void sk_rows_task(const SkLevelsArgs& A, const SkItem& I, double* zs)
             double acc[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) acc[c] = hasb ? base[c] : 0.0;
-            const double* z = zs + ((left ? 0 : 2) + (isv ? 0 : 1)) * 256;
+            const double* z = zs + ((left ? 0 : 2) + (isv ? 0 : 1)) * kBlk;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 if (q >= k) break;
 #pragma unroll
-                for (int c = 0; c < 16; ++c) acc[c] = fma(-mrow[q], z[q * 16 + c], acc[c]);
+                for (int c = 0; c < 16; ++c) acc[c] = fma(-mrow[q], z[q * kLd + c], acc[c]);
             }
             double* dst = A.pool + (isv ? pr.nv : pr.nw);
 #pragma unroll
