@@ -300,7 +300,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) k_sk_solve(SkSolveArgs A) {
         }
     }
     unsigned target = 0;
-    sk_stamp(A.trace, 0, 1);  // D-stage done (this CTA)
     grid_barrier(A.bar, target);
 
     // ---- reduced solve, level by level (task A: level ph, task B: level ph-1)
@@ -311,6 +310,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) k_sk_solve(SkSolveArgs A) {
             const SkLevel L = A.levels[ph];
             for (int a = gw; a < L.npairs; a += nwarps) sv_pair_task<NR>(A, A.pairs[L.pair0 + a], lane);
         }
+        sk_stamp(A.trace, ph, 1);
         if (ph >= 1) {  // first on the CTAs without a pair of task A
             const int npA = ph < A.nlevels ? A.levels[ph].npairs : 0;
             const int ctasA = min((int)gridDim.x, (npA + kSvWarps - 1) / kSvWarps);
