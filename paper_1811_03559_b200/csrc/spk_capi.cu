@@ -504,6 +504,7 @@ struct spk_fact {
     // general programs' transposed sweeps read is made at their first use
     std::atomic<bool> tfac_ready{true};
     std::mutex tfac_mu;
+    bool want_tfac = false;  // the symbolic has seen transposed solves (setup_fact)
     std::shared_ptr<struct Symbolic> sym;  // cached geometry + programs (shared by equal factorizations)
     std::vector<long long> factor_sweeps;
     int boost_count = 0, boost_warnings = 0;
@@ -1594,10 +1595,17 @@ struct Exec {
                         const bool generic_only = generic_path();
                         const int kmax = std::max(f.kl, f.ku);
                         if (!f.piv_on && !generic_only && kmax <= 160) {
-                            FastLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac, f.d_tfac,
-                                         f.d_dinv, f.d_piv, f.boost_eps, f.d_boost};
+                            // the DMMA LU (k <= 160) writes the packed factor only; the
+                            // row-major copy is made when a transposed solve needs it
+                            // the DMMA LU (k <= 160) writes the row-major copy only
+                            // where transposed solves have been seen for this shape;
+                            // otherwise it is made on demand (ensure_tfac)
+                            const bool wt = kmax <= 16 || f.want_tfac;
+                            FastLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac,
+                                         wt ? f.d_tfac : nullptr, f.d_dinv, f.d_piv, f.boost_eps, f.d_boost};
                             if (launch_band_lu_fast((const int*)jobs, st.njobs, kmax, A, s)) {
                                 lu_fast_done = true;
+                                if (!wt) f.tfac_ready.store(false);
                                 break;
                             }
                         }
@@ -1723,6 +1731,9 @@ struct Symbolic {
     };
     std::mutex dev_mu;
     std::map<int, DevTables> dev;
+    // a transposed solve has run on a factorization of this shape: later
+    // ones write the row-major copy inside their LU (instead of on demand)
+    std::atomic<bool> want_tfac{false};
 };
 
 namespace {
@@ -1851,6 +1862,7 @@ void setup_fact(spk_fact& f, cudaStream_t s) {
         f.sk_nlevels = y.sk_nlevels;
         f.sk_mmax = y.sk_mmax;
         f.sk_rmax = y.sk_rmax;
+        f.want_tfac = y.want_tfac.load();
         tr.mark("symbolic (cached)");
         alloc_fact(f, s, y.blob);
         return;
@@ -2078,6 +2090,7 @@ void ensure_tfac(const spk_fact* fc) {
     launch_transpose_factors(f.d_parts, f.p, mx, f.d_fac, f.d_tfac, f.d_dinv, f.stream);
     mark_ready(f, f.stream);
     f.tfac_ready.store(true);
+    if (f.sym && !f.sk) f.sym->want_tfac.store(true);
 }
 
 // order work on s after the factorization (a no-op on its own stream)
@@ -2963,7 +2976,7 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     spk_fact& f = const_cast<spk_fact&>(*fc);
     const long long n = f.n;
     const bool sk_kernel = sk_kernel_solve(f, transpose, nrhs);
-    if (!sk_kernel) ensure_tfac(fc);
+    if (transpose) ensure_tfac(fc);  // only the transposed sweeps read the row-major copy
     wait_ready(f, s);
     auto x = std::make_unique<spk_xsolve>();
     x->f = &f;
@@ -3070,10 +3083,8 @@ void solve_host_pipelined(const spk_fact* fc, int32_t transpose, const double* F
     // are used, and fin_mu keeps a concurrent finish from swapping them while
     // this call enqueues
     spk_fact& fm = const_cast<spk_fact&>(*fc);
-    if (fm.sk) {
-        ensure_finished(fc);  // a small-k fallback replaces the hierarchy at the finish
-        ensure_tfac(fc);
-    }
+    if (fm.sk) ensure_finished(fc);  // (the small-k engine has no device-guarded programs)
+    if (transpose) ensure_tfac(fc);
     std::lock_guard<std::mutex> lk(fm.fin_mu);
     if (!fm.pending.load() && fm.fin_status != SPK_OK) fail(fm.fin_status, fm.fin_msg);
     CopyStreams& cs = copy_streams();

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
     const int gi = lane >> 2, q = lane & 3;  // accumulator fragment: row gi, columns 2q, 2q+1
     const int ald = A.akl + A.aku + 1;
     double* F = A.fac + P.fofs;
-    double* TF = A.tfac + P.tofs;
+    double* TF = A.tfac ? A.tfac + P.tofs : nullptr;
     const int nblk = (m + 7) / 8;
     const unsigned full = 0xffffffffu;
     // LU-space (i, c) -> input band: base + sg * (c * (ald - 1) + i) (UL: reversed)
@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
         const int c = idx / ku, off = idx - c * ku + 1;
         if (c < m && off > c) F[(long long)c * rows + d - off] = 0.0;
     }
-    for (int idx = threadIdx.x; idx < kl * kl; idx += blockDim.x) {
+    // the row-major copy is optional (null: the transposed sweeps' copy is
+    // made from the packed factor when a transposed solve first needs it)
+    const bool wt = A.tfac != nullptr;
+    for (int idx = threadIdx.x; idx < kl * kl && wt; idx += blockDim.x) {
         const int r = idx / kl, off = idx - r * kl + 1;
         if (r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
     }
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 const double* sD = sm + S::D + par * 64;
                 // L columns (packed column-major) and U rows (row-major copy): one
                 // contiguous run per warp
-                for (int sgm = orank; sgm < 16 && orank >= 0; sgm += NW - 1) {
+                for (int sgm = orank; sgm < (wt ? 16 : 8) && orank >= 0; sgm += NW - 1) {
                     const int qq = sgm & 7, c = j0 + qq;
                     if (c >= m) continue;
                     if (sgm < 8) {
@@ -525,7 +528,8 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 }
                 // L rows (row-major copy) and U columns (packed): runs of <= 8
                 // contiguous entries, 8 lanes per run (4 runs per warp store)
-                for (int e = orank * 32 + lane; e < tr_n * 8 && orank >= 0; e += 32 * (NW - 1)) {
+                for (int e = (wt ? 0 : (7 + kl) * 8) + orank * 32 + lane; e < tr_n * 8 && orank >= 0;
+                     e += 32 * (NW - 1)) {
                     const int t = e >> 3, qq = e & 7;
                     const bool lrun = t < 7 + kl;
                     const int x = lrun ? t + 1 : t - (7 + kl);  // rr (L row) or cc (U column)
