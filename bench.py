@@ -271,9 +271,13 @@ def profile_roofline(spk, cfg, steps, ms):
         if e.value:
             prof[name] = dict(ms=a.value / steps, flops=b.value / steps, bytes=d.value / steps,
                               launches=e.value // steps)
-    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", dict(ms=1, flops=0, bytes=0, launches=1))
-    peaks = measured_peaks()
     bound = cfg["bound"]
+    # the dominant class; for HBM-bound configurations the dominant class that
+    # moves algorithmic bytes (the small-k engine's level kernel moves k x k
+    # tips only and is reported in `classes`)
+    cand = {kk: v for kk, v in prof.items() if bound != "hbm" or v["bytes"] > 0} or prof
+    top = max(cand.items(), key=lambda kv: kv[1]["ms"]) if cand else ("none", dict(ms=1, flops=0, bytes=0, launches=1))
+    peaks = measured_peaks()
     tms = top[1]["ms"]
     if bound == "hbm":
         ach = top[1]["bytes"] / (tms * 1e-3) / 1e9
