@@ -2929,13 +2929,14 @@ struct spk_xsolve {
     cudaStream_t s = nullptr;
     double *S = nullptr, *T = nullptr, *AUX = nullptr, *tF = nullptr, *tX = nullptr;
     double *XCH = nullptr, *XIN = nullptr;
-    // small-k engine (k_sk_solve): grid-barrier words
+    // small-k engine (k_sk_solve): grid-barrier words + tree counters, z blocks
     bool sk = false;
     unsigned* bar = nullptr;
+    double* ZS = nullptr;
     Bufs B;
 
     ~spk_xsolve() {
-        for (double* q : {S, T, AUX, tF, tX, XCH, XIN})
+        for (double* q : {S, T, AUX, tF, tX, XCH, XIN, ZS})
             if (q) dfree(q, s);
         if (bar) dfree(bar, s);
     }
@@ -2950,7 +2951,7 @@ struct spk_xsolve {
                           reinterpret_cast<const SkPair*>(blob + f->sk_pairs),
                           reinterpret_cast<const SkItem*>(blob + f->sk_items),
                           reinterpret_cast<const SkLevel*>(blob + f->sk_levels), f->sk_nlevels, B.p[B_F], B.ld[B_F],
-                          B.p[B_X], B.ld[B_X], T, bar, f->sk_mmax, f->sk_rmax,
+                          B.p[B_X], B.ld[B_X], T, ZS, bar + 2, bar, f->sk_mmax, f->sk_rmax,
                           g_sk_trace ? g_sk_trace + 4096 * 16 : nullptr};
             ProfScope ps(ST_SWEEP, s, 8.0 * f->n * f->k * nrhs, 16.0 * f->n * (f->kl + f->ku + 1));
             launch_sk_solve(A, s);
@@ -3048,8 +3049,11 @@ std::unique_ptr<spk_xsolve> open_solve(const spk_fact* fc, int32_t transpose, co
     if (sk_kernel) {
         x->sk = true;
         const long long H = 2LL * f.p * f.k;
-        x->bar = static_cast<unsigned*>(arena().alloc(2 * sizeof(unsigned), s));
-        ck(cudaMemsetAsync(x->bar, 0, 2 * sizeof(unsigned), s), "memset");
+        // grid-barrier words, then the reduced-solve tree's per-pair counters
+        const size_t nw = 2 + (size_t)std::max(f.npairs, 1);
+        x->bar = static_cast<unsigned*>(arena().alloc(nw * sizeof(unsigned), s));
+        ck(cudaMemsetAsync(x->bar, 0, nw * sizeof(unsigned), s), "memset");
+        x->ZS = dalloc<double>((size_t)std::max(f.npairs, 1) * 32 * 8, s);
         B.ld[B_T] = H;
         B.p[B_T] = x->T;
     }

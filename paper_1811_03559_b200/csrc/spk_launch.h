@@ -215,6 +215,8 @@ struct SkSolveArgs {
     double* X;
     long long ldx;
     double* T;  // reduced right-hand sides (2pk x nrhs, ld 2pk), updated in place
+    double* ZS;     // per pair: z2 and z1 (2 x 16 x NR, row-major), for the deferred row updates
+    unsigned* cnt;  // per-pair arrival counters of the reduced-solve tree, zeroed
     unsigned* bar;
     int mmax, rmax;  // longest partition, largest packed column height
     unsigned long long* trace;  // debug: globaltimer per (phase, CTA, mark), or null

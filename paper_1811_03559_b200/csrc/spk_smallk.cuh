@@ -25,7 +25,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(bar, 1u);
-        while (ld_acquire_u32(bar) < target) __nanosleep(1000);
+        while (ld_acquire_u32(bar) < target) __nanosleep(32);
     }
     __syncthreads();
 }

@@ -137,7 +137,7 @@ __device__ __forceinline__ void sv_sweeps(const PartDev& P, const double* Fs, co
 
 // task A of the reduced solve: one warp per pair, lanes 0..15 = rows
 template <int NR>
-__device__ void sv_pair_task(const SkSolveArgs& A, const SkPair& pr, int lane) {
+__device__ void sv_pair_task(const SkSolveArgs& A, const SkPair& pr, int pg, int lane) {
     const unsigned full = 0xffffffffu;
     const int k = A.k, nr = A.nrhs;
     const long long H = 2LL * A.p * k;
@@ -192,9 +192,12 @@ __device__ void sv_pair_task(const SkSolveArgs& A, const SkPair& pr, int lane) {
     mv(Vt, z2, a);
     mv(Wb, z1, b);
     if (rv) {
+        double* zp = A.ZS + (long long)pg * 32 * NR;  // [z2 | z1], row t at t * NR
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
-            if (c >= nr) break;
+            zp[r * NR + c] = z2[c];
+            zp[16 * NR + r * NR + c] = z1[c];
+            if (c >= nr) continue;
             double* Tc = A.T + (long long)c * H + zb;
             Tc[hL - k + r] = z1[c];
             Tc[hL + r] = z2[c];
@@ -204,43 +207,73 @@ __device__ void sv_pair_task(const SkSolveArgs& A, const SkPair& pr, int lane) {
     }
 }
 
-// task B: rows [k, hL-k) -= vl z2, rows [hL+k, H-k) -= wr z1 of a merged unit
+// The tree of pair tasks as dataflow (no grid barrier per level): unit u of
+// level l complete -> arrive at the consuming pair's counter; the second
+// arrival runs that pair at once on the same warp.  Carried units pass through.
 template <int NR>
-__device__ void sv_rows_task(const SkSolveArgs& A, const SkItem& I, double* zs) {
-    if (I.pair < 0) return;  // carried unit: its rows stay
-    const int k = A.k, nr = A.nrhs, tid = threadIdx.x;
-    const long long H = 2LL * A.p * k;
-    const SkPair pr = A.pairs[I.pair];
-    const SkUnit uL = A.units[pr.left], uR = A.units[pr.left + 1];
-    const int hL = uL.uh, hR = uR.uh, Hu = hL + hR;
-    const long long zb = uL.uoff;
-    __syncthreads();
-    for (int e = tid; e < 2 * 16 * NR; e += blockDim.x) {  // zs[0]: z2 (16 x NR), zs[1]: z1
-        const int w = e / (16 * NR), q = e - w * 16 * NR, t = q / NR, c = q - t * NR;
-        zs[e] = (t < k && c < nr) ? A.T[(long long)c * H + zb + (w == 0 ? hL : hL - k) + t] : 0.0;
-    }
-    __syncthreads();
-    for (int rr = I.row0 + tid; rr < Hu && rr < I.row0 + kSkChunk; rr += blockDim.x) {
-        const bool left = rr >= k && rr < hL - k;
-        const bool right = rr >= hL + k && rr < Hu - k;
-        if (!left && !right) continue;
-        const double* M = left ? A.pool + uL.voff : A.pool + uR.woff;
-        const int hm = left ? hL : hR, ro = left ? rr : rr - hL;
-        const double* z = zs + (left ? 0 : 16 * NR);
-        double mrow[16], v[NR];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) mrow[t] = t < k ? M[(long long)t * hm + ro] : 0.0;
-#pragma unroll
-        for (int c = 0; c < NR; ++c) v[c] = c < nr ? A.T[(long long)c * H + zb + rr] : 0.0;
-#pragma unroll
-        for (int t = 0; t < 16; ++t)
-#pragma unroll
-            for (int c = 0; c < NR; ++c) v[c] = fma(-mrow[t], z[t * NR + c], v[c]);
-#pragma unroll
-        for (int c = 0; c < NR; ++c)
-            if (c < nr) A.T[(long long)c * H + zb + rr] = v[c];
+__device__ void sv_tree_from(const SkSolveArgs& A, int l, int u, int lane) {
+    const unsigned full = 0xffffffffu;
+    while (l < A.nlevels) {
+        const SkLevel L = A.levels[l];
+        const int a = u >> 1;
+        if (a < L.npairs) {
+            __syncwarp();
+            __threadfence();  // every lane's writes before the arrival
+            unsigned c = 0;
+            if (lane == 0) c = atomicAdd(A.cnt + L.pair0 + a, 1u);
+            c = __shfl_sync(full, c, 0);
+            if (c == 0) return;  // the sibling's warp continues
+            __threadfence();
+            sv_pair_task<NR>(A, A.pairs[L.pair0 + a], L.pair0 + a, lane);
+        }
+        u = a;
+        ++l;
     }
 }
+
+// Deferred row updates, after the tree: reduced row r picks up, in level
+// order, the update of every level where it is an interior row of its merged
+// unit (once interior, always interior; tip and middle rows were written by
+// the pair tasks): y -= vl_row z2 (left rows), y -= wr_row z1 (right rows).
+template <int NR>
+__device__ void sv_row_pass(const SkSolveArgs& A, long long r) {
+    const int k = A.k, nr = A.nrhs;
+    const long long H = 2LL * A.p * k;
+    double y[NR];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) y[c] = c < nr ? A.T[(long long)c * H + r] : 0.0;
+    const int u0 = (int)(r / (2 * k));
+    for (int l = 0; l < A.nlevels; ++l) {
+        const SkLevel L = A.levels[l];
+        const int a = (u0 >> l) >> 1;
+        if (a >= L.npairs) continue;  // carried unit
+        const SkPair pr = A.pairs[L.pair0 + a];
+        const int hL = pr.hL, Hu = hL + pr.hR, ro = (int)(r - pr.zb);
+        const bool left = ro >= k && ro < hL - k;
+        const bool right = ro >= hL + k && ro < Hu - k;
+        if (!left && !right) continue;
+        any = true;
+        const double* M = A.pool + (left ? pr.vl : pr.wr);
+        const int hm = left ? hL : pr.hR, rl = left ? ro : ro - hL;
+        const double* z = A.ZS + (long long)(L.pair0 + a) * 32 * NR + (left ? 0 : 16 * NR);
+        double mrow[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) mrow[t] = t < k ? M[(long long)t * hm + rl] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (t >= k) break;  // (z rows past k are never written)
+#pragma unroll
+            for (int c = 0; c < NR; ++c) y[c] = fma(-mrow[t], z[t * NR + c], y[c]);
+        }
+    }
+    if (any) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c)
+            if (c < nr) A.T[(long long)c * H + r] = y[c];
+    }
+}
+
 }  // namespace
 
 template <int NR>
@@ -302,29 +335,24 @@ __global__ void __launch_bounds__(kSvThreads, 1) k_sk_solve(SkSolveArgs A) {
     unsigned target = 0;
     grid_barrier(A.bar, target);
 
-    // ---- reduced solve, level by level (task A: level ph, task B: level ph-1)
-    double* zs = sv_smem + kSvWarps * wsm;
-    for (int ph = 0; ph <= A.nlevels; ++ph) {
-        sk_stamp(A.trace, ph, 0);
-        if (ph < A.nlevels) {
-            const SkLevel L = A.levels[ph];
-            for (int a = gw; a < L.npairs; a += nwarps) sv_pair_task<NR>(A, A.pairs[L.pair0 + a], lane);
+    // ---- reduced solve (solve.cpp:33-43): the tree of pair tasks (dataflow),
+    //      then every row's deferred updates
+    sk_stamp(A.trace, 0, 0);
+    if (A.nlevels > 0) {
+        const SkLevel L0 = A.levels[0];
+        const int ntask = L0.npairs + (L0.carry >= 0 ? 1 : 0);
+        for (int a = gw; a < ntask; a += nwarps) {
+            if (a < L0.npairs) sv_pair_task<NR>(A, A.pairs[L0.pair0 + a], L0.pair0 + a, lane);
+            sv_tree_from<NR>(A, 1, a, lane);
         }
-        sk_stamp(A.trace, ph, 1);
-        if (ph >= 1) {  // first on the CTAs without a pair of task A
-            const int npA = ph < A.nlevels ? A.levels[ph].npairs : 0;
-            const int ctasA = min((int)gridDim.x, (npA + kSvWarps - 1) / kSvWarps);
-            const SkLevel L = A.levels[ph - 1];
-            const int nb = (int)gridDim.x - ctasA;
-            const int b0 = nb > 0 ? (int)blockIdx.x - ctasA : (int)blockIdx.x;
-            if (b0 >= 0)
-                for (int it = b0; it < L.nitems; it += (nb > 0 ? nb : (int)gridDim.x))
-                    sv_rows_task<NR>(A, A.items[L.item0 + it], zs);
-        }
-        sk_stamp(A.trace, ph, 2);
-        grid_barrier(A.bar, target);
-        sk_stamp(A.trace, ph, 3);
     }
+    sk_stamp(A.trace, 0, 1);
+    grid_barrier(A.bar, target);
+    sk_stamp(A.trace, 0, 2);
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < H; r += (long long)gridDim.x * blockDim.x)
+        sv_row_pass<NR>(A, r);
+    grid_barrier(A.bar, target);
+    sk_stamp(A.trace, 0, 3);
 
     // ---- retrieval (solve.cpp:180-223): X_i = A_i^-1 (F_i - B^_i xi - C^_i eta)
     for (int i = gw; i < p; i += nwarps) {
