@@ -70,6 +70,15 @@ __device__ unsigned long long g_piv_prof[8];
     } while (0)
 #endif
 
+// Row-exchange scratch per warp: indexed by window position when it fits
+// (one slot per row), packed otherwise (piv_xslot: tile 0 plus the <= 8 pivot
+// rows outside it) -- the packed slots cost popcounts on every exchange.
+template <int TRW, int TCW>
+struct PivXs {
+    static constexpr bool kFull = (size_t)TCW * 8 * TRW * 8 * 8 <= 96u * 1024;
+    static constexpr int kRows = kFull ? 8 * TRW : 16;
+};
+
 // shared memory (doubles unless noted)
 template <int TRW, int TCW>
 struct PivDmmaSmem {
@@ -82,7 +91,7 @@ struct PivDmmaSmem {
     double l21[2][TRW * 64];  // -L21 per tile row (tile 0 unused), A-fragment order
     double srow[2][8 * RLD];  // staged entering row tile of step J (rows 8(J+TRW).., window columns)
     double scol[2][8 * TRW * 8];  // staged entering column block for the panel warp of step J+1
-    double xs[TCW][16 * 8];       // per-warp row exchange scratch, by slot (piv_xslot)
+    double xs[TCW][PivXs<TRW, TCW>::kRows * 8];  // per-warp row exchange scratch (PivXs)
     int src[2][8 * TRW];          // original position of the row at each final position
     unsigned mv_out[2][(8 * TRW + 31) / 32];  // rows leaving their position (by original position)
     unsigned mv_in[2][(8 * TRW + 31) / 32];   // positions receiving another row
@@ -338,7 +347,8 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
             for (int t = 0; t < TRW; ++t) {
                 const unsigned mo = S.mv_out[par][(8 * t) >> 5];
                 if (t == 0 || ((mo >> (((8 * t) & 31) + gi)) & 1u))
-                    *reinterpret_cast<double2*>(&xs[piv_xslot<NW>(mvo, 8 * t + gi) * 8 + 2 * q]) =
+                    *reinterpret_cast<double2*>(
+                        &xs[(PivXs<TRW, TCW>::kFull ? 8 * t + gi : piv_xslot<NW>(mvo, 8 * t + gi)) * 8 + 2 * q]) =
                         make_double2(acc[t][0], acc[t][1]);
             }
             __syncwarp();
@@ -346,7 +356,8 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
             for (int t = 0; t < TRW; ++t) {
                 const unsigned mi = S.mv_in[par][(8 * t) >> 5];
                 if (t == 0 || ((mi >> (((8 * t) & 31) + gi)) & 1u)) {
-                    const int sl = piv_xslot<NW>(mvo, S.src[par][8 * t + gi]);
+                    const int sl = PivXs<TRW, TCW>::kFull ? S.src[par][8 * t + gi]
+                                                          : piv_xslot<NW>(mvo, S.src[par][8 * t + gi]);
                     const double2 v = *reinterpret_cast<const double2*>(&xs[sl * 8 + 2 * q]);
                     acc[t][0] = v.x;
                     acc[t][1] = v.y;
