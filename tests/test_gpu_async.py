@@ -255,3 +255,24 @@ def test_generic_path_matches_tuned_kernels(oracle, spk, piv):
     assert spk.generic_launch_count(reset=True) > 0
     for t, g in zip(tuned, gen):
         assert rel_componentwise(t, g) <= 1e-11
+
+
+def test_row_major_copy_lazy_and_in_kernel_agree(oracle, spk):
+    """The DMMA LU writes the row-major factor copy only for shapes that have
+    met a transposed solve; the first factorization of a shape makes it on
+    demand (k_transpose_factors).  Transposed solves through either copy are
+    bit-identical and match the oracle; forward solves never need it."""
+    n, kl, ku = 6000, 33, 29  # a shape no other test uses
+    band = oracle.generate_band(515, n, kl, ku, 1.5)
+    F = np.asfortranarray(oracle.generate_rhs(516, n, 5))
+    a = spk.BandedMatrix(n, kl, ku, band)
+    plan = spk.gpu_plan(n, kl, ku, 5, False, 7)
+    f1 = spk.factorize(a, plan)  # first of its shape: the copy is made on demand
+    y1 = spk.solve(f1, F)
+    x1 = spk.transpose_solve(f1, F)
+    f2 = spk.factorize(a, plan)  # the shape has met a transposed solve: the copy comes from the LU
+    x2 = spk.transpose_solve(f2, F)
+    xo = oracle.oracle_solve(band, n, kl, ku, F, True, True)
+    assert rel_componentwise(x1, xo) <= 1e-10 and rel_componentwise(x2, xo) <= 1e-10
+    assert np.array_equal(x1, x2)
+    assert np.array_equal(y1, spk.solve(f2, F))
