@@ -621,6 +621,31 @@ def impl_ours(args, cfg):
     roofline = profile_roofline(spk, cfg, nprof, ms)
     l2_note = "inputs larger than L2" if flush is None else "L2 flushed between steps"
 
+    # configurations whose step has no transposed solve: one A^T X = F from the
+    # step's factorization, reported beside the step (north_star: transpose
+    # solves for both variants; C4's is the pivoted transposed path)
+    tr_info = None
+    if not cfg["transpose"]:
+        fact = spk.factorize_device(band.data_ptr(), n, k, k, plan, opts, sptr)
+        spk.solve_device(fact, F.data_ptr(), n, nrhs, XT.data_ptr(), n, True, sptr)  # (row-major copy made here)
+        torch.cuda.synchronize()
+        tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for a_, b_ in tev:
+            if flush is not None:
+                flush.zero_()
+            a_.record(stream)
+            spk.solve_device(fact, F.data_ptr(), n, nrhs, XT.data_ptr(), n, True, sptr)
+            b_.record(stream)
+        torch.cuda.synchronize()
+        tms = sum(a_.elapsed_time(b_) for a_, b_ in tev) / len(tev)
+        tberr = spk.backward_error_device(band.data_ptr(), n, k, k, XT.data_ptr(), n, F.data_ptr(), n, nrhs, True,
+                                          sptr)
+        tr_info = {"ms": round(tms, 4), "gflops": round((12.0 if cfg["piv"] else 8.0) * n * k * nrhs /
+                                                        (tms * 1e-3) / 1e9, 3),
+                   "backward_error": tberr,
+                   "note": "one transposed solve from the step's factorization (not part of the timed step)"}
+        del fact
+
     # e2e through the public C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -720,6 +745,8 @@ def impl_ours(args, cfg):
                 "clocks": clk.summary(), "impl": "ours"}
         if small is not None:
             line["small_k"] = small
+        if tr_info is not None:
+            line["transpose_solve"] = tr_info
         print(json.dumps(line))
     return 0
 
