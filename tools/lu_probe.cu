@@ -11,6 +11,7 @@
 
 namespace spk {
 void count_launch(int) {}
+void set_smem_attr(const void* fn, int bytes) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); }
 }
 
 int main(int argc, char** argv) {
@@ -84,7 +85,7 @@ int main(int argc, char** argv) {
 #ifdef SPK_LU_PROFILE
         cudaMemcpyFromSymbol(pr, spk::g_lu_prof, sizeof(pr));
 #endif
-        const int steps = (m + 7) / 8, nw = k <= 32 ? 4 : k <= 64 ? 8 : k <= 96 ? 12 : 16;
+        const int steps = (m + 7) / 8, nw = (k + 7) / 8;  // NW = T - 1 warps, T = k/8 + 1
         printf("m=%d k=%d parts=%d: %.3f ms, %.0f clk/step (wall at 1.965 GHz) err=%s\n", m, k, nparts, ms,
                ms * 1e-3 * 1.965e9 / steps, cudaGetErrorString(cudaGetLastError()));
         const char* names[8] = {"stage issue", "phase 1 (1a+1b)", "S1 wait", "ro1 publish+reload",
