@@ -14,18 +14,6 @@
 #include "spk_sweep_dmma.cuh"
 
 namespace spk {
-struct FastLuArgs {
-    const int* units;
-    const PartDev* parts;
-    const double* band;
-    int akl, aku;
-    double* fac;
-    double* tfac;
-    double* dinv;
-    int* piv;
-    double boost_eps;
-    int* boost_cnt;
-};
 struct PivLuArgs {  // spk_lu_fast.cu
     const int* units;
     const PartDev* parts;
@@ -1406,6 +1394,7 @@ struct Exec {
     const double* F = nullptr;
     long long ldf = 0, n = 0;
     const double* band = nullptr;  // factorization input (device)
+    long long band_cols = 0, band_col0 = 0;  // its readable columns: [-band_col0, band_cols - band_col0)
     bool lu_fast_done = false;
 
     bool run_fast_sweep(const Stage& st, const SweepJob* jobs, int nc) {
@@ -1602,7 +1591,8 @@ struct Exec {
                             // otherwise it is made on demand (ensure_tfac)
                             const bool wt = kmax <= 16 || f.want_tfac;
                             FastLuArgs A{(const int*)jobs, f.d_parts, band, f.kl, f.ku, f.d_fac,
-                                         wt ? f.d_tfac : nullptr, f.d_dinv, f.d_piv, f.boost_eps, f.d_boost};
+                                         wt ? f.d_tfac : nullptr, f.d_dinv, f.d_piv, f.boost_eps, f.d_boost,
+                                         band_cols, band_col0};
                             if (launch_band_lu_fast((const int*)jobs, st.njobs, kmax, A, s)) {
                                 lu_fast_done = true;
                                 if (!wt) f.tfac_ready.store(false);
@@ -2639,6 +2629,8 @@ static spk_status factorize_impl(const double* band, int32_t band_mem, int64_t n
         Exec ex{*f, s, B, f->k};
         ex.n = n;
         ex.band = dband;
+        ex.band_cols = n + hl + hr;
+        ex.band_col0 = hl;
         ex.run(f->prog_factor, f->d_blob);
         ex.run(f->prog_levels, f->d_blob);
         mark_ready(*f, s);

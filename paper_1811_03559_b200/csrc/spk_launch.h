@@ -80,7 +80,23 @@ bool launch_sweep_fast_fut(int tr, int nc, bool piv, int nwarps, dim3 grid, size
                            cudaStream_t s);
 bool launch_sweep_fast_blt(int tr, int nc, bool piv, int nwarps, dim3 grid, size_t smem, const FastSweepArgs& A,
                            cudaStream_t s);
-struct FastLuArgs;
+// non-pivoting blocked DMMA band LU (spk_lu_fast.cu)
+struct FastLuArgs {
+    const int* units;
+    const PartDev* parts;
+    const double* band;  // input band (kl+ku+1) x n, column-major; column 0 of the partitions' rows
+    int akl, aku;
+    double* fac;
+    double* tfac;  // row-major copy, or null (made on demand)
+    double* dinv;
+    int* piv;
+    double boost_eps;
+    int* boost_cnt;
+    // readable band columns around `band` (TMA staging of the entering
+    // blocks): columns [-col0, ncols - col0); ncols = 0 disables TMA
+    long long ncols;
+    long long col0;
+};
 bool launch_band_lu_fast(const int* d_units, int nunits, int kmax, const FastLuArgs& A, cudaStream_t s);
 // blocked pivoted band LU on the tensor cores (spk_lu_piv_dmma.cu); false
 // when the band is wider than its tile windows (kl+ku > 192)

@@ -14,6 +14,8 @@
 // and, if a boost would have fired, re-runs its partition with the now-known
 // threshold (exact reference semantics; never taken for diagonally dominant
 // input).
+#include <cuda.h>
+
 #include "spk_device.cuh"
 #include "spk_launch.h"
 #include "spk_sweep_fast.cuh"
@@ -21,21 +23,10 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
+#include <cstring>
 
 namespace spk {
 
-struct FastLuArgs {
-    const int* units;
-    const PartDev* parts;
-    const double* band;  // input band (kl+ku+1) x n, column-major
-    int akl, aku;
-    double* fac;
-    double* tfac;
-    double* dinv;
-    int* piv;
-    double boost_eps;
-    int* boost_cnt;
-};
 
 // ===========================================================================
 // Blocked variant on the FP64 tensor cores (kl, ku <= 128).
@@ -72,7 +63,7 @@ __device__ __forceinline__ void lu_dmma(double& d0, double& d1, double a, double
 }
 
 template <int T, int TR>
-struct LuDmmaSmem {  // offsets in doubles
+struct LuDmmaSmem {  // offsets in doubles (from a 128-byte aligned base)
     static constexpr int NW = T - 1;
     static constexpr int D = 0;                  // [2][64] factored diagonal block, row-major
     static constexpr int DINV = D + 128;         // [2][8]  1/u_jj
@@ -81,17 +72,46 @@ struct LuDmmaSmem {  // offsets in doubles
     static constexpr int PROW = UI + 128;        // [2][T][64] panel row of step J (parity J), accumulator order
     static constexpr int L = PROW + 2 * 64 * T;  // [2][T][64] -L21 by row offset, A-fragment order
     static constexpr int U = L + 2 * 64 * T;     // [2][T][64] U12 by column offset, B-fragment order
-    static constexpr int ST = U + 2 * 64 * T;    // staging: [2][T][64] column tiles, then [2][T][64] row tiles
+    // staging of the entering blocks, in the TMA box layouts (column-major,
+    // padded strides: conflict-free fragment reads; both 128-byte aligned):
+    // column block [8 columns][SC rows], row block [8T columns][SR rows]
+    static constexpr int SC = 8 * T + 2, SR = 10;
+    static constexpr int CB = 8 * SC, RB = 8 * T * SR;
+    static constexpr int ST = U + 2 * 64 * T;    // [2][CB] column blocks, then [2][RB] row blocks
     static constexpr int NS = T - TR;            // column offsets held in shared memory per tile row
-    static constexpr int WIN = ST + 4 * T * 64;  // [NW][NS][32] double2, circular by step
+    static constexpr int WIN = ST + 2 * CB + 2 * RB;  // [NW][NS][32] double2, circular by step
     static constexpr int TOTAL = WIN + NW * NS * 64;
+    static_assert(ST % 16 == 0 && CB % 16 == 0 && RB % 16 == 0, "TMA destinations must stay 128-byte aligned");
 };
 
+// TMA tile load (2-D tensor map) into shared memory, completion on an mbarrier
+__device__ __forceinline__ void lu_tma_2d(void* dst, const CUtensorMap* tm, int x, int y, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(tm), "r"(x), "r"(y), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+__device__ __forceinline__ void lu_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+#ifdef SPK_LU_PROFILE
+__device__ int g_lu_dbg;  // tools/lu_probe.cu: bit 0 no column TMA, bit 1 no row TMA, bit 2 no zeroing
+#define LU_DBG(bit) (g_lu_dbg & (bit))
+#else
+#define LU_DBG(bit) 0
+#endif
 #ifdef SPK_LU_PROFILE
 // tools/lu_probe.cu: per-phase clock totals of CTA 0 (lane 0 of each warp)
 __device__ unsigned long long g_lu_prof[8];
+__device__ volatile int* g_lu_where;  // mapped host memory: last (step, mark) per warp
 #define LU_MARK(slot)                                                          \
     do {                                                                       \
+        if (g_lu_where && lane == 0) g_lu_where[blockIdx.x * 32 + w] = J * 16 + (slot); \
         if (blockIdx.x == 0 && lane == 0) {                                    \
             const long long now = clock64();                                  \
             atomicAdd(&g_lu_prof[(slot)], (unsigned long long)(now - tprev)); \
@@ -114,12 +134,15 @@ __device__ __forceinline__ int bfrag(int k, int n) { return (k >> 2) * 32 + n * 
 // J), so the per-step rotation moves one tile in and one out.  T = 21 (k <=
 // 160) needs it: 20 warps leave 96 registers per thread.
 template <int T, int TR>
-__global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(FastLuArgs A) {
+__global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(FastLuArgs A, const __grid_constant__ CUtensorMap tmc,
+                                                                           const __grid_constant__ CUtensorMap tmr,
+                                                                           int tma_sh) {
     using S = LuDmmaSmem<T, TR>;
     constexpr int NS = T - TR;
     constexpr int NW = T - 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* sm = reinterpret_cast<double*>(smem_raw);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    __shared__ unsigned long long s_mb[2];  // TMA staging barriers, by issuing-step parity
     __shared__ double s_red[2 * 32];
     __shared__ int s_cnt[32];
 
@@ -144,35 +167,84 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
     };
 
     // staging for the recycle at step Jr: the entering block nb = Jr + T as a
-    // column (window rows 8(Jr+1) .. x 8 columns, by row offset; read at step Jr)
-    // and as a row (8 rows x the window columns 8(Jr+1) .., by column offset;
-    // read at step Jr+1 by the warp taking it).  Column tiles of step J+1 and
-    // row tiles of step J are issued at the start of step J (double buffers:
-    // nobody reads the buffer being refilled).  Rows fastest within a band
-    // column, so the gathers coalesce; out-of-band slots are fixed, zeroed once.
-    auto stage_elem = [&](int idx, int Jr, int& i, int& c, int& off) {  // idx < 64T: column tiles
-        if (idx < 64 * T) {
-            const int jj = idx / (8 * T), ri = idx - jj * 8 * T;
-            i = 8 * (Jr + 1) + ri;
-            c = 8 * (Jr + T) + jj;
-            off = (Jr & 1) * T * 64 + (ri >> 3) * 64 + (ri & 7) * 8 + jj;
-        } else {
-            const int e = idx - 64 * T, ci = e >> 3, ii = e & 7;
-            i = 8 * (Jr + T) + ii;
-            c = 8 * (Jr + 1) + ci;
-            off = 2 * T * 64 + (Jr & 1) * T * 64 + (ci >> 3) * 64 + ii * 8 + (ci & 7);
-        }
+    // column (window rows 8(Jr+1) .. x 8 columns; read at step Jr) and as a row
+    // (8 rows x the window columns 8(Jr+1) ..; read at step Jr+1 by the warp
+    // taking it).  Column block of step J+1 and row block of step J are issued
+    // at the start of step J (double buffers: nobody reads the buffer being
+    // refilled).  TMA (one thread, two 2-D tiles through the aliased band view
+    // of launch_lu_dmma) while both blocks lie inside the partition; the last
+    // steps (and bands the view cannot describe) gather element-wise with
+    // cp.async.  Buffers hold the TMA box layouts; a reversed (UL) partition's
+    // boxes arrive mirrored (index BOX-1-L), and the element path writes them
+    // the same way.  Slots outside the band are not cleared: readers mask them.
+    const bool mir = P.rev != 0;
+    auto tma_ok = [&](int Jr) { return tma_sh >= 0 && Jr >= 0 && Jr < nblk && 8 * (Jr + T) + 8 <= m; };
+    // box origins at Jr = 0 (column box x, y; row box x, y), 8 rows / columns
+    // further (reversed: back) per step; kept in shared memory, read by the
+    // issuing thread only
+    // TMA box rows must start on 16-byte boundaries (even x): a box whose
+    // first row would be odd starts one row early (reversed: one late), so its
+    // data sit one slot later (earlier) in the buffer -- every staging access,
+    // the element path's included, is shifted by dsh (the same for both boxes
+    // and all steps: x moves by 8 per step)
+    int dsh = 0;
+    if (tma_sh >= 0 && ((P.r0 + A.aku + A.col0 + tma_sh + (mir ? m : 0)) & 1)) dsh = mir ? -1 : 1;
+    __shared__ int s_tc[4];
+    if (threadIdx.x == 0 && tma_sh >= 0) {
+        const long long xo = A.aku + A.col0 + tma_sh - dsh, yo = A.col0, r0 = P.r0, e = P.r0 + m - 1;
+        s_tc[0] = (int)(xo + (mir ? e - 8 - (S::SC - 1) : r0 + 8));
+        s_tc[1] = (int)(yo + (mir ? e - 8 * T - 7 : r0 + 8 * T));
+        s_tc[2] = (int)(xo + (mir ? e - 8 * T - (S::SR - 1) : r0 + 8 * T));
+        s_tc[3] = (int)(yo + (mir ? e - 8 - (8 * T - 1) : r0 + 8));
+    }
+    auto tma_issue = [&](int Jr, bool rows, unsigned long long* bar) {
+        const int dx = (mir ? -8 : 8) * Jr;
+        if (!rows) lu_tma_2d(sm + S::ST + (Jr & 1) * S::CB, &tmc, s_tc[0] + dx, s_tc[1] + dx, bar);
+        else lu_tma_2d(sm + S::ST + 2 * S::CB + (Jr & 1) * S::RB, &tmr, s_tc[2] + dx, s_tc[3] + dx, bar);
     };
-    for (int idx = threadIdx.x; idx < 2 * 64 * T; idx += blockDim.x)
-        for (int b2 = 0; b2 < 2; ++b2) {
-            int i, c, off;
-            stage_elem(idx, b2, i, c, off);
-            if (i - c > kl || c - i > ku) sm[S::ST + off] = 0.0;
+    // readers: column block element (window row ri, column jj), row block
+    // element (row ii, window column ci)
+    auto colv = [&](const double* buf, int ri, int jj) -> double {
+        const int L = jj * S::SC + ri;
+        return buf[(mir ? S::CB - 1 - L : L) + dsh];
+    };
+    auto rowv = [&](const double* buf, int ii, int ci) -> double {
+        const int L = ci * S::SR + ii;
+        return buf[(mir ? S::RB - 1 - L : L) + dsh];
+    };
+    // the slots outside the band hold whatever the box covered (other band
+    // entries) or stale data: before the readers, the warp taking the entering
+    // row this step (ro == NW) zeroes them in the column block of step J (read
+    // after the mid-step barrier) and the row block of step J-1 (read by itself)
+    auto zero_outside = [&](int J) {
+        constexpr int c8 = 8 * (T - 1);
+        double* cb = sm + S::ST + (J & 1) * S::CB;
+        {
+            const int jj = lane & 7, lo = min(jj + c8 - ku, c8);  // rows above the band (readers: < c8)
+            for (int ri = lane >> 3; ri < lo; ri += 4) {
+                const int L = jj * S::SC + ri;
+                cb[(mir ? S::CB - 1 - L : L) + dsh] = 0.0;
+            }
         }
-    // issue: each warp instruction covers 4 rows x 8 columns of one tile, so
-    // the 32 smem destinations are 32 consecutive doubles (no bank conflicts)
-    // and the global sources are 8 sectors (4 consecutive rows per column)
-    // (warp `rank` of `nrank`: the diagonal warp of the step stays out)
+        if (J > 0) {
+            double* rb = sm + S::ST + 2 * S::CB + ((J + 1) & 1) * S::RB;
+            const int ii = lane & 7, lo = min(c8 + ii - kl, 8 * T), hi = ii + c8 + ku;  // left of / right of the band
+            for (int ci = lane >> 3; ci < lo; ci += 4) {
+                const int L = ci * S::SR + ii;
+                rb[(mir ? S::RB - 1 - L : L) + dsh] = 0.0;
+            }
+            for (int ci = hi + 1 + (lane >> 3); ci < 8 * T; ci += 4) {
+                const int L = ci * S::SR + ii;
+                rb[(mir ? S::RB - 1 - L : L) + dsh] = 0.0;
+            }
+        }
+        // generic writes before the buffer's next TMA fill (after a CTA barrier)
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+    };
+    // element path: each warp instruction covers 4 rows x 8 columns of one
+    // tile (global sources: 8 sectors, 4 consecutive rows per column); warp
+    // `rank` of `nrank` (the diagonal warp of the step stays out)
     auto stage_load = [&](int Jr, bool rows, int rank, int nrank) {
         if (Jr < 0 || Jr >= nblk || rank < 0) return;
         const int cc = lane & 7, r4 = lane >> 3;
@@ -183,13 +255,15 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
             if (!rows) {  // entering column block: window rows 8(Jr+1) + 8 tile + rr, column cc
                 i = 8 * (Jr + 1) + 8 * tile + rr;
                 c = 8 * (Jr + T) + cc;
-                dst = sm + S::ST + (Jr & 1) * T * 64 + tile * 64 + rr * 8 + cc;
+                const int L = cc * S::SC + 8 * tile + rr;
+                dst = sm + S::ST + (Jr & 1) * S::CB + (mir ? S::CB - 1 - L : L) + dsh;
             } else {      // entering row block: row rr, window column 8(Jr+1) + 8 tile + cc
                 i = 8 * (Jr + T) + rr;
                 c = 8 * (Jr + 1) + 8 * tile + cc;
-                dst = sm + S::ST + 2 * T * 64 + (Jr & 1) * T * 64 + tile * 64 + rr * 8 + cc;
+                const int L = (8 * tile + cc) * S::SR + rr;
+                dst = sm + S::ST + 2 * S::CB + (Jr & 1) * S::RB + (mir ? S::RB - 1 - L : L) + dsh;
             }
-            if (i - c > kl || c - i > ku) continue;  // zero, never loaded
+            if (i - c > kl || c - i > ku) continue;  // outside the band: masked by the readers
             if (i < m && c < m) cp_async8(dst, bbase + sg * ((long long)c * (ald - 1) + i));
             else *dst = i == c ? 1.0 : 0.0;
         }
@@ -343,8 +417,26 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 prow[(T + c - 1) * 32] = make_double2(t0, t1);
             }
         }
-        stage_load(0, false, w, NW);
+        // TMA issues run at steps -1 (column block of step 0, barrier 1), 0, 1,
+        // .. while tma_ok holds (monotone in the step), so the issue of step s
+        // is phase (s + 1) >> 1 of barrier s & 1; re-armed for each attempt
+        if (threadIdx.x == 0) {
+            if (attempt > 0) {  // idle since the last step of the first pass
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_mb[0])) : "memory");
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_mb[1])) : "memory");
+            }
+            mbar_init(&s_mb[0], 1);
+            mbar_init(&s_mb[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tma_ok(0) && threadIdx.x == 0) {
+            lu_expect_tx(&s_mb[1], S::CB * 8);
+            tma_issue(0, false, &s_mb[1]);
+        }
+        if (!tma_ok(0)) stage_load(0, false, w, NW);
         cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
 
         int ro = w + 1;
@@ -356,9 +448,21 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
             // the warp that factors the next diagonal block this step (ro == 1)
             // does no staging and no output writes: they are off its chain
             const int orank = ro == 1 ? -1 : ro - 2;
-            stage_load(J + 1, false, orank, NW - 1);
-            stage_load(J, true, orank, NW - 1);
-            cp_async_commit();
+            // the blocks staged by TMA at step J-1 (read this step) have landed
+            if (tma_ok(J > 0 ? J - 1 : 0) && !LU_DBG(8)) mbar_wait(&s_mb[(J - 1) & 1], (J >> 1) & 1);
+            if (ro == NW && !LU_DBG(4)) zero_outside(J);
+            {
+                const bool tc = tma_ok(J + 1), trw = tma_ok(J);
+                if ((tc || trw) && threadIdx.x == 0 && !LU_DBG(16)) {
+                    unsigned long long* bar = &s_mb[J & 1];
+                    lu_expect_tx(bar, (tc && !LU_DBG(1) ? S::CB * 8 : 0) + (trw && !LU_DBG(2) ? S::RB * 8 : 0));
+                    if (tc && !LU_DBG(1)) tma_issue(J + 1, false, bar);
+                    if (trw && !LU_DBG(2)) tma_issue(J, true, bar);
+                }
+                if (!tc) stage_load(J + 1, false, orank, NW - 1);
+                if (!trw) stage_load(J, true, orank, NW - 1);
+                cp_async_commit();
+            }
             LU_MARK(0);
             double* sLc = sm + S::L + par * 64 * T;
             double* sUc = sm + S::U + par * 64 * T;
@@ -366,14 +470,13 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
             const double* sUp = sm + S::U + (par ^ 1) * 64 * T;
             // a warp that took the entering row block last step reads it from staging
             const bool fresh = ro == NW && J > 0;
-            const double* stp = sm + S::ST + 2 * T * 64 + ((J + 1) & 1) * T * 64;  // row tiles of step J-1
+            const double* stp = sm + S::ST + 2 * S::CB + ((J + 1) & 1) * S::RB;  // row block of step J-1
             // 1a. L21 of my tile row: (panel-column tile) x U11^-1
             {
                 double a0 = acc[0][0], a1 = acc[0][1];
                 if (fresh) {
-                    const double2 v = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
-                    a0 = v.x;
-                    a1 = v.y;
+                    a0 = rowv(stp, gi, 2 * q);
+                    a1 = rowv(stp, gi, 2 * q + 1);
                 }
                 // accumulator -> A fragments: A[gi][q + 4 ks] sits in lane gi*4 + 2ks + q/2
                 double af[2];
@@ -418,20 +521,23 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 sUc[co * 64 + bfrag(gi, 2 * q + 1)] = u1;
             }
             LU_MARK(1);
-            cp_async_wait<1>();  // this step's staging (committed a step ago) has landed
             __syncthreads();
             LU_MARK(2);
 
-            const double* stc = sm + S::ST + (J & 1) * T * 64;  // column tiles of step J (by row offset - 1)
+            const double* stc = sm + S::ST + (J & 1) * S::CB;  // column block of step J
             if (ro == 1) {
                 // my row is the next panel row, already published one step ago
                 // (this step's update is applied by 1b of the next step) except
                 // its far tile, the entering column block; then update and factor
                 // the next diagonal tile.  Next step I take the entering row block.
-                const double2 cv = *reinterpret_cast<const double2*>(stc + gi * 8 + 2 * q);
+                const double2 cv = make_double2(colv(stc, gi, 2 * q), colv(stc, gi, 2 * q + 1));
                 prow[((par ^ 1) * T + T - 1) * 32] = cv;
                 if (8 * (J + 1) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
                 double d0 = acc[1][0], d1 = acc[1][1];
+                // my tiles are dead from here (next step I take the entering row
+                // block): constants free their registers across the chain below
+#pragma unroll
+                for (int c = 0; c < TR; ++c) acc[c][0] = acc[c][1] = 0.0;
                 LU_MARK(3);
                 lu_dmma(d0, d1, sLc[64 + lane], sUc[64 + lane]);
                 lu_dmma(d0, d1, sLc[64 + 32 + lane], sUc[64 + 32 + lane]);
@@ -446,14 +552,13 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                     const bool live = 8 * (J - 1 + T) + gi < m;
 #pragma unroll
                     for (int c = 1; c < T; ++c) {
-                        const double2 v = *reinterpret_cast<const double2*>(stp + c * 64 + gi * 8 + 2 * q);
-                        double t0 = v.x, t1 = v.y;
+                        double t0 = rowv(stp, gi, 8 * c + 2 * q), t1 = rowv(stp, gi, 8 * c + 2 * q + 1);
                         if (live) amax = fmax(amax, fmax(fabs(t0), fabs(t1)));
                         lu_dmma(t0, t1, la0, sUc[c * 64 + lane]);
                         lu_dmma(t0, t1, la1, sUc[c * 64 + 32 + lane]);
                         put(J + 1, c - 1, t0, t1);
                     }
-                    const double2 v0 = *reinterpret_cast<const double2*>(stp + gi * 8 + 2 * q);
+                    const double2 v0 = make_double2(rowv(stp, gi, 2 * q), rowv(stp, gi, 2 * q + 1));
                     if (live) amax = fmax(amax, fmax(fabs(v0.x), fabs(v0.y)));
                 } else {
                     // register tiles k-slice-major: a tile's two DMMAs are TR-1
@@ -488,7 +593,7 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                         acc[TR - 1][1] = t1;
                     }
                 }
-                const double2 cv = *reinterpret_cast<const double2*>(stc + (ro - 1) * 64 + gi * 8 + 2 * q);
+                const double2 cv = make_double2(colv(stc, 8 * (ro - 1) + gi, 2 * q), colv(stc, 8 * (ro - 1) + gi, 2 * q + 1));
                 put(J + 1, T - 1, cv.x, cv.y);
                 if (8 * (J + ro) + gi < m) amax = fmax(amax, fmax(fabs(cv.x), fabs(cv.y)));
                 if (ro == 2) {
@@ -546,6 +651,7 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
             }
             LU_MARK(6);
             ro = ro == 1 ? NW : ro - 1;
+            cp_async_wait<0>();  // element-path staging of this step, read next step
             __syncthreads();
             LU_MARK(7);
         }
@@ -586,12 +692,69 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
     for (int j = threadIdx.x; j < m; j += blockDim.x) A.piv[P.r0 + j] = j;
 }
 
+// The band seen by TMA: element (R, C) sits at band[C*ald + aku + R - C] =
+// base[(C + col0) * (ald - 1) + (R + aku + col0)], i.e. a 2-D tensor with
+// x = R + aku + col0 (contiguous) and y = C + col0 (stride (ald - 1) doubles)
+// whose rows overlap in memory -- TMA only computes addresses, so a box is
+// "rows x0.. of columns y0..", the band's diagonal structure flattened.  Rows
+// past the readable columns come back as zeros (out-of-bounds fill).  Needs
+// (ald - 1) * 8 to be a multiple of 16 (kl + ku even); the base is aligned
+// down to 16 bytes by shifting x.  tma_sh = -1: no maps, element path only.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            (void)cudaGetLastError();
+            return (EncodeTiledFn) nullptr;
+        }
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+static int band_tensor_maps(const FastLuArgs& A, unsigned sc, unsigned sr, unsigned bw, CUtensorMap* tmc,
+                            CUtensorMap* tmr) {
+    const long long ald = A.akl + A.aku + 1;
+    if (A.ncols <= 0 || ((ald - 1) * 8) % 16 != 0) return -1;
+    const EncodeTiledFn enc = encode_tiled();
+    if (!enc) return -1;
+    const double* base = A.band - A.col0 * ald;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base);
+    if (a % 8) return -1;
+    const int sh = (int)((a % 16) / 8);
+    base -= sh;
+    const cuuint64_t dims[2] = {(cuuint64_t)(A.ncols + A.aku + sh), (cuuint64_t)A.ncols};
+    if (dims[0] >= (1ull << 31) || dims[1] >= (1ull << 31)) return -1;  // int coordinates
+    const cuuint64_t strides[1] = {(cuuint64_t)(ald - 1) * 8};
+    const cuuint32_t boxc[2] = {sc, 8}, boxr[2] = {sr, bw}, es[2] = {1, 1};
+    void* g = const_cast<double*>(base);
+    if (enc(tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, g, dims, strides, boxc, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+    if (enc(tmr, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, g, dims, strides, boxr, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+    return sh;
+}
+
 template <int T, int TR>
 static bool launch_lu_dmma(const int* d_units, int nunits, const FastLuArgs& A, cudaStream_t s) {
-    const size_t smem = sizeof(double) * LuDmmaSmem<T, TR>::TOTAL;
+    using S = LuDmmaSmem<T, TR>;
+    const size_t smem = sizeof(double) * S::TOTAL + 128;  // + alignment of the base
     if (smem > 227 * 1024) return false;
     set_smem_attr((const void*)k_band_lu_dmma<T, TR>, (int)smem);
-    k_band_lu_dmma<T, TR><<<nunits, 32 * (T - 1), smem, s>>>(A);
+    CUtensorMap tmc, tmr;
+    memset(&tmc, 0, sizeof(tmc));
+    memset(&tmr, 0, sizeof(tmr));
+    const int sh = band_tensor_maps(A, S::SC, S::SR, 8 * T, &tmc, &tmr);
+    k_band_lu_dmma<T, TR><<<nunits, 32 * (T - 1), smem, s>>>(A, tmc, tmr, sh);
     count_launch();
     return true;
 }

@@ -1,6 +1,6 @@
 // lu_probe.cu -- phase timing of the blocked DMMA band LU on one partition.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DSPK_LU_PROFILE \
-//        -o tools/lu_probe tools/lu_probe.cu && tools/lu_probe [m] [k]
+//        -o tools/lu_probe tools/lu_probe.cu && tools/lu_probe [m] [k] [parts] [tma 0/1]
 // Prints the per-step clock totals of CTA 0, summed over its warps (slot 3/4:
 // the warp publishing the panel row and factoring the next diagonal block).
 #include "../paper_1811_03559_b200/csrc/spk_lu_fast.cu"
@@ -66,7 +66,28 @@ int main(int argc, char** argv) {
     cudaMemcpy(d_parts, parts.data(), sizeof(spk::PartDev) * nparts, cudaMemcpyHostToDevice);
     cudaMemcpy(d_units, units.data(), sizeof(int) * nparts, cudaMemcpyHostToDevice);
     cudaMemset(d_boost, 0, sizeof(int) * nparts);
-    spk::FastLuArgs A{d_units, d_parts, d_band, k, k, d_fac, d_tfac, d_dinv, d_piv, 1.49e-8, d_boost};
+    spk::FastLuArgs A{d_units, d_parts, d_band, k, k, d_fac, d_tfac, d_dinv, d_piv, 1.49e-8, d_boost, n, 0};
+    if (argc > 4 && atoi(argv[4]) == 0) A.ncols = 0;  // element-path staging only
+    {
+        CUtensorMap a, b;
+        printf("TMA staging: %s\n", spk::band_tensor_maps(A, 170, 10, 168, &a, &b) >= 0 ? "yes" : "no");
+    }
+#ifdef SPK_LU_PROFILE
+    {
+        const int dbg = getenv("LU_DBG") ? atoi(getenv("LU_DBG")) : 0;
+        cudaMemcpyToSymbol(spk::g_lu_dbg, &dbg, sizeof(int));
+    }
+#endif
+    int* h_where = nullptr;
+#ifdef SPK_LU_PROFILE
+    if (getenv("LU_WHERE")) {  // last (step, mark) per warp in mapped host memory (survives a fault)
+        cudaHostAlloc(&h_where, sizeof(int) * 32 * nparts, cudaHostAllocMapped);
+        for (int i = 0; i < 32 * nparts; ++i) h_where[i] = -1;
+        int* dw = nullptr;
+        cudaHostGetDevicePointer(&dw, h_where, 0);
+        cudaMemcpyToSymbol(spk::g_lu_where, &dw, sizeof(dw));
+    }
+#endif
     for (int rep = 0; rep < 2; ++rep) {
         unsigned long long z[8] = {0};
 #ifdef SPK_LU_PROFILE
@@ -86,8 +107,19 @@ int main(int argc, char** argv) {
         cudaMemcpyFromSymbol(pr, spk::g_lu_prof, sizeof(pr));
 #endif
         const int steps = (m + 7) / 8, nw = (k + 7) / 8;  // NW = T - 1 warps, T = k/8 + 1
-        printf("m=%d k=%d parts=%d: %.3f ms, %.0f clk/step (wall at 1.965 GHz) err=%s\n", m, k, nparts, ms,
-               ms * 1e-3 * 1.965e9 / steps, cudaGetErrorString(cudaGetLastError()));
+        std::vector<int> bc(nparts);
+        cudaMemcpy(bc.data(), d_boost, sizeof(int) * nparts, cudaMemcpyDeviceToHost);
+        long long nb = 0;
+        for (int v : bc) nb += v;
+        if (h_where && cudaGetLastError() != cudaSuccess) {
+            for (int b = 0; b < nparts && b < 6; ++b) {
+                printf("  cta %d:", b);
+                for (int w = 0; w < (k + 7) / 8; ++w) printf(" %d/%d", h_where[b * 32 + w] >> 4, h_where[b * 32 + w] & 15);
+                printf("\n");
+            }
+        }
+        printf("m=%d k=%d parts=%d: %.3f ms, %.0f clk/step (wall at 1.965 GHz) boosts=%lld err=%s\n", m, k, nparts, ms,
+               ms * 1e-3 * 1.965e9 / steps, nb, cudaGetErrorString(cudaGetLastError()));
         const char* names[8] = {"stage issue", "phase 1 (1a+1b)", "S1 wait", "ro1 publish+reload",
                                 "ro1 diag update+factor", "update+shift", "outputs", "S0 wait"};
         for (int i = 0; i < 8; ++i)
