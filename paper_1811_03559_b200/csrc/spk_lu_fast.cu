@@ -99,8 +99,11 @@ __device__ __forceinline__ void lu_expect_tx(unsigned long long* bar, unsigned b
                  : "memory");
 }
 
-#ifdef SPK_LU_PROFILE
-__device__ int g_lu_dbg;  // tools/lu_probe.cu: bit 0 no column TMA, bit 1 no row TMA, bit 2 no zeroing
+#if defined(SPK_LU_PROFILE) || defined(SPK_LU_DBG)
+// tools/lu_probe.cu (timing experiments, wrong results): bit 0 no column TMA,
+// 1 no row TMA, 2 no zeroing, 3 no TMA waits, 4 no TMA arming, 5 no outputs,
+// 6 no diagonal factorization, 7 no trailing update
+__device__ int g_lu_dbg;
 #define LU_DBG(bit) (g_lu_dbg & (bit))
 #else
 #define LU_DBG(bit) 0
@@ -357,9 +360,6 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
 
     double2* prow = reinterpret_cast<double2*>(sm + S::PROW) + lane;  // + parity * T * 32 + offset * 32
     double2* win = reinterpret_cast<double2*>(sm + S::WIN) + (size_t)w * NS * 32 + lane;
-    // transposed factor writes (row-major L rows, packed U columns): runs of
-    // <= 8 entries, one per L row below / U column right of the panel
-    const int tr_n = 15 + kl + ku;
     for (int attempt = 0; attempt < 2; ++attempt) {
         double acc[TR][2];  // my tile row, by column offset from the panel (offsets < TR)
         // offset c of my row as seen at step J: registers or window slot
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 LU_MARK(3);
                 lu_dmma(d0, d1, sLc[64 + lane], sUc[64 + lane]);
                 lu_dmma(d0, d1, sLc[64 + 32 + lane], sUc[64 + 32 + lane]);
-                diag_factor(d0, d1, J + 1);
+                if (!LU_DBG(64)) diag_factor(d0, d1, J + 1);
                 LU_MARK(4);
             }
             if (ro != 1) {
@@ -608,43 +608,74 @@ __global__ void __launch_bounds__(32 * (T - 1), T <= 13 ? 2 : 1) k_band_lu_dmma(
                 LU_MARK(5);
             }
             // write L columns j0.. and U rows j0.. (both packed layouts) and 1/u_jj
-            if (j0 < m) {
+            if (j0 < m && !LU_DBG(32)) {
                 const double* sD = sm + S::D + par * 64;
                 // L columns (packed column-major) and U rows (row-major copy): one
-                // contiguous run per warp
-                for (int sgm = orank; sgm < (wt ? 16 : 8) && orank >= 0; sgm += NW - 1) {
+                // contiguous run per warp, its (<= 5) loads issued before its stores
+                constexpr int KIT = (8 * (T - 1) + 32) / 32;  // <= k + 1 entries per run
+                const int nseg = wt ? 16 : 8;
+                for (int sgm = orank; sgm < nseg && orank >= 0; sgm += NW - 1) {
                     const int qq = sgm & 7, c = j0 + qq;
                     if (c >= m) continue;
-                    if (sgm < 8) {
-                        double* dst = F + (long long)c * rows + d;
-                        for (int off = lane + 1; off <= kl; off += 32) {
-                            const int rr = qq + off;
-                            const double v = rr < 8 ? sD[rr * 8 + qq] : -sLc[(rr >> 3) * 64 + afrag(rr & 7, qq)];
-                            dst[off] = c + off < m ? v : 0.0;
-                        }
-                    } else {
-                        double* dst = TF + (long long)c * rowsT + kl;
-                        for (int off = lane; off <= ku; off += 32) {
-                            const int cc = qq + off;
-                            const double v = cc < 8 ? sD[qq * 8 + cc] : sUc[(cc >> 3) * 64 + bfrag(qq, cc & 7)];
-                            dst[off] = c + off < m ? v : 0.0;
+                    const bool lseg = sgm < 8;
+                    double* dst = lseg ? F + (long long)c * rows + d : TF + (long long)c * rowsT + kl;
+                    const int o0 = lseg ? 1 : 0, oe = lseg ? kl : ku;
+                    double v[KIT];
+#pragma unroll
+                    for (int it = 0; it < KIT; ++it) {
+                        const int off = o0 + lane + 32 * it, rc = qq + off;
+                        v[it] = 0.0;
+                        if (off <= oe) {
+                            if (lseg) v[it] = rc < 8 ? sD[rc * 8 + qq] : -sLc[(rc >> 3) * 64 + afrag(rc & 7, qq)];
+                            else v[it] = rc < 8 ? sD[qq * 8 + rc] : sUc[(rc >> 3) * 64 + bfrag(qq, rc & 7)];
                         }
                     }
+#pragma unroll
+                    for (int it = 0; it < KIT; ++it) {
+                        const int off = o0 + lane + 32 * it;
+                        if (off <= oe) dst[off] = c + off < m ? v[it] : 0.0;
+                    }
                 }
-                // L rows (row-major copy) and U columns (packed): runs of <= 8
-                // contiguous entries, 8 lanes per run (4 runs per warp store)
-                for (int e = (wt ? 0 : (7 + kl) * 8) + orank * 32 + lane; e < tr_n * 8 && orank >= 0;
-                     e += 32 * (NW - 1)) {
-                    const int t = e >> 3, qq = e & 7;
-                    const bool lrun = t < 7 + kl;
-                    const int x = lrun ? t + 1 : t - (7 + kl);  // rr (L row) or cc (U column)
-                    const bool in = lrun ? (qq < x && x - qq <= kl) : (qq <= x && x - qq <= ku);
-                    if (!in || j0 + x >= m || j0 + qq >= m) continue;
-                    double v;
-                    if (x < 8) v = lrun ? sD[x * 8 + qq] : sD[qq * 8 + x];
-                    else v = lrun ? -sLc[(x >> 3) * 64 + afrag(x & 7, qq)] : sUc[(x >> 3) * 64 + afrag(x & 7, qq)];
+                // L rows (row-major copy) and U columns (packed): run x holds the
+                // <= 8 entries of rows / columns j0..j0+7 of L row j0+x / U column
+                // j0+x; one lane per run (two 4-entry fragment runs in shared
+                // memory, 16-byte stores), starting on the warps without a column
+                const int nl = wt ? 7 + kl : 0, nrun = nl + 8 + ku;
+                const int brank = (orank + (NW - 1) - nseg % (NW - 1)) % (NW - 1);
+                for (int t = brank * 32 + lane; t < nrun && orank >= 0; t += 32 * (NW - 1)) {
+                    const bool lrun = t < nl;
+                    const int x = lrun ? t + 1 : t - nl;
+                    if (j0 + x >= m) continue;
+                    const int lo = max(0, x - (lrun ? kl : ku)), hi = min(lrun ? x - 1 : x, min(7, m - 1 - j0));
                     double* dst = lrun ? TF + (long long)(j0 + x) * rowsT + kl - x : F + (long long)(j0 + x) * rows + d - x;
-                    dst[qq] = v;
+                    double v[8];
+                    if (x >= 8) {
+                        const double* src = (lrun ? sLc : sUc) + (x >> 3) * 64 + (x & 7) * 4;
+                        const double2 p0 = *reinterpret_cast<const double2*>(src);
+                        const double2 p1 = *reinterpret_cast<const double2*>(src + 2);
+                        const double2 p2 = *reinterpret_cast<const double2*>(src + 32);
+                        const double2 p3 = *reinterpret_cast<const double2*>(src + 34);
+                        const double sg1 = lrun ? -1.0 : 1.0;
+                        v[0] = sg1 * p0.x, v[1] = sg1 * p0.y, v[2] = sg1 * p1.x, v[3] = sg1 * p1.y;
+                        v[4] = sg1 * p2.x, v[5] = sg1 * p2.y, v[6] = sg1 * p3.x, v[7] = sg1 * p3.y;
+                    } else {
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq) v[qq] = lrun ? sD[x * 8 + qq] : sD[qq * 8 + x];
+                    }
+                    if (lo == 0 && hi == 7) {
+                        const bool al = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+                        double* d2 = al ? dst : dst + 1;
+                        if (!al) dst[0] = v[0];
+                        *reinterpret_cast<double2*>(d2) = al ? make_double2(v[0], v[1]) : make_double2(v[1], v[2]);
+                        *reinterpret_cast<double2*>(d2 + 2) = al ? make_double2(v[2], v[3]) : make_double2(v[3], v[4]);
+                        *reinterpret_cast<double2*>(d2 + 4) = al ? make_double2(v[4], v[5]) : make_double2(v[5], v[6]);
+                        if (al) *reinterpret_cast<double2*>(d2 + 6) = make_double2(v[6], v[7]);
+                        else dst[7] = v[7];
+                    } else {
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq)
+                            if (qq >= lo && qq <= hi) dst[qq] = v[qq];
+                    }
                 }
                 if (threadIdx.x < 8 && j0 + threadIdx.x < m)
                     A.dinv[P.r0 + j0 + threadIdx.x] = sm[S::DINV + par * 8 + threadIdx.x];

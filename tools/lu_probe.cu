@@ -72,7 +72,7 @@ int main(int argc, char** argv) {
         CUtensorMap a, b;
         printf("TMA staging: %s\n", spk::band_tensor_maps(A, 170, 10, 168, &a, &b) >= 0 ? "yes" : "no");
     }
-#ifdef SPK_LU_PROFILE
+#if defined(SPK_LU_PROFILE) || defined(SPK_LU_DBG)
     {
         const int dbg = getenv("LU_DBG") ? atoi(getenv("LU_DBG")) : 0;
         cudaMemcpyToSymbol(spk::g_lu_dbg, &dbg, sizeof(int));
