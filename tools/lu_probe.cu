@@ -1,6 +1,6 @@
 // lu_probe.cu -- phase timing of the blocked DMMA band LU on one partition.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DSPK_LU_PROFILE \
-//        -o tools/lu_probe tools/lu_probe.cu && tools/lu_probe [m] [k] [parts] [tma 0/1]
+//        -o tools/lu_probe tools/lu_probe.cu && tools/lu_probe [m] [k] [parts] [tma 0/1] [row-major copy 0/1]
 // Prints the per-step clock totals of CTA 0, summed over its warps (slot 3/4:
 // the warp publishing the panel row and factoring the next diagonal block).
 #include "../paper_1811_03559_b200/csrc/spk_lu_fast.cu"
@@ -68,6 +68,7 @@ int main(int argc, char** argv) {
     cudaMemset(d_boost, 0, sizeof(int) * nparts);
     spk::FastLuArgs A{d_units, d_parts, d_band, k, k, d_fac, d_tfac, d_dinv, d_piv, 1.49e-8, d_boost, n, 0};
     if (argc > 4 && atoi(argv[4]) == 0) A.ncols = 0;  // element-path staging only
+    if (argc > 5 && atoi(argv[5]) == 0) A.tfac = nullptr;  // no row-major copy (factorizations without transposed solves)
     {
         CUtensorMap a, b;
         printf("TMA staging: %s\n", spk::band_tensor_maps(A, 170, 10, 168, &a, &b) >= 0 ? "yes" : "no");
