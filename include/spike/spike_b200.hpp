@@ -222,6 +222,50 @@ struct RefineResult {
 RefineResult iterative_refine(const SpikeFactorization& fact, const BandedMatrix& a, const DenseBlock& f,
                               const DenseBlock& x0, int max_iters, double tol, bool transpose = false);
 
+// ---------------------------------------------------------------- spike2x2.hpp
+// The two-partition SPIKE kernel (spike2x2.hpp:25-87, spike2x2.cpp:28-289):
+// LU on the top half, UL on the bottom half (split at ceil(n/2)), one factored
+// 2k coupling block [[I, vtip], [wtip, I]].  On the GPU the two cooperating
+// host threads of the reference are the two partitions of a p = 2
+// factorization: both halves are factored by the same launch (one CTA each,
+// the bottom half on the reversed view), their interface tips meet in the
+// coupling unit, and the std::barrier points are the kernel boundaries of the
+// stage program.  The *_task entry points (a CPU threading protocol) have no
+// GPU counterpart; the standalone wrappers below keep their signatures,
+// results, sweep budgets and exceptions.
+struct SpikeTips {
+    DenseBlock vt, vb, wt, wb;
+};
+
+class Spike2x2Factors {
+public:
+    Spike2x2Factors() = default;
+    int n() const { return n_; }
+    int k() const { return k_; }
+    int split() const { return split_; }
+    int boost_count() const { return fact_.boost_count; }
+    // bottom tip of A1^-1 [0; Bint] and top tip of A2^-1 [Cint; 0]
+    const DenseBlock& vtip() const { return vtip_; }
+    const DenseBlock& wtip() const { return wtip_; }
+    const LUFactors& reduced() const { return reduced_; }
+    // the HBM-resident p = 2 factorization behind it (extension)
+    const SpikeFactorization& factorization() const { return fact_; }
+
+private:
+    friend Spike2x2Factors factor_2x2(const BandedMatrix&, bool, double);
+    int n_ = 0, k_ = 0, split_ = 0;
+    DenseBlock vtip_, wtip_;
+    LUFactors reduced_;
+    SpikeFactorization fact_;
+};
+
+Spike2x2Factors factor_2x2(const BandedMatrix& a, bool pivoting, double boost_eps = default_boost_eps());
+DenseBlock solve_2x2(const Spike2x2Factors& fac, const DenseBlock& f, bool transpose = false,
+                     SweepCounter* counter = nullptr);
+// tips of V = A^-1 [0; bhat] and W = A^-1 [chat; 0] (the enclosing partition's spikes)
+SpikeTips spikes_2x2(const Spike2x2Factors& fac, const DenseBlock& bhat, const DenseBlock& chat,
+                     SweepCounter* counter = nullptr);
+
 // ---------------------------------------------------------------- band ops
 DenseBlock band_matmul(const BandedMatrix& a, const DenseBlock& x, bool transpose = false);
 double relative_residual(const BandedMatrix& a, const DenseBlock& x, const DenseBlock& f, bool transpose = false);

@@ -313,6 +313,73 @@ DenseBlock transpose_solve(const SpikeFactorization& fact, const DenseBlock& f, 
     return solve_impl(fact, f, stats, true);
 }
 
+// ------------------------------------------------------------------ 2x2 kernel
+// spike2x2.cpp:246-289 (the standalone wrappers) over a p = 2 factorization
+Spike2x2Factors factor_2x2(const BandedMatrix& a, bool pivoting, double boost_eps) {
+    const int n = a.n(), k = std::max(a.kl(), a.ku());
+    // spike2x2.cpp:37-38
+    if (n < 2 * (a.kl() + a.ku() + 1)) throw std::invalid_argument("Spike2x2Factors: partition too small for its band");
+    Spike2x2Factors fac;
+    fac.n_ = n;
+    fac.k_ = k;
+    fac.split_ = (n + 1) / 2;
+    PartitionPlan plan;
+    plan.p = 2;
+    plan.bounds = {0, fac.split_, n};
+    plan.kinds = {PartitionKind::FirstLast, PartitionKind::FirstLast};
+    plan.threads_used = 2;
+    FactorOptions opts;
+    opts.pivoting = pivoting;
+    opts.boost_eps = boost_eps;
+    fac.fact_ = factorize(a, plan, opts);
+    if (k > 0) {
+        fac.vtip_ = fac.fact_.vb[0];
+        fac.wtip_ = fac.fact_.wt[1];
+        if (!fac.fact_.levels.pairs.empty() && !fac.fact_.levels.pairs[0].empty())
+            fac.reduced_ = fac.fact_.levels.pairs[0][0];
+    }
+    return fac;
+}
+
+DenseBlock solve_2x2(const Spike2x2Factors& fac, const DenseBlock& f, bool transpose, SweepCounter* counter) {
+    DenseBlock x = transpose ? transpose_solve(fac.factorization(), f) : solve(fac.factorization(), f);
+    // two half-sweep pairs per solve (spike2x2.hpp:36-41)
+    if (counter) counter->full_sweeps_solve += 2;
+    return x;
+}
+
+SpikeTips spikes_2x2(const Spike2x2Factors& fac, const DenseBlock& bhat, const DenseBlock& chat,
+                     SweepCounter* counter) {
+    const int n = fac.n(), k = fac.k();
+    if (bhat.rows != k || bhat.cols != k || chat.rows != k || chat.cols != k)
+        throw std::invalid_argument("spikes_2x2: corner blocks must be k x k");
+    SpikeTips t;
+    t.vt = DenseBlock(k, k);
+    t.vb = DenseBlock(k, k);
+    t.wt = DenseBlock(k, k);
+    t.wb = DenseBlock(k, k);
+    if (k > 0) {
+        // one solve with the 2k columns [0; bhat] and [chat; 0]
+        DenseBlock rhs(n, 2 * k);
+        for (int c = 0; c < k; ++c)
+            for (int i = 0; i < k; ++i) {
+                rhs.at(n - k + i, c) = bhat.at(i, c);
+                rhs.at(i, k + c) = chat.at(i, c);
+            }
+        const DenseBlock x = solve(fac.factorization(), rhs);
+        for (int c = 0; c < k; ++c)
+            for (int i = 0; i < k; ++i) {
+                t.vt.at(i, c) = x.at(i, c);
+                t.vb.at(i, c) = x.at(n - k + i, c);
+                t.wt.at(i, c) = x.at(i, k + c);
+                t.wb.at(i, c) = x.at(n - k + i, k + c);
+            }
+    }
+    // three half-sweep pairs for spike generation (spike2x2.hpp:46-48)
+    if (counter) counter->full_sweeps_factor += 3;
+    return t;
+}
+
 static DenseBlock reduced_impl(const ReducedLevels& levels, const DenseBlock& y, long* couplings, bool transpose) {
     if (y.rows != 2 * levels.p * levels.k)
         throw std::invalid_argument(transpose ? "reduced_solve_transpose: tip block has wrong height"

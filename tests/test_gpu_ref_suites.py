@@ -6,6 +6,7 @@ band_ops from the reference sources).  SURVEY.md Appendix B.
   proj/tests/test_solve_stage.cpp   solve / transpose_solve / reduced solves / refine
   proj/tests/test_factor_ds.cpp     factorize: tips, DS identity, reduced levels
   proj/tests/test_acceptance.cpp    the acceptance criteria (ACCEPTANCE ... PASS lines)
+  proj/tests/test_spike2x2.cpp      the two-partition kernel: factor_2x2 / solve_2x2 / spikes_2x2
 
 Excluded from the acceptance suite:
 * "accuracy study against condition number" shells out to the reference CLI
@@ -30,7 +31,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 EXCLUDE = {"test_acceptance": ["accuracy study against condition number", "scaled speed sanity"]}
 
 
-@pytest.mark.parametrize("suite", ["test_solve_stage", "test_factor_ds", "test_acceptance"])
+@pytest.mark.parametrize("suite", ["test_solve_stage", "test_factor_ds", "test_acceptance", "test_spike2x2"])
 def test_reference_suite_passes(spk, suite, tmp_path):
     exe = os.path.join(ROOT, "oracle", "_ref", "suite_" + suite)
     if not os.path.exists(exe):
