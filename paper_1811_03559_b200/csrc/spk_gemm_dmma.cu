@@ -7,9 +7,12 @@
 // retrieval corner products.
 //
 // sm_100a has no tcgen05 FP64 kind; FP64 tensor math is the
-// warp-level mma.sync.m8n8k4.f64 (SASS DMMA).  CTA tile 64x64, K-chunk 16,
-// 4 warps each owning a 32x32 sub-tile = 4x4 DMMA accumulators; A and B
-// chunks are staged through shared memory (cp.async, double-buffered).
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA).  CTA tile 64 x TN, K-chunk 16,
+// 4 warps each owning a 32 x TN/2 sub-tile = 4 x NB DMMA accumulators; A and B
+// chunks are staged through shared memory (cp.async, double-buffered).  TN is
+// 64 (NB = 4) or 80 (NB = 5), whichever pads the job's columns less: k = nrhs
+// = 160 is two 80-column tiles instead of three 64-column ones (a sixth of
+// the tensor work was padding).
 #include "spk_device.cuh"
 
 #include <algorithm>
@@ -19,7 +22,7 @@
 namespace spk {
 
 namespace {
-constexpr int TM = 64, TN = 64, TK = 16;
+constexpr int TM = 64, TK = 16;
 // padded strides (doubles): 20 = 40 words keeps each 16-lane phase of the
 // 8-byte fragment loads on distinct banks
 constexpr int SA = TK + 4;  // A tile stored [m][k]
@@ -54,8 +57,10 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Split-K (ws != nullptr): blockIdx.z takes K range [z*ks, (z+1)*ks) and writes
 // its partial tile to ws[((job * tiles + tile) * nsplit + z) * TM*TN]; the
 // reduction kernel sums the splits in order (deterministic, no atomics).
-__global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
+template <int NB>
+__global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
                                                    double* __restrict__ ws, int nsplit, int tiles_max) {
+    constexpr int TN = 16 * NB;
     const GemmJob& Jg = jobs[blockIdx.x];
     if (!guard_ok(B.flags, Jg.guard)) return;
     const int nc = Jg.nc >= 0 ? Jg.nc : ncols;
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
     __shared__ __align__(16) double sA[2][TM * SA];
     __shared__ __align__(16) double sB[2][TN * SB];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NB);
     const int g = lane >> 2, q = lane & 3;
     const int row0 = tr * TM, col0 = tc * TN;
 
@@ -128,11 +133,11 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
         cp_async_commit();
     };
 
-    double acc[4][4][2];
+    double acc[4][NB][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
     const int nk = kend > kbeg ? (kend - kbeg + TK - 1) / TK : 0;
     if (nk > 0) stage(0, kbeg);
@@ -149,15 +154,15 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
         const double* b_s = sB[buf];
 #pragma unroll
         for (int ks = 0; ks < TK; ks += 4) {
-            double af[4], bf[4];
+            double af[4], bf[NB];
 #pragma unroll
             for (int a = 0; a < 4; ++a) af[a] = a_s[(wm + 8 * a + g) * SA + ks + q];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) bf[b] = b_s[(wn + 8 * b + g) * SB + ks + q];
+            for (int b = 0; b < NB; ++b) bf[b] = b_s[(wn + 8 * b + g) * SB + ks + q];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+                for (int b = 0; b < NB; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
         }
         __syncthreads();
     }
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
+            for (int b = 0; b < NB; ++b)
                 *reinterpret_cast<double2*>(part + (wm + 8 * a + g) * TN + wn + 8 * b + 2 * q) =
                     make_double2(acc[a][b][0], acc[a][b][1]);
         __threadfence();
@@ -190,13 +195,13 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+            for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         for (int z = 0; z < nsplit; ++z) {
             const double* pz = tile + (size_t)z * (TM * TN);
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
+                for (int b = 0; b < NB; ++b) {
                     const double2 v = __ldcg(reinterpret_cast<const double2*>(pz + (wm + 8 * a + g) * TN + wn + 8 * b + 2 * q));
                     acc[a][b][0] += v.x;
                     acc[a][b][1] += v.y;
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
+            for (int b = 0; b < NB; ++b)
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     if (i0 + 8 * a < jr && c0 + 8 * b + e < nc)
@@ -226,15 +231,22 @@ __global__ void __launch_bounds__(128, 4) k_gemm_dmma(const GemmJob* __restrict_
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < NB; ++b)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
                 if (i0 + 8 * a < jr && c0 + 8 * b + e < nc) P0[8 * a * sr + (8 * b + e) * ld] = acc[a][b][e];
 }
 
+// the column tile that pads max_nc less (64 on ties)
+static int gemm_tn(int max_nc) {
+    const int p64 = (max_nc + 63) / 64 * 64, p80 = (max_nc + 79) / 80 * 80;
+    return p80 < p64 ? 80 : 64;
+}
+
 int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk) {
     // few output tiles over a long K (the transposed reduced-system updates):
     // spread K over CTAs, ~512 per split, enough CTAs for the SMs
+    const int TN = gemm_tn(max_nc);
     const long long tiles = (long long)njobs * ((max_r + TM - 1) / TM) * ((max_nc + TN - 1) / TN);
     if (max_kk < 1024 || tiles >= 296) return 1;
     int ns = (max_kk + 511) / 512;
@@ -244,6 +256,7 @@ int gemm_splitk_factor(int njobs, int max_r, int max_nc, int max_kk) {
 
 // doubles: partial tiles, then one int counter per output tile
 size_t gemm_splitk_workspace(int njobs, int max_r, int max_nc, int nsplit) {
+    const int TN = gemm_tn(max_nc);
     const size_t tiles = (size_t)((max_r + TM - 1) / TM) * ((max_nc + TN - 1) / TN);
     return (size_t)njobs * tiles * nsplit * TM * TN + ((size_t)njobs * tiles + 1) / 2;
 }
@@ -251,17 +264,19 @@ size_t gemm_splitk_workspace(int njobs, int max_r, int max_nc, int nsplit) {
 void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, const Bufs& B, int ncols,
                       cudaStream_t s, double* ws, int nsplit) {
     if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
+    const int TN = gemm_tn(max_nc);
     const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
+    auto* fn = TN == 80 ? k_gemm_dmma<5> : k_gemm_dmma<4>;
     if (ws && nsplit > 1) {
         const size_t tiles = (size_t)njobs * tr * tc;
         cudaMemsetAsync(ws + tiles * nsplit * TM * TN, 0, sizeof(int) * tiles, s);  // split counters
         dim3 g(njobs, tr * tc, nsplit);
-        k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
+        fn<<<g, 128, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
         count_launch();
         return;
     }
     dim3 g(njobs, tr * tc);
-    k_gemm_dmma<<<g, 128, 0, s>>>(d_jobs, B, ncols, nullptr, 1, tr * tc);
+    fn<<<g, 128, 0, s>>>(d_jobs, B, ncols, nullptr, 1, tr * tc);
     count_launch();
 }
 
