@@ -16,8 +16,13 @@
 //     rows and formed the diagonal-block inverses on one warp meanwhile);
 //   * the producers also form the stage's diagonal-block inverses (off the
 //     compute warps' path), so a block is X = Tinv P (2 DMMA) + the update;
-//   * right-hand-side rows entering the window come straight from global
-//     memory through a small register queue, LA blocks ahead.
+//   * right-hand-side rows entering the window come through a per-warp
+//     shared-memory ring filled by cp.async kDmma2Ring blocks ahead (each lane
+//     copies and later reads its own two entries: no synchronisation beyond
+//     cp.async.wait_group).  A register queue filled by plain loads stalled
+//     the warp at the top of every block -- ptxas reuses the load's target
+//     register and moves the value out at once, which waits for the load
+//     (ncu: 11% of the kernel's samples on that move, long scoreboard).
 // Out-of-band stage slots are zeroed once and never loaded; rows past the sweep
 // end are masked in the consumer (their window rows are never stored).
 #pragma once
@@ -35,6 +40,7 @@ __device__ __forceinline__ void dmma2_acc(double& d0, double& d1, double a, doub
 
 constexpr int kDmma2Producers = 2;  // producer warps per CTA
 constexpr int kDmma2Stages = 3;     // factor stages in flight
+constexpr int kDmma2Ring = 6;       // right-hand-side ring depth per compute warp, blocks (512 B each)
 
 template <int NTW>
 struct Dmma2Geom {
@@ -48,7 +54,7 @@ inline size_t dmma2_sweep_smem(int ntw, int ncw = 0, bool pair = false) {
     const int KWT = 8 * (ntw - 1);
     const int SR = ((8 + KWT + 15) / 16) * 16 + 4;
     return (size_t)kDmma2Stages * (32 * SR + 32 + 4 * 64) * 8 + 2 * kDmma2Stages * 8 + 16 +
-           (pair ? (size_t)(ncw / 2) * (4 * 64 * 8 + 16) : 0);
+           (pair ? (size_t)(ncw / 2) * (4 * 64 * 8 + 16) : (size_t)ncw * kDmma2Ring * 512);
 }
 
 // PAIR (narrow solves, <= 8 right-hand sides): two compute warps share the 8
@@ -65,7 +71,6 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
     constexpr int KWT = Dmma2Geom<NTW>::KWT;
     constexpr int STG = Dmma2Geom<NTW>::STAGE;
     constexpr int NST = kDmma2Stages;
-    constexpr int LA = NTW <= 17 ? 4 : 2;  // right-hand-side lookahead, blocks (register budget)
     constexpr bool kAsc = (MODE == SW_FWD_L || MODE == SW_FWD_UT);
     constexpr bool kDiag = (MODE == SW_BWD_U || MODE == SW_FWD_UT);
     constexpr int kV = kAsc ? 1 : -1;  // factor vectors run forward (L columns, U rows) or backward
@@ -354,9 +359,22 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
     double Wt[NTW][2];
 #pragma unroll
     for (int T = 0; T < NTW; ++T) rhs(8 * T + g, Wt[T][0], Wt[T][1]);
-    double qv[LA][2];
+    // incoming rows: ring slot j holds this lane's two entries of a block
+    double* const ring = reinterpret_cast<double*>(empty + NST) + (size_t)warp * (kDmma2Ring * 64) + 2 * lane;
+    auto fetch = [&](int blk, int slot) {  // rows 8 blk + g -> slot (zero past the sweep / the columns)
+        const int u = 8 * blk + g;
+        double* dst = ring + slot * 64;
+        const bool ok = u < nsteps;
+        const long long pr = ok ? phys(rowof(u)) : 0;
+        if (ok && cv0) cp_async8(dst, cp0 + pr);
+        else dst[0] = 0.0;
+        if (ok && cv1) cp_async8(dst + 1, cp1 + pr);
+        else dst[1] = 0.0;
+        cp_async_commit();
+    };
 #pragma unroll
-    for (int j = 0; j < LA; ++j) rhs(8 * (NTW + j) + g, qv[j][0], qv[j][1]);
+    for (int j = 0; j < kDmma2Ring; ++j) fetch(NTW + j, j);
+    int rslot = 0;
 
     const int nblocks = (nsteps + 7) / 8;
     for (int b = 0; b < nblocks; ++b) {
@@ -407,32 +425,23 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
-        // rotate; the freed slot takes the queued rows 8(b+NTW)+g
+        // rotate; the freed slot takes rows 8(b+NTW)+g from the ring, whose
+        // slot is refilled kDmma2Ring blocks ahead
 #pragma unroll
         for (int i = 0; i < NTW - 1; ++i) {
             Wt[i][0] = Wt[i + 1][0];
             Wt[i][1] = Wt[i + 1][1];
         }
-        Wt[NTW - 1][0] = qv[0][0];
-        Wt[NTW - 1][1] = qv[0][1];
-#pragma unroll
-        for (int j = 0; j + 1 < LA; ++j) {
-            qv[j][0] = qv[j + 1][0];
-            qv[j][1] = qv[j + 1][1];
-        }
-        rhs(8 * (b + 1 + NTW + LA - 1) + g, qv[LA - 1][0], qv[LA - 1][1]);
+        cp_async_wait<kDmma2Ring - 1>();
         {
-            // L2 prefetch of the rows the queue takes PF blocks later: the
-            // register queue alone (LA blocks) is shorter than HBM latency
-            constexpr int PF = 8;
-            const int u = 8 * (b + 1 + NTW + LA - 1 + PF) + g;
-            if (u < nsteps) {
-                const long long pr = phys(rowof(u));
-                if (cv0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp0 + pr));
-                if (cv1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cp1 + pr));
-            }
+            const double2 t = *reinterpret_cast<const double2*>(ring + rslot * 64);
+            Wt[NTW - 1][0] = t.x;
+            Wt[NTW - 1][1] = t.y;
         }
+        fetch(b + NTW + kDmma2Ring, rslot);
+        rslot = rslot + 1 == kDmma2Ring ? 0 : rslot + 1;
     }
+    cp_async_wait<0>();
     }
 }
 
