@@ -138,12 +138,22 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
                 if (R >= NST) mbar_wait(empty + s, ((R / NST) - 1) & 1);
                 double* st = s_st + s * STG;
                 const int u0 = 32 * R;
-                for (int e = pt; e < 32 * (8 + KWT); e += npt) {
-                    const int t = e / (8 + KWT), r = e - t * (8 + KWT);
-                    const int dl = r - (t & 7) - 1;
-                    const int u = u0 + t;
-                    if (dl >= 0 && dl < kw && u < nsteps)
-                        cp_async8(st + t * SR + r, vbase + (long long)rowof(u) * vstride + kV * dl);
+                // thread pt copies entries dl = pt, pt + npt, ... of each of the
+                // round's 32 vectors: the source steps by one factor vector per
+                // t and the slot offsets are compile-time (t unrolled), a few
+                // instructions per entry.  (One flat loop over the stage with a
+                // division per entry made a producer as busy as a compute warp.)
+                const int nv = min(32, nsteps - u0);
+                const double* src = vbase + (long long)rowof(u0) * vstride + kV * pt;
+                const long long sstep = kAsc ? vstride : -vstride;
+                double* dst = st + pt + 1;
+#pragma unroll 8
+                for (int t = 0; t < 32; ++t) {
+                    if (t < nv) {
+                        for (int dl = pt, o = 0; dl < kw; dl += npt, o += npt)
+                            cp_async8(dst + t * SR + (t & 7) + o, src + kV * o);
+                    }
+                    src += sstep;
                 }
                 if (kDiag && pt < 32 && u0 + pt < nsteps)
                     cp_async8(st + 32 * SR + pt, A.dinv + P.r0 + rowof(u0 + pt));
