@@ -22,11 +22,14 @@ timeout 600 python tools/profile_case.py --n 1000000 --k 160 --nrhs 160 --transp
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_sweep_dmma2 -s 2 -c 2 -o $O/prof_sweep python tools/profile_case.py --n 1000000 --k 160 --nrhs 160 --transpose --reps 1 > $O/ncu_sweep.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_band_lu_dmma -c 1 -o $O/prof_lu python tools/profile_case.py --n 1000000 --k 160 --nrhs 160 --transpose --reps 1 > $O/ncu_lu.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_sk_ -s 3 -c 3 -o $O/prof_sk python tools/sk_probe.py > $O/ncu_sk.log 2>&1
+C3C="python tools/profile_case.py --n 1000000 --k 160 --nrhs 160 --transpose --reps 1"
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_gemm_dmma -s 4 -c 6 -o $O/prof_gemm $C3C > $O/ncu_gemm.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_schur_inverse -c 2 -o $O/prof_schur $C3C > $O/ncu_schur.log 2>&1
 # summaries on the box (the reports themselves exceed what gpurun brings back)
-for r in sweep lu sk; do
+for r in sweep lu sk gemm schur; do
   [ -f $O/prof_$r.ncu-rep ] || continue
   python tools/ncu_summary.py report $O/prof_$r.ncu-rep "round 2 $r" "see tools/prof_round.sh" > $O/summary_$r.txt 2>&1
-  for kern in k_sweep_dmma2 k_band_lu_dmma k_sk_parts k_sk_levels k_sk_solve; do
+  for kern in k_sweep_dmma2 k_band_lu_dmma k_sk_parts k_sk_levels k_sk_solve k_gemm_dmma k_schur_inverse; do
     python tools/ncu_inst.py $O/prof_$r.ncu-rep $kern 40 > $O/lines_${r}_$kern.txt 2>/dev/null
     [ -s $O/lines_${r}_$kern.txt ] || rm -f $O/lines_${r}_$kern.txt
   done
