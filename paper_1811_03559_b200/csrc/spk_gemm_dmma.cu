@@ -57,7 +57,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // Split-K (ws != nullptr): blockIdx.z takes K range [z*ks, (z+1)*ks) and writes
 // its partial tile to ws[((job * tiles + tile) * nsplit + z) * TM*TN]; the
 // reduction kernel sums the splits in order (deterministic, no atomics).
-template <int NB>
+// NS = cp.async stages in flight (dynamic shared memory, NS * (TM*SA + TN*SB)
+// doubles).  With two stages the warps of the 64 x 80 variant (three CTAs per
+// SM) spent 28-30% of their stall samples on the next chunk's loads
+// (profiles/r02_gemm_schur_ncu.txt); three stages keep two chunks in flight.
+template <int NB, int NS>
 __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
                                                    double* __restrict__ ws, int nsplit, int tiles_max) {
     constexpr int TN = 16 * NB;
@@ -70,8 +74,9 @@ __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJo
     const int tc = blockIdx.y / tiles_r;
     if (tc * TN >= nc || jr <= 0) return;
     const RV va = resolve(B, Jg.a), vb = resolve(B, Jg.b), vc = resolve(B, Jg.c);
-    __shared__ __align__(16) double sA[2][TM * SA];
-    __shared__ __align__(16) double sB[2][TN * SB];
+    extern __shared__ __align__(16) double gemm_sm[];
+    double* const sA = gemm_sm;                 // [NS][TM * SA]
+    double* const sB = gemm_sm + NS * TM * SA;  // [NS][TN * SB]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NB);
     const int g = lane >> 2, q = lane & 3;
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJo
 #pragma unroll
             for (int j = 0; j < TK / 2; ++j) {
                 const int l = a_l + 2 * j;
-                double* dst = &sA[buf][a_i * SA + l];
+                double* dst = &sA[buf * TM * SA + a_i * SA + l];
                 if (a_rok && k0 + l < kend) cp_async8(dst, src + (long long)(2 * j) * va.ld);
                 else *dst = 0.0;
             }
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJo
 #pragma unroll
             for (int j = 0; j < TM / 8; ++j) {
                 const int i = t_i + 8 * j;
-                double* dst = &sA[buf][i * SA + t_l];
+                double* dst = &sA[buf * TM * SA + i * SA + t_l];
                 if (lok && row0 + i < jr) cp_async8(dst, src + (long long)i * va.ld);
                 else *dst = 0.0;
             }
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJo
 #pragma unroll
             for (int j = 0; j < TN / 8; ++j) {
                 const int c = b_c + 8 * j;
-                double* dst = &sB[buf][c * SB + b_l];
+                double* dst = &sB[buf * TN * SB + c * SB + b_l];
                 if (lok && col0 + c < nc) cp_async8(dst, src + (long long)c * vb.ld);
                 else *dst = 0.0;
             }
@@ -140,18 +145,20 @@ __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJo
         for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
     const int nk = kend > kbeg ? (kend - kbeg + TK - 1) / TK : 0;
-    if (nk > 0) stage(0, kbeg);
+    // NS - 1 chunks in flight; one commit group per chunk slot (empty past the end)
+#pragma unroll
+    for (int c = 0; c < NS - 1; ++c) {
+        if (c < nk) stage(c, kbeg + c * TK);
+        else cp_async_commit();
+    }
     for (int kc = 0; kc < nk; ++kc) {
-        const int buf = kc & 1;
-        if (kc + 1 < nk) {
-            stage(buf ^ 1, kbeg + (kc + 1) * TK);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        const int buf = kc % NS;
+        if (kc + NS - 1 < nk) stage((kc + NS - 1) % NS, kbeg + (kc + NS - 1) * TK);
+        else cp_async_commit();
+        cp_async_wait<NS - 1>();
         __syncthreads();
-        const double* a_s = sA[buf];
-        const double* b_s = sB[buf];
+        const double* a_s = sA + buf * TM * SA;
+        const double* b_s = sB + buf * TN * SB;
 #pragma unroll
         for (int ks = 0; ks < TK; ks += 4) {
             double af[4], bf[NB];
@@ -266,17 +273,19 @@ void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, c
     if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
     const int TN = gemm_tn(max_nc);
     const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
-    auto* fn = TN == 80 ? k_gemm_dmma<5> : k_gemm_dmma<4>;
+    auto* fn = TN == 80 ? k_gemm_dmma<5, 3> : k_gemm_dmma<4, 2>;
+    const int smem = (TN == 80 ? 3 : 2) * (TM * SA + TN * SB) * (int)sizeof(double);
+    set_smem_attr((const void*)fn, smem);
     if (ws && nsplit > 1) {
         const size_t tiles = (size_t)njobs * tr * tc;
         cudaMemsetAsync(ws + tiles * nsplit * TM * TN, 0, sizeof(int) * tiles, s);  // split counters
         dim3 g(njobs, tr * tc, nsplit);
-        fn<<<g, 128, 0, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
+        fn<<<g, 128, smem, s>>>(d_jobs, B, ncols, ws, nsplit, tr * tc);
         count_launch();
         return;
     }
     dim3 g(njobs, tr * tc);
-    fn<<<g, 128, 0, s>>>(d_jobs, B, ncols, nullptr, 1, tr * tc);
+    fn<<<g, 128, smem, s>>>(d_jobs, B, ncols, nullptr, 1, tr * tc);
     count_launch();
 }
 

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
 
     if (warp >= ncw) {
         // ---- producers: round R -> stage R % NST, loads issued two rounds ahead
-        const int pt = threadIdx.x - ncw * 32, npt = kDmma2Producers * 32;
+        const int pt = threadIdx.x - ncw * 32, npt = blockDim.x - ncw * 32;  // (run-time on purpose: see DESIGN 4)
         auto issue = [&](int R) {
             if (R < nrounds) {
                 const int s = R % NST;
@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
 #pragma unroll
     for (int T = 0; T < NTW; ++T) rhs(8 * T + g, Wt[T][0], Wt[T][1]);
     // incoming rows: ring slot j holds this lane's two entries of a block
-    double* const ring = reinterpret_cast<double*>(empty + NST) + (size_t)warp * (kDmma2Ring * 64) + 2 * lane;
+    // (slot layout [2 columns][32 lanes]: the 8-byte copies of a warp fall on distinct banks)
+    double* const ring = reinterpret_cast<double*>(empty + NST) + (size_t)warp * (kDmma2Ring * 64) + lane;
     auto fetch = [&](int blk, int slot) {  // rows 8 blk + g -> slot (zero past the sweep / the columns)
         const int u = 8 * blk + g;
         double* dst = ring + slot * 64;
@@ -378,8 +379,8 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
         const long long pr = ok ? phys(rowof(u)) : 0;
         if (ok && cv0) cp_async8(dst, cp0 + pr);
         else dst[0] = 0.0;
-        if (ok && cv1) cp_async8(dst + 1, cp1 + pr);
-        else dst[1] = 0.0;
+        if (ok && cv1) cp_async8(dst + 32, cp1 + pr);
+        else dst[32] = 0.0;
         cp_async_commit();
     };
 #pragma unroll
@@ -444,9 +445,8 @@ __global__ void __launch_bounds__(512) k_sweep_dmma2(FastSweepArgs A) {
         }
         cp_async_wait<kDmma2Ring - 1>();
         {
-            const double2 t = *reinterpret_cast<const double2*>(ring + rslot * 64);
-            Wt[NTW - 1][0] = t.x;
-            Wt[NTW - 1][1] = t.y;
+            Wt[NTW - 1][0] = ring[rslot * 64];
+            Wt[NTW - 1][1] = ring[rslot * 64 + 32];
         }
         fetch(b + NTW + kDmma2Ring, rslot);
         rslot = rslot + 1 == kDmma2Ring ? 0 : rslot + 1;
