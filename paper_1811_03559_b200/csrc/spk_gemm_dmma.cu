@@ -59,8 +59,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // reduction kernel sums the splits in order (deterministic, no atomics).
 // NS = cp.async stages in flight (dynamic shared memory, NS * (TM*SA + TN*SB)
 // doubles).  With two stages the warps of the 64 x 80 variant (three CTAs per
-// SM) spent 28-30% of their stall samples on the next chunk's loads
-// (profiles/r02_gemm_schur_ncu.txt); three stages keep two chunks in flight.
+// SM) spend 28-30% of their stall samples on the next chunk's loads
+// (profiles/r02_gemm_schur_ncu.txt), but three stages measured slower (C3's
+// GEMMs 5.73 -> 6.05 ms): both variants run NS = 2.
 template <int NB, int NS>
 __global__ void __launch_bounds__(128, NB == 5 ? 3 : 4) k_gemm_dmma(const GemmJob* __restrict__ jobs, Bufs B, int ncols,
                                                    double* __restrict__ ws, int nsplit, int tiles_max) {
@@ -273,8 +274,8 @@ void launch_gemm_dmma(const GemmJob* d_jobs, int njobs, int max_r, int max_nc, c
     if (njobs <= 0 || max_r <= 0 || max_nc <= 0) return;
     const int TN = gemm_tn(max_nc);
     const int tr = (max_r + TM - 1) / TM, tc = (max_nc + TN - 1) / TN;
-    auto* fn = TN == 80 ? k_gemm_dmma<5, 3> : k_gemm_dmma<4, 2>;
-    const int smem = (TN == 80 ? 3 : 2) * (TM * SA + TN * SB) * (int)sizeof(double);
+    auto* fn = TN == 80 ? k_gemm_dmma<5, 2> : k_gemm_dmma<4, 2>;
+    const int smem = 2 * (TM * SA + TN * SB) * (int)sizeof(double);
     set_smem_attr((const void*)fn, smem);
     if (ws && nsplit > 1) {
         const size_t tiles = (size_t)njobs * tr * tc;
