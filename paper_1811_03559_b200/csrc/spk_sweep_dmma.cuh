@@ -126,34 +126,46 @@ __global__ void __launch_bounds__(512) k_sweep_dmma(FastSweepArgs A) {
     double* const cp0 = bbase + (long long)(c0 + (cv0 ? lc0 : 0)) * ld;
     double* const cp1 = bbase + (long long)(c0 + (cv1 ? lc0 + 1 : 0)) * ld;
 
+    // Staging, a few instructions per entry: a thread keeps one factor vector
+    // of the round (step vt, entries vj, vj + nwarps, ...) and one row of the
+    // incoming right-hand sides (row rt, columns rc0, rc0 + nwarps, ...), so the
+    // stage offsets are fixed and the sources step by constants.  Out-of-band
+    // stage slots are zeroed once (both buffers) and never loaded; vectors past
+    // the sweep end keep stale finite data that the zero rows of Tinv cancel.
+    // (One flat loop over the stage, with a division per entry and the zero
+    // slots rewritten every round, was a third of the kernel's instructions.)
+    const int vt = threadIdx.x / nwarps, vj = threadIdx.x - vt * nwarps;
+    const int sdst = vt * SR + (vt & 7) + 1 + vj;
+    const int rt = threadIdx.x & 31, rc0 = threadIdx.x >> 5;
+    for (int idx = threadIdx.x; idx < 2 * 4 * 8 * SR; idx += blockDim.x) s_A[idx] = 0.0;
+    __syncthreads();
     auto load_round = [&](int R) {
         const int st = R & 1;
         const int u0 = 32 * R;
         if (u0 < nsteps) {
             double* dA = s_A + (size_t)st * 4 * 8 * SR;
-            for (int idx = threadIdx.x; idx < 4 * 8 * SR; idx += blockDim.x) {
-                const int bt = idx / SR, r = idx - bt * SR;  // bt = 8*bb + t
-                const int t = bt & 7;
-                const int u = u0 + bt;
-                const int dl = r - t - 1;
-                if (dl >= 0 && dl < kw && r < 8 + KWT && u < nsteps)
-                    cp_async8(dA + idx, vbase + (long long)rowof(u) * vstride + vdir * dl);
-                else
-                    dA[idx] = 0.0;
+            if (u0 + vt < nsteps) {
+                const double* src = vbase + (long long)rowof(u0 + vt) * vstride + vdir * vj;
+                double* dst = dA + sdst;
+                for (int dl = vj; dl < kw; dl += nwarps) {
+                    cp_async8(dst, src);
+                    dst += nwarps;
+                    src += vdir * nwarps;
+                }
             }
             if (kDiag && threadIdx.x < 32) {
                 const int u = u0 + threadIdx.x;
                 if (u < nsteps) cp_async8(s_dg + st * 32 + threadIdx.x, A.dinv + P.r0 + rowof(u));
             }
-            double* di = s_in + (size_t)st * 32 * sin_ld;
-            for (int idx = threadIdx.x; idx < 32 * ncta; idx += blockDim.x) {
-                const int t = idx & 31, col = idx >> 5;
-                const int uu = u0 + t + 8 * NTW;
-                double* dst = di + t * sin_ld + col;
-                if (uu < nsteps && col < ncta_valid)
-                    cp_async8(dst, bbase + phys(rowof(uu)) + (long long)(c0 + col) * ld);
-                else
-                    *dst = 0.0;
+            double* dst = s_in + (size_t)st * 32 * sin_ld + rt * sin_ld + rc0;
+            const int uu = u0 + rt + 8 * NTW;
+            const bool ok = uu < nsteps;
+            const double* src = bbase + (ok ? phys(rowof(uu)) : 0) + (long long)(c0 + rc0) * ld;
+            for (int col = rc0; col < ncta; col += nwarps) {
+                if (ok && col < ncta_valid) cp_async8(dst, src);
+                else *dst = 0.0;
+                dst += nwarps;
+                src += (long long)nwarps * ld;
             }
         }
         cp_async_commit();
