@@ -133,3 +133,23 @@ def test_product_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src).lower() or fn == "__init__.py", fn
+
+
+def test_cpp_api_surface_links(spk, tmp_path):
+    """The reference's C++ entry points of the path (factorize / solve /
+    transpose_solve, the planner, the 2x2 kernel's wrappers, band ops and I/O)
+    exist in include/spike and link against libspike_b200.so; nothing is
+    called, so no GPU is needed."""
+    import shutil
+    import subprocess
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("no g++")
+    exe = str(tmp_path / "api_surface")
+    libdir = os.path.dirname(spk.LIB_PATH)
+    subprocess.run([cxx, "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "api_surface.cpp"), "-L" + libdir, "-lspike_b200",
+                    "-Wl,-rpath," + libdir, "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "api surface ok" in r.stdout
