@@ -2023,13 +2023,6 @@ void alloc_fact(spk_fact& f, cudaStream_t s, const std::vector<char>& blob) {
     f.lblk_trw = (!f.reduced_only && f.piv_on) ? piv_trw(f.kl, f.ku) : 0;
     if (f.lblk_trw)
         f.d_lblk = dalloc<double>((f.bounds[p] / 8 + nparts + 2) * piv_rec_size(f.lblk_trw), s);
-    // Pivoted factorizations: the blocked LU (spk_lu_piv_dmma.cu) leaves some
-    // slots of the row-major copy unwritten, and the truncated U^T sweeps of
-    // the edge partitions read them against zero right-hand-side rows: they
-    // have to be finite whatever the block held before (found by the
-    // SPK_POISON runs of tools/fuzz_parity.py; ~0.3 ms on C4).
-    if (f.piv_on && !f.reduced_only && f.tfac_size > 0 && !getenv("SPK_NO_TFAC_MEMSET"))  // TEMP env
-        ck(cudaMemsetAsync(f.d_tfac, 0, sizeof(double) * f.tfac_size, s), "memset");
     tr.mark("allocations");
     f.d_flags = dalloc<int>(std::max(f.npairs, 1), s);
     ck(cudaMemsetAsync(f.d_flags, 0, sizeof(int) * std::max(f.npairs, 1), s), "memset");

@@ -158,6 +158,19 @@ __global__ void __launch_bounds__(32 * TCW, 1) k_band_lu_piv_dmma(PivDmmaArgs A)
         const int r = idx / kl, off = idx - r * kl + 1;
         if (!DENSE && r < m && off > r) TF[(long long)r * rowsT + kl - off] = 0.0;
     }
+    // row-major U slots right of column m - 1 and the partition's padding: no
+    // step writes them, and the truncated U^T sweeps of the edge partitions
+    // read them against zero right-hand-side rows -- they must be finite
+    // whatever the block held before (found by the SPK_POISON runs of
+    // tools/fuzz_parity.py: NaN from transposed pivoted solves)
+    for (int idx = threadIdx.x; idx < ubw * ubw; idx += blockDim.x) {
+        const int i = m - 1 - idx / ubw, off = idx % ubw + 1;
+        if (!DENSE && i >= 0 && i + off >= m) TF[(long long)i * rowsT + kl + off] = 0.0;
+    }
+    if (!DENSE && threadIdx.x < 8) {
+        const long long e = (long long)m * rowsT + threadIdx.x;
+        if (e < ((long long)m * rowsT + 7) / 8 * 8) TF[e] = 0.0;
+    }
 
     double acc[TRW][2];
     auto load_block = [&](int r0, int cb) {  // rows r0 .., column block cb (direct, start-up only)
