@@ -1,7 +1,7 @@
 """Randomised parity sweep: the GPU path against the CPU oracle's direct banded
 solve over random shapes (asymmetric and one-sided bands, ragged nrhs, odd
 partition counts, both factorization variants, forward and transpose, device
-and host buffers).  Prints one JSON line per failure and a summary line.
+and host buffers, the former with padded leading dimensions).  Prints one JSON line per failure and a summary line.
 
   python tools/fuzz_parity.py [--cases N] [--seed S] [--seconds T]
 """
@@ -57,8 +57,12 @@ def draw(rng):
     dd = float(rng.choice([1.2, 1.5, 2.0]))  # dominant: the direct solve is the bar (non-dominant
     # bands need the same-plan SPIKE oracle: tests/test_gpu_parity.py PIV_CASES)
     planner = rng.choice(["gpu", "ref"], p=[0.7, 0.3])
-    return dict(n=n, kl=kl, ku=ku, nrhs=nrhs, p=p, piv=piv, dd=dd, planner=str(planner),
-                seed=int(rng.integers(1, 2**31 - 2)))
+    c = dict(n=n, kl=kl, ku=ku, nrhs=nrhs, p=p, piv=piv, dd=dd, planner=str(planner),
+             seed=int(rng.integers(1, 2**31 - 2)))
+    # (drawn last: the shapes of a seed stay what they were before this option existed)
+    c["device"] = bool(rng.random() < 0.5)
+    c["padf"], c["padx"] = int(rng.choice([0, 1, 5, 64])), int(rng.choice([0, 3, 8]))
+    return c
 
 
 def run_case(o, c):
@@ -75,11 +79,34 @@ def run_case(o, c):
         r12, r13 = spk.compute_ratios(1.0, nrhs, max(kl, ku, 1))
         plan = spk.make_plan(n, kl, ku, c["p"], r12, r13)
     c["p_used"] = plan.p
-    fact = spk.factorize(a, plan, spk.FactorOptions(pivoting=c["piv"]))
+    dev = c.get("device", False)
+    if dev:
+        # device-resident band, F and X with padded leading dimensions (NaN in
+        # the padding rows: they must be neither read into the result nor written)
+        import torch
+        s = torch.cuda.current_stream().cuda_stream
+        dband = torch.from_numpy(np.ascontiguousarray(band)).cuda()
+        ldf, ldx = n + c["padf"], n + c["padx"]
+        dF = torch.full((nrhs, ldf), float("nan"), dtype=torch.float64, device="cuda")
+        dF[:, :n] = torch.from_numpy(np.ascontiguousarray(F.T)).cuda()
+        dX = torch.full((nrhs, ldx), float("nan"), dtype=torch.float64, device="cuda")
+        fact = spk.factorize_device(dband.data_ptr(), n, kl, ku, plan, spk.FactorOptions(pivoting=c["piv"]), s)
+    else:
+        fact = spk.factorize(a, plan, spk.FactorOptions(pivoting=c["piv"]))
     out = {}
     for tr in (False, True):
         xo = o.oracle_solve(band, n, kl, ku, F, tr, True)  # pivoted direct banded solve
-        X = spk.transpose_solve(fact, F) if tr else spk.solve(fact, F)
+        if dev:
+            dX.fill_(float("nan"))
+            spk.solve_device(fact, dF.data_ptr(), ldf, nrhs, dX.data_ptr(), ldx, tr, s)
+            torch.cuda.synchronize()
+            if c["padx"] and not bool(torch.isnan(dX[:, n:]).all()):
+                raise AssertionError("solve wrote X's padding rows")
+            if not bool(torch.equal(dF[:, :n].cpu(), torch.from_numpy(np.ascontiguousarray(F.T)))):
+                raise AssertionError("solve modified F")
+            X = np.asfortranarray(dX[:, :n].cpu().numpy().T)
+        else:
+            X = spk.transpose_solve(fact, F) if tr else spk.solve(fact, F)
         res = o.relative_residual(band, n, kl, ku, X, F, tr)
         gap = rel_componentwise(X, xo)
         ores = o.relative_residual(band, n, kl, ku, xo, F, tr)
